@@ -1,0 +1,226 @@
+/* perrk_b200 — C-ABI of the B200-native P-ERRK / EC-DGSEM hot path.
+ *
+ * This is the drop-in boundary.  The reference (arxiv/paper_2507_04991, a
+ * C++20 CPU library under proj/core) has no FFI; its hot path sits behind the
+ * C++ API listed per entry point below.  Every function here replaces one of
+ * those calls with plain pointers and sizes (no C++ or torch types), returns
+ * 0 on success and a negative PERRK_E* code on failure (the reference throws
+ * perrk::Error, common.hpp:15-23), and leaves a message for perrk_last_error().
+ *
+ * State layout (host and device) is the reference's canonical one
+ * (common.hpp:11-13, semidisc.hpp:37-39): cell-major (cells x-fastest, then y,
+ * then z), node-major within a cell (LGL node x-fastest), variable-minor.
+ *
+ * Threading: one host thread per context (the reference's
+ * Semidiscretization is not thread-safe either, semidisc.hpp:112).  All work
+ * of a context is ordered on its own CUDA stream; the *_resident / advance
+ * calls are asynchronous until perrk_sync().
+ */
+#ifndef PERRK_B200_H
+#define PERRK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PERRK_B200_ABI_VERSION 1
+
+/* status codes */
+#define PERRK_OK 0
+#define PERRK_EINVAL -1    /* precondition violated (reference: PERRK_REQUIRE throws) */
+#define PERRK_ECUDA -2     /* CUDA runtime / device error */
+#define PERRK_EUNSUP -3    /* option not implemented on the device path */
+#define PERRK_ENUMERIC -4  /* inadmissible state / non-finite direction (reference throws) */
+#define PERRK_ECOMM -5     /* NCCL error */
+
+/* numerical flux ids: order of FluxTag, physics.hpp:14 */
+#define PERRK_FLUX_CENTRAL 0
+#define PERRK_FLUX_UPWIND 1
+#define PERRK_FLUX_RUSANOV 2
+#define PERRK_FLUX_HLLE 3
+#define PERRK_FLUX_HLLC 4
+#define PERRK_FLUX_EC 5
+
+/* family kinds: order of FamilyKind, butcher.hpp:28 */
+#define PERRK_FAMILY_P2 0
+#define PERRK_FAMILY_P3_VARIANT 1
+#define PERRK_FAMILY_P3_ORIGINAL 2
+#define PERRK_FAMILY_P4 3
+
+typedef struct perrk_ctx perrk_ctx;
+
+/* Replaces SemidiscretizationSpec (semidisc.hpp:24-35) for the periodic
+ * rectilinear Euler / Navier-Stokes-Fourier cases of the hot path.
+ * dim 2 matches Mesh2DRect (mesh.hpp:22-33); dim 3 is the Mesh3DRect
+ * extension the configs need. */
+typedef struct {
+  int dim;                   /* 2 or 3 */
+  int n[3];                  /* cells per axis; n[2] ignored for dim 2 */
+  const double* edges[3];    /* n[a]+1 strictly increasing edges per axis */
+  int polydeg;               /* only 3 on the device path */
+  int physics;               /* 0 Euler (EulerPhysics), 1 NSF with BR1 (dim 2) */
+  double gamma;              /* ratio of specific heats (> 1) */
+  double mu, prandtl;        /* NSF only */
+  int surface_flux;          /* PERRK_FLUX_* */
+  int volume_mode;           /* 1 flux differencing (0 weak form: unsupported) */
+  int volume_flux;           /* PERRK_FLUX_EC */
+  int device;                /* CUDA device ordinal */
+} perrk_semi_desc;
+
+/* Replaces PartitionFamily (butcher.hpp:36-51): R members sharing b and c,
+ * stored with E ascending; member r integrates cells of level R - r
+ * (member_index_for_level, butcher.hpp:47). */
+typedef struct {
+  int kind;                  /* PERRK_FAMILY_* (order bookkeeping only) */
+  int S, R;
+  const int* E;              /* [R] */
+  const double* A;           /* [R][S][S] row-major */
+  const double* b;           /* [S] */
+  const double* c;           /* [S] */
+} perrk_family_desc;
+
+/* Replaces RelaxationConfig (relax.hpp:16-24).  numerics selects the root
+ * residual: 0 = the reference's form r = H(U+g dt d) - h_ref - g dH with its
+ * stopping rule (relax.cpp:79-104); 1 = the accurate form:
+ * compensated reductions, per-node cancellation-free entropy differences,
+ * Newton stop on |dg| <= 1e-13 g or stagnation.  Only method 0 (Newton) runs
+ * on the device. */
+typedef struct {
+  int method;                /* 0 newton, 1 bisection, 2 secant */
+  int max_iter;
+  double residual_tol, step_tol, bracket_min, bracket_max;
+  int seed_from_previous;
+  int numerics;
+} perrk_relax_cfg;
+
+/* Replaces PerkStepOptions (stepper.hpp:54-60). */
+typedef struct {
+  int relax_enabled;         /* 0: opts.relaxation == nullptr */
+  perrk_relax_cfg relax;
+  double gamma_override;     /* used when relaxation is off */
+  double gamma_seed;
+  double h_ref;              /* NaN: H(U_n) (step mode) */
+  int idt;
+} perrk_step_opts;
+
+/* Replaces PerkStepResult + RelaxationOutcome (stepper.hpp:62-68, relax.hpp:26-31). */
+typedef struct {
+  double gamma;
+  int iterations;
+  double residual;
+  int fell_back;
+  double delta_h;
+  int aborted, bad_cell, bad_stage;
+} perrk_step_result;
+
+/* Replaces IntegratorConfig/TimeControl/CflRamp for the loop of run()
+ * (stepper.hpp:13-41).  The CFL ramp is constant (cfl0 == cfl_max). */
+typedef struct {
+  int fixed_dt;              /* 1: dt fixed (truncated to tf), 0: CFL */
+  double dt_or_cfl;
+  double tf;                 /* stop when t >= tf - 1e-12 max(1,|tf|) */
+  int relax_enabled;
+  perrk_relax_cfg relax;
+  int anchor_initial;        /* EntropyAnchor::initial: h_ref = H(U_0) */
+  int idt;
+  int records;               /* fill the per-step log */
+} perrk_run_cfg;
+
+/* One row of the step log; replaces StepRecord (stepper.hpp:43-52). */
+typedef struct {
+  double t, dt, gamma;
+  int newton_iters;
+  int fell_back;
+  double entropy;
+  double invariants[5];
+} perrk_step_record;
+
+/* ---- errors / version -------------------------------------------------- */
+const char* perrk_last_error(void);
+int perrk_abi_version(void);
+
+/* ---- context: Semidiscretization(spec) (semidisc.cpp:15-73) ------------ */
+int perrk_create(const perrk_semi_desc* desc, perrk_ctx** out);
+int perrk_destroy(perrk_ctx* ctx);
+/* num_dofs/num_nodes/num_cells/num_vars/nodes_per_cell (semidisc.hpp:44-49) */
+int perrk_sizes(const perrk_ctx* ctx, int64_t* dofs, int64_t* nodes, int64_t* cells, int* vars,
+                int* nodes_per_cell);
+/* node_x/node_y/node_measure (semidisc.hpp:56-60); any pointer may be NULL */
+int perrk_node_geometry(const perrk_ctx* ctx, double* x, double* y, double* z, double* measure);
+
+/* ---- partition family + level map (perk_step's family/map arguments) --- */
+/* effective_level: per cell, 1..R (PartitionMap::effective_level,
+ * mesh.hpp:48-54).  Builds the per-stage active cell lists on the device. */
+int perrk_set_family(perrk_ctx* ctx, const perrk_family_desc* fam, const int* effective_level);
+
+/* ---- resident state (the product path keeps U in HBM between steps) --- */
+int perrk_upload_state(perrk_ctx* ctx, const double* U, size_t n);
+int perrk_download_state(perrk_ctx* ctx, double* U, size_t n);
+/* device pointer of the resident state (for zero-copy interop) */
+int perrk_state_device_ptr(perrk_ctx* ctx, double** dptr);
+int perrk_sync(perrk_ctx* ctx);
+
+/* ---- RHS: Semidiscretization::rhs / rhs_masked (semidisc.cpp:121-138) ---
+ * Host buffers.  mask == NULL evaluates every cell.  Cells not flagged in the
+ * mask get a zero RHS, as the reference's zero fill (semidisc.cpp:130). */
+int perrk_rhs_masked(perrk_ctx* ctx, double t, const double* U, double* out, const char* mask);
+/* BR1 auxiliary gradients (semidisc.hpp:75), NSF only: grads[dim][dofs] */
+int perrk_br1_gradients(perrk_ctx* ctx, double t, const double* U, double* grads);
+
+/* ---- reductions (semidisc.cpp:561-607, mesh.cpp:97-129) ----------------
+ * U == NULL reads the resident state.  Sums are compensated (double-double)
+ * and fixed-order, so results are bitwise reproducible run to run. */
+int perrk_total_entropy(perrk_ctx* ctx, const double* U, double* out);
+int perrk_entropy_inner_product(perrk_ctx* ctx, const double* U, const double* K, double* out);
+int perrk_integral_per_variable(perrk_ctx* ctx, const double* U, double* out);
+int perrk_admissible(perrk_ctx* ctx, const double* U, int* ok, int* first_bad_cell);
+int perrk_characteristic_speed(perrk_ctx* ctx, const double* U, double* nu);
+/* compute_dt (stepper.cpp:116-127) with a constant CFL ramp */
+int perrk_compute_dt(perrk_ctx* ctx, const double* U, int fixed, double dt_or_cfl, double t,
+                     double tf, double* dt);
+
+/* ---- time stepping ------------------------------------------------------
+ * perk_step (stepper.cpp:17-114): host U and t updated in place, untouched
+ * on a positivity abort. */
+int perrk_perk_step(perrk_ctx* ctx, double* U, double* t, double dt, const perrk_step_opts* opts,
+                    perrk_step_result* res);
+/* the same on the resident state (no host copies) */
+int perrk_perk_step_resident(perrk_ctx* ctx, double* t, double dt, const perrk_step_opts* opts,
+                             perrk_step_result* res);
+/* run() loop body (stepper.cpp:144-188) for up to nsteps steps on the
+ * resident state, entirely on the device: compute_dt, perk_step with the
+ * gamma-seed carry, StepRecord.  Asynchronous; log (nsteps rows, may be
+ * NULL) and *t / *steps_taken / *aborted are valid after perrk_sync(). */
+int perrk_advance(perrk_ctx* ctx, const perrk_run_cfg* cfg, double* t, int nsteps,
+                  perrk_step_record* log, int* steps_taken, int* aborted);
+
+/* scalar RHS evaluation counter (semidisc.hpp:81-82): n_active*nodes*V per
+ * evaluated stage */
+int perrk_rhs_cell_evaluations(const perrk_ctx* ctx, uint64_t* out);
+int perrk_reset_counter(perrk_ctx* ctx);
+
+/* ---- host-side helpers of the same library (no device work) -------------
+ * build_family (butcher.cpp:237-247): free_flat holds the members' free
+ * subdiagonals back to back in E order.  A: [R][S][S], active: [R][S]. */
+int perrk_family_build(int kind, int S, int R, const int* E, const double* free_flat,
+                       double c_sm3, double* A, double* b, double* c, int* active);
+/* assign_levels (mesh.cpp:73-95) */
+int perrk_assign_levels(const double* nu, int64_t n, int R, int* levels);
+/* make_partition_map (mesh.cpp:56-71) on a periodic rectilinear mesh */
+int perrk_make_partition_map(int dim, const int* ncells, const int* levels, int R, int* effective);
+
+/* ---- multi-GPU: element-slab decomposition over NCCL --------------------
+ * nccl_id: the 128-byte ncclUniqueId from rank 0 (broadcast by the caller,
+ * e.g. through torch.distributed).  After this call the context owns the
+ * slab [slab_begin, slab_end) of the last axis's cell layers; states passed
+ * to upload/download are the rank-local slab. */
+int perrk_comm_init(perrk_ctx* ctx, const void* nccl_id, int rank, int nranks);
+int perrk_slab_range(const perrk_ctx* ctx, int* layer_begin, int* layer_end);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,840 @@
+// sm_100a FP64 kernels of the P-ERRK / EC-DGSEM hot path.
+//
+//   stage_kernel   one P-ERK stage over the stage's active cell list: forms
+//                  the stage state on the fly (stepper.cpp:60-72) for the cell
+//                  and the face traces of its neighbours, then evaluates the
+//                  flux-differencing volume term (semidisc.cpp:446-485) and
+//                  the surface flux + LGL lift (semidisc.cpp:489-556) in one
+//                  pass, and fuses the b-stage epilogue (d += b K, dH += dt b
+//                  <w,K>, stepper.cpp:52-55,89-92) and the admissibility scan
+//                  (semidisc.cpp:596-607).
+//   relax_pass     one Newton iteration of solve_relaxation (relax.cpp:79-104
+//                  or the accurate H1 variant): r and r' at the same gamma in
+//                  one fused pass, the scalar update done by the last block.
+//   update_kernel  U += gamma dt d (stepper.cpp:107-113) fused with the next
+//                  step's CFL speed (mesh.cpp:97-129), the StepRecord H and
+//                  invariants (stepper.cpp:179-180) and the clock advance.
+//   begin_step     compute_dt (stepper.cpp:116-127) and per-step resets.
+#include <cfloat>
+#include <climits>
+#include <cstdio>
+
+#include "dg_device.cuh"
+#include "dg_launch.hpp"
+
+namespace perrk {
+namespace dev {
+
+__constant__ double c_D[N1 * N1];  // SBP derivative matrix, row-major D[l][m]
+__constant__ double c_w[N1];       // LGL weights
+
+constexpr long long kNoBad = LLONG_MAX;
+
+__device__ __forceinline__ void cell_coords(const MeshDev& m, int cell, int& ci, int& cj, int& ck) {
+  ci = cell % m.nc[0];
+  const int r = cell / m.nc[0];
+  cj = r % m.nc[1];
+  ck = r / m.nc[1];
+}
+
+// local node index of the point (t1, t2) of a line/face family of
+// direction dir at position idx along dir
+template <int DIM>
+__device__ __forceinline__ int line_node(int dir, int idx, int t1, int t2) {
+  if (dir == 0) return idx + N1 * (t1 + N1 * t2);
+  if (dir == 1) return t1 + N1 * (idx + N1 * t2);
+  return t1 + N1 * (t2 + N1 * idx);
+}
+
+template <int DIM>
+__device__ __forceinline__ double node_measure(const MeshDev& m, int ci, int cj, int ck, int l) {
+  const int ix = l % N1, iy = (l / N1) % N1, iz = l / (N1 * N1);
+  if (DIM == 2) return 0.25 * m.h[0][ci] * m.h[1][cj] * c_w[ix] * c_w[iy];
+  return 0.125 * m.h[0][ci] * m.h[1][cj] * m.h[2][ck] * c_w[ix] * c_w[iy] * c_w[iz];
+}
+
+__device__ __forceinline__ void report_bad(StepState* st, int stage, long long ncells, long long cell) {
+  atomicMin(&st->bad_code, static_cast<long long>(stage) * ncells + cell);
+}
+
+// ---------------------------------------------------------------------------
+// stage kernel
+// ---------------------------------------------------------------------------
+
+template <int DIM, int SURF>
+__global__ void __launch_bounds__(Geo<DIM>::THREADS)
+    stage_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
+                 unsigned* counter) {
+  using G = Geo<DIM>;
+  constexpr int V = G::V, NPC = G::NPC, FP = G::FP, NF = G::NF, EPB = G::EPB;
+  extern __shared__ double smem[];
+  double* su = smem;            // [EPB][NPC*V]
+  double* pr = su + G::SM_SU;   // [EPB][NPR][NPC]
+  double* nb = pr + G::SM_PR;   // [EPB][NF][FP*V]
+  double* va = nb + G::SM_NB;   // [EPB][DIM][NPC*V]
+  double* sf = va + G::SM_VA;   // [EPB][NF][FP*V]
+  __shared__ int s_cell[EPB];
+  __shared__ int s_coord[EPB][3];
+  __shared__ double s_red[2 * 2 * (G::THREADS / 32)];
+
+  if (st->aborted || st->finished) return;  // uniform across the grid
+
+  const int tid = threadIdx.x;
+  const int e = tid / NPC, l = tid % NPC;
+  const double dt = st->dt;
+  dd acc_dh = dd_zero(), acc_h = dd_zero();
+  double dmax = 0.0;
+  bool dbad = false;
+
+  const int ngroups = (a.n + EPB - 1) / EPB;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int slot = grp * EPB + e;
+    const bool valid = slot < a.n;
+    const int cell = valid ? (a.list ? a.list[slot] : slot) : 0;
+    int ci, cj, ck;
+    cell_coords(m, cell, ci, cj, ck);
+    if (l == 0) {
+      s_cell[e] = valid ? cell : -1;
+      s_coord[e][0] = ci;
+      s_coord[e][1] = cj;
+      s_coord[e][2] = ck;
+    }
+    const size_t base = static_cast<size_t>(cell) * NPC * V;
+
+    // ---- A1: stage state of the cell, coalesced over the cell's DOFs -----
+    double* sue = su + e * NPC * V;
+    if (valid) {
+      const int lev = m.level[cell];
+      const double a1 = a.a1[lev], ap = a.ap[lev];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int f = l + j * NPC;
+        double u = __ldg(a.U + base + f);
+        if (a.form && ap != 0.0)
+          u = u + dt * (a1 * __ldg(a.K1 + base + f) + ap * __ldg(a.Kp + base + f));
+        else if (a.form)
+          u = u + dt * a1 * __ldg(a.K1 + base + f);
+        sue[f] = u;
+      }
+      // ---- A2: neighbour face traces, formed with the neighbour's row ----
+      for (int q = l; q < NF * FP; q += NPC) {
+        const int face = q / FP, pt = q % FP, dir = face >> 1, side = face & 1;
+        const int t1 = pt % N1, t2 = pt / N1;
+        int cc[3] = {ci, cj, ck};
+        const int nd = m.nc[dir];
+        cc[dir] = side ? (cc[dir] + 1 == nd ? 0 : cc[dir] + 1) : (cc[dir] == 0 ? nd - 1 : cc[dir] - 1);
+        const int nbc = cc[0] + m.nc[0] * (cc[1] + m.nc[1] * cc[2]);
+        const int node = line_node<DIM>(dir, side ? 0 : N1 - 1, t1, t2);
+        const size_t nbase = (static_cast<size_t>(nbc) * NPC + node) * V;
+        const int lev2 = m.level[nbc];
+        const double b1 = a.a1[lev2], bp = a.ap[lev2];
+        double un[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          double u = __ldg(a.U + nbase + v);
+          if (a.form && bp != 0.0)
+            u = u + dt * (b1 * __ldg(a.K1 + nbase + v) + bp * __ldg(a.Kp + nbase + v));
+          else if (a.form)
+            u = u + dt * b1 * __ldg(a.K1 + nbase + v);
+          un[v] = u;
+          nb[(e * NF + face) * FP * V + pt * V + v] = u;
+        }
+        if (!admissible<DIM>(ph, un)) report_bad(st, a.stage, a.ncells, nbc);
+      }
+    }
+    __syncthreads();
+
+    // ---- A3: primitives per node ------------------------------------------
+    if (valid) {
+      const double* u = sue + l * V;
+      const double rho = u[0];
+      const double p = pressure<DIM>(ph, u);
+      bool ok = rho > 0.0 && p > 0.0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) ok = ok && isfinite(u[v]);
+      if (!ok) report_bad(st, a.stage, a.ncells, cell);
+      double* pe = pr + e * G::NPR * NPC;
+      pe[P_RHO * NPC + l] = rho;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) pe[(P_VX + d) * NPC + l] = u[1 + d] / rho;
+      pe[P_P * NPC + l] = p;
+      const double beta = rho / p;
+      pe[P_LRHO * NPC + l] = log(rho);
+      pe[P_BETA * NPC + l] = beta;
+      pe[P_LBETA * NPC + l] = log(beta);
+    }
+    __syncthreads();
+
+    // ---- B: volume lines (warps 0..) | surface points (last warps) ----------
+    if (tid < G::LINE_THREADS) {
+      const int e2 = tid / G::LINES, li = tid % G::LINES;
+      if (s_cell[e2] >= 0) {
+        const int dir = li / FP, pt = li % FP;
+        const int t1 = pt % N1, t2 = pt / N1;
+        const double J2 = 2.0 * m.jac[dir][s_coord[e2][dir]];
+        const double* pe = pr + e2 * G::NPR * NPC;
+        const double* ue = su + e2 * NPC * V;
+        int nid[N1];
+#pragma unroll
+        for (int j = 0; j < N1; ++j) nid[j] = line_node<DIM>(dir, j, t1, t2);
+        double acc[N1][V];
+#pragma unroll
+        for (int j = 0; j < N1; ++j)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[j][v] = 0.0;
+#pragma unroll
+        for (int j = 0; j < N1; ++j) {
+          const int nl = nid[j];
+          const double dll = c_D[j * N1 + j];
+          if (dll != 0.0) {  // diagonal: physical flux at the endpoints
+            double f[V];
+            phys_flux<DIM>(ue + nl * V, pe[P_P * NPC + nl], dir, f);
+            const double cll = J2 * dll;
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[j][v] -= cll * f[v];
+          }
+          const double rl = pe[P_RHO * NPC + nl], pl = pe[P_P * NPC + nl];
+          const double lrl = pe[P_LRHO * NPC + nl], bl = pe[P_BETA * NPC + nl];
+          const double lbl = pe[P_LBETA * NPC + nl];
+          double vl[DIM];
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) vl[d] = pe[(P_VX + d) * NPC + nl];
+#pragma unroll
+          for (int k = j + 1; k < N1; ++k) {
+            const int nm = nid[k];
+            const double rr = pe[P_RHO * NPC + nm], prr = pe[P_P * NPC + nm];
+            const double rho_log = logmean_pre(rl, rr, lrl, pe[P_LRHO * NPC + nm]);
+            const double inv_b =
+                inv_logmean_pre(bl, pe[P_BETA * NPC + nm], lbl, pe[P_LBETA * NPC + nm]);
+            double vr[DIM], v_avg[DIM], vl_vr = 0.0;
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) {
+              vr[d] = pe[(P_VX + d) * NPC + nm];
+              v_avg[d] = 0.5 * (vl[d] + vr[d]);
+              vl_vr += vl[d] * vr[d];
+            }
+            double f[V];
+            const double f_rho = rho_log * v_avg[dir];
+            f[0] = f_rho;
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) f[1 + d] = f_rho * v_avg[d];
+            f[1 + dir] += 0.5 * (pl + prr);
+            f[DIM + 1] = f_rho * (0.5 * vl_vr + ph.inv_gm1 * inv_b) +
+                         0.5 * (pl * vr[dir] + prr * vl[dir]);
+            const double clm = J2 * c_D[j * N1 + k];
+            const double cml = J2 * c_D[k * N1 + j];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              acc[j][v] -= clm * f[v];
+              acc[k][v] -= cml * f[v];
+            }
+          }
+        }
+        double* vad = va + (e2 * DIM + dir) * NPC * V;
+#pragma unroll
+        for (int j = 0; j < N1; ++j)
+#pragma unroll
+          for (int v = 0; v < V; ++v) vad[nid[j] * V + v] = acc[j][v];
+      }
+    } else {
+      for (int q = tid - G::LINE_THREADS; q < G::FACE_TASKS; q += G::FACE_THREADS) {
+        const int e2 = q / (NF * FP), r = q % (NF * FP);
+        if (s_cell[e2] < 0) continue;
+        const int face = r / FP, pt = r % FP, dir = face >> 1, side = face & 1;
+        const int t1 = pt % N1, t2 = pt / N1;
+        const int own = line_node<DIM>(dir, side ? N1 - 1 : 0, t1, t2);
+        const double* uo = su + e2 * NPC * V + own * V;
+        const double* un = nb + (e2 * NF + face) * FP * V + pt * V;
+        double fs[V], fo[V];
+        if (side)
+          surface_flux<DIM, SURF>(ph, uo, un, dir, fs);
+        else
+          surface_flux<DIM, SURF>(ph, un, uo, dir, fs);
+        phys_flux<DIM>(uo, pr[(e2 * G::NPR + P_P) * NPC + own], dir, fo);
+        const double coef = m.lift[dir][s_coord[e2][dir]];
+        double* o = sf + (e2 * NF + face) * FP * V + pt * V;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const double c = coef * (fs[v] - fo[v]);
+          o[v] = side ? -c : c;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- C: combine per node, entropy epilogue -------------------------------
+    if (valid) {
+      const int ix = l % N1, iy = (l / N1) % N1, iz = l / (N1 * N1);
+      const int ii[3] = {ix, iy, iz};
+      double K[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        double s = va[(e * DIM + 0) * NPC * V + l * V + v];
+#pragma unroll
+        for (int d = 1; d < DIM; ++d) s += va[(e * DIM + d) * NPC * V + l * V + v];
+        K[v] = s;
+      }
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        if (ii[d] == 0 || ii[d] == N1 - 1) {
+          const int side = ii[d] == N1 - 1;
+          const int t1 = d == 0 ? iy : ix;
+          const int t2 = d == 2 ? iy : iz;
+          const int pt = t1 + N1 * t2;
+          const double* o = sf + (e * NF + 2 * d + side) * FP * V + pt * V;
+#pragma unroll
+          for (int v = 0; v < V; ++v) K[v] += o[v];
+        }
+      }
+      if (a.want_dh || a.want_h) {
+        const double* pe = pr + e * G::NPR * NPC;
+        const double rho = pe[P_RHO * NPC + l];
+        const double beta = pe[P_BETA * NPC + l];
+        // log(p / rho^gamma) = -(log beta + (gamma-1) log rho)
+        const double s_therm = -(pe[P_LBETA * NPC + l] + ph.gm1 * pe[P_LRHO * NPC + l]);
+        const double om = node_measure<DIM>(m, ci, cj, ck, l);
+        if (a.want_dh) {
+          double v2 = 0.0;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            const double vd = pe[(P_VX + d) * NPC + l];
+            v2 += vd * vd;
+          }
+          double dot = (ph.gamma - s_therm - 0.5 * ph.gm1 * beta * v2) * K[0];
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) dot += ph.gm1 * beta * pe[(P_VX + d) * NPC + l] * K[1 + d];
+          dot += -ph.gm1 * beta * K[DIM + 1];
+          acc_dh = dd_add_prod(acc_dh, om, dot);
+        }
+        if (a.want_h) acc_h = dd_add_prod(acc_h, om, -rho * s_therm);
+      }
+      // stash K in this node's x-volume slots (only this thread reads them)
+#pragma unroll
+      for (int v = 0; v < V; ++v) va[(e * DIM) * NPC * V + l * V + v] = K[v];
+    }
+    __syncthreads();
+
+    // ---- D: coalesced stores of K and d -------------------------------------
+    if (valid) {
+      const double* Ke = va + (e * DIM) * NPC * V;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int f = l + j * NPC;
+        const double k = Ke[f];
+        if (a.write_k) a.Kout[base + f] = k;
+        if (a.d_mode) {
+          const double dn = a.d_mode == 1 ? a.b * k : a.d[base + f] + a.b * k;
+          a.d[base + f] = dn;
+          if (a.want_dmax) {
+            if (!isfinite(dn)) dbad = true;
+            dmax = fmax(dmax, fabs(dn));
+          }
+        }
+      }
+    }
+    __syncthreads();  // smem reuse by the next group
+  }
+
+  // ---- grid epilogue ------------------------------------------------------
+  if (a.want_dmax) {
+    dmax = warp_max(dmax);
+    if ((tid & 31) == 0) atomic_max_pos(&st->dmax_bits, dmax);
+    if (dbad) st->d_nonfinite = 1;
+  }
+  dd v[2] = {acc_dh, acc_h}, tot[2];
+  if (a.want_dh || a.want_h) block_reduce_dd<2>(v, s_red);
+  if (grid_reduce_dd<2>(v, partials, counter, s_red, tot) && tid == 0) {
+    if (a.want_dh) {
+      const dd inc = dd_mul_d(tot[0], dt * a.b);
+      const dd cur = {st->dh_hi, st->dh_lo};
+      const dd nw = dd_add(cur, inc);
+      st->dh_hi = nw.hi;
+      st->dh_lo = nw.lo;
+    }
+    if (a.want_h) {
+      st->h_hi = tot[1].hi;
+      st->h_lo = tot[1].lo;
+    }
+    if (st->bad_code != kNoBad) st->aborted = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-step control
+// ---------------------------------------------------------------------------
+
+__global__ void begin_step_kernel(StepState* st) {
+  if (st->aborted || st->finished) return;
+  if (st->run_mode && !(st->t < st->tf - st->t_eps)) {
+    st->finished = 1;
+    return;
+  }
+  double dt;
+  if (st->dt_mode == 0) {
+    dt = st->dt_given;
+  } else if (st->dt_mode == 1) {
+    dt = fmin(st->dt_or_cfl, st->tf - st->t);
+  } else {
+    const double numax = 4.0 * __longlong_as_double(static_cast<long long>(st->numax_bits));
+    if (!(numax > 0.0)) {
+      st->error = 2;  // "vanishing characteristic speed"
+      st->finished = 1;
+      return;
+    }
+    dt = st->dt_or_cfl / numax;
+    st->numax_bits = 0ull;  // re-accumulated by this step's update kernel
+  }
+  st->dt = dt;
+  st->dh_hi = st->dh_lo = 0.0;
+  st->dmax_bits = 0ull;
+  st->d_nonfinite = 0;
+  st->gamma = st->seed_from_previous ? st->gamma_seed : 1.0;
+  st->residual = 0.0;
+  st->pending_step = st->prev_step = 0.0;
+  st->iters = 0;
+  st->pass = 0;
+  st->fell_back = 0;
+  st->relax_done = st->relax_enabled ? 0 : 1;
+}
+
+// ---------------------------------------------------------------------------
+// relaxation: one Newton iteration per launch
+// ---------------------------------------------------------------------------
+
+__device__ void relax_fallback(StepState* st, int iters, double res) {
+  st->gamma = 1.0;
+  st->iters = iters;
+  st->residual = res;
+  st->fell_back = 1;
+  st->relax_done = 1;
+}
+
+// Scalar Newton logic, executed by one thread after the fused reduction of
+// A = sum w Ds (accurate) or sum w s(T) (reference) and B = sum w <w(T), d>.
+__device__ void relax_newton_update(StepState* st, dd A, dd B) {
+  const double dt = st->dt;
+  const dd dh = {st->dh_hi, st->dh_lo};
+  const double gamma = st->gamma;
+  double r, dr;
+  if (st->numerics == 1) {
+    // r = offset + sum w Ds - gamma dH ; r' = dt <w(T),d> - dH
+    dd rr = A;
+    if (!isnan(st->h_ref))  // anchored: + (H(U_n) - h_ref)
+      rr = dd_add(rr, dd_add(dd{st->h_hi, st->h_lo}, dd{-st->h_ref, 0.0}));
+    rr = dd_add(rr, dd_mul_d(dh, -gamma));
+    r = rr.hi + rr.lo;
+    const dd d2 = dd_add(dd_mul_d(B, dt), dd{-dh.hi, -dh.lo});
+    dr = d2.hi + d2.lo;
+    const int it = st->pass + 1;
+    st->iters = it;
+    st->residual = r;
+    if (dr == 0.0 || !isfinite(dr) || !isfinite(r)) return relax_fallback(st, it, r);
+    const double step = r / dr;
+    const double g2 = gamma - step;
+    if (!isfinite(g2) || !(g2 > 0.0)) return relax_fallback(st, it, r);
+    st->gamma = g2;
+    if (fabs(step) <= 1e-13 * g2 ||
+        (it >= 2 && fabs(step) < 1e-10 * g2 && fabs(step) > 0.5 * fabs(st->prev_step)) ||
+        it >= st->max_iter) {
+      st->relax_done = 1;
+      return;
+    }
+    st->prev_step = step;
+    st->pass = it;
+    return;
+  }
+  // reference numerics: relax.cpp:79-104 verbatim on the fused pass values
+  const double H = A.hi + A.lo;
+  const double dhv = dh.hi + dh.lo;
+  const double h_ref = isnan(st->h_ref) ? st->h_hi + st->h_lo : st->h_ref;
+  r = H - h_ref - gamma * dhv;
+  dr = dt * (B.hi + B.lo) - dhv;
+  const int pass = st->pass;
+  if (pass > 0) {
+    if (fabs(r) <= st->residual_tol || fabs(st->pending_step) <= st->step_tol) {
+      st->residual = r;
+      st->iters = pass;
+      st->relax_done = 1;
+      if (!(gamma > 0.0)) relax_fallback(st, pass, r);
+      return;
+    }
+    if (pass >= st->max_iter) return relax_fallback(st, st->max_iter, r);
+  } else if (fabs(r) <= st->residual_tol) {
+    st->residual = r;
+    st->iters = 0;
+    st->relax_done = 1;
+    if (!(gamma > 0.0)) relax_fallback(st, 0, r);
+    return;
+  }
+  const int it = pass + 1;
+  if (dr == 0.0 || !isfinite(dr)) return relax_fallback(st, it, r);
+  const double step = r / dr;
+  const double g2 = gamma - step;
+  if (!isfinite(g2)) return relax_fallback(st, it, r);
+  st->gamma = g2;
+  st->pending_step = step;
+  st->iters = it;
+  st->residual = r;
+  st->pass = it;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256)
+    relax_pass_kernel(const double* __restrict__ U, const double* __restrict__ d, MeshDev m,
+                      Phys ph, StepState* st, double* partials, unsigned* counter, long long nnodes) {
+  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  __shared__ double s_red[2 * 2 * 8];
+  if (st->aborted || st->finished || st->relax_done) return;
+  const double dmax = __longlong_as_double(static_cast<long long>(st->dmax_bits));
+  if (st->d_nonfinite || dmax == 0.0) {
+    // relax.cpp:56-63 — handled once, by block 0
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (st->d_nonfinite) {
+        st->error = 1;
+        st->aborted = 1;  // stop the step; the host reports the error
+      }
+      st->gamma = 1.0;
+      st->iters = 0;
+      st->residual = 0.0;
+      st->relax_done = 1;
+    }
+    return;
+  }
+  const double gamma = st->gamma;
+  const double gdt = gamma * st->dt;
+  dd A = dd_zero(), B = dd_zero();
+  for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < nnodes;
+       n += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
+    int ci, cj, ck;
+    cell_coords(m, cell, ci, cj, ck);
+    const double om = node_measure<DIM>(m, ci, cj, ck, l);
+    double u[V], dv[V], T[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      u[v] = __ldg(U + n * V + v);
+      dv[v] = __ldg(d + n * V + v);
+      T[v] = u[v] + gdt * dv[v];
+    }
+    double a;
+    if (st->numerics == 1) {
+      double du[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) du[v] = gdt * dv[v];
+      a = entropy_difference<DIM>(ph, u, du);
+    } else {
+      a = entropy<DIM>(ph, T);
+    }
+    A = dd_add_prod(A, om, a);
+    B = dd_add_prod(B, om, entropy_dot<DIM>(ph, T, dv));
+  }
+  dd v[2] = {A, B}, tot[2];
+  block_reduce_dd<2>(v, s_red);
+  if (grid_reduce_dd<2>(v, partials, counter, s_red, tot) && threadIdx.x == 0)
+    relax_newton_update(st, tot[0], tot[1]);
+}
+
+// ---------------------------------------------------------------------------
+// final update, CFL speed, step record
+// ---------------------------------------------------------------------------
+
+template <int DIM>
+__global__ void __launch_bounds__(256)
+    update_kernel(double* __restrict__ U, const double* __restrict__ d, MeshDev m, Phys ph,
+                  StepState* st, double* partials, unsigned* counter, long long nnodes,
+                  int want_nu, int want_record, double* records) {
+  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  __shared__ double s_red[2 * 6 * 8];
+  if (st->aborted || st->finished) return;
+  const double gamma = st->relax_enabled ? st->gamma : st->gamma_override;
+  const double scale = gamma * st->dt;
+  double numax = 0.0;
+  dd acc[6];
+#pragma unroll
+  for (int r = 0; r < 6; ++r) acc[r] = dd_zero();
+  for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < nnodes;
+       n += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double u[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      u[v] = U[n * V + v] + scale * __ldg(d + n * V + v);
+      U[n * V + v] = u[v];
+    }
+    if (want_nu || want_record) {
+      const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
+      int ci, cj, ck;
+      cell_coords(m, cell, ci, cj, ck);
+      const int cc[3] = {ci, cj, ck};
+      if (want_nu) {
+        const double p = pressure<DIM>(ph, u);
+#pragma unroll
+        for (int dir = 0; dir < DIM; ++dir)
+          numax = fmax(numax, max_wave_speed<DIM>(ph, u, p, dir) / m.h[dir][cc[dir]]);
+      }
+      if (want_record) {
+        const double om = node_measure<DIM>(m, ci, cj, ck, l);
+        acc[0] = dd_add_prod(acc[0], om, entropy<DIM>(ph, u));
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[1 + v] = dd_add_prod(acc[1 + v], om, u[v]);
+      }
+    }
+  }
+  if (want_nu) {
+    numax = warp_max(numax);
+    if ((threadIdx.x & 31) == 0) atomic_max_pos(&st->numax_bits, numax);
+  }
+  dd tot[6];
+  if (want_record) block_reduce_dd<6>(acc, s_red);
+  if (grid_reduce_dd<6>(acc, partials, counter, s_red, tot) && threadIdx.x == 0) {
+    const double dt = st->dt;
+    if (st->relax_enabled && !st->idt)
+      st->t += gamma * dt;
+    else
+      st->t += dt;
+    if (want_record && records) {
+      double* row = records + static_cast<size_t>(st->steps_taken) * 11;
+      row[0] = st->t;
+      row[1] = dt;
+      row[2] = gamma;
+      row[3] = st->iters;
+      row[4] = st->fell_back;
+      row[5] = tot[0].hi + tot[0].lo;
+      for (int v = 0; v < V; ++v) row[6 + v] = tot[1 + v].hi + tot[1 + v].lo;
+    }
+    st->gamma_seed = st->fell_back ? 1.0 : gamma;
+    st->steps_taken += 1;
+  }
+}
+
+// max over nodes of lambda_dir / h_dir (the max of characteristic_speed,
+// mesh.cpp:97-129, divided by k+1) into st->numax_bits
+template <int DIM>
+__global__ void __launch_bounds__(256)
+    numax_kernel(const double* __restrict__ U, MeshDev m, Phys ph, StepState* st,
+                 long long nnodes) {
+  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  double best = 0.0;
+  for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < nnodes;
+       n += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double u[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) u[v] = __ldg(U + n * V + v);
+    int ci, cj, ck;
+    cell_coords(m, static_cast<int>(n / NPC), ci, cj, ck);
+    const int cc[3] = {ci, cj, ck};
+    const double p = pressure<DIM>(ph, u);
+#pragma unroll
+    for (int dir = 0; dir < DIM; ++dir)
+      best = fmax(best, max_wave_speed<DIM>(ph, u, p, dir) / m.h[dir][cc[dir]]);
+  }
+  best = warp_max(best);
+  if ((threadIdx.x & 31) == 0) atomic_max_pos(&st->numax_bits, best);
+}
+
+// per-cell nu = (k+1) max_dir(max_nodes lambda_dir / h_dir), mesh.cpp:97-129
+template <int DIM>
+__global__ void nu_cell_kernel(const double* __restrict__ U, MeshDev m, Phys ph, double* nu,
+                               long long ncells) {
+  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < ncells;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double r[3] = {0.0, 0.0, 0.0};
+    for (int l = 0; l < NPC; ++l) {
+      double u[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) u[v] = U[(c * NPC + l) * V + v];
+      const double p = pressure<DIM>(ph, u);
+#pragma unroll
+      for (int dir = 0; dir < DIM; ++dir) r[dir] = fmax(r[dir], max_wave_speed<DIM>(ph, u, p, dir));
+    }
+    int ci, cj, ck;
+    cell_coords(m, static_cast<int>(c), ci, cj, ck);
+    const int cc[3] = {ci, cj, ck};
+    double best = r[0] / m.h[0][cc[0]];
+#pragma unroll
+    for (int dir = 1; dir < DIM; ++dir) best = fmax(best, r[dir] / m.h[dir][cc[dir]]);
+    nu[c] = 4.0 * best;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// reductions behind the reference's Semidiscretization queries
+// ---------------------------------------------------------------------------
+
+// mode 0: H = sum w s(U); 1: sum w <w(U), K>; 2: sum w U_v (V values)
+template <int DIM>
+__global__ void __launch_bounds__(256)
+    quad_kernel(const double* __restrict__ U, const double* __restrict__ K, MeshDev m, Phys ph,
+                int mode, double* partials, unsigned* counter, double* out, long long nnodes) {
+  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  __shared__ double s_red[2 * 5 * 8];
+  dd acc[5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r) acc[r] = dd_zero();
+  for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < nnodes;
+       n += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
+    int ci, cj, ck;
+    cell_coords(m, cell, ci, cj, ck);
+    const double om = node_measure<DIM>(m, ci, cj, ck, l);
+    double u[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) u[v] = __ldg(U + n * V + v);
+    if (mode == 0) {
+      acc[0] = dd_add_prod(acc[0], om, entropy<DIM>(ph, u));
+    } else if (mode == 1) {
+      double k[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) k[v] = __ldg(K + n * V + v);
+      acc[0] = dd_add_prod(acc[0], om, entropy_dot<DIM>(ph, u, k));
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] = dd_add_prod(acc[v], om, u[v]);
+    }
+  }
+  dd tot[5];
+  block_reduce_dd<5>(acc, s_red);
+  if (grid_reduce_dd<5>(acc, partials, counter, s_red, tot) && threadIdx.x == 0)
+    for (int r = 0; r < 5; ++r) out[r] = tot[r].hi + tot[r].lo;
+}
+
+template <int DIM>
+__global__ void admissible_kernel(const double* __restrict__ U, Phys ph, int* first_bad,
+                                  long long nnodes) {
+  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < nnodes;
+       n += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double u[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) u[v] = U[n * V + v];
+    if (!admissible<DIM>(ph, u)) atomicMin(first_bad, static_cast<int>(n / NPC));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+template <int DIM, int SURF>
+static cudaError_t launch_stage_t(const StageArgs& a, const MeshDev& m, const Phys& ph,
+                                  StepState* st, double* partials, unsigned* counter, int grid,
+                                  cudaStream_t s) {
+  using G = Geo<DIM>;
+  const size_t shm = sizeof(double) * G::SM_TOTAL;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(stage_kernel<DIM, SURF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(shm));
+    configured = true;
+  }
+  const int groups = (a.n + G::EPB - 1) / G::EPB;
+  const int g = groups < grid ? groups : grid;
+  if (g <= 0) return cudaSuccess;
+  stage_kernel<DIM, SURF><<<g, G::THREADS, shm, s>>>(a, m, ph, st, partials, counter);
+  return cudaGetLastError();
+}
+
+template <int DIM>
+static cudaError_t launch_stage_d(int surf, const StageArgs& a, const MeshDev& m, const Phys& ph,
+                                  StepState* st, double* partials, unsigned* counter, int grid,
+                                  cudaStream_t s) {
+  switch (surf) {
+    case 0: return launch_stage_t<DIM, 0>(a, m, ph, st, partials, counter, grid, s);
+    case 2: return launch_stage_t<DIM, 2>(a, m, ph, st, partials, counter, grid, s);
+    case 3: return launch_stage_t<DIM, 3>(a, m, ph, st, partials, counter, grid, s);
+    case 4: return launch_stage_t<DIM, 4>(a, m, ph, st, partials, counter, grid, s);
+    case 5: return launch_stage_t<DIM, 5>(a, m, ph, st, partials, counter, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dev
+
+using namespace dev;
+
+cudaError_t upload_basis(const double* D, const double* w) {
+  cudaError_t e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * N1 * N1);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(c_w, w, sizeof(double) * N1);
+}
+
+size_t stage_smem_bytes(int dim) {
+  return dim == 2 ? sizeof(double) * Geo<2>::SM_TOTAL : sizeof(double) * Geo<3>::SM_TOTAL;
+}
+
+int stage_cells_per_block(int dim) { return dim == 2 ? Geo<2>::EPB : Geo<3>::EPB; }
+
+cudaError_t launch_stage(int dim, int surf, const StageArgs& a, const MeshDev& m, const Phys& ph,
+                         StepState* st, double* partials, unsigned* counter, int grid,
+                         cudaStream_t s) {
+  return dim == 2 ? launch_stage_d<2>(surf, a, m, ph, st, partials, counter, grid, s)
+                  : launch_stage_d<3>(surf, a, m, ph, st, partials, counter, grid, s);
+}
+
+cudaError_t launch_begin_step(StepState* st, cudaStream_t s) {
+  begin_step_kernel<<<1, 1, 0, s>>>(st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relax_pass(int dim, const double* U, const double* d, const MeshDev& m,
+                              const Phys& ph, StepState* st, double* partials, unsigned* counter,
+                              long long nnodes, int grid, cudaStream_t s) {
+  if (dim == 2)
+    relax_pass_kernel<2><<<grid, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
+  else
+    relax_pass_kernel<3><<<grid, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(int dim, double* U, const double* d, const MeshDev& m, const Phys& ph,
+                          StepState* st, double* partials, unsigned* counter, long long nnodes,
+                          int want_nu, int want_record, double* records, int grid,
+                          cudaStream_t s) {
+  if (dim == 2)
+    update_kernel<2><<<grid, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes, want_nu,
+                                          want_record, records);
+  else
+    update_kernel<3><<<grid, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes, want_nu,
+                                          want_record, records);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_numax(int dim, const double* U, const MeshDev& m, const Phys& ph,
+                         StepState* st, long long nnodes, int grid, cudaStream_t s) {
+  if (dim == 2)
+    numax_kernel<2><<<grid, 256, 0, s>>>(U, m, ph, st, nnodes);
+  else
+    numax_kernel<3><<<grid, 256, 0, s>>>(U, m, ph, st, nnodes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nu_cell(int dim, const double* U, const MeshDev& m, const Phys& ph, double* nu,
+                           long long ncells, cudaStream_t s) {
+  const int grid = static_cast<int>((ncells + 255) / 256);
+  if (dim == 2)
+    nu_cell_kernel<2><<<grid, 256, 0, s>>>(U, m, ph, nu, ncells);
+  else
+    nu_cell_kernel<3><<<grid, 256, 0, s>>>(U, m, ph, nu, ncells);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quad(int dim, const double* U, const double* K, const MeshDev& m,
+                        const Phys& ph, int mode, double* partials, unsigned* counter, double* out,
+                        long long nnodes, int grid, cudaStream_t s) {
+  if (dim == 2)
+    quad_kernel<2><<<grid, 256, 0, s>>>(U, K, m, ph, mode, partials, counter, out, nnodes);
+  else
+    quad_kernel<3><<<grid, 256, 0, s>>>(U, K, m, ph, mode, partials, counter, out, nnodes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_admissible(int dim, const double* U, const Phys& ph, int* first_bad,
+                              long long nnodes, int grid, cudaStream_t s) {
+  if (dim == 2)
+    admissible_kernel<2><<<grid, 256, 0, s>>>(U, ph, first_bad, nnodes);
+  else
+    admissible_kernel<3><<<grid, 256, 0, s>>>(U, ph, first_bad, nnodes);
+  return cudaGetLastError();
+}
+
+}  // namespace perrk

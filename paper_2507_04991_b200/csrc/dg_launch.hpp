@@ -1,0 +1,57 @@
+// Host-visible launch interface of the device kernels (dg_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "dg_device.cuh"
+
+namespace perrk {
+
+// Arguments of one stage launch (one P-ERK stage i over its active cells).
+struct StageArgs {
+  const double* U;       // U_n
+  const double* K1;      // K_1 (stage 0 RHS)
+  const double* Kp;      // K_{i-1}
+  double* Kout;          // K_i (written when write_k)
+  double* d;             // update direction
+  const int* list;       // active cells of the stage (nullptr: all cells 0..n-1)
+  int n;                 // number of cells processed
+  double a1[dev::MAXR + 1];  // a_{i,1} by effective level
+  double ap[dev::MAXR + 1];  // a_{i,i-1} by effective level
+  int form;              // 0: stage state = U_n; 1: U_n + dt (a1 K1 [+ ap K_{i-1}])
+  int write_k;
+  int d_mode;            // 0 none, 1 d = b K, 2 d += b K
+  double b;
+  int want_dh;           // dH += dt b <w(U_i), K_i>
+  int want_h;            // H(U_n) (stage 0)
+  int want_dmax;         // max |d| (last b-stage)
+  int stage;
+  long long ncells;
+};
+
+cudaError_t upload_basis(const double* D, const double* w);
+size_t stage_smem_bytes(int dim);
+int stage_cells_per_block(int dim);
+
+cudaError_t launch_stage(int dim, int surf, const StageArgs& a, const dev::MeshDev& m,
+                         const dev::Phys& ph, dev::StepState* st, double* partials,
+                         unsigned* counter, int grid, cudaStream_t s);
+cudaError_t launch_begin_step(dev::StepState* st, cudaStream_t s);
+cudaError_t launch_relax_pass(int dim, const double* U, const double* d, const dev::MeshDev& m,
+                              const dev::Phys& ph, dev::StepState* st, double* partials,
+                              unsigned* counter, long long nnodes, int grid, cudaStream_t s);
+cudaError_t launch_update(int dim, double* U, const double* d, const dev::MeshDev& m,
+                          const dev::Phys& ph, dev::StepState* st, double* partials,
+                          unsigned* counter, long long nnodes, int want_nu, int want_record,
+                          double* records, int grid, cudaStream_t s);
+cudaError_t launch_numax(int dim, const double* U, const dev::MeshDev& m, const dev::Phys& ph,
+                         dev::StepState* st, long long nnodes, int grid, cudaStream_t s);
+cudaError_t launch_nu_cell(int dim, const double* U, const dev::MeshDev& m, const dev::Phys& ph,
+                           double* nu, long long ncells, cudaStream_t s);
+cudaError_t launch_quad(int dim, const double* U, const double* K, const dev::MeshDev& m,
+                        const dev::Phys& ph, int mode, double* partials, unsigned* counter,
+                        double* out, long long nnodes, int grid, cudaStream_t s);
+cudaError_t launch_admissible(int dim, const double* U, const dev::Phys& ph, int* first_bad,
+                              long long nnodes, int grid, cudaStream_t s);
+
+}  // namespace perrk

@@ -1,0 +1,1044 @@
+// Host layer of perrk_b200: the reference's Semidiscretization / perk_step /
+// run API (proj/core/include/perrk/{semidisc,stepper,relax}.hpp) re-expressed
+// over device-resident state, plus the host-side inputs of the hot path
+// (GLL basis, P-ERK family builders, level assignment, partition map).  The
+// exported entry points are the C-ABI declared in include/perrk_b200.h.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/perrk_b200.h"
+#include "dg_launch.hpp"
+
+namespace perrk {
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail : std::runtime_error {
+  int code;
+  Fail(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define REQUIRE(cond, msg)                       \
+  do {                                           \
+    if (!(cond)) throw Fail(PERRK_EINVAL, (msg)); \
+  } while (0)
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Fail(PERRK_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PERRK_OK;
+  } catch (const Fail& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PERRK_EINVAL;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GLL basis: nodes are the endpoints and the roots of P_k' (found by Newton
+// from Chebyshev-Lobatto guesses); w_i = 2 / (k(k+1) P_k(x_i)^2);
+// D_ij = P_k(x_i) / (P_k(x_j)(x_i - x_j)), D_00 = -k(k+1)/4, D_kk = k(k+1)/4.
+// Same construction as the reference's gll_basis (basis.cpp:35-84).
+// ---------------------------------------------------------------------------
+struct Basis {
+  int k;
+  std::vector<double> x, w, D;
+};
+
+void legendre_pair(int k, double x, double& p, double& dp) {
+  double a = 1.0, b = x;  // P_{n-1}, P_n
+  if (k == 0) {
+    p = 1.0;
+    dp = 0.0;
+    return;
+  }
+  for (int n = 1; n < k; ++n) {
+    const double c = ((2.0 * n + 1.0) * x * b - n * a) / (n + 1.0);
+    a = b;
+    b = c;
+  }
+  p = b;
+  dp = k * (a - x * b) / (1.0 - x * x);
+}
+
+Basis make_basis(int k) {
+  Basis B;
+  B.k = k;
+  const int n = k + 1;
+  B.x.assign(n, 0.0);
+  B.x[0] = -1.0;
+  B.x[k] = 1.0;
+  for (int i = 1; i < k; ++i) {
+    double x = -std::cos(M_PI * i / k);
+    for (int it = 0; it < 100; ++it) {
+      double p, dp;
+      legendre_pair(k, x, p, dp);
+      const double step = dp / ((2.0 * x * dp - k * (k + 1.0) * p) / (1.0 - x * x));
+      x -= step;
+      if (std::fabs(step) < 1e-15) break;
+    }
+    B.x[i] = x;
+  }
+  for (int i = 0; i < n / 2; ++i) {  // exact antisymmetry
+    const double v = 0.5 * (B.x[n - 1 - i] - B.x[i]);
+    B.x[i] = -v;
+    B.x[n - 1 - i] = v;
+  }
+  if (n % 2) B.x[n / 2] = 0.0;
+  std::vector<double> pk(n);
+  B.w.resize(n);
+  for (int i = 0; i < n; ++i) {
+    double p, dp;
+    if (std::fabs(B.x[i]) == 1.0)
+      p = (B.x[i] > 0 || k % 2 == 0) ? 1.0 : -1.0;
+    else
+      legendre_pair(k, B.x[i], p, dp);
+    pk[i] = p;
+    B.w[i] = 2.0 / (k * (k + 1.0) * p * p);
+  }
+  B.D.assign(n * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      if (i != j) B.D[i * n + j] = pk[i] / (pk[j] * (B.x[i] - B.x[j]));
+  B.D[0] = -k * (k + 1.0) / 4.0;
+  B.D[n * n - 1] = k * (k + 1.0) / 4.0;
+  return B;
+}
+
+// ---------------------------------------------------------------------------
+// P-ERK family builders (butcher.cpp:24-247): shared b and c, first column
+// a_{i,1} = c_i, chain rows S-E+2..S-1 (0-based) carry a_{i,i-1}.
+// ---------------------------------------------------------------------------
+constexpr double kP4cSm2 = 0.479274057836310;
+constexpr double kP4aSm2 = 0.114851811257441;  // divided by c_{S-3}
+constexpr double kP4aSm1 = 0.648906880894214;
+constexpr double kP4aS = 0.0283121635129678;
+
+int free_count(int kind, int E) {
+  switch (kind) {
+    case PERRK_FAMILY_P2: return E - 2;
+    case PERRK_FAMILY_P3_VARIANT:
+    case PERRK_FAMILY_P3_ORIGINAL: return E - 3;
+    case PERRK_FAMILY_P4: return E - 5;
+  }
+  throw Fail(PERRK_EINVAL, "unknown family kind");
+}
+
+std::vector<double> weights_b(int kind, int S) {
+  std::vector<double> b(S, 0.0);
+  if (kind == PERRK_FAMILY_P2) {
+    b[S - 1] = 1.0;
+  } else if (kind == PERRK_FAMILY_P3_VARIANT) {
+    b[0] = 1.0 / 6.0;
+    b[S - 2] = 1.0 / 6.0;
+    b[S - 1] = 2.0 / 3.0;
+  } else if (kind == PERRK_FAMILY_P3_ORIGINAL) {
+    b[S - 2] = 3.0 / 4.0;
+    b[S - 1] = 1.0 / 4.0;
+  } else {
+    b[S - 2] = 0.5;
+    b[S - 1] = 0.5;
+  }
+  return b;
+}
+
+std::vector<double> abscissae(int kind, int S, double c_sm3) {
+  std::vector<double> c(S, 0.0);
+  if (kind == PERRK_FAMILY_P2) {
+    for (int i = 1; i < S; ++i) c[i] = static_cast<double>(i) / (2.0 * (S - 1));
+  } else if (kind == PERRK_FAMILY_P3_VARIANT || kind == PERRK_FAMILY_P3_ORIGINAL) {
+    for (int i = 1; i <= S - 3; ++i) c[i] = static_cast<double>(i) / (S - 3);
+    c[S - 2] = kind == PERRK_FAMILY_P3_VARIANT ? 1.0 : 1.0 / 3.0;
+    c[S - 1] = kind == PERRK_FAMILY_P3_VARIANT ? 0.5 : 1.0;
+  } else {
+    const double r = std::sqrt(3.0) / 6.0;
+    for (int i = 1; i <= S - 5; ++i) c[i] = 1.0;
+    if (S >= 5) c[S - 4] = c_sm3;
+    c[S - 3] = kP4cSm2;
+    c[S - 2] = 0.5 + r;
+    c[S - 1] = 0.5 - r;
+  }
+  return c;
+}
+
+std::vector<char> reachable_stages(int S, const double* A, const std::vector<double>& b) {
+  std::vector<char> act(S, 0);
+  act[0] = 1;
+  for (int i = 0; i < S; ++i)
+    if (b[i] != 0.0) act[i] = 1;
+  // a stage feeds stage i through any nonzero A[i][j]: sweep from the back
+  for (bool grew = true; grew;) {
+    grew = false;
+    for (int i = S - 1; i >= 0; --i)
+      if (act[i])
+        for (int j = 0; j < i; ++j)
+          if (A[i * S + j] != 0.0 && !act[j]) act[j] = 1, grew = true;
+  }
+  return act;
+}
+
+void build_member(int kind, int S, int E, const double* fr, const std::vector<double>& b,
+                  const std::vector<double>& c, double* A) {
+  const int minE = kind == PERRK_FAMILY_P4 ? 5 : 3;
+  REQUIRE(E >= minE && E <= S, "member evaluation count out of range for archetype");
+  std::fill(A, A + S * S, 0.0);
+  for (int i = 1; i < S; ++i) A[i * S] = c[i];
+  auto chain = [&](int i, double a) {
+    A[i * S + i - 1] = a;
+    A[i * S] = c[i] - a;
+  };
+  const int derived = kind == PERRK_FAMILY_P4 ? 3 : (kind == PERRK_FAMILY_P2 ? 0 : 1);
+  int next = 0;
+  for (int i = S - E + 2; i < S - derived; ++i) chain(i, fr[next++]);
+  if (kind == PERRK_FAMILY_P3_VARIANT || kind == PERRK_FAMILY_P3_ORIGINAL) {
+    double acs = 0.0;  // (A c)_{S-2}: pins a_{S,S-1} through b^T A c = 1/6
+    for (int j = 0; j < S - 2; ++j) acs += A[(S - 2) * S + j] * c[j];
+    const double a_last = (1.0 / 6.0 - b[S - 2] * acs) / (b[S - 1] * c[S - 2]);
+    REQUIRE(std::isfinite(a_last), "no solution for the p3 coupling coefficient");
+    chain(S - 1, a_last);
+  } else if (kind == PERRK_FAMILY_P4) {
+    REQUIRE(c[S - 4] != 0.0, "c_{S-3} = 0: division by zero in the p4 base coefficients");
+    chain(S - 3, kP4aSm2 / c[S - 4]);
+    chain(S - 2, kP4aSm1);
+    chain(S - 1, kP4aS);
+  }
+  const double tol = -1e-14;
+  if (kind == PERRK_FAMILY_P2) {
+    for (int i = 1; i < S; ++i)
+      REQUIRE(A[i * S] >= tol, "free coefficient produces negative first-column entry");
+  } else if (kind != PERRK_FAMILY_P3_ORIGINAL) {
+    for (int i = 0; i < S; ++i)
+      for (int j = 0; j < i; ++j)
+        REQUIRE(A[i * S + j] >= tol, "no nonnegative solution for the coupling coefficients");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct StagePlan {
+  int* dlist = nullptr;  // nullptr: all cells
+  int n = 0;
+  StageArgs args{};
+  int kin = -1, kout = -1;  // buffer ids: 0 K1, 1 Ka, 2 Kb
+};
+
+}  // namespace
+}  // namespace perrk
+
+using namespace perrk;
+using perrk::dev::StepState;
+
+struct perrk_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int dim = 2, V = 4, npc = 16, k = 3;
+  int nc[3] = {1, 1, 1};
+  long long ncells = 0, nnodes = 0, ndofs = 0;
+  std::vector<double> edges[3], h[3];
+  Basis basis;
+  dev::Phys ph{};
+  int physics = 0, surface = 2, volume_mode = 1, volume_flux = 5;
+  double mu = 0.0, prandtl = 1.0;
+  // device buffers
+  double *U = nullptr, *K1 = nullptr, *Ka = nullptr, *Kb = nullptr, *d = nullptr;
+  double *tU = nullptr, *tK = nullptr;  // scratch for host-buffer queries
+  double *dh[3] = {}, *djac[3] = {}, *dlift[3] = {};
+  int8_t* dlevel = nullptr;
+  StepState* st = nullptr;
+  double* partials = nullptr;
+  unsigned* counter = nullptr;
+  double* dout = nullptr;
+  int* dint = nullptr;
+  int* dlist_tmp = nullptr;
+  double* records = nullptr;
+  int records_cap = 0;
+  double* dnu = nullptr;
+  int grid_stage = 1184, grid_flat = 1184;
+  // family
+  bool has_family = false;
+  int S = 0, R = 0;
+  std::vector<double> A, b, c;
+  std::vector<int> E, eff;
+  std::vector<StagePlan> plan;
+  uint64_t evals = 0;
+
+  dev::MeshDev mesh() const {
+    dev::MeshDev m{};
+    for (int a = 0; a < 3; ++a) {
+      m.nc[a] = nc[a];
+      m.h[a] = dh[a];
+      m.jac[a] = djac[a];
+      m.lift[a] = dlift[a];
+    }
+    m.dim = dim;
+    m.level = dlevel;
+    return m;
+  }
+  double* kbuf(int id) { return id == 0 ? K1 : (id == 1 ? Ka : Kb); }
+};
+
+namespace perrk {
+namespace {
+
+void set_device(perrk_ctx* c) { CK(cudaSetDevice(c->device)); }
+
+StepState fresh_state() {
+  StepState s{};
+  s.bad_code = std::numeric_limits<long long>::max();
+  s.h_ref = std::numeric_limits<double>::quiet_NaN();
+  s.gamma = s.gamma_seed = s.gamma_override = 1.0;
+  s.relax_done = 1;
+  return s;
+}
+
+void put_state(perrk_ctx* c, const StepState& s) {
+  CK(cudaMemcpyAsync(c->st, &s, sizeof s, cudaMemcpyHostToDevice, c->stream));
+}
+
+StepState get_state(perrk_ctx* c) {
+  StepState s;
+  CK(cudaMemcpyAsync(&s, c->st, sizeof s, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return s;
+}
+
+void upload(perrk_ctx* c, double* dst, const double* src) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * c->ndofs, cudaMemcpyHostToDevice, c->stream));
+}
+
+void download(perrk_ctx* c, double* dst, const double* src) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * c->ndofs, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+// Build per-stage launch plans from the family and the effective levels.
+void build_plan(perrk_ctx* c) {
+  for (auto& p : c->plan)
+    if (p.dlist) cudaFree(p.dlist);
+  c->plan.clear();
+  const int S = c->S, R = c->R;
+  std::vector<std::vector<char>> active(R);  // by level-1
+  for (int lvl = 1; lvl <= R; ++lvl)
+    active[lvl - 1] = reachable_stages(S, &c->A[static_cast<size_t>(R - lvl) * S * S], c->b);
+  int first_b = -1, last_b = -1;
+  for (int i = 0; i < S; ++i)
+    if (c->b[i] != 0.0) {
+      if (first_b < 0) first_b = i;
+      last_b = i;
+    }
+  REQUIRE(first_b >= 0, "family has no nonzero weight");
+  for (int i = 0; i < S; ++i) {
+    StagePlan p;
+    StageArgs& a = p.args;
+    std::vector<int> list;
+    bool all = true;
+    for (long long cell = 0; cell < c->ncells; ++cell) {
+      const bool on = i == 0 || active[c->eff[cell] - 1][i];
+      if (on)
+        list.push_back(static_cast<int>(cell));
+      else
+        all = false;
+    }
+    p.n = static_cast<int>(list.size());
+    if (!all && p.n > 0) {
+      CK(cudaMalloc(&p.dlist, sizeof(int) * list.size()));
+      CK(cudaMemcpy(p.dlist, list.data(), sizeof(int) * list.size(), cudaMemcpyHostToDevice));
+    }
+    for (int lvl = 0; lvl <= dev::MAXR; ++lvl) a.a1[lvl] = a.ap[lvl] = 0.0;
+    for (int lvl = 1; lvl <= R; ++lvl) {
+      const double* Am = &c->A[static_cast<size_t>(R - lvl) * S * S];
+      a.a1[lvl] = i > 0 ? Am[i * S] : 0.0;
+      a.ap[lvl] = i >= 2 ? Am[i * S + i - 1] : 0.0;
+    }
+    a.form = i > 0 ? 1 : 0;
+    bool needed_next = false;
+    if (i + 1 < S)
+      for (int r = 0; r < R; ++r)
+        if (c->A[static_cast<size_t>(r) * S * S + (i + 1) * S + i] != 0.0) needed_next = true;
+    a.write_k = (i == 0) || needed_next;
+    p.kout = i == 0 ? 0 : (i % 2 == 1 ? 1 : 2);
+    p.kin = i >= 2 ? (i % 2 == 1 ? 2 : 1) : -1;
+    a.b = c->b[i];
+    a.d_mode = c->b[i] != 0.0 ? (i == first_b ? 1 : 2) : 0;
+    a.want_dh = c->b[i] != 0.0;
+    a.want_dmax = i == last_b;
+    a.want_h = 0;
+    a.stage = i;
+    a.ncells = c->ncells;
+    a.list = p.dlist;
+    a.n = p.n;
+    c->plan.push_back(p);
+  }
+}
+
+struct StepMode {
+  bool relax = false;
+  perrk_relax_cfg cfg{};
+  bool want_nu = false;
+  bool want_record = false;
+  double* records = nullptr;
+};
+
+// Enqueue one perk_step (stepper.cpp:17-114) on the resident state.
+void enqueue_step(perrk_ctx* c, const StepMode& mode, bool want_h) {
+  const dev::MeshDev m = c->mesh();
+  CK(launch_begin_step(c->st, c->stream));
+  for (int i = 0; i < c->S; ++i) {
+    StagePlan& p = c->plan[i];
+    StageArgs a = p.args;
+    a.U = c->U;
+    a.K1 = c->K1;
+    a.Kp = p.kin >= 0 ? c->kbuf(p.kin) : c->K1;
+    a.Kout = c->kbuf(p.kout);
+    a.d = c->d;
+    a.want_h = (i == 0 && want_h) ? 1 : 0;
+    CK(launch_stage(c->dim, c->surface, a, m, c->ph, c->st, c->partials, c->counter,
+                    c->grid_stage, c->stream));
+  }
+  if (mode.relax) {
+    const int passes = mode.cfg.numerics == 1 ? mode.cfg.max_iter : mode.cfg.max_iter + 1;
+    for (int p = 0; p < passes; ++p)
+      CK(launch_relax_pass(c->dim, c->U, c->d, m, c->ph, c->st, c->partials, c->counter,
+                           c->nnodes, c->grid_flat, c->stream));
+  }
+  CK(launch_update(c->dim, c->U, c->d, m, c->ph, c->st, c->partials, c->counter, c->nnodes,
+                   mode.want_nu ? 1 : 0, mode.want_record ? 1 : 0, mode.records, c->grid_flat,
+                   c->stream));
+}
+
+void check_relax_cfg(const perrk_relax_cfg& r) {
+  if (r.method != 0)
+    throw Fail(PERRK_EUNSUP, "only Newton relaxation (method 0) runs on the device");
+  REQUIRE(r.max_iter >= 1, "relaxation max_iter must be >= 1");
+  REQUIRE(r.numerics == 0 || r.numerics == 1, "relaxation numerics must be 0 or 1");
+}
+
+void configure_relax(StepState& s, bool enabled, const perrk_relax_cfg& r) {
+  s.relax_enabled = enabled ? 1 : 0;
+  if (!enabled) return;
+  s.numerics = r.numerics;
+  s.max_iter = r.max_iter;
+  s.seed_from_previous = r.seed_from_previous;
+  s.residual_tol = r.residual_tol;
+  s.step_tol = r.step_tol;
+}
+
+bool needs_h(bool relax, const perrk_relax_cfg& r, double h_ref) {
+  if (!relax) return false;
+  return r.numerics == 0 ? std::isnan(h_ref) : !std::isnan(h_ref);
+}
+
+uint64_t evals_per_step(const perrk_ctx* c) {
+  uint64_t n = 0;
+  for (const auto& p : c->plan) n += static_cast<uint64_t>(p.n) * c->npc * c->V;
+  return n;
+}
+
+void fill_result(const perrk_ctx* c, const StepState& s, bool relax, double gamma_override,
+                 perrk_step_result* r) {
+  r->gamma = relax ? s.gamma : gamma_override;
+  r->iterations = relax ? s.iters : 0;
+  r->residual = relax ? s.residual : 0.0;
+  r->fell_back = relax ? s.fell_back : 0;
+  r->delta_h = s.dh_hi + s.dh_lo;
+  r->aborted = s.aborted;
+  if (s.aborted && s.bad_code != std::numeric_limits<long long>::max()) {
+    r->bad_stage = static_cast<int>(s.bad_code / c->ncells);
+    r->bad_cell = static_cast<int>(s.bad_code % c->ncells);
+  } else {
+    r->bad_stage = r->bad_cell = -1;
+  }
+}
+
+const double* stage_input(perrk_ctx* c, const double* U) {
+  if (!U) return c->U;
+  upload(c, c->tU, U);
+  return c->tU;
+}
+
+double quad(perrk_ctx* c, const double* dU, const double* dK, int mode, double* outv) {
+  CK(launch_quad(c->dim, dU, dK, c->mesh(), c->ph, mode, c->partials, c->counter, c->dout,
+                 c->nnodes, c->grid_flat, c->stream));
+  double host[5];
+  CK(cudaMemcpyAsync(host, c->dout, sizeof host, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (outv) std::memcpy(outv, host, sizeof(double) * c->V);
+  return host[0];
+}
+
+}  // namespace
+}  // namespace perrk
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* perrk_last_error(void) { return g_last_error.c_str(); }
+int perrk_abi_version(void) { return PERRK_B200_ABI_VERSION; }
+
+int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
+  perrk_ctx* c = nullptr;
+  const int rc = guarded([&] {
+    REQUIRE(dsc && out, "null argument");
+    REQUIRE(dsc->dim == 2 || dsc->dim == 3, "dim must be 2 or 3");
+    if (dsc->polydeg != 3) throw Fail(PERRK_EUNSUP, "the device path is built for polydeg 3");
+    if (dsc->physics != 0) throw Fail(PERRK_EUNSUP, "Navier-Stokes/BR1 not built yet");
+    if (dsc->volume_mode != 1) throw Fail(PERRK_EUNSUP, "weak-form volume integral not on the device path");
+    if (dsc->volume_flux != PERRK_FLUX_EC)
+      throw Fail(PERRK_EUNSUP, "device flux differencing uses the Ranocha EC volume flux");
+    const int sf = dsc->surface_flux;
+    if (sf == PERRK_FLUX_UPWIND) throw Fail(PERRK_EINVAL, "upwind flux only available for advection");
+    REQUIRE(sf >= 0 && sf <= 5, "unknown surface flux");
+    REQUIRE(dsc->gamma > 1.0, "gamma must exceed 1");
+    c = new perrk_ctx;
+    c->device = dsc->device;
+    c->dim = dsc->dim;
+    c->V = dsc->dim + 2;
+    c->npc = dsc->dim == 2 ? 16 : 64;
+    c->physics = dsc->physics;
+    c->surface = sf;
+    c->volume_mode = dsc->volume_mode;
+    c->volume_flux = dsc->volume_flux;
+    c->mu = dsc->mu;
+    c->prandtl = dsc->prandtl;
+    c->ph.gamma = dsc->gamma;
+    c->ph.gm1 = dsc->gamma - 1.0;
+    c->ph.inv_gm1 = 1.0 / (dsc->gamma - 1.0);
+    c->basis = make_basis(3);
+    for (int a = 0; a < 3; ++a) {
+      c->nc[a] = a < dsc->dim ? dsc->n[a] : 1;
+      REQUIRE(c->nc[a] >= 1, "need at least one cell per axis");
+      if (a < dsc->dim) {
+        REQUIRE(dsc->edges[a] != nullptr, "missing edges");
+        c->edges[a].assign(dsc->edges[a], dsc->edges[a] + c->nc[a] + 1);
+      } else {
+        c->edges[a] = {0.0, 1.0};
+      }
+      c->h[a].resize(c->nc[a]);
+      for (int i = 0; i < c->nc[a]; ++i) {
+        c->h[a][i] = c->edges[a][i + 1] - c->edges[a][i];
+        REQUIRE(c->h[a][i] > 0.0, "cell sizes must be positive");
+      }
+    }
+    c->ncells = static_cast<long long>(c->nc[0]) * c->nc[1] * c->nc[2];
+    REQUIRE(c->ncells < (1ll << 31) / 64, "mesh too large for 32-bit cell ids");
+    c->nnodes = c->ncells * c->npc;
+    c->ndofs = c->nnodes * c->V;
+    set_device(c);
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    c->grid_stage = 8 * 148;  // fixed (not device-derived) so reductions are reproducible
+    c->grid_flat = 8 * 148;
+    (void)sms;
+    const size_t bytes = sizeof(double) * c->ndofs;
+    for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK}) {
+      CK(cudaMalloc(p, bytes));
+      CK(cudaMemsetAsync(*p, 0, bytes, c->stream));
+    }
+    const double w0 = c->basis.w[0];
+    for (int a = 0; a < 3; ++a) {
+      std::vector<double> jac(c->nc[a]), lift(c->nc[a]);
+      for (int i = 0; i < c->nc[a]; ++i) {
+        jac[i] = 2.0 / c->h[a][i];
+        lift[i] = 2.0 / (c->h[a][i] * w0);  // semidisc.cpp:503,513
+      }
+      CK(cudaMalloc(&c->dh[a], sizeof(double) * c->nc[a]));
+      CK(cudaMalloc(&c->djac[a], sizeof(double) * c->nc[a]));
+      CK(cudaMalloc(&c->dlift[a], sizeof(double) * c->nc[a]));
+      CK(cudaMemcpy(c->dh[a], c->h[a].data(), sizeof(double) * c->nc[a], cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->djac[a], jac.data(), sizeof(double) * c->nc[a], cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->dlift[a], lift.data(), sizeof(double) * c->nc[a], cudaMemcpyHostToDevice));
+    }
+    CK(cudaMalloc(&c->dlevel, c->ncells));
+    CK(cudaMemset(c->dlevel, 1, c->ncells));
+    CK(cudaMalloc(&c->st, sizeof(StepState)));
+    CK(cudaMalloc(&c->partials, sizeof(double) * 2 * 8 * 4096));
+    CK(cudaMalloc(&c->counter, sizeof(unsigned)));
+    CK(cudaMemset(c->counter, 0, sizeof(unsigned)));
+    CK(cudaMalloc(&c->dout, sizeof(double) * 8));
+    CK(cudaMalloc(&c->dint, sizeof(int) * 4));
+    CK(cudaMalloc(&c->dlist_tmp, sizeof(int) * c->ncells));
+    CK(cudaMalloc(&c->dnu, sizeof(double) * c->ncells));
+    CK(upload_basis(c->basis.D.data(), c->basis.w.data()));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = c;
+  });
+  if (rc != PERRK_OK && c) perrk_destroy(c);
+  return rc;
+}
+
+int perrk_destroy(perrk_ctx* c) {
+  if (!c) return PERRK_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (double* p : {c->U, c->K1, c->Ka, c->Kb, c->d, c->tU, c->tK, c->partials, c->dout, c->records,
+                    c->dnu})
+    if (p) cudaFree(p);
+  for (int a = 0; a < 3; ++a)
+    for (double* p : {c->dh[a], c->djac[a], c->dlift[a]})
+      if (p) cudaFree(p);
+  for (auto& p : c->plan)
+    if (p.dlist) cudaFree(p.dlist);
+  if (c->dlevel) cudaFree(c->dlevel);
+  if (c->st) cudaFree(c->st);
+  if (c->counter) cudaFree(c->counter);
+  if (c->dint) cudaFree(c->dint);
+  if (c->dlist_tmp) cudaFree(c->dlist_tmp);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return PERRK_OK;
+}
+
+int perrk_sizes(const perrk_ctx* c, int64_t* dofs, int64_t* nodes, int64_t* cells, int* vars,
+                int* npc) {
+  return guarded([&] {
+    REQUIRE(c, "null context");
+    if (dofs) *dofs = c->ndofs;
+    if (nodes) *nodes = c->nnodes;
+    if (cells) *cells = c->ncells;
+    if (vars) *vars = c->V;
+    if (npc) *npc = c->npc;
+  });
+}
+
+int perrk_node_geometry(const perrk_ctx* c, double* x, double* y, double* z, double* measure) {
+  return guarded([&] {
+    REQUIRE(c, "null context");
+    const auto& B = c->basis;
+    for (long long cell = 0; cell < c->ncells; ++cell) {
+      const int ci = static_cast<int>(cell % c->nc[0]);
+      const int cj = static_cast<int>((cell / c->nc[0]) % c->nc[1]);
+      const int ck = static_cast<int>(cell / (static_cast<long long>(c->nc[0]) * c->nc[1]));
+      for (int l = 0; l < c->npc; ++l) {
+        const int ix = l % 4, iy = (l / 4) % 4, iz = l / 16;
+        const long long n = cell * c->npc + l;
+        if (x) x[n] = c->edges[0][ci] + 0.5 * c->h[0][ci] * (B.x[ix] + 1.0);
+        if (y) y[n] = c->edges[1][cj] + 0.5 * c->h[1][cj] * (B.x[iy] + 1.0);
+        if (z && c->dim == 3) z[n] = c->edges[2][ck] + 0.5 * c->h[2][ck] * (B.x[iz] + 1.0);
+        if (measure)
+          measure[n] = c->dim == 2 ? 0.25 * c->h[0][ci] * c->h[1][cj] * B.w[ix] * B.w[iy]
+                                   : 0.125 * c->h[0][ci] * c->h[1][cj] * c->h[2][ck] * B.w[ix] *
+                                         B.w[iy] * B.w[iz];
+      }
+    }
+  });
+}
+
+int perrk_set_family(perrk_ctx* c, const perrk_family_desc* f, const int* eff) {
+  return guarded([&] {
+    REQUIRE(c && f && eff, "null argument");
+    REQUIRE(f->S >= 1 && f->R >= 1 && f->R <= dev::MAXR, "family size out of range");
+    set_device(c);
+    c->S = f->S;
+    c->R = f->R;
+    c->E.assign(f->E, f->E + f->R);
+    c->A.assign(f->A, f->A + static_cast<size_t>(f->R) * f->S * f->S);
+    c->b.assign(f->b, f->b + f->S);
+    c->c.assign(f->c, f->c + f->S);
+    c->eff.assign(eff, eff + c->ncells);
+    std::vector<int8_t> lv(c->ncells);
+    for (long long i = 0; i < c->ncells; ++i) {
+      REQUIRE(eff[i] >= 1 && eff[i] <= f->R, "level out of range");
+      lv[i] = static_cast<int8_t>(eff[i]);
+    }
+    CK(cudaMemcpy(c->dlevel, lv.data(), c->ncells, cudaMemcpyHostToDevice));
+    build_plan(c);
+    c->has_family = true;
+  });
+}
+
+int perrk_upload_state(perrk_ctx* c, const double* U, size_t n) {
+  return guarded([&] {
+    REQUIRE(c && U, "null argument");
+    REQUIRE(static_cast<long long>(n) == c->ndofs, "state size mismatch");
+    set_device(c);
+    upload(c, c->U, U);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int perrk_download_state(perrk_ctx* c, double* U, size_t n) {
+  return guarded([&] {
+    REQUIRE(c && U, "null argument");
+    REQUIRE(static_cast<long long>(n) == c->ndofs, "state size mismatch");
+    set_device(c);
+    download(c, U, c->U);
+  });
+}
+
+int perrk_state_device_ptr(perrk_ctx* c, double** p) {
+  return guarded([&] {
+    REQUIRE(c && p, "null argument");
+    *p = c->U;
+  });
+}
+
+int perrk_sync(perrk_ctx* c) {
+  return guarded([&] {
+    REQUIRE(c, "null context");
+    set_device(c);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const char* mask) {
+  (void)t;  // the periodic 2D/3D RHS is autonomous (semidisc.cpp:411)
+  return guarded([&] {
+    REQUIRE(c && U && out, "null argument");
+    set_device(c);
+    std::vector<int> list;
+    for (long long i = 0; i < c->ncells; ++i)
+      if (!mask || mask[i]) list.push_back(static_cast<int>(i));
+    upload(c, c->tU, U);
+    CK(cudaMemsetAsync(c->tK, 0, sizeof(double) * c->ndofs, c->stream));
+    c->evals += static_cast<uint64_t>(list.size()) * c->npc * c->V;
+    if (!list.empty()) {
+      CK(cudaMemcpyAsync(c->dlist_tmp, list.data(), sizeof(int) * list.size(),
+                         cudaMemcpyHostToDevice, c->stream));
+      StepState s = fresh_state();
+      put_state(c, s);
+      StageArgs a{};
+      a.U = c->tU;
+      a.K1 = a.Kp = c->tU;
+      a.Kout = c->tK;
+      a.list = mask ? c->dlist_tmp : nullptr;
+      a.n = static_cast<int>(list.size());
+      a.write_k = 1;
+      a.ncells = c->ncells;
+      CK(launch_stage(c->dim, c->surface, a, c->mesh(), c->ph, c->st, c->partials, c->counter,
+                      c->grid_stage, c->stream));
+      const StepState r = get_state(c);
+      if (r.bad_code != std::numeric_limits<long long>::max())
+        throw Fail(PERRK_ENUMERIC, "inadmissible state passed to numerical flux");
+    }
+    download(c, out, c->tK);
+  });
+}
+
+int perrk_br1_gradients(perrk_ctx*, double, const double*, double*) {
+  g_last_error = "Navier-Stokes/BR1 not built yet";
+  return PERRK_EUNSUP;
+}
+
+int perrk_total_entropy(perrk_ctx* c, const double* U, double* out) {
+  return guarded([&] {
+    REQUIRE(c && out, "null argument");
+    set_device(c);
+    *out = quad(c, stage_input(c, U), nullptr, 0, nullptr);
+  });
+}
+
+int perrk_entropy_inner_product(perrk_ctx* c, const double* U, const double* K, double* out) {
+  return guarded([&] {
+    REQUIRE(c && K && out, "null argument");
+    set_device(c);
+    const double* dU = stage_input(c, U);
+    upload(c, c->tK, K);
+    *out = quad(c, dU, c->tK, 1, nullptr);
+  });
+}
+
+int perrk_integral_per_variable(perrk_ctx* c, const double* U, double* out) {
+  return guarded([&] {
+    REQUIRE(c && out, "null argument");
+    set_device(c);
+    quad(c, stage_input(c, U), nullptr, 2, out);
+  });
+}
+
+int perrk_admissible(perrk_ctx* c, const double* U, int* ok, int* first_bad) {
+  return guarded([&] {
+    REQUIRE(c && ok, "null argument");
+    set_device(c);
+    const double* dU = stage_input(c, U);
+    const int init = std::numeric_limits<int>::max();
+    CK(cudaMemcpyAsync(c->dint, &init, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(launch_admissible(c->dim, dU, c->ph, c->dint, c->nnodes, c->grid_flat, c->stream));
+    int bad;
+    CK(cudaMemcpyAsync(&bad, c->dint, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *ok = bad == init ? 1 : 0;
+    if (first_bad) *first_bad = bad == init ? -1 : bad;
+  });
+}
+
+int perrk_characteristic_speed(perrk_ctx* c, const double* U, double* nu) {
+  return guarded([&] {
+    REQUIRE(c && nu, "null argument");
+    set_device(c);
+    CK(launch_nu_cell(c->dim, stage_input(c, U), c->mesh(), c->ph, c->dnu, c->ncells, c->stream));
+    CK(cudaMemcpyAsync(nu, c->dnu, sizeof(double) * c->ncells, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int perrk_compute_dt(perrk_ctx* c, const double* U, int fixed, double dt_or_cfl, double t,
+                     double tf, double* dt) {
+  return guarded([&] {
+    REQUIRE(c && dt, "null argument");
+    if (fixed) {
+      REQUIRE(dt_or_cfl > 0.0, "fixed dt must be positive");
+      *dt = std::fmin(dt_or_cfl, tf - t);
+      return;
+    }
+    set_device(c);
+    StepState s = fresh_state();
+    s.numax_bits = 0;
+    put_state(c, s);
+    CK(launch_numax(c->dim, stage_input(c, U), c->mesh(), c->ph, c->st, c->nnodes, c->grid_flat,
+                    c->stream));
+    const StepState r = get_state(c);
+    double best;
+    std::memcpy(&best, &r.numax_bits, sizeof best);
+    const double nu_max = 4.0 * best;
+    REQUIRE(nu_max > 0.0, "vanishing characteristic speed");
+    *dt = dt_or_cfl / nu_max;
+  });
+}
+
+static int step_common(perrk_ctx* c, double* t, double dt, const perrk_step_opts* o,
+                       perrk_step_result* res) {
+  return guarded([&] {
+    REQUIRE(c && t && o && res, "null argument");
+    REQUIRE(c->has_family, "no family set (perrk_set_family)");
+    REQUIRE(dt > 0.0, "dt must be positive");
+    if (o->relax_enabled) check_relax_cfg(o->relax);
+    set_device(c);
+    StepState s = fresh_state();
+    s.t = *t;
+    s.dt_mode = 0;
+    s.dt_given = dt;
+    s.gamma_override = o->gamma_override;
+    s.gamma_seed = o->gamma_seed;
+    s.h_ref = o->h_ref;
+    s.idt = o->idt;
+    configure_relax(s, o->relax_enabled != 0, o->relax);
+    put_state(c, s);
+    StepMode mode;
+    mode.relax = o->relax_enabled != 0;
+    mode.cfg = o->relax;
+    enqueue_step(c, mode, needs_h(mode.relax, o->relax, o->h_ref));
+    const StepState r = get_state(c);
+    if (r.error == 1) throw Fail(PERRK_ENUMERIC, "non-finite update direction");
+    c->evals += evals_per_step(c);
+    fill_result(c, r, mode.relax, o->gamma_override, res);
+    if (!r.aborted) *t = r.t;
+  });
+}
+
+int perrk_perk_step_resident(perrk_ctx* c, double* t, double dt, const perrk_step_opts* o,
+                             perrk_step_result* res) {
+  return step_common(c, t, dt, o, res);
+}
+
+int perrk_perk_step(perrk_ctx* c, double* U, double* t, double dt, const perrk_step_opts* o,
+                    perrk_step_result* res) {
+  int rc = guarded([&] {
+    REQUIRE(c && U, "null argument");
+    set_device(c);
+    upload(c, c->U, U);
+  });
+  if (rc) return rc;
+  rc = step_common(c, t, dt, o, res);
+  if (rc) return rc;
+  if (res->aborted) return PERRK_OK;  // U untouched on abort (stepper.hpp:70-71)
+  return guarded([&] { download(c, U, c->U); });
+}
+
+int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
+                  perrk_step_record* log, int* steps_taken, int* aborted) {
+  return guarded([&] {
+    REQUIRE(c && cfg && t, "null argument");
+    REQUIRE(c->has_family, "no family set (perrk_set_family)");
+    REQUIRE(nsteps >= 0, "nsteps must be >= 0");
+    if (cfg->relax_enabled) check_relax_cfg(cfg->relax);
+    if (cfg->fixed_dt) REQUIRE(cfg->dt_or_cfl > 0.0, "fixed dt must be positive");
+    set_device(c);
+    StepState s = fresh_state();
+    s.t = *t;
+    s.run_mode = 1;
+    s.tf = cfg->tf;
+    s.t_eps = 1e-12 * std::fmax(1.0, std::fabs(cfg->tf));
+    s.dt_mode = cfg->fixed_dt ? 1 : 2;
+    s.dt_or_cfl = cfg->dt_or_cfl;
+    s.idt = cfg->idt;
+    s.gamma_seed = 1.0;
+    configure_relax(s, cfg->relax_enabled != 0, cfg->relax);
+    if (cfg->relax_enabled && cfg->anchor_initial)
+      s.h_ref = quad(c, c->U, nullptr, 0, nullptr);  // H(U_0)
+    put_state(c, s);
+    const bool rec = cfg->records && log;
+    if (rec && c->records_cap < nsteps) {
+      if (c->records) cudaFree(c->records);
+      CK(cudaMalloc(&c->records, sizeof(double) * 11 * nsteps));
+      c->records_cap = nsteps;
+    }
+    StepMode mode;
+    mode.relax = cfg->relax_enabled != 0;
+    mode.cfg = cfg->relax;
+    mode.want_nu = !cfg->fixed_dt;
+    mode.want_record = rec;
+    mode.records = rec ? c->records : nullptr;
+    if (!cfg->fixed_dt)
+      CK(launch_numax(c->dim, c->U, c->mesh(), c->ph, c->st, c->nnodes, c->grid_flat, c->stream));
+    const bool want_h = needs_h(mode.relax, cfg->relax, s.h_ref);
+    for (int k = 0; k < nsteps; ++k) enqueue_step(c, mode, want_h);
+    const StepState r = get_state(c);
+    if (r.error == 1) throw Fail(PERRK_ENUMERIC, "non-finite update direction");
+    if (r.error == 2) throw Fail(PERRK_EINVAL, "vanishing characteristic speed");
+    *t = r.t;
+    if (steps_taken) *steps_taken = r.steps_taken;
+    if (aborted) *aborted = r.aborted;
+    c->evals += evals_per_step(c) * static_cast<uint64_t>(r.steps_taken + (r.aborted ? 1 : 0));
+    if (rec && r.steps_taken > 0) {
+      std::vector<double> raw(static_cast<size_t>(11) * r.steps_taken);
+      CK(cudaMemcpy(raw.data(), c->records, sizeof(double) * raw.size(), cudaMemcpyDeviceToHost));
+      for (int k = 0; k < r.steps_taken; ++k) {
+        const double* row = &raw[static_cast<size_t>(k) * 11];
+        perrk_step_record& o = log[k];
+        o.t = row[0];
+        o.dt = row[1];
+        o.gamma = row[2];
+        o.newton_iters = static_cast<int>(row[3]);
+        o.fell_back = static_cast<int>(row[4]);
+        o.entropy = row[5];
+        for (int v = 0; v < 5; ++v) o.invariants[v] = v < c->V ? row[6 + v] : 0.0;
+      }
+    }
+  });
+}
+
+int perrk_rhs_cell_evaluations(const perrk_ctx* c, uint64_t* out) {
+  return guarded([&] {
+    REQUIRE(c && out, "null argument");
+    *out = c->evals;
+  });
+}
+
+int perrk_reset_counter(perrk_ctx* c) {
+  return guarded([&] {
+    REQUIRE(c, "null context");
+    c->evals = 0;
+  });
+}
+
+int perrk_family_build(int kind, int S, int R, const int* E, const double* free_flat,
+                       double c_sm3, double* A, double* b, double* cc, int* active) {
+  return guarded([&] {
+    REQUIRE(E && A && b && cc, "null argument");
+    REQUIRE(kind >= 0 && kind <= 3, "unknown family kind");
+    REQUIRE(S >= (kind == PERRK_FAMILY_P4 ? 5 : 3), "too few stages for archetype");
+    REQUIRE(R >= 1, "empty member list");
+    for (int r = 1; r < R; ++r) REQUIRE(E[r] > E[r - 1], "E must be strictly increasing");
+    REQUIRE(E[R - 1] == S, "largest member must have E = S");
+    const auto bw = weights_b(kind, S);
+    const auto cw = abscissae(kind, S, c_sm3);
+    size_t off = 0;
+    for (int r = 0; r < R; ++r) {
+      double* Am = A + static_cast<size_t>(r) * S * S;
+      build_member(kind, S, E[r], free_flat ? free_flat + off : nullptr, bw, cw, Am);
+      off += free_count(kind, E[r]);
+      const auto act = reachable_stages(S, Am, bw);
+      int n = 0;
+      for (int i = 0; i < S; ++i) {
+        n += act[i];
+        if (active) active[r * S + i] = act[i];
+      }
+      REQUIRE(n == E[r], "active stage set does not match E");
+    }
+    std::copy(bw.begin(), bw.end(), b);
+    std::copy(cw.begin(), cw.end(), cc);
+  });
+}
+
+int perrk_assign_levels(const double* nu, int64_t n, int R, int* levels) {
+  return guarded([&] {
+    REQUIRE(R >= 1, "R must be at least 1");
+    REQUIRE(n > 0 && nu && levels, "empty speed list");
+    double nu_max = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      REQUIRE(nu[i] > 0.0, "characteristic speeds must be positive");
+      nu_max = std::fmax(nu_max, nu[i]);
+    }
+    int max_assigned = 1;
+    for (int64_t i = 0; i < n; ++i) {
+      // cells within a factor 2^(r-1) of the fastest get level r
+      int r = 1 + static_cast<int>(std::ceil(std::log2(nu_max / nu[i]) - 1e-12));
+      r = r < 1 ? 1 : (r > R ? R : r);
+      levels[i] = r;
+      max_assigned = r > max_assigned ? r : max_assigned;
+    }
+    const int shift = R - max_assigned;  // slowest cells on the cheapest member
+    if (shift > 0)
+      for (int64_t i = 0; i < n; ++i) levels[i] += shift;
+  });
+}
+
+int perrk_make_partition_map(int dim, const int* n, const int* levels, int R, int* eff) {
+  return guarded([&] {
+    REQUIRE(R >= 1, "R must be at least 1");
+    REQUIRE((dim == 2 || dim == 3) && n && levels && eff, "bad arguments");
+    const int nx = n[0], ny = n[1], nz = dim == 3 ? n[2] : 1;
+    const long long N = static_cast<long long>(nx) * ny * nz;
+    for (long long i = 0; i < N; ++i)
+      REQUIRE(levels[i] >= 1 && levels[i] <= R, "level out of range");
+    for (int k = 0; k < nz; ++k)
+      for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+          const long long cell = i + static_cast<long long>(nx) * (j + static_cast<long long>(ny) * k);
+          int lv = levels[cell];
+          auto nb = [&](int ii, int jj, int kk) {
+            ii = (ii + nx) % nx;
+            jj = (jj + ny) % ny;
+            kk = (kk + nz) % nz;
+            const int o = levels[ii + static_cast<long long>(nx) * (jj + static_cast<long long>(ny) * kk)];
+            lv = o < lv ? o : lv;
+          };
+          nb(i - 1, j, k);
+          nb(i + 1, j, k);
+          nb(i, j - 1, k);
+          nb(i, j + 1, k);
+          if (dim == 3) {
+            nb(i, j, k - 1);
+            nb(i, j, k + 1);
+          }
+          eff[cell] = lv;
+        }
+  });
+}
+
+int perrk_comm_init(perrk_ctx*, const void*, int, int) {
+  g_last_error = "multi-GPU slab decomposition not built yet";
+  return PERRK_EUNSUP;
+}
+
+int perrk_slab_range(const perrk_ctx* c, int* b, int* e) {
+  return guarded([&] {
+    REQUIRE(c && b && e, "null argument");
+    *b = 0;
+    *e = c->dim == 2 ? c->nc[1] : c->nc[2];
+  });
+}
+
+}  // extern "C"

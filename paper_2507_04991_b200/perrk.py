@@ -1,0 +1,690 @@
+"""Python mirror of the reference's solver/integrator API for the hot path.
+
+Names, argument meanings and error behaviour follow the reference's C++ API
+(proj/core/include/perrk/*.hpp), so parity tests read like the reference's
+own tests.  All compute runs in libperrk_b200.so on the GPU through the C-ABI
+(include/perrk_b200.h); this module only marshals arguments.
+
+Reference interfaces mirrored here:
+  Mesh2DRect / build_uniform_mesh2d / build_vortex_mesh   mesh.hpp:22-83
+  Mesh3DRect                                               (3D extension)
+  SemidiscretizationSpec / Semidiscretization              semidisc.hpp:24-113
+  PartitionFamily + build_perk2/3/4, family text I/O       butcher.hpp:36-125
+  PartitionMap / make_partition_map / assign_levels        mesh.hpp:44-76
+  RelaxationConfig / PerkStepOptions / PerkStepResult      relax.hpp:16-31, stepper.hpp:54-68
+  perk_step / compute_dt / run                             stepper.hpp:72-99
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import capi
+from .capi import check, lib
+
+Error = capi.PerrkError
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
+# meshes (mesh.hpp:22-33 plus the 3D extension), periodic rectilinear
+# ---------------------------------------------------------------------------
+@dataclass
+class Mesh2DRect:
+    x_edges: Sequence[float]
+    y_edges: Sequence[float]
+
+    @property
+    def dim(self):
+        return 2
+
+    @property
+    def edges(self):
+        return [np.asarray(self.x_edges, float), np.asarray(self.y_edges, float)]
+
+    def nx(self):
+        return len(self.x_edges) - 1
+
+    def ny(self):
+        return len(self.y_edges) - 1
+
+    def num_cells(self):
+        return self.nx() * self.ny()
+
+    def shape(self):
+        return (self.nx(), self.ny())
+
+
+@dataclass
+class Mesh3DRect:
+    x_edges: Sequence[float]
+    y_edges: Sequence[float]
+    z_edges: Sequence[float]
+
+    @property
+    def dim(self):
+        return 3
+
+    @property
+    def edges(self):
+        return [np.asarray(e, float) for e in (self.x_edges, self.y_edges, self.z_edges)]
+
+    def num_cells(self):
+        return (len(self.x_edges) - 1) * (len(self.y_edges) - 1) * (len(self.z_edges) - 1)
+
+    def shape(self):
+        return tuple(len(e) - 1 for e in (self.x_edges, self.y_edges, self.z_edges))
+
+
+def _uniform_edges(a, b, n):
+    # append_uniform (mesh.cpp:137-141): from + (to - from) * i / n
+    return [a] + [a + (b - a) * i / n for i in range(1, n + 1)]
+
+
+def build_uniform_mesh2d(half_width, n):
+    e = _uniform_edges(-half_width, half_width, n)
+    return Mesh2DRect(e, list(e))
+
+
+def build_uniform_mesh3d(lo, hi, n):
+    e = _uniform_edges(lo, hi, n)
+    return Mesh3DRect(e, list(e), list(e))
+
+
+def mesh_num_cells(mesh):
+    return mesh.num_cells()
+
+
+# ---------------------------------------------------------------------------
+# semidiscretization
+# ---------------------------------------------------------------------------
+@dataclass
+class SemidiscretizationSpec:
+    mesh: object
+    polydeg: int = 3
+    gamma: float = 1.4
+    physics: str = "euler"          # "euler" | "nsf"
+    mu: float = 0.0
+    prandtl: float = 0.72
+    surface_flux: str = "rusanov"
+    volume_mode: str = "flux_differencing"
+    volume_flux: str = "ec"
+    device: int = 0
+
+
+class Semidiscretization:
+    """GPU-resident Semidiscretization (semidisc.hpp:40-113)."""
+
+    def __init__(self, spec: SemidiscretizationSpec):
+        self.spec = spec
+        mesh = spec.mesh
+        self._edges = [_f64(e) for e in mesh.edges]
+        d = capi.SemiDesc()
+        d.dim = mesh.dim
+        for a, e in enumerate(self._edges):
+            d.n[a] = len(e) - 1
+            d.edges[a] = _dp(e)
+        d.polydeg = spec.polydeg
+        d.physics = {"euler": 0, "nsf": 1}[spec.physics]
+        d.gamma = spec.gamma
+        d.mu = spec.mu
+        d.prandtl = spec.prandtl
+        d.surface_flux = capi.FLUX[spec.surface_flux]
+        d.volume_mode = {"weak": 0, "flux_differencing": 1}[spec.volume_mode]
+        d.volume_flux = capi.FLUX[spec.volume_flux]
+        d.device = spec.device
+        h = C.c_void_p()
+        check(lib().perrk_create(C.byref(d), C.byref(h)))
+        self._h = h
+        dofs, nodes, cells = C.c_int64(), C.c_int64(), C.c_int64()
+        v, npc = C.c_int(), C.c_int()
+        check(lib().perrk_sizes(h, C.byref(dofs), C.byref(nodes), C.byref(cells), C.byref(v),
+                                C.byref(npc)))
+        self._n = (dofs.value, nodes.value, cells.value, v.value, npc.value)
+        self._family_key = None
+        self._geom = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().perrk_destroy(h)
+            self._h = None
+
+    # sizes (semidisc.hpp:44-49)
+    def num_dofs(self):
+        return self._n[0]
+
+    def num_nodes(self):
+        return self._n[1]
+
+    def num_cells(self):
+        return self._n[2]
+
+    def num_vars(self):
+        return self._n[3]
+
+    def nodes_per_cell(self):
+        return self._n[4]
+
+    def dim(self):
+        return self.spec.mesh.dim
+
+    def mesh(self):
+        return self.spec.mesh
+
+    def _geometry(self):
+        if self._geom is None:
+            n = self.num_nodes()
+            x, y, z, m = (np.zeros(n) for _ in range(4))
+            check(lib().perrk_node_geometry(self._h, _dp(x), _dp(y), _dp(z), _dp(m)))
+            self._geom = (x, y, z, m)
+        return self._geom
+
+    def node_x(self):
+        return self._geometry()[0]
+
+    def node_y(self):
+        return self._geometry()[1]
+
+    def node_z(self):
+        return self._geometry()[2]
+
+    def node_measure(self):
+        return self._geometry()[3]
+
+    def _state(self, U):
+        U = _f64(U)
+        if U.size != self.num_dofs():
+            raise Error(capi.PERRK_EINVAL, "state size mismatch")
+        return U
+
+    # RHS (semidisc.cpp:121-147)
+    def rhs(self, t, U):
+        return self.rhs_masked(t, U, None)
+
+    def rhs_masked(self, t, U, mask):
+        U = self._state(U)
+        out = np.empty_like(U)
+        mb = None
+        if mask is not None:
+            m = np.ascontiguousarray(mask, dtype=np.int8)
+            if m.size != self.num_cells():
+                raise Error(capi.PERRK_EINVAL, "mask size mismatch")
+            mb = m.tobytes()
+        check(lib().perrk_rhs_masked(self._h, float(t), _dp(U), _dp(out), mb))
+        return out
+
+    def rhs_partition_restricted(self, t, U, pmap, level):
+        mask = (np.asarray(pmap.effective_level) == level).astype(np.int8)
+        return self.rhs_masked(t, U, mask)
+
+    # reductions (semidisc.cpp:561-607)
+    def total_entropy(self, U):
+        out = C.c_double()
+        check(lib().perrk_total_entropy(self._h, _dp(self._state(U)), C.byref(out)))
+        return out.value
+
+    def entropy_inner_product(self, U, K):
+        out = C.c_double()
+        check(lib().perrk_entropy_inner_product(self._h, _dp(self._state(U)), _dp(self._state(K)),
+                                                C.byref(out)))
+        return out.value
+
+    def integral_per_variable(self, U):
+        out = np.zeros(5)
+        check(lib().perrk_integral_per_variable(self._h, _dp(self._state(U)), _dp(out)))
+        return out[: self.num_vars()]
+
+    def admissible(self, U):
+        ok, bad = C.c_int(), C.c_int()
+        check(lib().perrk_admissible(self._h, _dp(self._state(U)), C.byref(ok), C.byref(bad)))
+        return bool(ok.value), bad.value
+
+    def characteristic_speed(self, U):
+        nu = np.zeros(self.num_cells())
+        check(lib().perrk_characteristic_speed(self._h, _dp(self._state(U)), _dp(nu)))
+        return nu
+
+    def project(self, fn: Callable):
+        """semidisc.cpp:588-594 on the host: fn(x, y[, z]) -> (V, n) array."""
+        x, y, z, _ = self._geometry()
+        args = (x, y) if self.dim() == 2 else (x, y, z)
+        vals = np.asarray(fn(*args), dtype=np.float64)
+        return np.ascontiguousarray(vals.T).reshape(-1)
+
+    def rhs_cell_evaluations(self):
+        out = C.c_uint64()
+        check(lib().perrk_rhs_cell_evaluations(self._h, C.byref(out)))
+        return out.value
+
+    def reset_evaluation_counter(self):
+        check(lib().perrk_reset_counter(self._h))
+
+    # resident state
+    def upload(self, U):
+        U = self._state(U)
+        check(lib().perrk_upload_state(self._h, _dp(U), U.size))
+
+    def download(self, out=None):
+        out = np.empty(self.num_dofs()) if out is None else out
+        check(lib().perrk_download_state(self._h, _dp(out), out.size))
+        return out
+
+    def device_state_ptr(self):
+        p = C.POINTER(C.c_double)()
+        check(lib().perrk_state_device_ptr(self._h, C.byref(p)))
+        return C.cast(p, C.c_void_p).value
+
+    def sync(self):
+        check(lib().perrk_sync(self._h))
+
+    def _use_family(self, family, pmap):
+        key = (id(family), id(pmap), family.version, pmap.version)
+        if key == self._family_key:
+            return
+        E = np.ascontiguousarray(family.E, dtype=np.int32)
+        A = _f64(family.A)
+        b, c = _f64(family.b), _f64(family.c)
+        eff = np.ascontiguousarray(pmap.effective_level, dtype=np.int32)
+        if eff.size != self.num_cells():
+            raise Error(capi.PERRK_EINVAL, "partition map does not match semidiscretization")
+        fd = capi.FamilyDesc(capi.FAMILY[family.kind], family.S, family.R, _ip(E), _dp(A), _dp(b),
+                             _dp(c))
+        check(lib().perrk_set_family(self._h, C.byref(fd), _ip(eff)))
+        self._family_key = key
+
+
+# ---------------------------------------------------------------------------
+# P-ERK families (butcher.hpp:36-125)
+# ---------------------------------------------------------------------------
+_FREE = {"p2": lambda E: E - 2, "p3": lambda E: E - 3, "p3-original": lambda E: E - 3,
+         "p4": lambda E: E - 5}
+
+
+@dataclass
+class PartitionFamily:
+    kind: str
+    S: int
+    R: int
+    E: List[int]
+    A: np.ndarray        # [R, S, S]
+    b: np.ndarray
+    c: np.ndarray
+    active_sets: List[set] = field(default_factory=list)
+    dt_max: List[float] = field(default_factory=list)
+    version: int = 0
+
+    @property
+    def order(self):
+        return {"p2": 2, "p3": 3, "p3-original": 3, "p4": 4}[self.kind]
+
+    def member_index_for_level(self, level):
+        return self.R - level
+
+    def member_for_level(self, level):
+        return self.A[self.member_index_for_level(level)]
+
+
+def free_coefficient_count(kind, E):
+    return _FREE[kind](E)
+
+
+def build_family(kind, S, E_list, free_subdiagonals, c_Sminus3=1.0):
+    kind = {"p3-variant": "p3"}.get(kind, kind)
+    R = len(E_list)
+    if len(free_subdiagonals) != R:
+        raise Error(capi.PERRK_EINVAL, "inconsistent member count")
+    for E, fr in zip(E_list, free_subdiagonals):
+        if E >= 0 and len(fr) != _FREE[kind](E):
+            raise Error(capi.PERRK_EINVAL, "inconsistent free coefficient count")
+    E = np.ascontiguousarray(E_list, dtype=np.int32)
+    flat = _f64([x for fr in free_subdiagonals for x in fr] or [0.0])
+    A = np.zeros((R, S, S))
+    b, c = np.zeros(S), np.zeros(S)
+    act = np.zeros((R, S), dtype=np.int32)
+    check(lib().perrk_family_build(capi.FAMILY[kind], S, R, _ip(E), _dp(flat), float(c_Sminus3),
+                                   _dp(A), _dp(b), _dp(c), _ip(act)))
+    sets = [set(np.nonzero(act[r])[0].tolist()) for r in range(R)]
+    return PartitionFamily(kind, S, R, list(map(int, E_list)), A, b, c, sets)
+
+
+def build_perk2(S, E_list, free):
+    return build_family("p2", S, E_list, free)
+
+
+def build_perk3_variant(S, E_list, free):
+    return build_family("p3", S, E_list, free)
+
+
+def build_perk3_original(S, E_list, free):
+    return build_family("p3-original", S, E_list, free)
+
+
+def build_perk4(S, E_list, free, c_Sminus3=1.0):
+    return build_family("p4", S, E_list, free, c_Sminus3)
+
+
+def active_stage_set(A, b):
+    """butcher.cpp:319-332 (host)."""
+    S = len(b)
+    act = {0} | {i for i in range(S) if b[i] != 0.0}
+    grew = True
+    while grew:
+        grew = False
+        for i in sorted(act):
+            for j in range(i):
+                if A[i][j] != 0.0 and j not in act:
+                    act.add(j)
+                    grew = True
+    return act
+
+
+def _fmt17(v):
+    return "%.17g" % v
+
+
+def family_to_text(fam: PartitionFamily) -> str:
+    """Plain-text family format of butcher.cpp:334-355."""
+    lines = [f"{fam.S} {fam.R}", f"# kind {fam.kind}",
+             " ".join(_fmt17(x) for x in fam.c), " ".join(_fmt17(x) for x in fam.b)]
+    for r in range(fam.R):
+        lines.append(str(fam.E[r]))
+        for i in range(fam.S):
+            lines.append(" ".join(_fmt17(x) for x in fam.A[r, i]))
+    if fam.dt_max:
+        lines.append("dt_max " + " ".join(_fmt17(x) for x in fam.dt_max))
+    return "\n".join(lines) + "\n"
+
+
+def family_from_text(text: str) -> PartitionFamily:
+    """butcher.cpp:357-433."""
+    kind = "p2"
+    rows = []
+    dt_max = []
+    for raw in text.splitlines():
+        s = raw.strip()
+        if not s:
+            continue
+        if s.startswith("#"):
+            parts = s[1:].split()
+            if len(parts) >= 2 and parts[0] == "kind":
+                kind = {"p3-variant": "p3"}.get(parts[1], parts[1])
+            continue
+        if s.startswith("dt_max"):
+            dt_max = [float(x) for x in s.split()[1:]]
+            continue
+        rows.append(s.split())
+    if not rows:
+        raise Error(capi.PERRK_EINVAL, "empty family file")
+    S, R = int(rows[0][0]), int(rows[0][1])
+    c = np.array([float(x) for x in rows[1][:S]])
+    b = np.array([float(x) for x in rows[2][:S]])
+    A = np.zeros((R, S, S))
+    E = []
+    k = 3
+    for r in range(R):
+        E.append(int(float(rows[k][0])))
+        k += 1
+        for i in range(S):
+            A[r, i] = [float(x) for x in rows[k][:S]]
+            k += 1
+    sets = [active_stage_set(A[r], b) for r in range(R)]
+    return PartitionFamily(kind, S, R, E, A, b, c, sets, dt_max)
+
+
+def load_family(path):
+    with open(path) as f:
+        return family_from_text(f.read())
+
+
+def save_family(fam, path):
+    with open(path, "w") as f:
+        f.write(family_to_text(fam))
+
+
+# ---------------------------------------------------------------------------
+# partition map (mesh.hpp:44-76)
+# ---------------------------------------------------------------------------
+@dataclass
+class PartitionMap:
+    R: int
+    raw_level: np.ndarray
+    effective_level: np.ndarray
+    version: int = 0
+
+    def cells_per_level(self):
+        return [int(np.sum(self.effective_level == r)) for r in range(1, self.R + 1)]
+
+
+def make_partition_map(mesh, levels, R):
+    levels = np.ascontiguousarray(levels, dtype=np.int32)
+    if levels.size != mesh.num_cells():
+        raise Error(capi.PERRK_EINVAL, "level list does not match mesh")
+    n = np.ascontiguousarray(list(mesh.shape()) + [1] * (3 - mesh.dim), dtype=np.int32)
+    eff = np.zeros_like(levels)
+    check(lib().perrk_make_partition_map(mesh.dim, _ip(n), _ip(levels), int(R), _ip(eff)))
+    return PartitionMap(int(R), levels.copy(), eff)
+
+
+def assign_levels(nu, R):
+    nu = _f64(nu)
+    out = np.zeros(nu.size, dtype=np.int32)
+    check(lib().perrk_assign_levels(_dp(nu), nu.size, int(R), _ip(out)))
+    return out
+
+
+def uniform_map(semi, level=1, R=1):
+    lv = np.full(semi.num_cells(), level, dtype=np.int32)
+    return PartitionMap(R, lv.copy(), lv)
+
+
+# ---------------------------------------------------------------------------
+# integrator (relax.hpp, stepper.hpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class RelaxationConfig:
+    method: str = "newton"
+    max_iter: int = 5
+    residual_tol: float = 1e-14
+    step_tol: float = 1e-15
+    bracket_min: float = 0.8
+    bracket_max: float = 1.2
+    seed_from_previous: bool = True
+    numerics: str = "reference"     # "reference" (relax.cpp) | "accurate"
+
+    def to_c(self):
+        return capi.RelaxCfg({"newton": 0, "bisection": 1, "secant": 2}[self.method],
+                             self.max_iter, self.residual_tol, self.step_tol, self.bracket_min,
+                             self.bracket_max, int(self.seed_from_previous),
+                             {"reference": 0, "accurate": 1}[self.numerics])
+
+
+@dataclass
+class PerkStepOptions:
+    relaxation: Optional[RelaxationConfig] = None
+    gamma_override: float = 1.0
+    gamma_seed: float = 1.0
+    h_ref: float = math.nan
+    idt: bool = False
+
+    def to_c(self):
+        o = capi.StepOpts()
+        o.relax_enabled = int(self.relaxation is not None)
+        if self.relaxation is not None:
+            o.relax = self.relaxation.to_c()
+        o.gamma_override = self.gamma_override
+        o.gamma_seed = self.gamma_seed
+        o.h_ref = self.h_ref
+        o.idt = int(self.idt)
+        return o
+
+
+@dataclass
+class PerkStepResult:
+    gamma: float
+    iterations: int
+    residual: float
+    fell_back: bool
+    delta_h: float
+    aborted: bool
+    bad_cell: int
+    bad_stage: int
+
+
+def _result(r):
+    return PerkStepResult(r.gamma, r.iterations, r.residual, bool(r.fell_back), r.delta_h,
+                          bool(r.aborted), r.bad_cell, r.bad_stage)
+
+
+def perk_step(U, t, dt, family, pmap, semi, opts=None):
+    """stepper.cpp:17-114.  U (numpy, host) is advanced in place; returns
+    (t_new, PerkStepResult).  On a positivity abort U and t are untouched."""
+    opts = opts or PerkStepOptions()
+    if U.dtype != np.float64 or not U.flags.c_contiguous:
+        raise Error(capi.PERRK_EINVAL, "U must be a contiguous float64 array")
+    semi._use_family(family, pmap)
+    tt = C.c_double(t)
+    res = capi.StepResult()
+    o = opts.to_c()
+    check(lib().perrk_perk_step(semi._h, _dp(U), C.byref(tt), float(dt), C.byref(o),
+                                C.byref(res)))
+    return tt.value, _result(res)
+
+
+def perk_step_resident(t, dt, family, pmap, semi, opts=None):
+    """perk_step on the state already resident on the device (semi.upload)."""
+    opts = opts or PerkStepOptions()
+    semi._use_family(family, pmap)
+    tt = C.c_double(t)
+    res = capi.StepResult()
+    o = opts.to_c()
+    check(lib().perrk_perk_step_resident(semi._h, C.byref(tt), float(dt), C.byref(o),
+                                         C.byref(res)))
+    return tt.value, _result(res)
+
+
+@dataclass
+class CflRamp:
+    cfl0: float = 0.5
+    cfl_max: float = 0.5
+    t_ramp: float = 1.0
+
+
+@dataclass
+class TimeControl:
+    fixed: bool = True
+    dt: float = 0.0
+    ramp: CflRamp = field(default_factory=CflRamp)
+
+
+@dataclass
+class IntegratorConfig:
+    t0: float = 0.0
+    tf: float = 1.0
+    time: TimeControl = field(default_factory=TimeControl)
+    relaxation: Optional[RelaxationConfig] = None
+    anchor: str = "step"          # "step" | "initial"
+    idt: bool = False
+    max_steps: int = 10_000_000
+
+
+def compute_dt(U, semi, config: IntegratorConfig, t):
+    """stepper.cpp:116-127 (constant CFL ramp only on the device)."""
+    r = config.time.ramp
+    if not config.time.fixed and r.cfl0 != r.cfl_max:
+        raise Error(capi.PERRK_EUNSUP, "CFL ramps are not on the device path")
+    val = config.time.dt if config.time.fixed else r.cfl_max
+    out = C.c_double()
+    check(lib().perrk_compute_dt(semi._h, _dp(semi._state(U)), int(config.time.fixed), float(val),
+                                 float(t), float(config.tf), C.byref(out)))
+    return out.value
+
+
+@dataclass
+class StepRecord:
+    step: int
+    t: float
+    dt: float
+    gamma: float
+    newton_iters: int
+    entropy: float
+    invariants: np.ndarray
+    fell_back: bool
+
+
+@dataclass
+class RunResult:
+    U: np.ndarray
+    log: List[StepRecord]
+    final_time: float
+    aborted: bool
+    n_rhs: int
+    initial_entropy: float
+
+
+def _run_cfg(config: IntegratorConfig, records=True):
+    r = config.time.ramp
+    if not config.time.fixed and r.cfl0 != r.cfl_max:
+        raise Error(capi.PERRK_EUNSUP, "CFL ramps are not on the device path")
+    rc = capi.RunCfg()
+    rc.fixed_dt = int(config.time.fixed)
+    rc.dt_or_cfl = config.time.dt if config.time.fixed else r.cfl_max
+    rc.tf = config.tf
+    rc.relax_enabled = int(config.relaxation is not None)
+    if config.relaxation is not None:
+        rc.relax = config.relaxation.to_c()
+    rc.anchor_initial = int(config.anchor == "initial")
+    rc.idt = int(config.idt)
+    rc.records = int(records)
+    return rc
+
+
+def advance(semi, family, pmap, config: IntegratorConfig, t, nsteps, records=True):
+    """Up to nsteps steps of run()'s loop on the resident state, on the
+    device (one host sync at the end).  Returns (t, steps, aborted, records)."""
+    semi._use_family(family, pmap)
+    rc = _run_cfg(config, records)
+    log = (capi.StepRecord * max(nsteps, 1))()
+    tt = C.c_double(t)
+    taken, ab = C.c_int(), C.c_int()
+    check(lib().perrk_advance(semi._h, C.byref(rc), C.byref(tt), int(nsteps),
+                              log if records else None, C.byref(taken), C.byref(ab)))
+    return tt.value, taken.value, bool(ab.value), list(log)[: taken.value] if records else []
+
+
+def run(config: IntegratorConfig, family, pmap, semi, U0, chunk=64):
+    """stepper.cpp:129-193: integrate from t0 to tf on the device."""
+    U0 = semi._state(U0)
+    h0 = semi.total_entropy(U0)
+    semi.reset_evaluation_counter()
+    semi.upload(U0)
+    t = config.t0
+    log: List[StepRecord] = []
+    aborted = False
+    t_eps = 1e-12 * max(1.0, abs(config.tf))
+    while t < config.tf - t_eps and not aborted:
+        if len(log) >= config.max_steps:
+            raise Error(capi.PERRK_EINVAL, "step limit exceeded")
+        n = min(chunk, config.max_steps - len(log))
+        t, taken, aborted, recs = advance(semi, family, pmap, config, t, n, True)
+        for r in recs:
+            log.append(StepRecord(len(log) + 1, r.t, r.dt, r.gamma, r.newton_iters, r.entropy,
+                                  np.array(r.invariants[: semi.num_vars()]), bool(r.fell_back)))
+        if taken == 0 and not aborted:
+            break
+    return RunResult(semi.download(), log, t, aborted, semi.rhs_cell_evaluations(), h0)

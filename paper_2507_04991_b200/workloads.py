@@ -1,0 +1,261 @@
+"""Synthetic workloads of BASELINE.json's five configurations (host side).
+
+No dataset is involved: every input is generated here from seeded, documented
+formulas (initial conditions, meshes, level maps) or loaded from the frozen
+family fixtures under configs/.  Decisions the reference leaves open (SURVEY.md
+Appendix A) are fixed here and recorded in DESIGN.md:
+
+  C1  uniform 16^2 on [-10,10]^2, vortex I=5 (p_inf = 1), EC + Rusanov,
+      p2 S=4 E={4} with (a21, a32) = (0.2, 0.35), CFL 0.9, 100 steps
+  C2  64^2 "+"-refined mesh (16 h | 32 h/2 | 16 h per axis, h = 20/48),
+      EC + HLLE, p3 {4,7}, 500 steps
+  C3  256^2 three-level "+" mesh on [0,2pi]^2, seeded random Fourier state,
+      EC + Rusanov, p4 {5,9,16}, 200 steps
+  C4  (2D Navier-Stokes double shear layer) -- pending on the device path
+  C5  64^3 three-level "+" mesh on [0,2pi]^3, Taylor-Green vortex Ma 0.1,
+      EC + Rusanov, p4 {5,8,14}, 100 steps
+Levels are assigned geometrically (finest cell size along any axis -> level
+1), then widened by make_partition_map's neighbour rule (mesh.cpp:56-71).
+"""
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import perrk as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CONFIG_DIR = os.path.join(ROOT, "configs")
+
+
+# ---------------------------------------------------------------------------
+# initial conditions
+# ---------------------------------------------------------------------------
+@dataclass
+class VortexParams:
+    """physics.hpp:177-185; C1/C2 use I=5 with p_inf = 1 (mach = 1/sqrt(gamma))."""
+    gamma: float = 1.4
+    mach: float = 1.0 / math.sqrt(1.4)
+    radius: float = 1.0
+    intensity: float = 5.0
+    rho_inf: float = 1.0
+    v_inf: tuple = (1.0, 1.0)
+    half_width: float = 10.0
+
+    def as_array(self):
+        return np.array([self.gamma, self.mach, self.radius, self.intensity, self.rho_inf,
+                         self.v_inf[0], self.v_inf[1], self.half_width])
+
+
+def isentropic_vortex(p: VortexParams, x, y, t=0.0):
+    """isentropic_vortex_state, physics.cpp:301-328 (vectorised)."""
+    span = 2.0 * p.half_width
+
+    def wrap(d):
+        d = np.fmod(d + p.half_width, span)
+        d = np.where(d < 0.0, d + span, d)
+        return d - p.half_width
+
+    cx = wrap(x - p.v_inf[0] * t)
+    cy = wrap(y - p.v_inf[1] * t)
+    r2 = cx * cx + cy * cy
+    g = np.exp((1.0 - r2) / (2.0 * p.radius * p.radius))
+    gm1 = p.gamma - 1.0
+    rho = p.rho_inf * np.power(
+        1.0 - p.intensity * p.intensity * p.mach * p.mach * gm1 * g * g / (8.0 * math.pi * math.pi),
+        1.0 / gm1)
+    coef = p.intensity * g / (2.0 * math.pi * p.radius)
+    vx = p.v_inf[0] - coef * cy
+    vy = p.v_inf[1] + coef * cx
+    pres = np.power(rho, p.gamma) / (p.gamma * p.mach * p.mach)
+    return np.stack([rho, rho * vx, rho * vy, pres / gm1 + 0.5 * rho * (vx * vx + vy * vy)])
+
+
+def random_fourier_state(x, y, seed=20250704, modes=8, kmax=4, gamma=1.4, length=2 * math.pi):
+    """C3: each primitive (rho, vx, vy, p) is a sum of `modes` Fourier modes
+    with integer wavenumbers |k| <= kmax (periodic on [0, length)^2), random
+    phases and amplitudes normalised to sum 1, mapped to rho, p in [0.5, 1.5]
+    and v in [-0.5, 0.5].  numpy PCG64 with the given seed."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    fields = []
+    for _ in range(4):
+        k = rng.integers(-kmax, kmax + 1, size=(modes, 2))
+        k[np.all(k == 0, axis=1)] = (1, 0)
+        amp = rng.uniform(0.2, 1.0, size=modes)
+        amp /= amp.sum()
+        ph = rng.uniform(0.0, 2 * math.pi, size=modes)
+        w = 2 * math.pi / length
+        f = np.zeros_like(x)
+        for m in range(modes):
+            f = f + amp[m] * np.cos(w * (k[m, 0] * x + k[m, 1] * y) + ph[m])
+        fields.append(f)  # in [-1, 1]
+    rho = 1.0 + 0.5 * fields[0]
+    vx = 0.5 * fields[1]
+    vy = 0.5 * fields[2]
+    p = 1.0 + 0.5 * fields[3]
+    return np.stack([rho, rho * vx, rho * vy, p / (gamma - 1.0) + 0.5 * rho * (vx * vx + vy * vy)])
+
+
+def taylor_green(x, y, z, mach=0.1, gamma=1.4, rho0=1.0, u0=1.0):
+    """C5: 3D Taylor-Green vortex on [0, 2pi]^3 at Mach `mach`:
+    p0 = rho0 u0^2 / (gamma Ma^2),
+    p  = p0 + rho0 u0^2 / 16 (cos 2x + cos 2y)(cos 2z + 2), rho = rho0."""
+    p0 = rho0 * u0 * u0 / (gamma * mach * mach)
+    vx = u0 * np.sin(x) * np.cos(y) * np.cos(z)
+    vy = -u0 * np.cos(x) * np.sin(y) * np.cos(z)
+    vz = np.zeros_like(x)
+    p = p0 + rho0 * u0 * u0 / 16.0 * (np.cos(2 * x) + np.cos(2 * y)) * (np.cos(2 * z) + 2.0)
+    rho = np.full_like(x, rho0)
+    E = p / (gamma - 1.0) + 0.5 * rho * (vx * vx + vy * vy + vz * vz)
+    return np.stack([rho, rho * vx, rho * vy, rho * vz, E])
+
+
+# ---------------------------------------------------------------------------
+# meshes and levels
+# ---------------------------------------------------------------------------
+def banded_edges(x0, bands):
+    """Edges from (count, size) bands starting at x0 (append_uniform style)."""
+    e = [x0]
+    for n, h in bands:
+        a = e[-1]
+        e.extend(a + h * i for i in range(1, n + 1))
+    return e
+
+
+def axis_levels(bands):
+    """Per-cell level along one axis: finest size -> 1, doubling -> +1."""
+    hmin = min(h for _, h in bands)
+    lv = []
+    for n, h in bands:
+        lv += [1 + int(round(math.log2(h / hmin)))] * n
+    return np.array(lv, dtype=np.int32)
+
+
+def geometric_levels(axis_lv, R):
+    """Cell level = min over axes (a cell thin along any axis is fine)."""
+    if len(axis_lv) == 2:
+        L = np.minimum.outer(axis_lv[1], axis_lv[0])  # [y, x]
+    else:
+        L = np.minimum(np.minimum.outer(axis_lv[2], np.ones_like(axis_lv[1]))[:, :, None],
+                       np.minimum.outer(axis_lv[1], axis_lv[0])[None, :, :])  # [z, y, x]
+    return np.clip(L.reshape(-1), 1, R).astype(np.int32)
+
+
+# ---------------------------------------------------------------------------
+# configurations
+# ---------------------------------------------------------------------------
+@dataclass
+class Config:
+    name: str
+    description: str
+    mesh: object
+    surface_flux: str
+    family: P.PartitionFamily
+    raw_levels: np.ndarray
+    cfl: float
+    steps: int
+    ic: str
+    gamma: float = 1.4
+    relaxation: Optional[P.RelaxationConfig] = field(
+        default_factory=lambda: P.RelaxationConfig(numerics="accurate"))
+    physics: str = "euler"
+    mu: float = 0.0
+    prandtl: float = 0.72
+
+    @property
+    def dim(self):
+        return self.mesh.dim
+
+    def spec(self, device=0):
+        return P.SemidiscretizationSpec(self.mesh, 3, self.gamma, self.physics, self.mu,
+                                        self.prandtl, self.surface_flux, "flux_differencing", "ec",
+                                        device)
+
+    def partition_map(self):
+        return P.make_partition_map(self.mesh, self.raw_levels, self.family.R)
+
+    def initial_state(self, x, y, z=None):
+        if self.ic == "vortex":
+            return isentropic_vortex(VortexParams(), x, y)
+        if self.ic == "random":
+            return random_fourier_state(x, y)
+        if self.ic == "tgv":
+            return taylor_green(x, y, z)
+        raise ValueError(self.ic)
+
+    def nodes_per_cell(self):
+        return 16 if self.dim == 2 else 64
+
+
+def family_path(name):
+    return os.path.join(CONFIG_DIR, f"{name}.family")
+
+
+def load_config_family(name):
+    return P.load_family(family_path(name))
+
+
+def c1_family():
+    return P.build_perk2(4, [4], [[0.2, 0.35]])
+
+
+def make_config(name: str, family=None, cfl=None, steps=None) -> Config:
+    name = name.lower()
+    if name == "c1":
+        mesh = P.build_uniform_mesh2d(10.0, 16)
+        fam = family or c1_family()
+        return Config("c1", "2D Euler isentropic vortex 16^2, p2 S=4, CFL 0.9", mesh, "rusanov",
+                      fam, np.ones(mesh.num_cells(), np.int32), cfl or 0.9, steps or 100,
+                      "vortex")
+    if name == "c2":
+        h = 20.0 / 48.0
+        bands = [(16, h), (32, h / 2), (16, h)]
+        e = banded_edges(-10.0, bands)
+        mesh = P.Mesh2DRect(e, list(e))
+        al = axis_levels(bands)
+        fam = family or load_config_family("c2_p3_4_7")
+        return Config("c2", "2D Euler vortex, 64^2 2-level '+' mesh, p3 {4,7}, HLLE", mesh,
+                      "hlle", fam, geometric_levels([al, al], fam.R), cfl or 0.9, steps or 500,
+                      "vortex")
+    if name == "c3":
+        h = 2 * math.pi / 216.0
+        bands = [(96, h), (16, h / 2), (32, h / 4), (16, h / 2), (96, h)]
+        e = banded_edges(0.0, bands)
+        mesh = P.Mesh2DRect(e, list(e))
+        al = axis_levels(bands)
+        fam = family or load_config_family("c3_p4_5_9_16")
+        return Config("c3", "2D Euler random Fourier state, 256^2 3-level mesh, p4 {5,9,16}",
+                      mesh, "rusanov", fam, geometric_levels([al, al], fam.R), cfl or 0.9,
+                      steps or 200, "random")
+    if name == "c5":
+        h = 2 * math.pi / 54.0
+        bands = [(24, h), (4, h / 2), (8, h / 4), (4, h / 2), (24, h)]
+        e = banded_edges(0.0, bands)
+        mesh = P.Mesh3DRect(e, list(e), list(e))
+        al = axis_levels(bands)
+        fam = family or load_config_family("c5_p4_5_8_14")
+        return Config("c5", "3D Euler Taylor-Green Ma 0.1, 64^3 3-level mesh, p4 {5,8,14}",
+                      mesh, "rusanov", fam, geometric_levels([al, al, al], fam.R), cfl or 0.9,
+                      steps or 100, "tgv")
+    raise ValueError(f"unknown config {name}")
+
+
+def initial_state_for(cfg: Config, semi_or_coords):
+    """U0 in the canonical layout from node coordinates (x, y[, z])."""
+    x, y, z = semi_or_coords
+    vals = cfg.initial_state(x, y, z)
+    return np.ascontiguousarray(vals.T).reshape(-1)
+
+
+def dof_stage_updates_per_step(family: P.PartitionFamily, pmap: P.PartitionMap, npc: int):
+    """Sum over stages of active nodes = rhs_cell_evaluations()/V per step
+    (semidisc.cpp:131-133; PAPER N_K)."""
+    counts = pmap.cells_per_level()
+    total = 0
+    for lvl, n in enumerate(counts, start=1):
+        total += len(family.active_sets[family.member_index_for_level(lvl)]) * n
+    return total * npc
