@@ -30,6 +30,12 @@ __constant__ double c_w[N1];       // LGL weights
 
 constexpr long long kNoBad = LLONG_MAX;
 
+// select from a 3-array with a runtime index without spilling the array
+template <class T>
+__device__ __forceinline__ T pick3(const T (&a)[3], int i) {
+  return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]);
+}
+
 __device__ __forceinline__ void cell_coords(const MeshDev& m, int cell, int& ci, int& cj, int& ck) {
   ci = cell % m.nc[0];
   const int r = cell / m.nc[0];
@@ -58,6 +64,101 @@ __device__ __forceinline__ void report_bad(StepState* st, int stage, long long n
 }
 
 // ---------------------------------------------------------------------------
+// per-line volume term: flux differencing along one LGL line
+// (semidisc.cpp:447-484): endpoint diagonal with the physical flux, the six
+// symmetric pairs with the Ranocha EC flux (physics.cpp:157-179) built from
+// per-node primitives and precomputed logarithms.
+// ---------------------------------------------------------------------------
+template <int DIM, int DIR>
+__device__ __forceinline__ void line_task(const Phys& ph, const double* pe, const double* ue,
+                                          double* vab, int t1, int t2, double J2) {
+  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  int nid[N1];
+#pragma unroll
+  for (int j = 0; j < N1; ++j) nid[j] = line_node<DIM>(DIR, j, t1, t2);
+  double acc[N1][V];
+#pragma unroll
+  for (int j = 0; j < N1; ++j)
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[j][v] = 0.0;
+#pragma unroll
+  for (int j = 0; j < N1; ++j) {
+    const int nl = nid[j];
+    const double dll = c_D[j * N1 + j];
+    if (j == 0 || j == N1 - 1) {  // D_ll != 0 only at the endpoints (basis.cpp:80-81)
+      double f[V];
+      phys_flux<DIM>(ue + nl * V, pe[P_P * NPC + nl], DIR, f);
+      const double cll = J2 * dll;
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[j][v] -= cll * f[v];
+    }
+    const double rl = pe[P_RHO * NPC + nl], pl = pe[P_P * NPC + nl];
+    const double lrl = pe[P_LRHO * NPC + nl], bl = pe[P_BETA * NPC + nl];
+    const double lbl = pe[P_LBETA * NPC + nl];
+    double vl[DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) vl[d] = pe[(P_VX + d) * NPC + nl];
+#pragma unroll
+    for (int k = j + 1; k < N1; ++k) {
+      const int nm = nid[k];
+      const double rr = pe[P_RHO * NPC + nm], prr = pe[P_P * NPC + nm];
+      const double rho_log = logmean_pre(rl, rr, lrl, pe[P_LRHO * NPC + nm]);
+      const double inv_b = inv_logmean_pre(bl, pe[P_BETA * NPC + nm], lbl, pe[P_LBETA * NPC + nm]);
+      double vr[DIM], v_avg[DIM], vl_vr = 0.0;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        vr[d] = pe[(P_VX + d) * NPC + nm];
+        v_avg[d] = 0.5 * (vl[d] + vr[d]);
+        vl_vr += vl[d] * vr[d];
+      }
+      double f[V];
+      const double f_rho = rho_log * v_avg[DIR];
+      f[0] = f_rho;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) f[1 + d] = f_rho * v_avg[d];
+      f[1 + DIR] += 0.5 * (pl + prr);
+      f[DIM + 1] =
+          f_rho * (0.5 * vl_vr + ph.inv_gm1 * inv_b) + 0.5 * (pl * vr[DIR] + prr * vl[DIR]);
+      const double clm = J2 * c_D[j * N1 + k];
+      const double cml = J2 * c_D[k * N1 + j];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        acc[j][v] -= clm * f[v];
+        acc[k][v] -= cml * f[v];
+      }
+    }
+  }
+  double* vad = vab + DIR * NPC * V;
+#pragma unroll
+  for (int j = 0; j < N1; ++j)
+#pragma unroll
+    for (int v = 0; v < V; ++v) vad[nid[j] * V + v] = acc[j][v];
+}
+
+// per-face-point surface term (semidisc.cpp:492-556): numerical flux between
+// the own trace and the neighbour trace, lifted onto the own node as
+// -/+ 2/(h w0) (f* - f(u_own)); stored signed for the combine step.
+template <int DIM, int SURF, int DIR>
+__device__ __forceinline__ void face_task(const Phys& ph, const double* ue, const double* pp,
+                                          const double* un, double* o, int side, int t1, int t2,
+                                          double coef) {
+  constexpr int V = DIM + 2;
+  const int own = line_node<DIM>(DIR, side ? N1 - 1 : 0, t1, t2);
+  const double* uo = ue + own * V;
+  double fs[V], fo[V];
+  if (side)
+    surface_flux<DIM, SURF>(ph, uo, un, DIR, fs);
+  else
+    surface_flux<DIM, SURF>(ph, un, uo, DIR, fs);
+  phys_flux<DIM>(uo, pp[own], DIR, fo);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double c = coef * (fs[v] - fo[v]);
+    o[v] = side ? -c : c;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // stage kernel
 // ---------------------------------------------------------------------------
 
@@ -76,8 +177,17 @@ __global__ void __launch_bounds__(Geo<DIM>::THREADS)
   __shared__ int s_cell[EPB];
   __shared__ int s_coord[EPB][3];
   __shared__ double s_red[2 * 2 * (G::THREADS / 32)];
+  __shared__ double s_a1[MAXR + 1], s_ap[MAXR + 1];
 
   if (st->aborted || st->finished) return;  // uniform across the grid
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q <= MAXR; ++q) {
+      s_a1[q] = a.a1[q];
+      s_ap[q] = a.ap[q];
+    }
+  }
+  __syncthreads();
 
   const int tid = threadIdx.x;
   const int e = tid / NPC, l = tid % NPC;
@@ -105,7 +215,7 @@ __global__ void __launch_bounds__(Geo<DIM>::THREADS)
     double* sue = su + e * NPC * V;
     if (valid) {
       const int lev = m.level[cell];
-      const double a1 = a.a1[lev], ap = a.ap[lev];
+      const double a1 = s_a1[lev], ap = s_ap[lev];
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const int f = l + j * NPC;
@@ -120,14 +230,15 @@ __global__ void __launch_bounds__(Geo<DIM>::THREADS)
       for (int q = l; q < NF * FP; q += NPC) {
         const int face = q / FP, pt = q % FP, dir = face >> 1, side = face & 1;
         const int t1 = pt % N1, t2 = pt / N1;
-        int cc[3] = {ci, cj, ck};
-        const int nd = m.nc[dir];
-        cc[dir] = side ? (cc[dir] + 1 == nd ? 0 : cc[dir] + 1) : (cc[dir] == 0 ? nd - 1 : cc[dir] - 1);
-        const int nbc = cc[0] + m.nc[0] * (cc[1] + m.nc[1] * cc[2]);
+        int c0 = ci, c1 = cj, c2 = ck;
+        int& cd = dir == 0 ? c0 : (dir == 1 ? c1 : c2);
+        const int nd = pick3(m.nc, dir);
+        cd = side ? (cd + 1 == nd ? 0 : cd + 1) : (cd == 0 ? nd - 1 : cd - 1);
+        const int nbc = c0 + m.nc[0] * (c1 + m.nc[1] * c2);
         const int node = line_node<DIM>(dir, side ? 0 : N1 - 1, t1, t2);
         const size_t nbase = (static_cast<size_t>(nbc) * NPC + node) * V;
         const int lev2 = m.level[nbc];
-        const double b1 = a.a1[lev2], bp = a.ap[lev2];
+        const double b1 = s_a1[lev2], bp = s_ap[lev2];
         double un[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -166,98 +277,40 @@ __global__ void __launch_bounds__(Geo<DIM>::THREADS)
     __syncthreads();
 
     // ---- B: volume lines (warps 0..) | surface points (last warps) ----------
+    // dir is dispatched to compile-time constants so the small per-flux
+    // arrays stay in registers
     if (tid < G::LINE_THREADS) {
       const int e2 = tid / G::LINES, li = tid % G::LINES;
       if (s_cell[e2] >= 0) {
         const int dir = li / FP, pt = li % FP;
-        const int t1 = pt % N1, t2 = pt / N1;
-        const double J2 = 2.0 * m.jac[dir][s_coord[e2][dir]];
+        const double J2 = 2.0 * pick3(m.jac, dir)[s_coord[e2][dir]];
         const double* pe = pr + e2 * G::NPR * NPC;
         const double* ue = su + e2 * NPC * V;
-        int nid[N1];
-#pragma unroll
-        for (int j = 0; j < N1; ++j) nid[j] = line_node<DIM>(dir, j, t1, t2);
-        double acc[N1][V];
-#pragma unroll
-        for (int j = 0; j < N1; ++j)
-#pragma unroll
-          for (int v = 0; v < V; ++v) acc[j][v] = 0.0;
-#pragma unroll
-        for (int j = 0; j < N1; ++j) {
-          const int nl = nid[j];
-          const double dll = c_D[j * N1 + j];
-          if (dll != 0.0) {  // diagonal: physical flux at the endpoints
-            double f[V];
-            phys_flux<DIM>(ue + nl * V, pe[P_P * NPC + nl], dir, f);
-            const double cll = J2 * dll;
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc[j][v] -= cll * f[v];
-          }
-          const double rl = pe[P_RHO * NPC + nl], pl = pe[P_P * NPC + nl];
-          const double lrl = pe[P_LRHO * NPC + nl], bl = pe[P_BETA * NPC + nl];
-          const double lbl = pe[P_LBETA * NPC + nl];
-          double vl[DIM];
-#pragma unroll
-          for (int d = 0; d < DIM; ++d) vl[d] = pe[(P_VX + d) * NPC + nl];
-#pragma unroll
-          for (int k = j + 1; k < N1; ++k) {
-            const int nm = nid[k];
-            const double rr = pe[P_RHO * NPC + nm], prr = pe[P_P * NPC + nm];
-            const double rho_log = logmean_pre(rl, rr, lrl, pe[P_LRHO * NPC + nm]);
-            const double inv_b =
-                inv_logmean_pre(bl, pe[P_BETA * NPC + nm], lbl, pe[P_LBETA * NPC + nm]);
-            double vr[DIM], v_avg[DIM], vl_vr = 0.0;
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) {
-              vr[d] = pe[(P_VX + d) * NPC + nm];
-              v_avg[d] = 0.5 * (vl[d] + vr[d]);
-              vl_vr += vl[d] * vr[d];
-            }
-            double f[V];
-            const double f_rho = rho_log * v_avg[dir];
-            f[0] = f_rho;
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) f[1 + d] = f_rho * v_avg[d];
-            f[1 + dir] += 0.5 * (pl + prr);
-            f[DIM + 1] = f_rho * (0.5 * vl_vr + ph.inv_gm1 * inv_b) +
-                         0.5 * (pl * vr[dir] + prr * vl[dir]);
-            const double clm = J2 * c_D[j * N1 + k];
-            const double cml = J2 * c_D[k * N1 + j];
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              acc[j][v] -= clm * f[v];
-              acc[k][v] -= cml * f[v];
-            }
-          }
-        }
-        double* vad = va + (e2 * DIM + dir) * NPC * V;
-#pragma unroll
-        for (int j = 0; j < N1; ++j)
-#pragma unroll
-          for (int v = 0; v < V; ++v) vad[nid[j] * V + v] = acc[j][v];
+        double* vab = va + e2 * DIM * NPC * V;
+        if (dir == 0)
+          line_task<DIM, 0>(ph, pe, ue, vab, pt % N1, pt / N1, J2);
+        else if (dir == 1)
+          line_task<DIM, 1>(ph, pe, ue, vab, pt % N1, pt / N1, J2);
+        else if (DIM == 3)
+          line_task<DIM, DIM == 3 ? 2 : 0>(ph, pe, ue, vab, pt % N1, pt / N1, J2);
       }
     } else {
       for (int q = tid - G::LINE_THREADS; q < G::FACE_TASKS; q += G::FACE_THREADS) {
         const int e2 = q / (NF * FP), r = q % (NF * FP);
         if (s_cell[e2] < 0) continue;
-        const int face = r / FP, pt = r % FP, dir = face >> 1, side = face & 1;
-        const int t1 = pt % N1, t2 = pt / N1;
-        const int own = line_node<DIM>(dir, side ? N1 - 1 : 0, t1, t2);
-        const double* uo = su + e2 * NPC * V + own * V;
+        const int face = r / FP, pt = r % FP, dir = face >> 1;
+        const double coef = pick3(m.lift, dir)[s_coord[e2][dir]];
+        const double* ue = su + e2 * NPC * V;
+        const double* pp = pr + (e2 * G::NPR + P_P) * NPC;
         const double* un = nb + (e2 * NF + face) * FP * V + pt * V;
-        double fs[V], fo[V];
-        if (side)
-          surface_flux<DIM, SURF>(ph, uo, un, dir, fs);
-        else
-          surface_flux<DIM, SURF>(ph, un, uo, dir, fs);
-        phys_flux<DIM>(uo, pr[(e2 * G::NPR + P_P) * NPC + own], dir, fo);
-        const double coef = m.lift[dir][s_coord[e2][dir]];
         double* o = sf + (e2 * NF + face) * FP * V + pt * V;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const double c = coef * (fs[v] - fo[v]);
-          o[v] = side ? -c : c;
-        }
+        if (dir == 0)
+          face_task<DIM, SURF, 0>(ph, ue, pp, un, o, face & 1, pt % N1, pt / N1, coef);
+        else if (dir == 1)
+          face_task<DIM, SURF, 1>(ph, ue, pp, un, o, face & 1, pt % N1, pt / N1, coef);
+        else if (DIM == 3)
+          face_task<DIM, SURF, DIM == 3 ? 2 : 0>(ph, ue, pp, un, o, face & 1, pt % N1, pt / N1,
+                                                 coef);
       }
     }
     __syncthreads();

@@ -1,0 +1,274 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Oracles: `Ref` is the unmodified reference library (dim 2), `Orc` the C
+restatement (dim 2 and 3, accurate relaxation numerics).  Tolerances:
+  RHS / reductions   1e-12 relative to the field's max (FP64 statistical
+                     parity: CUDA libdevice log/sqrt vs glibc, FMA contraction,
+                     log a - log b in the EC flux)
+  states after N steps  1e-11 relative L2 per conserved variable (north_star)
+  gamma sequence, dH    1e-12 absolute (north_star), against the oracle with the
+                        same relaxation numerics
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import max_rel, mesh2d, mesh3d, rel_err, smooth_state
+from paper_2507_04991_b200 import perrk as P
+from paper_2507_04991_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+SURFACES = ["rusanov", "hlle", "hllc", "ec", "central"]
+
+
+def c1_setup():
+    cfg = W.make_config("c1")
+    semi = P.Semidiscretization(cfg.spec())
+    U0 = W.initial_state_for(cfg, (semi.node_x(), semi.node_y(), None))
+    return cfg, semi, U0
+
+
+# --------------------------------------------------------------------------- RHS
+def test_rhs_c1_initial_condition_vs_reference():
+    cfg, semi, U0 = c1_setup()
+    ref = O.Ref(cfg.mesh, surface_flux="rusanov")
+    r_ref = ref.rhs(0.0, U0)
+    r_gpu = semi.rhs(0.0, U0)
+    assert max_rel(r_gpu, r_ref) < 1e-12
+
+
+@pytest.mark.parametrize("surface", SURFACES)
+def test_rhs_2d_random_state_all_surface_fluxes(surface):
+    mesh = mesh2d(9, 7, seed=3)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux=surface))
+    U = smooth_state((semi.node_x(), semi.node_y()), 2, seed=11)
+    ref = O.Ref(mesh, surface_flux=surface)
+    assert max_rel(semi.rhs(0.0, U), ref.rhs(0.0, U)) < 1e-12
+
+
+def test_rhs_masked_matches_reference_and_zero_fill():
+    mesh = mesh2d(8, 8, seed=5)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux="hlle"))
+    U = smooth_state((semi.node_x(), semi.node_y()), 2, seed=2)
+    ref = O.Ref(mesh, surface_flux="hlle")
+    rng = np.random.default_rng(4)
+    for _ in range(3):
+        mask = rng.integers(0, 2, semi.num_cells()).astype(np.int8)
+        g = semi.rhs_masked(0.0, U, mask)
+        r = ref.rhs_masked(0.0, U, mask)
+        assert max_rel(g, r) < 1e-12
+        cellwise = g.reshape(semi.num_cells(), -1)
+        assert np.all(cellwise[mask == 0] == 0.0)
+
+
+def test_partition_restricted_union_equals_full():
+    """test_dg.cpp:302-346 on the device: disjoint supports, union = full."""
+    mesh = mesh2d(10, 6, seed=8)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh))
+    U = smooth_state((semi.node_x(), semi.node_y()), 2, seed=9)
+    levels = np.random.default_rng(1).integers(1, 3, semi.num_cells())
+    pm = P.make_partition_map(mesh, levels, 2)
+    full = semi.rhs(0.0, U)
+    r1 = semi.rhs_partition_restricted(0.0, U, pm, 1)
+    r2 = semi.rhs_partition_restricted(0.0, U, pm, 2)
+    assert np.all((r1 == 0.0) | (r2 == 0.0))
+    assert np.array_equal(r1 + r2, full)
+
+
+def test_free_stream_and_entropy_conservation():
+    """test_dg.cpp:84-102 and :157-172 on the device (EC surface flux)."""
+    mesh = P.Mesh2DRect(*[W.banded_edges(-10, [(4, 3.0), (4, 2.0)])] * 2)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux="ec"))
+    n = semi.num_nodes()
+    U = np.tile([1.0, 1.0, 1.0, 12.16], n)
+    assert np.abs(semi.rhs(0.0, U)).max() < 1e-11
+    U = W.isentropic_vortex(W.VortexParams(mach=0.4, radius=1.5, intensity=13.5),
+                            semi.node_x(), semi.node_y())
+    U = np.ascontiguousarray(U.T).reshape(-1)
+    assert abs(semi.entropy_inner_product(U, semi.rhs(0.0, U))) < 1e-11
+
+
+def test_conservation_of_quadrature_totals():
+    mesh = mesh2d(8, 8, seed=12)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux="hllc"))
+    U = smooth_state((semi.node_x(), semi.node_y()), 2, seed=3)
+    assert np.abs(semi.integral_per_variable(semi.rhs(0.0, U))).max() < 5e-12
+
+
+# --------------------------------------------------------------------------- reductions
+def test_reductions_vs_reference():
+    mesh = mesh2d(12, 10, seed=21)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh))
+    ref = O.Ref(mesh)
+    U = smooth_state((semi.node_x(), semi.node_y()), 2, seed=5)
+    K = smooth_state((semi.node_x(), semi.node_y()), 2, seed=6)
+    assert abs(semi.total_entropy(U) - ref.total_entropy(U)) < 1e-12 * abs(ref.total_entropy(U))
+    ip_ref = ref.entropy_inner_product(U, K)
+    assert abs(semi.entropy_inner_product(U, K) - ip_ref) < 1e-12 * max(1.0, abs(ip_ref))
+    assert np.allclose(semi.integral_per_variable(U), ref.integral_per_variable(U), rtol=1e-13)
+    nu_g, nu_r = semi.characteristic_speed(U), ref.characteristic_speed(U)
+    assert max_rel(nu_g, nu_r) < 1e-14
+    ok, bad = semi.admissible(U)
+    assert ok and bad == -1
+    Ub = U.copy()
+    Ub[(37 * semi.nodes_per_cell() + 3) * 4 + 0] = -1.0
+    Ub[(55 * semi.nodes_per_cell() + 1) * 4 + 3] = 0.0
+    assert semi.admissible(Ub) == ref.admissible(Ub) == (False, 37)
+
+
+# --------------------------------------------------------------------------- stepping
+def test_perk_step_c1_reference_numerics():
+    cfg, semi, U0 = c1_setup()
+    ref = O.Ref(cfg.mesh)
+    dt = ref.compute_dt(U0, False, 0.9)
+    opts = P.PerkStepOptions(relaxation=P.RelaxationConfig())
+    Ug = U0.copy()
+    tg, rg = P.perk_step(Ug, 0.0, dt, cfg.family, cfg.partition_map(), semi, opts)
+    Ur = U0.copy()
+    tr, rr = ref.perk_step(Ur, 0.0, dt, cfg.family, cfg.partition_map().effective_level,
+                           P.RelaxationConfig())
+    assert rel_err(Ug, Ur, 4) < 1e-13
+    assert abs(rg.gamma - rr.gamma) < 1e-12
+    assert abs(rg.delta_h - rr.delta_h) < 1e-12
+    assert rg.fell_back == bool(rr.fell_back)
+    assert abs(tg - tr) < 1e-12 * dt  # t advances by gamma dt
+
+
+def _run_c1(semi, cfg, U0, numerics, steps=100):
+    semi.upload(U0)
+    run_cfg = P.IntegratorConfig(tf=1e9, time=P.TimeControl(fixed=False, ramp=P.CflRamp(0.9, 0.9)),
+                                 relaxation=P.RelaxationConfig(numerics=numerics))
+    t, taken, aborted, recs = P.advance(semi, cfg.family, cfg.partition_map(), run_cfg, 0.0, steps)
+    assert taken == steps and not aborted
+    return semi.download(), recs
+
+
+def test_c1_100_steps_vs_oracle_accurate_relaxation():
+    """BASELINE C1: 100 relaxed P-ERRK steps at CFL 0.9 — state 1e-11 rel L2
+    per variable, gamma sequence and H within 1e-12 of the oracle."""
+    cfg, semi, U0 = c1_setup()
+    Ug, recs = _run_c1(semi, cfg, U0, "accurate")
+    orc = O.Orc(cfg.mesh)
+    Uo = U0.copy()
+    _, taken, log, _ = orc.run_steps(Uo, 0.0, 100, cfg.family, cfg.partition_map().effective_level,
+                                     P.RelaxationConfig(numerics="accurate"), False, 0.9)
+    assert taken == 100
+    assert rel_err(Ug, Uo, 4) < 1e-11
+    gam = np.array([r.gamma for r in recs])
+    assert np.abs(gam - log[:, 2]).max() < 1e-12
+    H = np.array([r.entropy for r in recs])
+    assert np.abs(H - log[:, 4]).max() < 1e-12
+    assert np.abs(np.array([r.t for r in recs]) - log[:, 0]).max() < 1e-11
+
+
+def test_c1_100_steps_vs_unmodified_reference():
+    cfg, semi, U0 = c1_setup()
+    Ug, recs = _run_c1(semi, cfg, U0, "reference")
+    ref = O.Ref(cfg.mesh)
+    Ur = U0.copy()
+    _, taken, log, _ = ref.run_steps(Ur, 0.0, 100, cfg.family, cfg.partition_map().effective_level,
+                                     P.RelaxationConfig(), False, 0.9)
+    assert taken == 100
+    assert rel_err(Ug, Ur, 4) < 1e-11
+    assert np.abs(np.array([r.gamma for r in recs]) - log[:, 2]).max() < 1e-12
+    assert sum(r.fell_back for r in recs) == int(log[:, 5].sum())
+
+
+def _multilevel(mesh, R, seed):
+    rng = np.random.default_rng(seed)
+    return P.make_partition_map(mesh, rng.integers(1, R + 1, mesh.num_cells()), R)
+
+
+@pytest.mark.parametrize("kind", ["p3", "p4"])
+def test_multilevel_steps_2d_vs_reference(kind):
+    """Multirate stage loop (active cell lists, per-level rows, neighbour
+    traces formed with the neighbour's row) against the reference."""
+    mesh = mesh2d(10, 8, seed=31)
+    if kind == "p3":
+        fam = P.build_perk3_variant(7, [4, 7], [[0.3], [0.2, 0.25, 0.3, 0.35]])
+    else:
+        fam = P.build_perk4(14, [5, 8, 14], [[], [0.5] * 3, [0.7] * 9])
+    pm = _multilevel(mesh, fam.R, 3)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux="hlle"))
+    ref = O.Ref(mesh, surface_flux="hlle")
+    U0 = smooth_state((semi.node_x(), semi.node_y()), 2, seed=17, amp=0.2)
+    dt = 0.3 * ref.compute_dt(U0, False, 1.0)
+    Ug, Ur = U0.copy(), U0.copy()
+    for _ in range(5):
+        P.perk_step(Ug, 0.0, dt, fam, pm, semi, P.PerkStepOptions())
+        ref.perk_step(Ur, 0.0, dt, fam, pm.effective_level)
+    assert rel_err(Ug, Ur, 4) < 1e-12
+    semi.reset_evaluation_counter()
+    P.perk_step(Ug, 0.0, dt, fam, pm, semi, P.PerkStepOptions())
+    assert semi.rhs_cell_evaluations() == W.dof_stage_updates_per_step(fam, pm, 16) * 4
+
+
+def test_multilevel_relaxed_accurate_vs_oracle():
+    mesh = mesh2d(10, 8, seed=41)
+    fam = P.build_perk4(14, [5, 8, 14], [[], [0.5] * 3, [0.7] * 9])
+    pm = _multilevel(mesh, fam.R, 5)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh))
+    orc = O.Orc(mesh)
+    U0 = smooth_state((semi.node_x(), semi.node_y()), 2, seed=19, amp=0.3)
+    dt = 0.3 * orc.compute_dt(U0, False, 1.0)
+    rx = P.RelaxationConfig(numerics="accurate")
+    Ug, Uo = U0.copy(), U0.copy()
+    tg = to = 0.0
+    for _ in range(5):
+        tg, rg = P.perk_step(Ug, tg, dt, fam, pm, semi, P.PerkStepOptions(relaxation=rx))
+        to, ro = orc.perk_step(Uo, to, dt, fam, pm.effective_level, rx)
+        assert abs(rg.gamma - ro.gamma) < 1e-12
+        assert abs(rg.delta_h - ro.delta_h) < 1e-12
+        assert not rg.fell_back and not ro.fell_back
+    assert rel_err(Ug, Uo, 4) < 1e-11
+
+
+def test_positivity_abort_leaves_state_untouched():
+    cfg, semi, U0 = c1_setup()
+    ref = O.Ref(cfg.mesh)
+    Ub = U0.copy()
+    Ub[(77 * 16 + 5) * 4 + 0] = -0.5
+    Ug, Ur = Ub.copy(), Ub.copy()
+    tg, rg = P.perk_step(Ug, 1.0, 0.01, cfg.family, cfg.partition_map(), semi, P.PerkStepOptions())
+    tr, rr = ref.perk_step(Ur, 1.0, 0.01, cfg.family, cfg.partition_map().effective_level)
+    assert rg.aborted and rr.aborted
+    assert (rg.bad_cell, rg.bad_stage) == (rr.bad_cell, rr.bad_stage) == (77, 0)
+    assert np.array_equal(Ug, Ub) and tg == 1.0
+
+
+# --------------------------------------------------------------------------- 3D
+def test_rhs_3d_vs_oracle():
+    mesh = mesh3d(5, 4, 3, seed=51)
+    for surface in ["rusanov", "hlle", "ec"]:
+        semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux=surface))
+        orc = O.Orc(mesh, surface_flux=surface)
+        U = smooth_state((semi.node_x(), semi.node_y(), semi.node_z()), 3, seed=23)
+        assert max_rel(semi.rhs(0.0, U), orc.rhs(0.0, U)) < 1e-12
+
+
+def test_3d_multilevel_relaxed_vs_oracle():
+    mesh = mesh3d(4, 5, 4, seed=61)
+    fam = P.build_perk4(14, [5, 8, 14], [[], [0.5] * 3, [0.7] * 9])
+    pm = _multilevel(mesh, 3, 7)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh))
+    orc = O.Orc(mesh)
+    U0 = smooth_state((semi.node_x(), semi.node_y(), semi.node_z()), 3, seed=29, amp=0.25)
+    dt = 0.3 * orc.compute_dt(U0, False, 1.0)
+    rx = P.RelaxationConfig(numerics="accurate")
+    Ug, Uo = U0.copy(), U0.copy()
+    for _ in range(3):
+        _, rg = P.perk_step(Ug, 0.0, dt, fam, pm, semi, P.PerkStepOptions(relaxation=rx))
+        _, ro = orc.perk_step(Uo, 0.0, dt, fam, pm.effective_level, rx)
+        assert abs(rg.gamma - ro.gamma) < 1e-12
+    assert rel_err(Ug, Uo, 5) < 1e-11
+
+
+def test_tgv_initial_rhs_3d_vs_oracle():
+    mesh = P.build_uniform_mesh3d(0.0, 2 * math.pi, 4)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh))
+    orc = O.Orc(mesh)
+    U = np.ascontiguousarray(W.taylor_green(semi.node_x(), semi.node_y(), semi.node_z()).T).reshape(-1)
+    assert max_rel(semi.rhs(0.0, U), orc.rhs(0.0, U)) < 1e-12
