@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""bench.py — P-ERRK DOF-stage updates/s (FP64) of the B200 hot path.
+
+Workload (BASELINE.json configs[4], the config the metric is quoted on at
+1/2/4/8 GPUs; it fits one GPU): 3D compressible Euler Taylor-Green vortex,
+Mach 0.1 on [0,2pi]^3, 3-level graded 64^3-element mesh (16.8M LGL nodes at
+polydeg 3), Ranocha EC volume flux + Rusanov surface flux, P-ERRK order 4 with
+stage families {5,8,14}, Newton relaxation on (accurate numerics), CFL step
+size recomputed on the device every step.  Synthetic, seeded (no dataset).
+
+A "step" is one full perk_step (stepper.cpp:17-114) of that workload plus the
+run() bookkeeping (compute_dt, StepRecord H/invariants).  One DOF-stage update
+= one node advanced through one active stage (= rhs_cell_evaluations()/V,
+semidisc.cpp:131-133).
+
+  value  device-resident run: CUDA events around K steps on the library's
+         stream (set to torch's current stream), max over ranks.
+  e2e    the reference-facing call perrk_perk_step with HOST (pinned) buffers:
+         upload of U, the step, download of U — every step.
+  roofline  the dominant kernel (stage_kernel): compulsory bytes / event-timed
+         device time of its launches, against the measured HBM copy peak; an
+         fp64 block gives its algorithmic FP64 rate against a measured DFMA peak.
+  cpu_baseline  the CPU oracle port (oracle/perrk_oracle.c; the reference
+         itself is 2D-only) on a bounded sample of the same workload.
+
+`--impl reference` times the reference CPU implementation of the path (the
+oracle port for 3D, since the reference has no 3D) on the host cores.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "P-ERRK DOF-stage updates/sec (FP64)"
+UNIT = "DOF-stage/s"
+FLOPS_PER_DOF_STAGE = {3: 380.0, 2: 250.0}  # SURVEY.md 8d counting rule (+,-,*,/,sqrt); logs apart
+LOGS_PER_DOF_STAGE = {3: 9.0, 2: 6.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="perrk", choices=["perrk", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.close()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        power = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        loaded = [s for s, p in zip(sm, power) if p > 0.4 * max(power)] if power else sm
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4)
+                          if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(loaded or sm), "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(power) if power else None}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+def traffic_fixture(config):
+    """dram bytes per stage-kernel launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return d.get(config)
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm: the oracle port on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_sample(config, threads):
+    import oracle as O  # checker library; only bench's cpu/reference legs use it
+    from paper_2507_04991_b200 import workloads as W
+    cfg = W.make_config(config)
+    sample = W.sample_config(cfg)
+    orc = O.Orc(sample.mesh, surface_flux=sample.surface_flux, threads=threads)
+    x, y, z, _ = orc.node_coords()
+    U0 = W.initial_state_for(sample, (x, y, z))
+    pm = sample.partition_map()
+    per_step = W.dof_stage_updates_per_step(sample.family, pm, sample.nodes_per_cell())
+    return sample, orc, U0, pm, per_step
+
+
+def run_cpu(config, threads, seconds=None, steps=None, warmup=0):
+    sample, orc, U0, pm, per_step = cpu_sample(config, threads)
+    U = U0.copy()
+    t = 0.0
+    if warmup:
+        t, _, _, _ = orc.run_steps(U, t, warmup, sample.family, pm.effective_level,
+                                   sample.relaxation, False, sample.cfl, records=False)
+    if steps is None:  # calibrate to the time budget
+        t, n1, _, s1 = orc.run_steps(U, t, 1, sample.family, pm.effective_level,
+                                     sample.relaxation, False, sample.cfl, records=False)
+        steps = max(1, int(seconds / max(s1, 1e-6)) - 1)
+        tot_steps, tot_s = n1, s1
+    else:
+        tot_steps, tot_s = 0, 0.0
+    t, n, _, secs = orc.run_steps(U, t, steps, sample.family, pm.effective_level,
+                                  sample.relaxation, False, sample.cfl, records=False)
+    tot_steps += n
+    tot_s += secs
+    desc = (f"oracle port (perrk_oracle.c, -O3 -ffp-contract=off, {threads} threads) on "
+            f"{sample.description}: {tot_steps} steps, {per_step} DOF-stage/step")
+    return per_step * tot_steps / tot_s, tot_steps, tot_s, desc
+
+
+def reference_arm(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    value, steps, secs, desc = run_cpu(args.config, threads, steps=args.steps,
+                                       warmup=args.warmup)
+    from paper_2507_04991_b200 import workloads as W
+    cfg = W.make_config(args.config)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / max(steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.description, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the B200 path
+# ---------------------------------------------------------------------------
+def perrk_arm(args):
+    import torch
+    from paper_2507_04991_b200 import perrk as P
+    from paper_2507_04991_b200 import workloads as W
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = W.make_config(args.config)
+    run = W.ConfigRun(cfg, device=local, rank=rank, world=world)
+    semi, fam, pm = run.semi, cfg.family, run.pmap
+    stream = torch.cuda.current_stream()
+    semi.set_stream(stream.cuda_stream)
+    U0 = run.initial_state()
+    semi.upload(U0)
+    per_step = run.dof_stage_updates_per_step()
+    rc = P.IntegratorConfig(tf=1e30, time=P.TimeControl(False, 0.0, P.CflRamp(cfg.cfl, cfg.cfl)),
+                            relaxation=cfg.relaxation)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # warm-up
+    t, taken, aborted, _ = P.advance(semi, fam, pm, rc, 0.0, args.warmup, records=False)
+    if aborted or taken != args.warmup:
+        raise RuntimeError(f"warm-up aborted after {taken} steps")
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    semi.profile(True)
+    l0 = semi.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    t, taken, aborted, recs = P.advance(semi, fam, pm, rc, t, args.steps, records=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = semi.launch_count() - l0
+    stage_ms, stage_launches, stage_bytes = semi.profile_read()
+    semi.profile(False)
+    clk = clocks.stop()
+    if aborted or taken != args.steps:
+        raise RuntimeError(f"timed run aborted after {taken} steps")
+    if world > 1:
+        import torch.distributed as dist
+        m = torch.tensor([ms], device="cuda")
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        ms = float(m.item())
+        tot = torch.tensor([float(per_step)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tot)
+        total_per_step = float(tot.item())
+    else:
+        total_per_step = float(per_step)
+    value = total_per_step * args.steps / (ms * 1e-3)
+    gammas = [r.gamma for r in recs]
+    fell_back = sum(int(r.fell_back) for r in recs)
+
+    # ---- e2e through the reference-facing call with host buffers ----------
+    e2e = None
+    if not args.no_e2e:
+        Uh = torch.empty(U0.size, dtype=torch.float64, pin_memory=True).numpy()
+        Uh[:] = semi.download()
+        dt = P.compute_dt(Uh, semi, rc, t)
+        opts = P.PerkStepOptions(relaxation=cfg.relaxation)
+        te = t
+        # one untimed call (first-call costs), then the timed ones
+        te, r = P.perk_step(Uh, te, dt, fam, pm, semi, opts)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            te, r = P.perk_step(Uh, te, dt, fam, pm, semi, opts)
+            if r.aborted:
+                raise RuntimeError("e2e step aborted")
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        wall = time.perf_counter() - w0
+        if world > 1:
+            import torch.distributed as dist
+            m = torch.tensor([ems], device="cuda")
+            dist.all_reduce(m, op=dist.ReduceOp.MAX)
+            ems = float(m.item())
+        e2e = {"value": total_per_step * args.steps / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(Uh.nbytes), "d2h_bytes_per_step": int(Uh.nbytes),
+               "ms_per_step": ems / args.steps, "wall_ms_per_step": 1e3 * wall / args.steps,
+               "path": "perrk_perk_step (include/perrk_b200.h) with pinned host U"}
+
+    # ---- roofline of the dominant kernel ------------------------------------
+    hbm, hbm_kind = peaks()
+    achieved = (stage_bytes / stage_launches) / ((stage_ms / stage_launches) * 1e-3) / 1e9
+    traffic = traffic_fixture(args.config)
+    fp64_peak = P.fp64_peak(local)
+    dof_stage_per_launch = per_step / len([p for p in range(fam.S)])
+    flops = FLOPS_PER_DOF_STAGE[cfg.dim] * per_step * args.steps
+    fp64_achieved = flops / (stage_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic,
+                "kernel": "stage_kernel<3,2> (volume + surface + lift + stage formation)",
+                "peak_kind": f"{hbm_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                "stage_kernel_share": stage_ms / ms,
+                "launches": stage_launches, "ms_per_launch": stage_ms / stage_launches,
+                "algorithmic_bytes_per_launch": stage_bytes / stage_launches,
+                "fp64": {"achieved_gflops": fp64_achieved, "peak_gflops": fp64_peak,
+                         "frac": fp64_achieved / fp64_peak,
+                         "flops_per_dof_stage": FLOPS_PER_DOF_STAGE[cfg.dim],
+                         "logs_per_dof_stage_not_counted": LOGS_PER_DOF_STAGE[cfg.dim],
+                         "peak_kind": "measured DFMA loop (perrk_fp64_peak)"}}
+    del dof_stage_per_launch
+
+    # ---- CPU baseline (rank 0, N = 1) ----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, n, s, desc = run_cpu(args.config, threads, seconds=args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.description, "nodes": int(run.total_nodes()),
+                       "dof_stage_per_step": int(total_per_step), "cfl": cfg.cfl,
+                       "family": f"{fam.kind} S={fam.S} E={fam.E}",
+                       "relaxation": "newton, accurate numerics (SURVEY 7.3 H1)",
+                       "l2": "inputs larger than L2 (state 5 x 640 MiB)",
+                       "parallelism": f"slab{world}" if world > 1 else "single"},
+            "gpu_launches": int(launches), "e2e": e2e, "roofline": roofline,
+            "cpu_baseline": cpu, "clocks": clk,
+            "run": {"gamma_min": min(gammas), "gamma_max": max(gammas), "fell_back": fell_back,
+                    "t_end": t},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        perrk_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,242 @@
+"""Generate the frozen P-ERK family fixtures of BASELINE configs C2-C5.
+
+BASELINE.json names the stage families ({4,7}, {5,9,16}, {4,8}, {5,8,14})
+but no free coefficients, and the reference's generator (specopt.cpp:554-594)
+needs Eigen, which is absent.  This script fixes them
+once, offline, by the same principle as the reference's optimiser: for each
+member, choose the free subdiagonals (butcher.cpp:51-105) that maximise the
+stable step on a model spectrum, subject to the archetype's sign constraints
+(butcher.cpp:89-104).  The output is the reference's family text format
+(butcher.cpp:334-355), consumed identically by the GPU path and the oracle.
+
+Model spectrum.  Bloch spectrum of the k=3 LGL DGSEM operator for
+u_t + u_x = 0 with upwind interface flux (what Rusanov/HLL reduce to for a
+single wave), h = 1, a = 1; in d dimensions the tensor-product operator's
+eigenvalues are sums of d 1D eigenvalues (worst case: a wave along the
+diagonal).  With the reference's dt = CFL / nu, nu = (k+1) max lambda/h
+(mesh.cpp:97-129, stepper.cpp:116-127), a cell of level r (h = 2^(r-1) h_min)
+sees z = CFL / (k+1) / 2^(r-1) * mu.  A family is stable at CFL if every
+member's |P(z)| <= 1 on the boundary of its (convex hull of the) spectrum
+(maximum modulus principle).
+
+Usage:  python configs/make_families.py   (rewrites configs/*.family)
+"""
+import os
+import sys
+
+import numpy as np
+from scipy.optimize import minimize
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+
+from paper_2507_04991_b200 import perrk as P  # noqa: E402  (host-only helpers)
+
+K = 3
+
+
+def gll(k=K):
+    x = np.polynomial.legendre.Legendre.basis(k).deriv().roots()
+    x = np.concatenate([[-1.0], np.sort(x), [1.0]])
+    Pk = np.polynomial.legendre.Legendre.basis(k)(x)
+    w = 2.0 / (k * (k + 1) * Pk ** 2)
+    n = k + 1
+    D = np.zeros((n, n))
+    for i in range(n):
+        for j in range(n):
+            if i != j:
+                D[i, j] = Pk[i] / (Pk[j] * (x[i] - x[j]))
+    D[0, 0] = -k * (k + 1) / 4.0
+    D[-1, -1] = k * (k + 1) / 4.0
+    return x, w, D
+
+
+def spectrum_1d(nth=96):
+    """Eigenvalues of the 1D upwind DGSEM operator (h = 1, a = 1)."""
+    _, w, D = gll()
+    n = K + 1
+    out = []
+    for th in np.linspace(0.0, 2 * np.pi, nth, endpoint=False):
+        L = -2.0 * D.astype(complex)
+        # left face: f* = u_{i-1}(N) = e^{-i th} u_i(N); strong-form correction
+        L[0, 0] += -2.0 / w[0]
+        L[0, n - 1] += 2.0 / w[0] * np.exp(-1j * th)
+        out.append(np.linalg.eigvals(L))
+    return np.concatenate(out)
+
+
+def hull(points):
+    from scipy.spatial import ConvexHull
+    xy = np.column_stack([points.real, points.imag])
+    h = ConvexHull(xy)
+    v = points[h.vertices]
+    return v
+
+
+def boundary_samples(verts, per_edge=24):
+    pts = []
+    m = len(verts)
+    for i in range(m):
+        a, b = verts[i], verts[(i + 1) % m]
+        t = np.linspace(0.0, 1.0, per_edge, endpoint=False)
+        pts.append(a + (b - a) * t)
+    return np.concatenate(pts)
+
+
+def model_boundary(dim):
+    v1 = hull(spectrum_1d())
+    v = v1
+    for _ in range(dim - 1):
+        v = hull((v[:, None] + v1[None, :]).reshape(-1))
+    return boundary_samples(v)
+
+
+def stability_poly(A, b):
+    """Monomial coefficients alpha_j (P(z) = sum alpha_j z^j) of a tableau."""
+    S = len(b)
+    alpha = [1.0]
+    v = np.ones(S)
+    for _ in range(S):
+        alpha.append(float(b @ v))
+        v = A @ v
+    return np.array(alpha)
+
+
+TOL = 1e-3  # per-step growth tolerated on the hull boundary: near the origin
+# the hull hugs the imaginary axis, where even-order polynomials sit at
+# |P| = 1 + O(|z|^(p+2)) although the true (dissipative) modes decay
+
+
+def max_scale(alpha, zb, lo=0.0, hi=400.0):
+    """Largest s with |P(s z)| <= 1 + TOL for z on the spectrum boundary."""
+    coeffs = alpha[::-1]
+
+    def ok(s):
+        return np.all(np.abs(np.polyval(coeffs, s * zb)) <= 1.0 + TOL)
+
+    # grow from below: the stable set in s may not be an interval
+    s, step = 0.0, 0.01
+    while s + step < hi and ok(s + step):
+        s += step
+    lo, hi = s, s + step
+    for _ in range(40):
+        mid = 0.5 * (lo + hi)
+        if ok(mid):
+            lo = mid
+        else:
+            hi = mid
+    return lo
+
+
+def member_poly(kind, S, E, theta, c_sm3=1.0):
+    if E == S:
+        fam = P.build_family(kind, S, [E], [list(theta)], c_sm3)
+    else:  # the host builder wants the E = S member present; a placeholder
+        top = [0.5 * b for _, b in theta_bounds(kind, S, S)]
+        fam = P.build_family(kind, S, [E, S], [list(theta), top], c_sm3)
+    return stability_poly(fam.A[0], fam.b)
+
+
+def abscissae(kind, S, c_sm3=1.0):
+    """default_abscissae (butcher.cpp:175-199)."""
+    c = np.zeros(S)
+    if kind == "p2":
+        c[1:] = np.arange(1, S) / (2.0 * (S - 1))
+    elif kind in ("p3", "p3-original"):
+        c[1:S - 2] = np.arange(1, S - 2) / (S - 3)
+        c[S - 2] = 1.0 if kind == "p3" else 1.0 / 3.0
+        c[S - 1] = 0.5 if kind == "p3" else 1.0
+    else:
+        r = np.sqrt(3.0) / 6.0
+        c[1:S - 4] = 1.0
+        c[S - 4] = c_sm3
+        c[S - 3:] = [0.479274057836310, 0.5 + r, 0.5 - r]
+    return c
+
+
+def theta_bounds(kind, S, E):
+    """Free subdiagonal a_{i,i-1} in (0, c_i] keeps a_{i,1} = c_i - a >= 0
+    (butcher.cpp:89-104) and the stage chain connected."""
+    c = abscissae(kind, S)
+    lo_row = S - E + 2
+    n = P.free_coefficient_count(kind, E)
+    return [(1e-6, float(c[lo_row + j])) for j in range(n)]
+
+
+def optimise_member(kind, S, E, zb, rng=None):
+    """Maximise the member's stable scale s over its free subdiagonals:
+    bisection on s, each trial a bounded least-squares feasibility solve of
+    max(|P_theta(s z)| - 1, 0) = 0 over the spectrum boundary, warm-started
+    from the last feasible theta (several random starts at the first)."""
+    from scipy.optimize import least_squares
+    n = P.free_coefficient_count(kind, E)
+    if n == 0:
+        return [], max_scale(member_poly(kind, S, E, []), zb)
+    bounds = theta_bounds(kind, S, E)
+    lo_b = np.array([b[0] for b in bounds])
+    hi_b = np.array([b[1] for b in bounds])
+    rng = rng or np.random.default_rng(12345)
+
+    def excess(theta, s):
+        try:
+            a = member_poly(kind, S, E, np.clip(theta, lo_b, hi_b))
+        except Exception:
+            return np.full(zb.size, 10.0)
+        return np.maximum(np.abs(np.polyval(a[::-1], s * zb)) - 1.0 - 0.5 * TOL, 0.0)
+
+    def solve(theta0, s):
+        r = least_squares(excess, theta0, args=(s,), bounds=(lo_b, hi_b), xtol=1e-12,
+                          ftol=1e-12, gtol=1e-12, max_nfev=200 * n)
+        th = np.clip(r.x, lo_b, hi_b)
+        return th, max_scale(member_poly(kind, S, E, th), zb)
+
+    starts = [0.5 * hi_b] + [rng.uniform(0.05, 0.95, n) * hi_b for _ in range(5)]
+    best_th, best_s = None, -1.0
+    for th0 in starts:
+        th, sc = solve(th0, 0.1 * E / 4)  # a modest target to find the basin
+        if sc > best_s:
+            best_th, best_s = th, sc
+    lo, hi = best_s, 3.0 * best_s + 1.0
+    for _ in range(14):
+        mid = 0.5 * (lo + hi)
+        th, sc = solve(best_th, mid)
+        if sc > best_s:
+            best_th, best_s = th, sc
+        if sc >= mid * (1 - 1e-3):
+            lo = max(lo, sc)
+        else:
+            hi = mid
+    return [float(x) for x in best_th], best_s
+
+
+def design(name, kind, S, Es, dim):
+    zb = model_boundary(dim)
+    free, scales = [], []
+    for E in Es:
+        th, s = optimise_member(kind, S, E, zb)
+        free.append(th)
+        scales.append(s)
+    fam = P.build_family(kind, S, list(Es), free)
+    R = len(Es)
+    # member r (E ascending) serves level R - r; level l has h = 2^(l-1) h_min
+    cfl = min(scales[r] * (K + 1) * 2 ** (R - r - 1) for r in range(R))
+    fam.dt_max = [scales[r] * (K + 1) for r in range(R)]
+    path = os.path.join(HERE, f"{name}.family")
+    P.save_family(fam, path)
+    print(f"{name}: kind {kind} S={S} E={Es} member CFL limits "
+          f"{[round(s * (K + 1), 3) for s in scales]} -> family CFL limit {cfl:.3f}")
+    return fam, cfl
+
+
+FAMILIES = [
+    ("c2_p3_4_7", "p3", 7, [4, 7], 2),
+    ("c3_p4_5_9_16", "p4", 16, [5, 9, 16], 2),
+    ("c4_p3_4_8", "p3", 8, [4, 8], 2),
+    ("c5_p4_5_8_14", "p4", 14, [5, 8, 14], 3),
+]
+
+if __name__ == "__main__":
+    only = set(sys.argv[1:])
+    for args in FAMILIES:
+        if not only or args[0] in only:
+            design(*args)

@@ -212,6 +212,24 @@ int perrk_assign_levels(const double* nu, int64_t n, int R, int* levels);
 /* make_partition_map (mesh.cpp:56-71) on a periodic rectilinear mesh */
 int perrk_make_partition_map(int dim, const int* ncells, const int* levels, int R, int* effective);
 
+/* ---- instrumentation (bench.py / profiling; no reference counterpart) ---
+ * set_stream: order the context's work on a caller stream (e.g. torch's
+ * current stream, so CUDA events recorded there bracket it); NULL restores a
+ * private stream.  profile: start (1, resets) / stop (0) recording an event
+ * pair around every stage-kernel launch; profile_read returns their summed
+ * device time, count and compulsory bytes.  launch_count: kernels launched
+ * by the context so far.  step_traffic: compulsory HBM bytes of one step's
+ * stage launches, of one relaxation pass and of the final update.
+ * fp64_peak: DFMA-loop FP64 throughput of the device (GFLOP/s). */
+int perrk_set_stream(perrk_ctx* ctx, void* cuda_stream);
+int perrk_profile(perrk_ctx* ctx, int enable);
+int perrk_profile_read(perrk_ctx* ctx, double* stage_ms, int64_t* stage_launches,
+                       double* stage_bytes);
+int perrk_launch_count(const perrk_ctx* ctx, int64_t* launches);
+int perrk_step_traffic(const perrk_ctx* ctx, double* stage_bytes, double* pass_bytes,
+                       double* update_bytes);
+int perrk_fp64_peak(int device, double* gflops);
+
 /* ---- multi-GPU: element-slab decomposition over NCCL --------------------
  * nccl_id: the 128-byte ncclUniqueId from rank 0 (broadcast by the caller,
  * e.g. through torch.distributed).  After this call the context owns the

@@ -98,6 +98,12 @@ _PROTOS = {
                                      _I]),
     "perrk_assign_levels": (C.c_int, [_D, C.c_int64, C.c_int, _I]),
     "perrk_make_partition_map": (C.c_int, [C.c_int, _I, _I, C.c_int, _I]),
+    "perrk_set_stream": (C.c_int, [_P, C.c_void_p]),
+    "perrk_profile": (C.c_int, [_P, C.c_int]),
+    "perrk_profile_read": (C.c_int, [_P, _D, C.POINTER(C.c_int64), _D]),
+    "perrk_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "perrk_step_traffic": (C.c_int, [_P, _D, _D, _D]),
+    "perrk_fp64_peak": (C.c_int, [C.c_int, _D]),
     "perrk_comm_init": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int]),
     "perrk_slab_range": (C.c_int, [_P, _I, _I]),
 }

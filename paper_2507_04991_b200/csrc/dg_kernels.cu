@@ -801,9 +801,52 @@ static cudaError_t launch_stage_d(int surf, const StageArgs& a, const MeshDev& m
   return cudaErrorInvalidValue;
 }
 
+// FP64 peak probe: 8 independent DFMA chains per thread (the FP64 pipe's
+// latency is hidden by chains x resident warps); one store keeps it live.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters, double a,
+                                                         double b) {
+  double x[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) x[q] = threadIdx.x * 1e-3 + q;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = fma(x[q], a, b);
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += x[q];
+  if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace dev
 
 using namespace dev;
+
+double measure_fp64_peak() {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  double* out = nullptr;
+  cudaMalloc(&out, sizeof(double));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, iters = 4096;
+  dfma_probe_kernel<<<blocks, 256>>>(out, iters, 0.999999, 1e-7);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    dfma_probe_kernel<<<blocks, 256>>>(out, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double flops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * 256.0;
+  return flops / (best * 1e-3) / 1e9;
+}
 
 cudaError_t upload_basis(const double* D, const double* w) {
   cudaError_t e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * N1 * N1);

@@ -29,6 +29,7 @@ struct StageArgs {
   long long ncells;
 };
 
+double measure_fp64_peak();  // GFLOP/s on the current device (DFMA loop)
 cudaError_t upload_basis(const double* D, const double* w);
 size_t stage_smem_bytes(int dim);
 int stage_cells_per_block(int dim);

@@ -237,6 +237,7 @@ void build_member(int kind, int S, int E, const double* fr, const std::vector<do
 struct StagePlan {
   int* dlist = nullptr;  // nullptr: all cells
   int n = 0;
+  double bytes = 0.0;    // compulsory HBM bytes of the launch (roofline)
   StageArgs args{};
   int kin = -1, kout = -1;  // buffer ids: 0 K1, 1 Ka, 2 Kb
 };
@@ -280,6 +281,13 @@ struct perrk_ctx {
   std::vector<int> E, eff;
   std::vector<StagePlan> plan;
   uint64_t evals = 0;
+  // instrumentation: launch counter and per-stage-launch event pairs
+  bool own_stream = true;
+  int64_t launches = 0;
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<double> ev_bytes;
 
   dev::MeshDev mesh() const {
     dev::MeshDev m{};
@@ -386,6 +394,20 @@ void build_plan(perrk_ctx* c) {
     a.ncells = c->ncells;
     a.list = p.dlist;
     a.n = p.n;
+    // compulsory traffic per active cell, in node-vectors of 8V bytes:
+    // read U (+K1 when the state is formed, +K_{i-1} on chain rows),
+    // write K_i, and d (write at the first b-stage, read-modify-write after)
+    double vecs = 0.0;
+    for (long long cell = 0; cell < c->ncells; ++cell) {
+      const int lv = c->eff[cell];
+      if (!(i == 0 || active[lv - 1][i])) continue;
+      double v = 1.0;
+      if (a.form) v += 1.0 + (a.ap[lv] != 0.0 ? 1.0 : 0.0);
+      if (a.write_k) v += 1.0;
+      v += a.d_mode == 1 ? 1.0 : (a.d_mode == 2 ? 2.0 : 0.0);
+      vecs += v;
+    }
+    p.bytes = vecs * c->npc * c->V * 8.0;
     c->plan.push_back(p);
   }
 }
@@ -411,9 +433,28 @@ void enqueue_step(perrk_ctx* c, const StepMode& mode, bool want_h) {
     a.Kout = c->kbuf(p.kout);
     a.d = c->d;
     a.want_h = (i == 0 && want_h) ? 1 : 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->profiling) {
+      if (c->ev_used + 2 > c->ev_pool.size()) {
+        for (int q = 0; q < 64; ++q) {
+          cudaEvent_t ev;
+          CK(cudaEventCreate(&ev));
+          c->ev_pool.push_back(ev);
+        }
+      }
+      e0 = c->ev_pool[c->ev_used++];
+      e1 = c->ev_pool[c->ev_used++];
+      c->ev_bytes.push_back(p.bytes);
+      CK(cudaEventRecord(e0, c->stream));
+    }
     CK(launch_stage(c->dim, c->surface, a, m, c->ph, c->st, c->partials, c->counter,
                     c->grid_stage, c->stream));
+    if (c->profiling) CK(cudaEventRecord(e1, c->stream));
+    c->launches += p.n > 0 ? 1 : 0;
   }
+  c->launches += 2 + (mode.relax ? (mode.cfg.numerics == 1 ? mode.cfg.max_iter
+                                                           : mode.cfg.max_iter + 1)
+                                 : 0);
   if (mode.relax) {
     const int passes = mode.cfg.numerics == 1 ? mode.cfg.max_iter : mode.cfg.max_iter + 1;
     for (int p = 0; p < passes; ++p)
@@ -605,7 +646,8 @@ int perrk_destroy(perrk_ctx* c) {
   if (c->counter) cudaFree(c->counter);
   if (c->dint) cudaFree(c->dint);
   if (c->dlist_tmp) cudaFree(c->dlist_tmp);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return PERRK_OK;
 }
@@ -900,8 +942,10 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
     mode.want_nu = !cfg->fixed_dt;
     mode.want_record = rec;
     mode.records = rec ? c->records : nullptr;
-    if (!cfg->fixed_dt)
+    if (!cfg->fixed_dt) {
       CK(launch_numax(c->dim, c->U, c->mesh(), c->ph, c->st, c->nnodes, c->grid_flat, c->stream));
+      c->launches += 1;
+    }
     const bool want_h = needs_h(mode.relax, cfg->relax, s.h_ref);
     for (int k = 0; k < nsteps; ++k) enqueue_step(c, mode, want_h);
     const StepState r = get_state(c);
@@ -1025,6 +1069,79 @@ int perrk_make_partition_map(int dim, const int* n, const int* levels, int R, in
           }
           eff[cell] = lv;
         }
+  });
+}
+
+int perrk_set_stream(perrk_ctx* c, void* stream) {
+  return guarded([&] {
+    REQUIRE(c, "null context");
+    set_device(c);
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->own_stream) CK(cudaStreamDestroy(c->stream));
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+      c->own_stream = false;
+    } else {
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+  });
+}
+
+int perrk_profile(perrk_ctx* c, int enable) {
+  return guarded([&] {
+    REQUIRE(c, "null context");
+    c->profiling = enable != 0;
+    c->ev_used = 0;
+    c->ev_bytes.clear();
+  });
+}
+
+int perrk_profile_read(perrk_ctx* c, double* stage_ms, int64_t* stage_launches,
+                       double* stage_bytes) {
+  return guarded([&] {
+    REQUIRE(c, "null context");
+    set_device(c);
+    CK(cudaStreamSynchronize(c->stream));
+    double ms = 0.0, bytes = 0.0;
+    int64_t n = 0;
+    for (size_t q = 0; q + 1 < c->ev_used; q += 2) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, c->ev_pool[q], c->ev_pool[q + 1]));
+      ms += t;
+      bytes += c->ev_bytes[q / 2];
+      ++n;
+    }
+    if (stage_ms) *stage_ms = ms;
+    if (stage_launches) *stage_launches = n;
+    if (stage_bytes) *stage_bytes = bytes;
+  });
+}
+
+int perrk_launch_count(const perrk_ctx* c, int64_t* out) {
+  return guarded([&] {
+    REQUIRE(c && out, "null argument");
+    *out = c->launches;
+  });
+}
+
+int perrk_step_traffic(const perrk_ctx* c, double* stage_bytes, double* pass_bytes,
+                       double* update_bytes) {
+  return guarded([&] {
+    REQUIRE(c, "null context");
+    double s = 0.0;
+    for (const auto& p : c->plan) s += p.bytes;
+    if (stage_bytes) *stage_bytes = s;
+    if (pass_bytes) *pass_bytes = 16.0 * c->V * c->nnodes;    // read U, d
+    if (update_bytes) *update_bytes = 24.0 * c->V * c->nnodes;  // read U, d; write U
+  });
+}
+
+int perrk_fp64_peak(int device, double* gflops) {
+  return guarded([&] {
+    REQUIRE(gflops, "null argument");
+    CK(cudaSetDevice(device));
+    *gflops = measure_fp64_peak();
   });
 }
 

@@ -293,6 +293,34 @@ class Semidiscretization:
     def sync(self):
         check(lib().perrk_sync(self._h))
 
+    # instrumentation (perrk_set_stream / perrk_profile*, include/perrk_b200.h)
+    def set_stream(self, cuda_stream):
+        """Order this context's work on a caller CUDA stream (int handle, 0/None:
+        back to a private stream)."""
+        check(lib().perrk_set_stream(self._h, C.c_void_p(cuda_stream or None)))
+
+    def profile(self, enable=True):
+        check(lib().perrk_profile(self._h, int(enable)))
+
+    def profile_read(self):
+        """(stage-kernel ms, stage launches, stage compulsory bytes) since profile(True)."""
+        ms, n, b = C.c_double(), C.c_int64(), C.c_double()
+        check(lib().perrk_profile_read(self._h, C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value, b.value
+
+    def launch_count(self):
+        n = C.c_int64()
+        check(lib().perrk_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def step_traffic(self, family, pmap):
+        """Compulsory HBM bytes: (stage launches of one step, one relaxation
+        pass, final update)."""
+        self._use_family(family, pmap)
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        check(lib().perrk_step_traffic(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
     def _use_family(self, family, pmap):
         key = (id(family), id(pmap), family.version, pmap.version)
         if key == self._family_key:
@@ -307,6 +335,13 @@ class Semidiscretization:
                              _dp(c))
         check(lib().perrk_set_family(self._h, C.byref(fd), _ip(eff)))
         self._family_key = key
+
+
+def fp64_peak(device=0):
+    """Measured FP64 DFMA throughput of the device, GFLOP/s."""
+    out = C.c_double()
+    check(lib().perrk_fp64_peak(int(device), C.byref(out)))
+    return out.value
 
 
 # ---------------------------------------------------------------------------

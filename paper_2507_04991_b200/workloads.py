@@ -14,6 +14,10 @@ Appendix A) are fixed here and recorded in DESIGN.md:
   C4  (2D Navier-Stokes double shear layer) -- pending on the device path
   C5  64^3 three-level "+" mesh on [0,2pi]^3, Taylor-Green vortex Ma 0.1,
       EC + Rusanov, p4 {5,8,14}, 100 steps
+Free coefficients of the C2-C5 families come from configs/make_families.py
+(model-spectrum stability optimisation; member CFL limits in DESIGN.md); the
+CFL numbers are ~75 % of each family's model limit (C2 1.37, C3 2.03,
+C5 1.45).
 Levels are assigned geometrically (finest cell size along any axis -> level
 1), then widened by make_partition_map's neighbour rule (mesh.cpp:56-71).
 """
@@ -140,7 +144,7 @@ def geometric_levels(axis_lv, R):
     if len(axis_lv) == 2:
         L = np.minimum.outer(axis_lv[1], axis_lv[0])  # [y, x]
     else:
-        L = np.minimum(np.minimum.outer(axis_lv[2], np.ones_like(axis_lv[1]))[:, :, None],
+        L = np.minimum(axis_lv[2][:, None, None],
                        np.minimum.outer(axis_lv[1], axis_lv[0])[None, :, :])  # [z, y, x]
     return np.clip(L.reshape(-1), 1, R).astype(np.int32)
 
@@ -219,7 +223,7 @@ def make_config(name: str, family=None, cfl=None, steps=None) -> Config:
         al = axis_levels(bands)
         fam = family or load_config_family("c2_p3_4_7")
         return Config("c2", "2D Euler vortex, 64^2 2-level '+' mesh, p3 {4,7}, HLLE", mesh,
-                      "hlle", fam, geometric_levels([al, al], fam.R), cfl or 0.9, steps or 500,
+                      "hlle", fam, geometric_levels([al, al], fam.R), cfl or 1.0, steps or 500,
                       "vortex")
     if name == "c3":
         h = 2 * math.pi / 216.0
@@ -229,7 +233,7 @@ def make_config(name: str, family=None, cfl=None, steps=None) -> Config:
         al = axis_levels(bands)
         fam = family or load_config_family("c3_p4_5_9_16")
         return Config("c3", "2D Euler random Fourier state, 256^2 3-level mesh, p4 {5,9,16}",
-                      mesh, "rusanov", fam, geometric_levels([al, al], fam.R), cfl or 0.9,
+                      mesh, "rusanov", fam, geometric_levels([al, al], fam.R), cfl or 1.5,
                       steps or 200, "random")
     if name == "c5":
         h = 2 * math.pi / 54.0
@@ -239,9 +243,74 @@ def make_config(name: str, family=None, cfl=None, steps=None) -> Config:
         al = axis_levels(bands)
         fam = family or load_config_family("c5_p4_5_8_14")
         return Config("c5", "3D Euler Taylor-Green Ma 0.1, 64^3 3-level mesh, p4 {5,8,14}",
-                      mesh, "rusanov", fam, geometric_levels([al, al, al], fam.R), cfl or 0.9,
+                      mesh, "rusanov", fam, geometric_levels([al, al, al], fam.R), cfl or 1.1,
                       steps or 100, "tgv")
     raise ValueError(f"unknown config {name}")
+
+
+def _scaled_bands(bands, factor, length):
+    """Same band structure with every count divided by factor (>= 1 cell)."""
+    counts = [max(1, n // factor) for n, _ in bands]
+    rel = [h for _, h in bands]
+    total = sum(n * r for n, r in zip(counts, rel))
+    scale = length / total
+    return [(n, r * scale) for n, r in zip(counts, rel)]
+
+
+def sample_config(cfg: Config) -> Config:
+    """A bounded CPU sample of a configuration: the same family, flux, initial
+    condition, CFL and level grading on a mesh with fewer cells per band
+    (C5: 16^3 instead of 64^3; C3: 32^2 instead of 256^2).  Used only for the
+    CPU baseline timing, never for parity."""
+    import copy
+    out = copy.copy(cfg)
+    if cfg.name == "c5":
+        bands = _scaled_bands([(24, 1.0), (4, 0.5), (8, 0.25), (4, 0.5), (24, 1.0)], 4,
+                              2 * math.pi)
+        e = banded_edges(0.0, bands)
+        out.mesh = P.Mesh3DRect(e, list(e), list(e))
+        al = axis_levels(bands)
+        out.raw_levels = geometric_levels([al, al, al], cfg.family.R)
+        out.description = "C5 sample: 16^3-element 3-level graded TGV mesh"
+    elif cfg.name == "c3":
+        bands = _scaled_bands([(96, 1.0), (16, 0.5), (32, 0.25), (16, 0.5), (96, 1.0)], 8,
+                              2 * math.pi)
+        e = banded_edges(0.0, bands)
+        out.mesh = P.Mesh2DRect(e, list(e))
+        al = axis_levels(bands)
+        out.raw_levels = geometric_levels([al, al], cfg.family.R)
+        out.description = "C3 sample: 32^2-element 3-level graded mesh"
+    return out
+
+
+class ConfigRun:
+    """A configuration instantiated on one device: semidiscretization,
+    partition map, initial state.  With world > 1 the context owns the
+    rank's element slab (perrk_comm_init)."""
+
+    def __init__(self, cfg: Config, device=0, rank=0, world=1, comm=None):
+        self.cfg = cfg
+        self.rank, self.world = rank, world
+        self.semi = P.Semidiscretization(cfg.spec(device))
+        self.pmap = cfg.partition_map()
+        if world > 1:
+            P.init_slabs(self.semi, rank, world, comm)
+
+    def initial_state(self):
+        s = self.semi
+        return initial_state_for(self.cfg, (s.node_x(), s.node_y(),
+                                            s.node_z() if self.cfg.dim == 3 else None))
+
+    def dof_stage_updates_per_step(self):
+        """This rank's share (all ranks when world == 1)."""
+        return dof_stage_updates_per_step(self.cfg.family, self.local_pmap(),
+                                          self.cfg.nodes_per_cell())
+
+    def local_pmap(self):
+        return self.pmap if self.world == 1 else P.slab_pmap(self.semi, self.pmap)
+
+    def total_nodes(self):
+        return self.cfg.mesh.num_cells() * self.cfg.nodes_per_cell()
 
 
 def initial_state_for(cfg: Config, semi_or_coords):
