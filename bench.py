@@ -40,6 +40,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+ORACLE_DIR = os.path.join(ROOT, "oracle")
 
 METRIC = "P-ERRK DOF-stage updates/sec (FP64)"
 UNIT = "DOF-stage/s"
@@ -139,7 +140,9 @@ def traffic_fixture(config):
 # CPU baseline / reference arm: the oracle port on a bounded sample
 # ---------------------------------------------------------------------------
 def cpu_sample(config, threads):
-    import oracle as O  # checker library; only bench's cpu/reference legs use it
+    if ORACLE_DIR not in sys.path:  # checker library; only bench's cpu/reference legs use it
+        sys.path.insert(0, ORACLE_DIR)
+    import oracle as O
     from paper_2507_04991_b200 import workloads as W
     cfg = W.make_config(config)
     sample = W.sample_config(cfg)
