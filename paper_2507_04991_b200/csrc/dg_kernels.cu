@@ -63,354 +63,13 @@ __device__ __forceinline__ void report_bad(StepState* st, int stage, long long n
   atomicMin(&st->bad_code, static_cast<long long>(stage) * ncells + cell);
 }
 
-// ---------------------------------------------------------------------------
-// per-line volume term: flux differencing along one LGL line
-// (semidisc.cpp:447-484): endpoint diagonal with the physical flux, the six
-// symmetric pairs with the Ranocha EC flux (physics.cpp:157-179) built from
-// per-node primitives and precomputed logarithms.
-// ---------------------------------------------------------------------------
-template <int DIM, int DIR>
-__device__ __forceinline__ void line_task(const Phys& ph, const double* pe, const double* ue,
-                                          double* vab, int t1, int t2, double J2) {
-  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
-  int nid[N1];
-#pragma unroll
-  for (int j = 0; j < N1; ++j) nid[j] = line_node<DIM>(DIR, j, t1, t2);
-  double acc[N1][V];
-#pragma unroll
-  for (int j = 0; j < N1; ++j)
-#pragma unroll
-    for (int v = 0; v < V; ++v) acc[j][v] = 0.0;
-#pragma unroll
-  for (int j = 0; j < N1; ++j) {
-    const int nl = nid[j];
-    const double dll = c_D[j * N1 + j];
-    if (j == 0 || j == N1 - 1) {  // D_ll != 0 only at the endpoints (basis.cpp:80-81)
-      double f[V];
-      phys_flux<DIM>(ue + nl * V, pe[P_P * NPC + nl], DIR, f);
-      const double cll = J2 * dll;
-#pragma unroll
-      for (int v = 0; v < V; ++v) acc[j][v] -= cll * f[v];
-    }
-    const double rl = pe[P_RHO * NPC + nl], pl = pe[P_P * NPC + nl];
-    const double lrl = pe[P_LRHO * NPC + nl], bl = pe[P_BETA * NPC + nl];
-    const double lbl = pe[P_LBETA * NPC + nl];
-    double vl[DIM];
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) vl[d] = pe[(P_VX + d) * NPC + nl];
-#pragma unroll
-    for (int k = j + 1; k < N1; ++k) {
-      const int nm = nid[k];
-      const double rr = pe[P_RHO * NPC + nm], prr = pe[P_P * NPC + nm];
-      const double rho_log = logmean_pre(rl, rr, lrl, pe[P_LRHO * NPC + nm]);
-      const double inv_b = inv_logmean_pre(bl, pe[P_BETA * NPC + nm], lbl, pe[P_LBETA * NPC + nm]);
-      double vr[DIM], v_avg[DIM], vl_vr = 0.0;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        vr[d] = pe[(P_VX + d) * NPC + nm];
-        v_avg[d] = 0.5 * (vl[d] + vr[d]);
-        vl_vr += vl[d] * vr[d];
-      }
-      double f[V];
-      const double f_rho = rho_log * v_avg[DIR];
-      f[0] = f_rho;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) f[1 + d] = f_rho * v_avg[d];
-      f[1 + DIR] += 0.5 * (pl + prr);
-      f[DIM + 1] =
-          f_rho * (0.5 * vl_vr + ph.inv_gm1 * inv_b) + 0.5 * (pl * vr[DIR] + prr * vl[DIR]);
-      const double clm = J2 * c_D[j * N1 + k];
-      const double cml = J2 * c_D[k * N1 + j];
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        acc[j][v] -= clm * f[v];
-        acc[k][v] -= cml * f[v];
-      }
-    }
-  }
-  double* vad = vab + DIR * NPC * V;
-#pragma unroll
-  for (int j = 0; j < N1; ++j)
-#pragma unroll
-    for (int v = 0; v < V; ++v) vad[nid[j] * V + v] = acc[j][v];
-}
+}  // namespace dev
+}  // namespace perrk
 
-// per-face-point surface term (semidisc.cpp:492-556): numerical flux between
-// the own trace and the neighbour trace, lifted onto the own node as
-// -/+ 2/(h w0) (f* - f(u_own)); stored signed for the combine step.
-template <int DIM, int SURF, int DIR>
-__device__ __forceinline__ void face_task(const Phys& ph, const double* ue, const double* pp,
-                                          const double* un, double* o, int side, int t1, int t2,
-                                          double coef) {
-  constexpr int V = DIM + 2;
-  const int own = line_node<DIM>(DIR, side ? N1 - 1 : 0, t1, t2);
-  const double* uo = ue + own * V;
-  double fs[V], fo[V];
-  if (side)
-    surface_flux<DIM, SURF>(ph, uo, un, DIR, fs);
-  else
-    surface_flux<DIM, SURF>(ph, un, uo, DIR, fs);
-  phys_flux<DIM>(uo, pp[own], DIR, fo);
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const double c = coef * (fs[v] - fo[v]);
-    o[v] = side ? -c : c;
-  }
-}
+#include "dg_stage.cuh"
 
-// ---------------------------------------------------------------------------
-// stage kernel
-// ---------------------------------------------------------------------------
-
-template <int DIM, int SURF>
-__global__ void __launch_bounds__(Geo<DIM>::THREADS)
-    stage_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
-                 unsigned* counter) {
-  using G = Geo<DIM>;
-  constexpr int V = G::V, NPC = G::NPC, FP = G::FP, NF = G::NF, EPB = G::EPB;
-  extern __shared__ double smem[];
-  double* su = smem;            // [EPB][NPC*V]
-  double* pr = su + G::SM_SU;   // [EPB][NPR][NPC]
-  double* nb = pr + G::SM_PR;   // [EPB][NF][FP*V]
-  double* va = nb + G::SM_NB;   // [EPB][DIM][NPC*V]
-  double* sf = va + G::SM_VA;   // [EPB][NF][FP*V]
-  __shared__ int s_cell[EPB];
-  __shared__ int s_coord[EPB][3];
-  __shared__ double s_red[2 * 2 * (G::THREADS / 32)];
-  __shared__ double s_a1[MAXR + 1], s_ap[MAXR + 1];
-
-  if (st->aborted || st->finished) return;  // uniform across the grid
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q <= MAXR; ++q) {
-      s_a1[q] = a.a1[q];
-      s_ap[q] = a.ap[q];
-    }
-  }
-  __syncthreads();
-
-  const int tid = threadIdx.x;
-  const int e = tid / NPC, l = tid % NPC;
-  const double dt = st->dt;
-  dd acc_dh = dd_zero(), acc_h = dd_zero();
-  double dmax = 0.0;
-  bool dbad = false;
-
-  const int ngroups = (a.n + EPB - 1) / EPB;
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int slot = grp * EPB + e;
-    const bool valid = slot < a.n;
-    const int cell = valid ? (a.list ? a.list[slot] : slot) : 0;
-    int ci, cj, ck;
-    cell_coords(m, cell, ci, cj, ck);
-    if (l == 0) {
-      s_cell[e] = valid ? cell : -1;
-      s_coord[e][0] = ci;
-      s_coord[e][1] = cj;
-      s_coord[e][2] = ck;
-    }
-    const size_t base = static_cast<size_t>(cell) * NPC * V;
-
-    // ---- A1: stage state of the cell, coalesced over the cell's DOFs -----
-    double* sue = su + e * NPC * V;
-    if (valid) {
-      const int lev = m.level[cell];
-      const double a1 = s_a1[lev], ap = s_ap[lev];
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const int f = l + j * NPC;
-        double u = __ldg(a.U + base + f);
-        if (a.form && ap != 0.0)
-          u = u + dt * (a1 * __ldg(a.K1 + base + f) + ap * __ldg(a.Kp + base + f));
-        else if (a.form)
-          u = u + dt * a1 * __ldg(a.K1 + base + f);
-        sue[f] = u;
-      }
-      // ---- A2: neighbour face traces, formed with the neighbour's row ----
-      for (int q = l; q < NF * FP; q += NPC) {
-        const int face = q / FP, pt = q % FP, dir = face >> 1, side = face & 1;
-        const int t1 = pt % N1, t2 = pt / N1;
-        int c0 = ci, c1 = cj, c2 = ck;
-        int& cd = dir == 0 ? c0 : (dir == 1 ? c1 : c2);
-        const int nd = pick3(m.nc, dir);
-        cd = side ? (cd + 1 == nd ? 0 : cd + 1) : (cd == 0 ? nd - 1 : cd - 1);
-        const int nbc = c0 + m.nc[0] * (c1 + m.nc[1] * c2);
-        const int node = line_node<DIM>(dir, side ? 0 : N1 - 1, t1, t2);
-        const size_t nbase = (static_cast<size_t>(nbc) * NPC + node) * V;
-        const int lev2 = m.level[nbc];
-        const double b1 = s_a1[lev2], bp = s_ap[lev2];
-        double un[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          double u = __ldg(a.U + nbase + v);
-          if (a.form && bp != 0.0)
-            u = u + dt * (b1 * __ldg(a.K1 + nbase + v) + bp * __ldg(a.Kp + nbase + v));
-          else if (a.form)
-            u = u + dt * b1 * __ldg(a.K1 + nbase + v);
-          un[v] = u;
-          nb[(e * NF + face) * FP * V + pt * V + v] = u;
-        }
-        if (!admissible<DIM>(ph, un)) report_bad(st, a.stage, a.ncells, nbc);
-      }
-    }
-    __syncthreads();
-
-    // ---- A3: primitives per node ------------------------------------------
-    if (valid) {
-      const double* u = sue + l * V;
-      const double rho = u[0];
-      const double p = pressure<DIM>(ph, u);
-      bool ok = rho > 0.0 && p > 0.0;
-#pragma unroll
-      for (int v = 0; v < V; ++v) ok = ok && isfinite(u[v]);
-      if (!ok) report_bad(st, a.stage, a.ncells, cell);
-      double* pe = pr + e * G::NPR * NPC;
-      pe[P_RHO * NPC + l] = rho;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) pe[(P_VX + d) * NPC + l] = u[1 + d] / rho;
-      pe[P_P * NPC + l] = p;
-      const double beta = rho / p;
-      pe[P_LRHO * NPC + l] = log(rho);
-      pe[P_BETA * NPC + l] = beta;
-      pe[P_LBETA * NPC + l] = log(beta);
-    }
-    __syncthreads();
-
-    // ---- B: volume lines (warps 0..) | surface points (last warps) ----------
-    // dir is dispatched to compile-time constants so the small per-flux
-    // arrays stay in registers
-    if (tid < G::LINE_THREADS) {
-      const int e2 = tid / G::LINES, li = tid % G::LINES;
-      if (s_cell[e2] >= 0) {
-        const int dir = li / FP, pt = li % FP;
-        const double J2 = 2.0 * pick3(m.jac, dir)[s_coord[e2][dir]];
-        const double* pe = pr + e2 * G::NPR * NPC;
-        const double* ue = su + e2 * NPC * V;
-        double* vab = va + e2 * DIM * NPC * V;
-        if (dir == 0)
-          line_task<DIM, 0>(ph, pe, ue, vab, pt % N1, pt / N1, J2);
-        else if (dir == 1)
-          line_task<DIM, 1>(ph, pe, ue, vab, pt % N1, pt / N1, J2);
-        else if (DIM == 3)
-          line_task<DIM, DIM == 3 ? 2 : 0>(ph, pe, ue, vab, pt % N1, pt / N1, J2);
-      }
-    } else {
-      for (int q = tid - G::LINE_THREADS; q < G::FACE_TASKS; q += G::FACE_THREADS) {
-        const int e2 = q / (NF * FP), r = q % (NF * FP);
-        if (s_cell[e2] < 0) continue;
-        const int face = r / FP, pt = r % FP, dir = face >> 1;
-        const double coef = pick3(m.lift, dir)[s_coord[e2][dir]];
-        const double* ue = su + e2 * NPC * V;
-        const double* pp = pr + (e2 * G::NPR + P_P) * NPC;
-        const double* un = nb + (e2 * NF + face) * FP * V + pt * V;
-        double* o = sf + (e2 * NF + face) * FP * V + pt * V;
-        if (dir == 0)
-          face_task<DIM, SURF, 0>(ph, ue, pp, un, o, face & 1, pt % N1, pt / N1, coef);
-        else if (dir == 1)
-          face_task<DIM, SURF, 1>(ph, ue, pp, un, o, face & 1, pt % N1, pt / N1, coef);
-        else if (DIM == 3)
-          face_task<DIM, SURF, DIM == 3 ? 2 : 0>(ph, ue, pp, un, o, face & 1, pt % N1, pt / N1,
-                                                 coef);
-      }
-    }
-    __syncthreads();
-
-    // ---- C: combine per node, entropy epilogue -------------------------------
-    if (valid) {
-      const int ix = l % N1, iy = (l / N1) % N1, iz = l / (N1 * N1);
-      const int ii[3] = {ix, iy, iz};
-      double K[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        double s = va[(e * DIM + 0) * NPC * V + l * V + v];
-#pragma unroll
-        for (int d = 1; d < DIM; ++d) s += va[(e * DIM + d) * NPC * V + l * V + v];
-        K[v] = s;
-      }
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        if (ii[d] == 0 || ii[d] == N1 - 1) {
-          const int side = ii[d] == N1 - 1;
-          const int t1 = d == 0 ? iy : ix;
-          const int t2 = d == 2 ? iy : iz;
-          const int pt = t1 + N1 * t2;
-          const double* o = sf + (e * NF + 2 * d + side) * FP * V + pt * V;
-#pragma unroll
-          for (int v = 0; v < V; ++v) K[v] += o[v];
-        }
-      }
-      if (a.want_dh || a.want_h) {
-        const double* pe = pr + e * G::NPR * NPC;
-        const double rho = pe[P_RHO * NPC + l];
-        const double beta = pe[P_BETA * NPC + l];
-        // log(p / rho^gamma) = -(log beta + (gamma-1) log rho)
-        const double s_therm = -(pe[P_LBETA * NPC + l] + ph.gm1 * pe[P_LRHO * NPC + l]);
-        const double om = node_measure<DIM>(m, ci, cj, ck, l);
-        if (a.want_dh) {
-          double v2 = 0.0;
-#pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            const double vd = pe[(P_VX + d) * NPC + l];
-            v2 += vd * vd;
-          }
-          double dot = (ph.gamma - s_therm - 0.5 * ph.gm1 * beta * v2) * K[0];
-#pragma unroll
-          for (int d = 0; d < DIM; ++d) dot += ph.gm1 * beta * pe[(P_VX + d) * NPC + l] * K[1 + d];
-          dot += -ph.gm1 * beta * K[DIM + 1];
-          acc_dh = dd_add_prod(acc_dh, om, dot);
-        }
-        if (a.want_h) acc_h = dd_add_prod(acc_h, om, -rho * s_therm);
-      }
-      // stash K in this node's x-volume slots (only this thread reads them)
-#pragma unroll
-      for (int v = 0; v < V; ++v) va[(e * DIM) * NPC * V + l * V + v] = K[v];
-    }
-    __syncthreads();
-
-    // ---- D: coalesced stores of K and d -------------------------------------
-    if (valid) {
-      const double* Ke = va + (e * DIM) * NPC * V;
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const int f = l + j * NPC;
-        const double k = Ke[f];
-        if (a.write_k) a.Kout[base + f] = k;
-        if (a.d_mode) {
-          const double dn = a.d_mode == 1 ? a.b * k : a.d[base + f] + a.b * k;
-          a.d[base + f] = dn;
-          if (a.want_dmax) {
-            if (!isfinite(dn)) dbad = true;
-            dmax = fmax(dmax, fabs(dn));
-          }
-        }
-      }
-    }
-    __syncthreads();  // smem reuse by the next group
-  }
-
-  // ---- grid epilogue ------------------------------------------------------
-  if (a.want_dmax) {
-    dmax = warp_max(dmax);
-    if ((tid & 31) == 0) atomic_max_pos(&st->dmax_bits, dmax);
-    if (dbad) st->d_nonfinite = 1;
-  }
-  dd v[2] = {acc_dh, acc_h}, tot[2];
-  if (a.want_dh || a.want_h) block_reduce_dd<2>(v, s_red);
-  if (grid_reduce_dd<2>(v, partials, counter, s_red, tot) && tid == 0) {
-    if (a.want_dh) {
-      const dd inc = dd_mul_d(tot[0], dt * a.b);
-      const dd cur = {st->dh_hi, st->dh_lo};
-      const dd nw = dd_add(cur, inc);
-      st->dh_hi = nw.hi;
-      st->dh_lo = nw.lo;
-    }
-    if (a.want_h) {
-      st->h_hi = tot[1].hi;
-      st->h_lo = tot[1].lo;
-    }
-    if (st->bad_code != kNoBad) st->aborted = 1;
-  }
-}
+namespace perrk {
+namespace dev {
 
 // ---------------------------------------------------------------------------
 // per-step control
@@ -769,21 +428,35 @@ __global__ void admissible_kernel(const double* __restrict__ U, Phys ph, int* fi
 // ---------------------------------------------------------------------------
 
 template <int DIM, int SURF>
-static cudaError_t launch_stage_t(const StageArgs& a, const MeshDev& m, const Phys& ph,
-                                  StepState* st, double* partials, unsigned* counter, int grid,
-                                  cudaStream_t s) {
-  using G = Geo<DIM>;
-  const size_t shm = sizeof(double) * G::SM_TOTAL;
+static void configure_stage() {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(stage_kernel<DIM, SURF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(shm));
+                         static_cast<int>(sizeof(double) * StageGeo<DIM>::SM_TOTAL));
     configured = true;
   }
-  const int groups = (a.n + G::EPB - 1) / G::EPB;
+}
+
+template <int DIM, int SURF>
+static int stage_occ_t() {
+  configure_stage<DIM, SURF>();
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, stage_kernel<DIM, SURF>, StageGeo<DIM>::T,
+                                                sizeof(double) * StageGeo<DIM>::SM_TOTAL);
+  return n;
+}
+
+template <int DIM, int SURF>
+static cudaError_t launch_stage_t(const StageArgs& a, const MeshDev& m, const Phys& ph,
+                                  StepState* st, double* partials, unsigned* counter, int grid,
+                                  cudaStream_t s) {
+  using G = StageGeo<DIM>;
+  configure_stage<DIM, SURF>();
+  const size_t shm = sizeof(double) * G::SM_TOTAL;
+  const int groups = (a.n + G::CPB - 1) / G::CPB;
   const int g = groups < grid ? groups : grid;
   if (g <= 0) return cudaSuccess;
-  stage_kernel<DIM, SURF><<<g, G::THREADS, shm, s>>>(a, m, ph, st, partials, counter);
+  stage_kernel<DIM, SURF><<<g, G::T, shm, s>>>(a, m, ph, st, partials, counter);
   return cudaGetLastError();
 }
 
@@ -855,10 +528,21 @@ cudaError_t upload_basis(const double* D, const double* w) {
 }
 
 size_t stage_smem_bytes(int dim) {
-  return dim == 2 ? sizeof(double) * Geo<2>::SM_TOTAL : sizeof(double) * Geo<3>::SM_TOTAL;
+  return dim == 2 ? sizeof(double) * StageGeo<2>::SM_TOTAL : sizeof(double) * StageGeo<3>::SM_TOTAL;
 }
 
-int stage_cells_per_block(int dim) { return dim == 2 ? Geo<2>::EPB : Geo<3>::EPB; }
+int stage_blocks_per_sm(int dim, int surf) {
+  switch (surf) {
+    case 0: return dim == 2 ? stage_occ_t<2, 0>() : stage_occ_t<3, 0>();
+    case 2: return dim == 2 ? stage_occ_t<2, 2>() : stage_occ_t<3, 2>();
+    case 3: return dim == 2 ? stage_occ_t<2, 3>() : stage_occ_t<3, 3>();
+    case 4: return dim == 2 ? stage_occ_t<2, 4>() : stage_occ_t<3, 4>();
+    case 5: return dim == 2 ? stage_occ_t<2, 5>() : stage_occ_t<3, 5>();
+  }
+  return 1;
+}
+
+int stage_cells_per_block(int dim) { return dim == 2 ? StageGeo<2>::CPB : StageGeo<3>::CPB; }
 
 cudaError_t launch_stage(int dim, int surf, const StageArgs& a, const MeshDev& m, const Phys& ph,
                          StepState* st, double* partials, unsigned* counter, int grid,

@@ -33,6 +33,7 @@ double measure_fp64_peak();  // GFLOP/s on the current device (DFMA loop)
 cudaError_t upload_basis(const double* D, const double* w);
 size_t stage_smem_bytes(int dim);
 int stage_cells_per_block(int dim);
+int stage_blocks_per_sm(int dim, int surf);  // resident stage blocks per SM
 
 cudaError_t launch_stage(int dim, int surf, const StageArgs& a, const dev::MeshDev& m,
                          const dev::Phys& ph, dev::StepState* st, double* partials,

@@ -1,0 +1,560 @@
+// Stage kernel (v2): one P-ERK stage over the stage's active cell list.
+//
+// Reference work it replaces, per active cell (semidisc.cpp:409-557 via
+// rhs_masked :126-138, plus stepper.cpp:60-92 around it):
+//   * stage-state formation U_i = U + dt (a_i1 K1 + a_i,i-1 K_{i-1}) with the
+//     cell's member row (stepper.cpp:60-72), for the cell and for the face
+//     traces of its neighbours (neighbour's own row);
+//   * flux-differencing volume term with the Ranocha EC two-point flux
+//     (semidisc.cpp:446-485, physics.cpp:157-179), diagonal via the
+//     physical flux at the LGL endpoints;
+//   * surface numerical flux + strong-form LGL lift (semidisc.cpp:489-556);
+//   * b-stage epilogue d (+)= b K, dH += dt b <w(U_i), K_i> (stepper.cpp:52-55,
+//     89-92) and the admissibility scan of every state it evaluates
+//     (semidisc.cpp:596-607; SURVEY.md 7.3 H9 option (a)).
+//
+// Mapping (B200, FP64 pipe bound): a block of 128 threads owns CPB cells
+// (3D: 8, 2D: 32), i.e. exactly one LGL line per thread per direction.  All
+// warps run the same code in lock-step phases:
+//   A   coalesced load + formation of the cells' stage states, per-node
+//       primitives (rho, v, p, E, log rho, beta = rho/p, log beta) to smem;
+//   per direction d:
+//     B_d  neighbour face traces of the two d-faces (formed, checked);
+//     L_d  one line task per thread: 6 symmetric EC pairs, 2 endpoint
+//          diagonal fluxes and the 2 endpoint surface fluxes + lift,
+//          accumulated into the cell's K tile (each node lies on exactly
+//          one d-line, so the phase is conflict free);
+//   E   per node epilogue (entropy products) and coalesced stores of K / d.
+// Divisions are reciprocal-multiplies (MUFU seed + 2 Newton steps); the
+// logarithmic means reuse the per-node logarithms, and the series branch of
+// logmean (physics.cpp:30-38) is kept with the reference's threshold.
+#pragma once
+
+namespace perrk {
+namespace dev {
+
+// 1/x to full double precision: MUFU seed, two Newton steps (rel. error of
+// the seed squared twice), no slow path (x is a finite positive/negative
+// normal number wherever it is used).
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ double fdiv(double a, double b) {
+  const double r = frcp(b);
+  const double q = a * r;
+  return fma(fma(-b, q, a), r, q);
+}
+
+template <int DIM>
+struct StageGeo {
+  static constexpr int V = DIM + 2;
+  static constexpr int NPC = DIM == 2 ? 16 : 64;  // nodes per cell
+  static constexpr int FP = DIM == 2 ? 4 : 16;    // points per face
+  static constexpr int NFP = 2 * DIM * FP;        // face points per cell
+  static constexpr int T = 128;                   // threads per block
+  static constexpr int CPB = T / NPC;             // cells per block (one node per thread)
+  static constexpr int NPR = DIM + 6;             // primitives per node (see slots)
+  // shared memory (doubles)
+  static constexpr int SM_PR = NPR * T;           // primitives, SoA [slot][cell*NPC+node]
+  static constexpr int SM_NB = CPB * NFP * V;     // neighbour traces [cell][face][pt][var]
+  static constexpr int SM_TOTAL = SM_PR + SM_NB;
+};
+
+// primitive slots: rho, v[DIM], p, E, log rho, beta, log beta
+template <int DIM>
+struct Slot {
+  static constexpr int RHO = 0, V0 = 1, P = DIM + 1, E = DIM + 2, LRHO = DIM + 3,
+                       BETA = DIM + 4, LBETA = DIM + 5;
+};
+
+// a state in the primitive form the fluxes use
+template <int DIM>
+struct Prim {
+  double rho, v[DIM], p, E;
+};
+
+template <int DIM>
+__device__ __forceinline__ Prim<DIM> prim_of(const Phys& ph, const double* u) {
+  Prim<DIM> q;
+  q.rho = u[0];
+  const double ir = frcp(u[0]);
+  double kin = 0.0;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    q.v[d] = u[1 + d] * ir;
+    kin = fma(u[1 + d], q.v[d], kin);
+  }
+  q.E = u[DIM + 1];
+  q.p = ph.gm1 * (q.E - 0.5 * kin);
+  return q;
+}
+
+template <int DIM>
+__device__ __forceinline__ bool prim_ok(const Prim<DIM>& q) {
+  bool ok = q.rho > 0.0 && q.p > 0.0 && isfinite(q.E);
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) ok = ok && isfinite(q.v[d]);
+  return ok;
+}
+
+template <int DIM>
+__device__ __forceinline__ double pick(const double (&v)[DIM], int d) {
+  if (DIM == 2) return d == 0 ? v[0] : v[1];
+  return d == 0 ? v[0] : (d == 1 ? v[1] : v[DIM - 1]);
+}
+
+// physical flux in direction d (physics.cpp:108-116)
+template <int DIM>
+__device__ __forceinline__ void pflux(const Prim<DIM>& q, int d, double* f) {
+  const double vd = pick<DIM>(q.v, d);
+  const double m = q.rho * vd;
+  f[0] = m;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) f[1 + i] = m * q.v[i] + (i == d ? q.p : 0.0);
+  f[DIM + 1] = (q.E + q.p) * vd;
+}
+
+// logmean (physics.cpp:30-38) with both logarithms precomputed.  Below the
+// reference's threshold u = ((a-b)/(a+b))^2 < 1e-4 the reference evaluates
+// 0.5 (a+b) / (1 + u/3 + u^2/5 + u^3/7); here the reciprocal of that
+// polynomial is taken as its series 1 - u/3 - 4u^2/45 - 44u^3/945 (the two
+// differ by O(u^4) < 1e-17 relative), so the branch needs no division and u
+// only to ~1e-12 relative (one Newton step on the reciprocal seed).  Above
+// it: (a - b) / (log a - log b).
+__device__ __forceinline__ double lmean(double a, double b, double la, double lb) {
+  const double s = a + b, dlt = a - b;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+  r = fma(r, fma(-s, r, 1.0), r);
+  const double f = dlt * r;
+  const double u = f * f;
+  if (u < 1e-4) {
+    const double ip = fma(u, fma(u, fma(u, -44.0 / 945.0, -4.0 / 45.0), -1.0 / 3.0), 1.0);
+    return 0.5 * s * ip;
+  }
+  return dlt * frcp(la - lb);
+}
+
+// 1 / logmean(a, b): 2 poly / (a + b) below the threshold
+__device__ __forceinline__ double inv_lmean(double a, double b, double la, double lb) {
+  const double s = a + b, dlt = a - b;
+  const double rs = frcp(s);
+  const double f = dlt * rs;
+  const double u = f * f;
+  if (u < 1e-4) {
+    const double poly = fma(u, fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0), 1.0);
+    return 2.0 * poly * rs;
+  }
+  return (la - lb) * frcp(dlt);
+}
+
+// Ranocha EC flux (physics.cpp:157-179) from primitives + logs
+template <int DIM>
+__device__ __forceinline__ void ec2(const Phys& ph, int d, double rl, const double (&vl)[DIM],
+                                    double pl, double lrl, double bl, double lbl, double rr,
+                                    const double (&vr)[DIM], double pr, double lrr, double br,
+                                    double lbr, double* f) {
+  const double rho_log = lmean(rl, rr, lrl, lrr);
+  const double inv_b = inv_lmean(bl, br, lbl, lbr);
+  double va[DIM], vlvr = 0.0;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    va[i] = 0.5 * (vl[i] + vr[i]);
+    vlvr = fma(vl[i], vr[i], vlvr);
+  }
+  const double fr = rho_log * pick<DIM>(va, d);
+  f[0] = fr;
+  const double pavg = 0.5 * (pl + pr);
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) f[1 + i] = fr * va[i] + (i == d ? pavg : 0.0);
+  f[DIM + 1] = fr * (0.5 * vlvr + ph.inv_gm1 * inv_b) +
+               0.5 * (pl * pick<DIM>(vr, d) + pr * pick<DIM>(vl, d));
+}
+
+// Roe-average wave speed estimates (physics.cpp:181-203)
+template <int DIM>
+__device__ __forceinline__ void wse(const Phys& ph, const Prim<DIM>& l, const Prim<DIM>& r, int d,
+                                    double& sl, double& sr) {
+  const double cl = sqrt(ph.gamma * l.p * frcp(l.rho)), cr = sqrt(ph.gamma * r.p * frcp(r.rho));
+  const double sql = sqrt(l.rho), sqr = sqrt(r.rho);
+  const double iw = frcp(sql + sqr);
+  const double hl = (l.E + l.p) * frcp(l.rho), hr = (r.E + r.p) * frcp(r.rho);
+  double v2 = 0.0, vd = 0.0;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    const double vroe = (sql * l.v[i] + sqr * r.v[i]) * iw;
+    v2 = fma(vroe, vroe, v2);
+    if (i == d) vd = vroe;
+  }
+  const double hroe = (sql * hl + sqr * hr) * iw;
+  const double croe = sqrt(fmax(0.0, ph.gm1 * (hroe - 0.5 * v2)));
+  sl = fmin(pick<DIM>(l.v, d) - cl, vd - croe);
+  sr = fmax(pick<DIM>(r.v, d) + cr, vd + croe);
+}
+
+template <int DIM>
+__device__ __forceinline__ void cons_of(const Prim<DIM>& q, double* u) {
+  u[0] = q.rho;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) u[1 + i] = q.rho * q.v[i];
+  u[DIM + 1] = q.E;
+}
+
+// surface numerical flux f*(l, r) in direction d (physics.cpp:40-65,181-258)
+template <int DIM, int SURF>
+__device__ __forceinline__ void sflux(const Phys& ph, const Prim<DIM>& l, const Prim<DIM>& r,
+                                      int d, double* f) {
+  constexpr int V = DIM + 2;
+  if constexpr (SURF == 5) {
+    const double bl = l.rho * frcp(l.p), br = r.rho * frcp(r.p);
+    ec2<DIM>(ph, d, l.rho, l.v, l.p, log(l.rho), bl, log(bl), r.rho, r.v, r.p, log(r.rho), br,
+             log(br), f);
+    return;
+  }
+  double fl[V], fr[V];
+  pflux<DIM>(l, d, fl);
+  pflux<DIM>(r, d, fr);
+  if constexpr (SURF == 0) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) f[v] = 0.5 * (fl[v] + fr[v]);
+  } else if constexpr (SURF == 2) {
+    const double lam = fmax(fabs(pick<DIM>(l.v, d)) + sqrt(ph.gamma * l.p * frcp(l.rho)),
+                            fabs(pick<DIM>(r.v, d)) + sqrt(ph.gamma * r.p * frcp(r.rho)));
+    double ul[V], ur[V];
+    cons_of<DIM>(l, ul);
+    cons_of<DIM>(r, ur);
+#pragma unroll
+    for (int v = 0; v < V; ++v) f[v] = 0.5 * (fl[v] + fr[v]) - 0.5 * lam * (ur[v] - ul[v]);
+  } else if constexpr (SURF == 3) {
+    double sl, sr;
+    wse<DIM>(ph, l, r, d, sl, sr);
+    if (sl >= 0.0) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) f[v] = fl[v];
+    } else if (sr <= 0.0) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) f[v] = fr[v];
+    } else {
+      double ul[V], ur[V];
+      cons_of<DIM>(l, ul);
+      cons_of<DIM>(r, ur);
+      const double inv = frcp(sr - sl);
+#pragma unroll
+      for (int v = 0; v < V; ++v) f[v] = (sr * fl[v] - sl * fr[v] + sl * sr * (ur[v] - ul[v])) * inv;
+    }
+  } else {  // SURF == 4: HLLC
+    double sl, sr;
+    wse<DIM>(ph, l, r, d, sl, sr);
+    if (sl >= 0.0) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) f[v] = fl[v];
+    } else if (sr <= 0.0) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) f[v] = fr[v];
+    } else {
+      const double vl = pick<DIM>(l.v, d), vr = pick<DIM>(r.v, d);
+      const double s_star = fdiv(r.p - l.p + l.rho * vl * (sl - vl) - r.rho * vr * (sr - vr),
+                                 l.rho * (sl - vl) - r.rho * (sr - vr));
+      const bool left = s_star >= 0.0;
+      const Prim<DIM>& k = left ? l : r;
+      const double sk = left ? sl : sr, vk = left ? vl : vr;
+      const double* fk = left ? fl : fr;
+      const double factor = fdiv(k.rho * (sk - vk), sk - s_star);
+      double uk[V], us[V];
+      cons_of<DIM>(k, uk);
+      us[0] = factor;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) us[1 + i] = factor * (i == d ? s_star : k.v[i]);
+      us[DIM + 1] = factor * (k.E * frcp(k.rho) +
+                              (s_star - vk) * (s_star + fdiv(k.p, k.rho * (sk - vk))));
+#pragma unroll
+      for (int v = 0; v < V; ++v) f[v] = fk[v] + sk * (us[v] - uk[v]);
+    }
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ int line_base(int d, int t1, int t2) {
+  if (DIM == 2) return d == 0 ? N1 * t1 : t1;
+  return d == 0 ? N1 * t1 + N1 * N1 * t2 : (d == 1 ? t1 + N1 * N1 * t2 : t1 + N1 * t2);
+}
+
+__device__ __forceinline__ int line_stride(int d) { return d == 0 ? 1 : (d == 1 ? N1 : N1 * N1); }
+
+__device__ __forceinline__ int pick_int3(const int (&a)[3], int i) {
+  return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]);
+}
+
+// Volume, diagonal and surface terms of one node along direction D
+// (compile-time, so velocity components, strides and flux slots resolve
+// statically).  cd: the cell's index along D; nbc: neighbour cells across
+// the -D / +D faces (for the positivity report).
+template <int DIM, int SURF, int D>
+__device__ __forceinline__ void direction_terms(const Phys& ph, const MeshDev& m, StepState* st,
+                                                const StageArgs& a, const double* pr,
+                                                const double* nb, int tid, int cs,
+                                                const int (&il)[3], int cd, const int* nbc,
+                                                const Prim<DIM>& own, double lr, double be,
+                                                double lb, double* K) {
+  using G = StageGeo<DIM>;
+  using S = Slot<DIM>;
+  constexpr int V = G::V, FP = G::FP, T = G::T;
+  constexpr int stride = D == 0 ? 1 : (D == 1 ? N1 : N1 * N1);
+  const int j = il[D];
+  const double J2 = 2.0 * m.jac[D][cd];
+  // ---- volume: the three partners on this node's D-line (semidisc.cpp:455-464;
+  // the EC flux is symmetric, so f(l, m) here is the reference's f(min, max)
+  // up to the order of commutative operations)
+#pragma unroll
+  for (int s = 1; s < N1; ++s) {
+    const int k = (j + s) & (N1 - 1);
+    const int qk = tid + (k - j) * stride;
+    double vk[DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) vk[i] = pr[(S::V0 + i) * T + qk];
+    double f[V];
+    ec2<DIM>(ph, D, own.rho, own.v, own.p, lr, be, lb, pr[S::RHO * T + qk], vk,
+             pr[S::P * T + qk], pr[S::LRHO * T + qk], pr[S::BETA * T + qk],
+             pr[S::LBETA * T + qk], f);
+    const double cjk = J2 * c_D[j * N1 + k];
+#pragma unroll
+    for (int v = 0; v < V; ++v) K[v] = fma(-cjk, f[v], K[v]);
+  }
+  // ---- endpoints: diagonal physical flux (D_ll != 0 only there,
+  // basis.cpp:80-81) and surface flux + strong-form lift (semidisc.cpp:492-556)
+  if (j == 0 || j == N1 - 1) {
+    const int e = j == 0 ? 0 : 1;
+    double fo[V];
+    pflux<DIM>(own, D, fo);
+    const int pt = D == 0 ? il[1] + N1 * il[2] : (D == 1 ? il[0] + N1 * il[2] : il[0] + N1 * il[1]);
+    const double* un = nb + ((cs * 2 * DIM + 2 * D + e) * FP + pt) * V;
+    double uu[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) uu[v] = un[v];
+    const Prim<DIM> nbp = prim_of<DIM>(ph, uu);
+    if (!prim_ok<DIM>(nbp)) report_bad(st, a.stage, a.ncells, nbc[e]);
+    double fs[V];
+    if (e)
+      sflux<DIM, SURF>(ph, own, nbp, D, fs);
+    else
+      sflux<DIM, SURF>(ph, nbp, own, D, fs);
+    const double lift = m.lift[D][cd];
+    const double cll = J2 * c_D[j * N1 + j];
+    const double sg = e ? -lift : lift;
+#pragma unroll
+    for (int v = 0; v < V; ++v) K[v] = fma(sg, fs[v] - fo[v], fma(-cll, fo[v], K[v]));
+  }
+}
+
+template <int DIM, int SURF>
+__global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
+    stage_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
+                 unsigned* counter) {
+  using G = StageGeo<DIM>;
+  using S = Slot<DIM>;
+  constexpr int V = G::V, NPC = G::NPC, FP = G::FP, NFP = G::NFP, CPB = G::CPB, T = G::T;
+  extern __shared__ double smem[];
+  double* pr = smem;            // [NPR][T]
+  double* nb = pr + G::SM_PR;   // [CPB][NFP][V]
+  __shared__ int s_cell[CPB];
+  __shared__ int s_coord[CPB][3];
+  __shared__ double s_ca1[CPB], s_cap[CPB];
+  __shared__ int s_nbc[CPB][2 * DIM];
+  __shared__ double s_na1[CPB][2 * DIM], s_nap[CPB][2 * DIM];
+  __shared__ double s_red[2 * 2 * (T / 32)];
+
+  if (st->aborted || st->finished) return;  // uniform across the grid
+  const int tid = threadIdx.x;
+  const double dt = st->dt;
+  const int cs = tid / NPC, l = tid % NPC;
+  const int il[3] = {l % N1, (l / N1) % N1, l / (N1 * N1)};  // node position per axis
+  dd acc_dh = dd_zero(), acc_h = dd_zero();
+  double dmax = 0.0;
+  bool dbad = false;
+  const int ngroups = (a.n + CPB - 1) / CPB;
+
+  // group descriptor of the first group, loaded by threads < CPB and
+  // thereafter prefetched one group ahead (the list -> cell -> level chain
+  // resolves while the current group computes)
+  int nx_cell = -1;
+  if (tid < CPB) {
+    const int slot = blockIdx.x * CPB + tid;
+    nx_cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
+  }
+
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    if (tid < CPB) {
+      const int cell = nx_cell;
+      s_cell[tid] = cell;
+      const int cc = cell < 0 ? 0 : cell;
+      int co[3] = {cc % m.nc[0], (cc / m.nc[0]) % m.nc[1], cc / (m.nc[0] * m.nc[1])};
+      s_coord[tid][0] = co[0];
+      s_coord[tid][1] = co[1];
+      s_coord[tid][2] = co[2];
+      const int lev = m.level[cc];
+      s_ca1[tid] = dt * a.a1[lev];
+      s_cap[tid] = dt * a.ap[lev];
+#pragma unroll
+      for (int f = 0; f < 2 * DIM; ++f) {  // periodic face neighbours, their rows
+        const int d = f >> 1, side = f & 1;
+        int c3[3] = {co[0], co[1], co[2]};
+        const int nd = m.nc[d];
+        c3[d] = side ? (c3[d] + 1 == nd ? 0 : c3[d] + 1) : (c3[d] == 0 ? nd - 1 : c3[d] - 1);
+        const int nbc = c3[0] + m.nc[0] * (c3[1] + m.nc[1] * c3[2]);
+        const int l2 = m.level[nbc];
+        s_nbc[tid][f] = nbc;
+        s_na1[tid][f] = dt * a.a1[l2];
+        s_nap[tid][f] = dt * a.ap[l2];
+      }
+      const int slot = (grp + gridDim.x) * CPB + tid;  // prefetch the next group
+      nx_cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
+    }
+    __syncthreads();
+    const int cell = s_cell[cs];
+
+    // ---- load: own node (coalesced: consecutive threads, consecutive nodes)
+    // and this thread's share of the cells' neighbour face traces ------------
+    Prim<DIM> own;
+    double lr = 0.0, be = 0.0, lb = 0.0;
+    if (cell >= 0) {
+      const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
+      double u[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
+      if (a.form) {
+        const double a1 = s_ca1[cs], ap = s_cap[cs];
+        double k1[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) k1[v] = __ldg(a.K1 + gi + v);
+        if (ap != 0.0) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) u[v] = u[v] + fma(a1, k1[v], ap * __ldg(a.Kp + gi + v));
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) u[v] = fma(a1, k1[v], u[v]);
+        }
+      }
+      own = prim_of<DIM>(ph, u);
+      if (!prim_ok<DIM>(own)) report_bad(st, a.stage, a.ncells, cell);
+      be = own.rho * frcp(own.p);
+      lr = log(own.rho);
+      lb = log(be);
+      pr[S::RHO * T + tid] = own.rho;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) pr[(S::V0 + i) * T + tid] = own.v[i];
+      pr[S::P * T + tid] = own.p;
+      pr[S::E * T + tid] = own.E;
+      pr[S::LRHO * T + tid] = lr;
+      pr[S::BETA * T + tid] = be;
+      pr[S::LBETA * T + tid] = lb;
+    }
+#pragma unroll
+    for (int q = tid; q < CPB * NFP; q += T) {
+      const int c2 = q / NFP, r = q % NFP, f = r / FP, pt = r % FP;
+      const int d = f >> 1, side = f & 1;
+      if (s_cell[c2] < 0) continue;
+      const int nbc = s_nbc[c2][f];
+      // the neighbour's node on the shared face: far end of the same line
+      const int node =
+          line_base<DIM>(d, pt % N1, pt / N1) + (side ? 0 : N1 - 1) * line_stride(d);
+      const size_t gi = (static_cast<size_t>(nbc) * NPC + node) * V;
+      double u[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
+      if (a.form) {
+        const double b1 = s_na1[c2][f], bp = s_nap[c2][f];
+        double k1[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) k1[v] = __ldg(a.K1 + gi + v);
+        if (bp != 0.0) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) u[v] = u[v] + fma(b1, k1[v], bp * __ldg(a.Kp + gi + v));
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) u[v] = fma(b1, k1[v], u[v]);
+        }
+      }
+      double* o = nb + q * V;
+#pragma unroll
+      for (int v = 0; v < V; ++v) o[v] = u[v];
+    }
+    __syncthreads();
+
+    double K[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) K[v] = 0.0;
+    if (cell >= 0) {
+      direction_terms<DIM, SURF, 0>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][0], &s_nbc[cs][2 * (0)], own, lr, be, lb, K);
+      direction_terms<DIM, SURF, 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][1], &s_nbc[cs][2 * (1)], own, lr, be, lb, K);
+      if constexpr (DIM == 3)
+        direction_terms<DIM, SURF, DIM - 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][DIM - 1], &s_nbc[cs][2 * (DIM - 1)], own, lr, be, lb, K);
+
+      // ---- epilogue: entropy products, K and d stores (coalesced) -------------
+      if (a.want_dh || a.want_h) {
+        // log(p / rho^gamma) = -(log beta + (gamma - 1) log rho)
+        const double s_therm = -(lb + ph.gm1 * lr);
+        const double om = node_measure<DIM>(m, s_coord[cs][0], s_coord[cs][1], s_coord[cs][2], l);
+        if (a.want_dh) {
+          double v2 = 0.0, dot = 0.0;
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) {
+            v2 = fma(own.v[i], own.v[i], v2);
+            dot = fma(ph.gm1 * be * own.v[i], K[1 + i], dot);
+          }
+          dot = fma(ph.gamma - s_therm - 0.5 * ph.gm1 * be * v2, K[0], dot);
+          dot = fma(-ph.gm1 * be, K[DIM + 1], dot);
+          acc_dh = dd_add_prod(acc_dh, om, dot);
+        }
+        if (a.want_h) acc_h = dd_add_prod(acc_h, om, -own.rho * s_therm);
+      }
+      const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
+      if (a.write_k)
+#pragma unroll
+        for (int v = 0; v < V; ++v) a.Kout[gi + v] = K[v];
+      if (a.d_mode) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const double dn = a.d_mode == 1 ? a.b * K[v] : fma(a.b, K[v], a.d[gi + v]);
+          a.d[gi + v] = dn;
+          if (a.want_dmax) {
+            dbad = dbad || !isfinite(dn);
+            dmax = fmax(dmax, fabs(dn));
+          }
+        }
+      }
+    }
+    __syncthreads();  // smem of this group consumed
+  }
+
+  // ---- grid epilogue --------------------------------------------------------
+  if (a.want_dmax) {
+    dmax = warp_max(dmax);
+    if ((tid & 31) == 0) atomic_max_pos(&st->dmax_bits, dmax);
+    if (dbad) st->d_nonfinite = 1;
+  }
+  dd v[2] = {acc_dh, acc_h}, tot[2];
+  if (a.want_dh || a.want_h) block_reduce_dd<2>(v, s_red);
+  if (grid_reduce_dd<2>(v, partials, counter, s_red, tot) && tid == 0) {
+    if (a.want_dh) {
+      const dd inc = dd_mul_d(tot[0], dt * a.b);
+      const dd cur = {st->dh_hi, st->dh_lo};
+      const dd nw = dd_add(cur, inc);
+      st->dh_hi = nw.hi;
+      st->dh_lo = nw.lo;
+    }
+    if (a.want_h) {
+      st->h_hi = tot[1].hi;
+      st->h_lo = tot[1].lo;
+    }
+    if (st->bad_code != kNoBad) st->aborted = 1;
+  }
+}
+
+}  // namespace dev
+}  // namespace perrk

@@ -588,10 +588,13 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     set_device(c);
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    c->grid_stage = 8 * 148;  // fixed (not device-derived) so reductions are reproducible
-    c->grid_flat = 8 * 148;
-    (void)sms;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    // persistent stage grid: exactly the resident capacity, so the active
+    // cells are swept in order and neighbour traces are L2 hits; a function
+    // of the device only, so block partials (and the sums) are reproducible
+    const int occ = stage_blocks_per_sm(c->dim, sf);
+    c->grid_stage = sms * (occ > 0 ? occ : 1);
+    c->grid_flat = 8 * sms;
     const size_t bytes = sizeof(double) * c->ndofs;
     for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK}) {
       CK(cudaMalloc(p, bytes));
