@@ -1,0 +1,70 @@
+// TEST: the drop-in as a reference maintainer would use it.  Compiled against
+// the UNMODIFIED reference headers and objects (oracle/_ref, built from
+// /root/reference) plus include/perrk_b200.hpp and libperrk_b200.so:
+// identical call sites, reference perk_step vs perrk_b200::perk_step.
+//   exit 0  parity within tolerance (GPU present)
+//   exit 3  no CUDA device: the adapter threw perrk::Error (fails loudly)
+#include <cmath>
+#include <cstdio>
+#include <memory>
+
+#include "perrk/butcher.hpp"
+#include "perrk/mesh.hpp"
+#include "perrk/physics.hpp"
+#include "perrk/relax.hpp"
+#include "perrk/semidisc.hpp"
+#include "perrk/stepper.hpp"
+#include "perrk_b200.hpp"
+
+int main() {
+  using namespace perrk;
+  SemidiscretizationSpec spec;
+  Mesh2DRect mesh = build_uniform_mesh2d(10.0, 16);
+  spec.mesh = mesh;
+  spec.polydeg = 3;
+  spec.physics = std::make_shared<EulerPhysics>(2, 1.4);
+  spec.surface_flux = FluxTag::rusanov;
+  spec.volume_mode = VolumeMode::flux_differencing;
+  spec.volume_flux = FluxTag::ec;
+  Semidiscretization ref(spec);
+  VortexParams vp;
+  vp.gamma = 1.4;
+  vp.mach = 1.0 / std::sqrt(1.4);
+  vp.radius = 1.0;
+  vp.intensity = 5.0;
+  vp.rho_inf = 1.0;
+  vp.v_inf[0] = vp.v_inf[1] = 1.0;
+  vp.half_width = 10.0;
+  StateVector U0 = ref.project([&](double x, double y, double* u) {
+    isentropic_vortex_state(vp, x, y, 0.0, u);
+  });
+  const PartitionFamily fam = build_perk2(4, {4}, {{0.2, 0.35}});
+  const PartitionMap map = make_partition_map(spec.mesh, std::vector<int>(mesh.num_cells(), 1), 1);
+  RelaxationConfig rc;
+  PerkStepOptions opts;
+  opts.relaxation = &rc;
+  const double dt = 0.02;
+
+  std::unique_ptr<perrk_b200::Semidiscretization> gpu;
+  try {
+    gpu = std::make_unique<perrk_b200::Semidiscretization>(spec);
+  } catch (const perrk::Error& e) {
+    std::printf("adapter: no device (%s)\n", e.what());
+    return 3;
+  }
+  StateVector Ur = U0, Ug = U0;
+  double tr = 0.0, tg = 0.0, worst_g = 0.0, worst_u = 0.0;
+  for (int k = 0; k < 5; ++k) {
+    const auto rr = perk_step(Ur, tr, dt, fam, map, ref, opts);
+    const auto rg = perrk_b200::perk_step(Ug, tg, dt, fam, map, *gpu, opts);
+    worst_g = std::fmax(worst_g, std::fabs(rr.outcome.gamma - rg.outcome.gamma));
+  }
+  double num = 0.0, den = 0.0;
+  for (std::size_t i = 0; i < Ur.size(); ++i) {
+    num += (Ur[i] - Ug[i]) * (Ur[i] - Ug[i]);
+    den += Ur[i] * Ur[i];
+  }
+  worst_u = std::sqrt(num / den);
+  std::printf("adapter parity: gamma %.3e state %.3e t %.3e\n", worst_g, worst_u, std::fabs(tr - tg));
+  return (worst_g < 1e-12 && worst_u < 1e-12 && std::fabs(tr - tg) < 1e-13) ? 0 : 1;
+}

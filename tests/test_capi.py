@@ -132,3 +132,17 @@ def test_dof_stage_count_matches_active_sets():
                  for lv, n in enumerate(counts, start=1))
     assert per_step == manual
     assert 5 * 64 ** 4 <= per_step <= 14 * 64 ** 4
+
+
+def test_cpp_adapter_fails_loudly_without_device():
+    """include/perrk_b200.hpp compiled against the reference headers/objects
+    (oracle/_ref/adapter_parity): with no CUDA device the drop-in throws
+    perrk::Error instead of falling back to the CPU."""
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "adapter_parity")
+    if not os.path.exists(exe):
+        pytest.skip("adapter_parity not built (make -C oracle adapter)")
+    if HAS_GPU:
+        pytest.skip("device present: covered by the gpu parity test")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 3, r.stdout + r.stderr

@@ -272,3 +272,16 @@ def test_tgv_initial_rhs_3d_vs_oracle():
     orc = O.Orc(mesh)
     U = np.ascontiguousarray(W.taylor_green(semi.node_x(), semi.node_y(), semi.node_z()).T).reshape(-1)
     assert max_rel(semi.rhs(0.0, U), orc.rhs(0.0, U)) < 1e-12
+
+
+def test_cpp_adapter_drop_in_parity():
+    """The reference's own perk_step vs perrk_b200::perk_step at identical C++
+    call sites (tests/cpp/adapter_parity.cpp, built against the unmodified
+    reference in oracle/_ref)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(O.REF_LIB), "adapter_parity")
+    if not os.path.exists(exe):
+        pytest.skip("adapter_parity not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr

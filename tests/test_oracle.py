@@ -306,3 +306,21 @@ def test_golden_family_text_roundtrip():
         assert np.array_equal(fam.A, g[f"A_{key}"])
         assert np.array_equal(fam.b, g[f"b_{key}"])
         assert np.array_equal(fam.c, g[f"c_{key}"])
+
+
+# --------------------------------------------------------------------------- the reference's own suites
+REF_TESTS = ["test_basis", "test_butcher", "test_dg", "test_mesh", "test_physics", "test_relax"]
+
+
+@pytest.mark.parametrize("name", REF_TESTS)
+def test_reference_own_suite_passes(name):
+    """The reference's Eigen-free doctest suites (proj/tests), compiled against
+    oracle/_ref through oracle/doctest_shim, pass: the checker library is
+    the reference as its authors test it."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(O.REF_LIB), name)
+    if not os.path.exists(exe):
+        pytest.skip("reference test binaries not built (make -C oracle ref-tests)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "failed: 0" in r.stdout
