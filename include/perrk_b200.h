@@ -230,13 +230,36 @@ int perrk_step_traffic(const perrk_ctx* ctx, double* stage_bytes, double* pass_b
                        double* update_bytes);
 int perrk_fp64_peak(int device, double* gflops);
 
-/* ---- multi-GPU: element-slab decomposition over NCCL --------------------
- * nccl_id: the 128-byte ncclUniqueId from rank 0 (broadcast by the caller,
- * e.g. through torch.distributed).  After this call the context owns the
- * slab [slab_begin, slab_end) of the last axis's cell layers; states passed
- * to upload/download are the rank-local slab. */
-int perrk_comm_init(perrk_ctx* ctx, const void* nccl_id, int rank, int nranks);
+/* ---- multi-GPU: element-slab decomposition ---------------
+ * No reference counterpart (the reference is single-process).  The mesh is
+ * cut into contiguous slabs of last-axis cell layers (z in 3D, y in 2D), one
+ * per rank (one process per GPU).  Per stage each rank packs the formed stage
+ * traces of its two boundary layers and exchanges them with the slab
+ * neighbours (periodic ring: ncclSend/ncclRecv); the reductions (dH, the
+ * Newton residual/derivative, max |d|, the CFL speed, H and invariants) are
+ * per-rank double-double partials all-gathered and summed in rank order.
+ *
+ * nccl_id: the 128-byte ncclUniqueId from perrk_nccl_id on rank 0 (broadcast
+ * by the caller, e.g. through torch.distributed).  layer_cuts: nranks+1
+ * increasing layer indices (NULL: uniform).  Call before perrk_set_family;
+ * afterwards upload/download/geometry refer to the rank's slab, while
+ * perrk_set_family still takes the GLOBAL effective-level array and
+ * positivity reports carry global cell ids.  nranks == 1 is a no-op. */
+int perrk_nccl_id(void* nccl_id_out);
+int perrk_comm_init(perrk_ctx* ctx, const void* nccl_id, int rank, int nranks,
+                    const int* layer_cuts);
 int perrk_slab_range(const perrk_ctx* ctx, int* layer_begin, int* layer_end);
+/* Test harness for the multi-rank logic on ONE device: the n contexts (same
+ * global mesh) become ranks 0..n-1 of a group sharing one stream; the halo
+ * and the gathers are stream-ordered device copies.  perrk_advance /
+ * perrk_perk_step_resident / perrk_compute_dt(U = NULL) on any member then
+ * step every member. */
+int perrk_loopback_group(perrk_ctx** ctxs, int n, const int* layer_cuts);
+/* Host helpers (no device work): balanced contiguous cuts from per-layer work
+ * (NULL: uniform), and the cell-local node indices of the last-axis face
+ * traces (side 0: bottom, 1: top) in exchange order. */
+int perrk_slab_cuts(int n_last, const double* layer_work, int nranks, int* cuts);
+int perrk_slab_trace_nodes(int dim, int side, int* nodes);
 
 #ifdef __cplusplus
 }

@@ -34,7 +34,7 @@ def build(force=False, verbose=False):
            "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"),
            *[os.path.join(CSRC, f) for f in SOURCES],
-           "-o", LIB + ".tmp", "-lcudart"]
+           "-o", LIB + ".tmp", "-lcudart", "-lnccl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

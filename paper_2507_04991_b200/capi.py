@@ -104,8 +104,12 @@ _PROTOS = {
     "perrk_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "perrk_step_traffic": (C.c_int, [_P, _D, _D, _D]),
     "perrk_fp64_peak": (C.c_int, [C.c_int, _D]),
-    "perrk_comm_init": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int]),
+    "perrk_nccl_id": (C.c_int, [C.c_void_p]),
+    "perrk_comm_init": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int, _I]),
     "perrk_slab_range": (C.c_int, [_P, _I, _I]),
+    "perrk_loopback_group": (C.c_int, [C.POINTER(_P), C.c_int, _I]),
+    "perrk_slab_cuts": (C.c_int, [C.c_int, _D, C.c_int, _I]),
+    "perrk_slab_trace_nodes": (C.c_int, [C.c_int, C.c_int, _I]),
 }
 EXPORTED = tuple(_PROTOS)
 

@@ -242,8 +242,16 @@ __global__ void __launch_bounds__(256)
   }
   dd v[2] = {A, B}, tot[2];
   block_reduce_dd<2>(v, s_red);
-  if (grid_reduce_dd<2>(v, partials, counter, s_red, tot) && threadIdx.x == 0)
-    relax_newton_update(st, tot[0], tot[1]);
+  if (grid_reduce_dd<2>(v, partials, counter, s_red, tot) && threadIdx.x == 0) {
+    if (st->slab) {  // gathered over ranks, then combine_kernel(COMBINE_RELAX)
+      st->red_local[R_A_HI] = tot[0].hi;
+      st->red_local[R_A_LO] = tot[0].lo;
+      st->red_local[R_B_HI] = tot[1].hi;
+      st->red_local[R_B_LO] = tot[1].lo;
+    } else {
+      relax_newton_update(st, tot[0], tot[1]);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -298,6 +306,13 @@ __global__ void __launch_bounds__(256)
   dd tot[6];
   if (want_record) block_reduce_dd<6>(acc, s_red);
   if (grid_reduce_dd<6>(acc, partials, counter, s_red, tot) && threadIdx.x == 0) {
+    if (st->slab) {  // gathered over ranks, then combine_kernel(COMBINE_UPDATE)
+      for (int r = 0; r < 6; ++r) {
+        st->red_local[R_REC0 + 2 * r] = tot[r].hi;
+        st->red_local[R_REC0 + 2 * r + 1] = tot[r].lo;
+      }
+      return;
+    }
     const double dt = st->dt;
     if (st->relax_enabled && !st->idt)
       st->t += gamma * dt;
@@ -490,9 +505,116 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters,
   if (s == 12345.678) out[0] = s;
 }
 
+// ---------------------------------------------------------------------------
+// slab decomposition: reduction points (stash local -> gather -> combine)
+// ---------------------------------------------------------------------------
+enum { COMBINE_STAGES = 0, COMBINE_RELAX = 1, COMBINE_UPDATE = 2, COMBINE_NUMAX = 3 };
+
+// copy this rank's partials kept in StepState fields into red_local
+__global__ void stash_kernel(StepState* st, int mode) {
+  double* r = st->red_local;
+  if (mode == COMBINE_STAGES) {
+    r[R_DH_HI] = st->dh_hi;
+    r[R_DH_LO] = st->dh_lo;
+    r[R_H_HI] = st->h_hi;
+    r[R_H_LO] = st->h_lo;
+    r[R_DMAX] = __longlong_as_double(static_cast<long long>(st->dmax_bits));
+    r[R_DBAD] = st->d_nonfinite;
+    r[R_BAD] = static_cast<double>(st->bad_code == kNoBad ? -1 : st->bad_code);
+  }
+  r[R_NUMAX] = __longlong_as_double(static_cast<long long>(st->numax_bits));
+}
+
+// all[nranks][NRED]: sums in rank order (double-double), maxima, minima;
+// then the scalar logic that the single-GPU kernels run in their last block
+__global__ void combine_kernel(StepState* st, const double* all, int nranks, int mode) {
+  auto sum = [&](int hi, int lo) {
+    dd acc = dd_zero();
+    for (int q = 0; q < nranks; ++q) acc = dd_add(acc, dd{all[q * NRED + hi], all[q * NRED + lo]});
+    return acc;
+  };
+  auto vmax = [&](int k) {
+    double v = all[k];
+    for (int q = 1; q < nranks; ++q) v = fmax(v, all[q * NRED + k]);
+    return v;
+  };
+  if (mode == COMBINE_NUMAX || mode == COMBINE_UPDATE) {
+    const double nu = vmax(R_NUMAX);
+    st->numax_bits = static_cast<unsigned long long>(__double_as_longlong(nu));
+  }
+  if (mode == COMBINE_STAGES) {
+    const dd dh = sum(R_DH_HI, R_DH_LO), h = sum(R_H_HI, R_H_LO);
+    st->dh_hi = dh.hi;
+    st->dh_lo = dh.lo;
+    st->h_hi = h.hi;
+    st->h_lo = h.lo;
+    st->dmax_bits = static_cast<unsigned long long>(__double_as_longlong(vmax(R_DMAX)));
+    st->d_nonfinite = vmax(R_DBAD) > 0.0 ? 1 : 0;
+    long long bad = kNoBad;
+    for (int q = 0; q < nranks; ++q) {
+      const double b = all[q * NRED + R_BAD];
+      if (b >= 0.0 && static_cast<long long>(b) < bad) bad = static_cast<long long>(b);
+    }
+    st->bad_code = bad;
+    st->aborted = bad != kNoBad ? 1 : st->aborted;
+  } else if (mode == COMBINE_RELAX) {
+    if (st->aborted || st->finished || st->relax_done) return;
+    relax_newton_update(st, sum(R_A_HI, R_A_LO), sum(R_B_HI, R_B_LO));
+  } else if (mode == COMBINE_UPDATE) {
+    if (st->aborted || st->finished) return;
+    const double gamma = st->relax_enabled ? st->gamma : st->gamma_override;
+    const double dt = st->dt;
+    st->t += (st->relax_enabled && !st->idt) ? gamma * dt : dt;
+    st->gamma_seed = st->fell_back ? 1.0 : gamma;
+    st->steps_taken += 1;
+  }
+}
+
+// StepRecord row from the gathered partials (COMBINE_UPDATE), written by the
+// host-side sequencing right after combine_kernel
+__global__ void record_kernel(StepState* st, const double* all, int nranks, int V, double* records) {
+  if (st->aborted || st->finished || !records) return;
+  double* row = records + static_cast<size_t>(st->steps_taken - 1) * 11;
+  row[0] = st->t;
+  row[1] = st->dt;
+  row[2] = st->relax_enabled ? st->gamma : st->gamma_override;
+  row[3] = st->iters;
+  row[4] = st->fell_back;
+  for (int r = 0; r < 1 + V; ++r) {
+    dd acc = dd_zero();
+    for (int q = 0; q < nranks; ++q)
+      acc = dd_add(acc, dd{all[q * NRED + R_REC0 + 2 * r], all[q * NRED + R_REC0 + 2 * r + 1]});
+    row[5 + r] = acc.hi + acc.lo;
+  }
+}
+
 }  // namespace dev
 
 using namespace dev;
+
+cudaError_t launch_pack_traces(int dim, const StageArgs& a, const MeshDev& m, StepState* st,
+                               double* send_lo, double* send_hi, cudaStream_t s) {
+  const int lc = dim == 3 ? m.nc[0] * m.nc[1] : m.nc[0];
+  const int fp = dim == 3 ? 16 : 4;
+  const int grid = (2 * lc * fp + 255) / 256;
+  if (dim == 2)
+    pack_traces_kernel<2><<<grid, 256, 0, s>>>(a, m, st, send_lo, send_hi);
+  else
+    pack_traces_kernel<3><<<grid, 256, 0, s>>>(a, m, st, send_lo, send_hi);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stash(StepState* st, int mode, cudaStream_t s) {
+  stash_kernel<<<1, 1, 0, s>>>(st, mode);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(StepState* st, const double* all, int nranks, int mode, int V,
+                           double* records, cudaStream_t s) {
+  combine_kernel<<<1, 1, 0, s>>>(st, all, nranks, mode);
+  if (mode == COMBINE_UPDATE && records) record_kernel<<<1, 1, 0, s>>>(st, all, nranks, V, records);
+  return cudaGetLastError();
+}
 
 double measure_fp64_peak() {
   int sms = 148;

@@ -26,7 +26,8 @@ struct StageArgs {
   int want_h;            // H(U_n) (stage 0)
   int want_dmax;         // max |d| (last b-stage)
   int stage;
-  long long ncells;
+  long long ncells;      // GLOBAL cells (positivity codes are stage * ncells + global cell)
+  long long cell_offset; // global id of local cell 0
 };
 
 double measure_fp64_peak();  // GFLOP/s on the current device (DFMA loop)
@@ -53,6 +54,14 @@ cudaError_t launch_nu_cell(int dim, const double* U, const dev::MeshDev& m, cons
 cudaError_t launch_quad(int dim, const double* U, const double* K, const dev::MeshDev& m,
                         const dev::Phys& ph, int mode, double* partials, unsigned* counter,
                         double* out, long long nnodes, int grid, cudaStream_t s);
+// element-slab decomposition
+enum { RED_STAGES = 0, RED_RELAX = 1, RED_UPDATE = 2, RED_NUMAX = 3 };
+cudaError_t launch_pack_traces(int dim, const StageArgs& a, const dev::MeshDev& m,
+                               dev::StepState* st, double* send_lo, double* send_hi,
+                               cudaStream_t s);
+cudaError_t launch_stash(dev::StepState* st, int mode, cudaStream_t s);
+cudaError_t launch_combine(dev::StepState* st, const double* all, int nranks, int mode, int V,
+                           double* records, cudaStream_t s);
 cudaError_t launch_admissible(int dim, const double* U, const dev::Phys& ph, int* first_bad,
                               long long nnodes, int grid, cudaStream_t s);
 

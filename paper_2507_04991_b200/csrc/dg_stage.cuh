@@ -299,7 +299,8 @@ template <int DIM, int SURF, int D>
 __device__ __forceinline__ void direction_terms(const Phys& ph, const MeshDev& m, StepState* st,
                                                 const StageArgs& a, const double* pr,
                                                 const double* nb, int tid, int cs,
-                                                const int (&il)[3], int cd, const int* nbc,
+                                                const int (&il)[3], int cd,
+                                                const long long* nbc,
                                                 const Prim<DIM>& own, double lr, double be,
                                                 double lb, double* K) {
   using G = StageGeo<DIM>;
@@ -365,7 +366,8 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
   __shared__ int s_cell[CPB];
   __shared__ int s_coord[CPB][3];
   __shared__ double s_ca1[CPB], s_cap[CPB];
-  __shared__ int s_nbc[CPB][2 * DIM];
+  __shared__ int s_nbc[CPB][2 * DIM];          // local neighbour, or -1 - face cell (ghost)
+  __shared__ long long s_nbg[CPB][2 * DIM];    // global id (positivity reports)
   __shared__ double s_na1[CPB][2 * DIM], s_nap[CPB][2 * DIM];
   __shared__ double s_red[2 * 2 * (T / 32)];
 
@@ -401,16 +403,29 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
       s_ca1[tid] = dt * a.a1[lev];
       s_cap[tid] = dt * a.ap[lev];
 #pragma unroll
-      for (int f = 0; f < 2 * DIM; ++f) {  // periodic face neighbours, their rows
+      for (int f = 0; f < 2 * DIM; ++f) {  // face neighbours (periodic / ghost), their rows
         const int d = f >> 1, side = f & 1;
         int c3[3] = {co[0], co[1], co[2]};
         const int nd = m.nc[d];
+        const bool ghost = m.slab && d == DIM - 1 && (side ? c3[d] + 1 == nd : c3[d] == 0);
         c3[d] = side ? (c3[d] + 1 == nd ? 0 : c3[d] + 1) : (c3[d] == 0 ? nd - 1 : c3[d] - 1);
         const int nbc = c3[0] + m.nc[0] * (c3[1] + m.nc[1] * c3[2]);
-        const int l2 = m.level[nbc];
-        s_nbc[tid][f] = nbc;
-        s_na1[tid][f] = dt * a.a1[l2];
-        s_nap[tid][f] = dt * a.ap[l2];
+        const long long layer_cells = DIM == 3 ? static_cast<long long>(m.nc[0]) * m.nc[1] : m.nc[0];
+        if (ghost) {
+          // traces received from the neighbouring slab; no formation here
+          const int fc = DIM == 3 ? co[0] + m.nc[0] * co[1] : co[0];
+          const int gl = side ? (m.layer0 + nd) % m.nlast : (m.layer0 - 1 + m.nlast) % m.nlast;
+          s_nbc[tid][f] = -1 - fc;
+          s_nbg[tid][f] = fc + layer_cells * gl;
+          s_na1[tid][f] = 0.0;
+          s_nap[tid][f] = 0.0;
+        } else {
+          const int l2 = m.level[nbc];
+          s_nbc[tid][f] = nbc;
+          s_nbg[tid][f] = nbc + a.cell_offset;
+          s_na1[tid][f] = dt * a.a1[l2];
+          s_nap[tid][f] = dt * a.ap[l2];
+        }
       }
       const int slot = (grp + gridDim.x) * CPB + tid;  // prefetch the next group
       nx_cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
@@ -441,7 +456,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
         }
       }
       own = prim_of<DIM>(ph, u);
-      if (!prim_ok<DIM>(own)) report_bad(st, a.stage, a.ncells, cell);
+      if (!prim_ok<DIM>(own)) report_bad(st, a.stage, a.ncells, cell + a.cell_offset);
       be = own.rho * frcp(own.p);
       lr = log(own.rho);
       lb = log(be);
@@ -460,6 +475,13 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
       const int d = f >> 1, side = f & 1;
       if (s_cell[c2] < 0) continue;
       const int nbc = s_nbc[c2][f];
+      double* o = nb + q * V;
+      if (nbc < 0) {  // slab boundary: formed trace from the neighbouring rank
+        const double* g = (side ? m.ghost_hi : m.ghost_lo) + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
+#pragma unroll
+        for (int v = 0; v < V; ++v) o[v] = g[v];
+        continue;
+      }
       // the neighbour's node on the shared face: far end of the same line
       const int node =
           line_base<DIM>(d, pt % N1, pt / N1) + (side ? 0 : N1 - 1) * line_stride(d);
@@ -480,7 +502,6 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
           for (int v = 0; v < V; ++v) u[v] = fma(b1, k1[v], u[v]);
         }
       }
-      double* o = nb + q * V;
 #pragma unroll
       for (int v = 0; v < V; ++v) o[v] = u[v];
     }
@@ -490,10 +511,10 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
 #pragma unroll
     for (int v = 0; v < V; ++v) K[v] = 0.0;
     if (cell >= 0) {
-      direction_terms<DIM, SURF, 0>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][0], &s_nbc[cs][2 * (0)], own, lr, be, lb, K);
-      direction_terms<DIM, SURF, 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][1], &s_nbc[cs][2 * (1)], own, lr, be, lb, K);
+      direction_terms<DIM, SURF, 0>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][0], &s_nbg[cs][2 * (0)], own, lr, be, lb, K);
+      direction_terms<DIM, SURF, 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][1], &s_nbg[cs][2 * (1)], own, lr, be, lb, K);
       if constexpr (DIM == 3)
-        direction_terms<DIM, SURF, DIM - 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][DIM - 1], &s_nbc[cs][2 * (DIM - 1)], own, lr, be, lb, K);
+        direction_terms<DIM, SURF, DIM - 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][DIM - 1], &s_nbg[cs][2 * (DIM - 1)], own, lr, be, lb, K);
 
       // ---- epilogue: entropy products, K and d stores (coalesced) -------------
       if (a.want_dh || a.want_h) {
@@ -553,6 +574,47 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
       st->h_lo = tot[1].lo;
     }
     if (st->bad_code != kNoBad) st->aborted = 1;
+  }
+}
+
+// Slab decomposition: formed stage traces of the slab's boundary layers,
+// packed for the neighbouring ranks (stepper.cpp:60-72 restricted to the
+// face nodes the neighbour's stage kernel reads).  send_lo: bottom face of
+// local layer 0 (-> the rank below, its ghost_hi); send_hi: top face of the
+// last local layer (-> the rank above, its ghost_lo).  [face cell][FP][V].
+template <int DIM>
+__global__ void __launch_bounds__(256)
+    pack_traces_kernel(StageArgs a, MeshDev m, StepState* st, double* send_lo, double* send_hi) {
+  using G = StageGeo<DIM>;
+  constexpr int V = G::V, NPC = G::NPC, FP = G::FP, D = DIM - 1;
+  if (st->aborted || st->finished) return;
+  const int layer_cells = DIM == 3 ? m.nc[0] * m.nc[1] : m.nc[0];
+  const int nloc = m.nc[D];
+  const double dt = st->dt;
+  const int total = 2 * layer_cells * FP;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
+    const int side = q / (layer_cells * FP), r = q % (layer_cells * FP);
+    const int fc = r / FP, pt = r % FP;
+    const int cell = fc + layer_cells * (side ? nloc - 1 : 0);
+    const int node = line_base<DIM>(D, pt % N1, pt / N1) + (side ? N1 - 1 : 0) * line_stride(D);
+    const size_t gi = (static_cast<size_t>(cell) * NPC + node) * V;
+    double u[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
+    if (a.form) {
+      const int lev = m.level[cell];
+      const double b1 = dt * a.a1[lev], bp = dt * a.ap[lev];
+      if (bp != 0.0) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) u[v] = u[v] + fma(b1, __ldg(a.K1 + gi + v), bp * __ldg(a.Kp + gi + v));
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) u[v] = fma(b1, __ldg(a.K1 + gi + v), u[v]);
+      }
+    }
+    double* o = (side ? send_hi : send_lo) + (static_cast<size_t>(fc) * FP + pt) * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v) o[v] = u[v];
   }
 }
 

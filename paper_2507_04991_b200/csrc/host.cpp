@@ -12,7 +12,10 @@
 #include <string>
 #include <vector>
 
+#include <memory>
+
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include "../../include/perrk_b200.h"
 #include "dg_launch.hpp"
@@ -243,10 +246,32 @@ struct StagePlan {
 };
 
 }  // namespace
+
 }  // namespace perrk
 
 using namespace perrk;
 using perrk::dev::StepState;
+
+struct perrk_ctx;
+namespace perrk {
+// A set of contexts that step together: one rank's context under NCCL (one
+// process per GPU), or several contexts on one device and one stream that
+// exchange through device copies (loopback; the test harness for the
+// multi-rank logic on a single GPU).
+struct Exchange {
+  virtual ~Exchange() = default;
+  // send_lo / send_hi of every rank -> ghost_hi of the rank below / ghost_lo above
+  virtual void halo(std::vector<perrk_ctx*>& g) = 0;
+  // StepState::red_local of every rank -> red_all[rank][NRED] on every rank
+  virtual void gather(std::vector<perrk_ctx*>& g) = 0;
+};
+
+struct Group {
+  std::vector<perrk_ctx*> members;
+  std::unique_ptr<Exchange> ex;  // null: a single context on the whole mesh
+};
+
+}  // namespace perrk
 
 struct perrk_ctx {
   int device = 0;
@@ -281,6 +306,15 @@ struct perrk_ctx {
   std::vector<int> E, eff;
   std::vector<StagePlan> plan;
   uint64_t evals = 0;
+  // element-slab decomposition: this context owns global
+  // layers [layer0, layer0 + nc[last]) of the last axis
+  bool slab = false;
+  int rank = 0, nranks = 1, layer0 = 0, nlast = 1;
+  int ncg[3] = {1, 1, 1};
+  long long ncells_global = 0, layer_cells = 0;
+  double *ghost_lo = nullptr, *ghost_hi = nullptr, *send_lo = nullptr, *send_hi = nullptr;
+  double* red_all = nullptr;  // [nranks][NRED]
+  std::shared_ptr<perrk::Group> group;
   // instrumentation: launch counter and per-stage-launch event pairs
   bool own_stream = true;
   int64_t launches = 0;
@@ -299,8 +333,19 @@ struct perrk_ctx {
     }
     m.dim = dim;
     m.level = dlevel;
+    const int L = dim - 1;
+    m.slab = slab ? 1 : 0;
+    m.layer0 = layer0;
+    m.nlast = nlast;
+    m.h[L] = dh[L] + layer0;
+    m.jac[L] = djac[L] + layer0;
+    m.lift[L] = dlift[L] + layer0;
+    m.ghost_lo = ghost_lo;
+    m.ghost_hi = ghost_hi;
     return m;
   }
+  size_t ndofs_() const { return static_cast<size_t>(ndofs); }
+  size_t trace_doubles() const { return static_cast<size_t>(layer_cells) * (dim == 3 ? 16 : 4) * V; }
   double* kbuf(int id) { return id == 0 ? K1 : (id == 1 ? Ka : Kb); }
 };
 
@@ -391,7 +436,8 @@ void build_plan(perrk_ctx* c) {
     a.want_dmax = i == last_b;
     a.want_h = 0;
     a.stage = i;
-    a.ncells = c->ncells;
+    a.ncells = c->ncells_global;
+    a.cell_offset = static_cast<long long>(c->layer0) * c->layer_cells;
     a.list = p.dlist;
     a.n = p.n;
     // compulsory traffic per active cell, in node-vectors of 8V bytes:
@@ -417,53 +463,101 @@ struct StepMode {
   perrk_relax_cfg cfg{};
   bool want_nu = false;
   bool want_record = false;
-  double* records = nullptr;
+  double* records = nullptr;  // non-null: each member writes its own c->records
+  double* records_of(perrk_ctx* c) const { return records ? c->records : nullptr; }
 };
 
-// Enqueue one perk_step (stepper.cpp:17-114) on the resident state.
-void enqueue_step(perrk_ctx* c, const StepMode& mode, bool want_h) {
-  const dev::MeshDev m = c->mesh();
-  CK(launch_begin_step(c->st, c->stream));
-  for (int i = 0; i < c->S; ++i) {
-    StagePlan& p = c->plan[i];
-    StageArgs a = p.args;
-    a.U = c->U;
-    a.K1 = c->K1;
-    a.Kp = p.kin >= 0 ? c->kbuf(p.kin) : c->K1;
-    a.Kout = c->kbuf(p.kout);
-    a.d = c->d;
-    a.want_h = (i == 0 && want_h) ? 1 : 0;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (c->profiling) {
-      if (c->ev_used + 2 > c->ev_pool.size()) {
-        for (int q = 0; q < 64; ++q) {
-          cudaEvent_t ev;
-          CK(cudaEventCreate(&ev));
-          c->ev_pool.push_back(ev);
-        }
+// Enqueue the stage launches of stage i of one context.
+void enqueue_stage(perrk_ctx* c, int i, bool want_h) {
+  StagePlan& p = c->plan[i];
+  StageArgs a = p.args;
+  a.U = c->U;
+  a.K1 = c->K1;
+  a.Kp = p.kin >= 0 ? c->kbuf(p.kin) : c->K1;
+  a.Kout = c->kbuf(p.kout);
+  a.d = c->d;
+  a.want_h = (i == 0 && want_h) ? 1 : 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) {
+    if (c->ev_used + 2 > c->ev_pool.size()) {
+      for (int q = 0; q < 64; ++q) {
+        cudaEvent_t ev;
+        CK(cudaEventCreate(&ev));
+        c->ev_pool.push_back(ev);
       }
-      e0 = c->ev_pool[c->ev_used++];
-      e1 = c->ev_pool[c->ev_used++];
-      c->ev_bytes.push_back(p.bytes);
-      CK(cudaEventRecord(e0, c->stream));
     }
-    CK(launch_stage(c->dim, c->surface, a, m, c->ph, c->st, c->partials, c->counter,
-                    c->grid_stage, c->stream));
-    if (c->profiling) CK(cudaEventRecord(e1, c->stream));
-    c->launches += p.n > 0 ? 1 : 0;
+    e0 = c->ev_pool[c->ev_used++];
+    e1 = c->ev_pool[c->ev_used++];
+    c->ev_bytes.push_back(p.bytes);
+    CK(cudaEventRecord(e0, c->stream));
   }
-  c->launches += 2 + (mode.relax ? (mode.cfg.numerics == 1 ? mode.cfg.max_iter
-                                                           : mode.cfg.max_iter + 1)
-                                 : 0);
+  CK(launch_stage(c->dim, c->surface, a, c->mesh(), c->ph, c->st, c->partials, c->counter,
+                  c->grid_stage, c->stream));
+  if (c->profiling) CK(cudaEventRecord(e1, c->stream));
+  c->launches += p.n > 0 ? 1 : 0;
+}
+
+void enqueue_pack(perrk_ctx* c, int i) {
+  StageArgs a = c->plan[i].args;
+  a.U = c->U;
+  a.K1 = c->K1;
+  a.Kp = c->plan[i].kin >= 0 ? c->kbuf(c->plan[i].kin) : c->K1;
+  CK(launch_pack_traces(c->dim, a, c->mesh(), c->st, c->send_lo, c->send_hi, c->stream));
+  c->launches += 1;
+}
+
+// One reduction point of the slab decomposition: local partials -> every
+// rank -> combined (sums in rank order, so every rank holds the same bits).
+void reduce_point(Group& g, int mode, bool stash, double* records = nullptr) {
+  if (stash)
+    for (perrk_ctx* c : g.members) CK(launch_stash(c->st, mode, c->stream));
+  g.ex->gather(g.members);
+  for (perrk_ctx* c : g.members) {
+    CK(launch_combine(c->st, c->red_all, c->nranks, mode, c->V,
+                      mode == RED_UPDATE ? (records ? c->records : nullptr) : nullptr, c->stream));
+    c->launches += (stash ? 1 : 0) + 1 + (records && mode == RED_UPDATE ? 1 : 0);
+  }
+}
+
+// Enqueue one perk_step (stepper.cpp:17-114) on the resident state of every
+// member of the group.  Single context on the whole mesh: each kernel's last
+// block finishes its own reduction (no host or collective in the chain).
+// Slab decomposition: per stage, the boundary traces are packed and
+// exchanged before the stage kernels; after the last stage, after every
+// relaxation pass and after the update the partials go through reduce_point.
+void enqueue_step(Group& g, const StepMode& mode, bool want_h) {
+  const bool slab = g.ex != nullptr;
+  for (perrk_ctx* c : g.members) {
+    CK(launch_begin_step(c->st, c->stream));
+    c->launches += 1;
+  }
+  const int S = g.members[0]->S;
+  for (int i = 0; i < S; ++i) {
+    if (slab) {
+      for (perrk_ctx* c : g.members) enqueue_pack(c, i);
+      g.ex->halo(g.members);
+    }
+    for (perrk_ctx* c : g.members) enqueue_stage(c, i, want_h);
+  }
+  if (slab) reduce_point(g, RED_STAGES, true);
   if (mode.relax) {
     const int passes = mode.cfg.numerics == 1 ? mode.cfg.max_iter : mode.cfg.max_iter + 1;
-    for (int p = 0; p < passes; ++p)
-      CK(launch_relax_pass(c->dim, c->U, c->d, m, c->ph, c->st, c->partials, c->counter,
-                           c->nnodes, c->grid_flat, c->stream));
+    for (int p = 0; p < passes; ++p) {
+      for (perrk_ctx* c : g.members) {
+        CK(launch_relax_pass(c->dim, c->U, c->d, c->mesh(), c->ph, c->st, c->partials,
+                             c->counter, c->nnodes, c->grid_flat, c->stream));
+        c->launches += 1;
+      }
+      if (slab) reduce_point(g, RED_RELAX, false);
+    }
   }
-  CK(launch_update(c->dim, c->U, c->d, m, c->ph, c->st, c->partials, c->counter, c->nnodes,
-                   mode.want_nu ? 1 : 0, mode.want_record ? 1 : 0, mode.records, c->grid_flat,
-                   c->stream));
+  for (perrk_ctx* c : g.members) {
+    CK(launch_update(c->dim, c->U, c->d, c->mesh(), c->ph, c->st, c->partials, c->counter,
+                     c->nnodes, mode.want_nu ? 1 : 0, mode.want_record ? 1 : 0,
+                     slab ? nullptr : mode.records_of(c), c->grid_flat, c->stream));
+    c->launches += 1;
+  }
+  if (slab) reduce_point(g, RED_UPDATE, true, mode.want_record ? mode.records : nullptr);
 }
 
 void check_relax_cfg(const perrk_relax_cfg& r) {
@@ -481,6 +575,138 @@ void configure_relax(StepState& s, bool enabled, const perrk_relax_cfg& r) {
   s.seed_from_previous = r.seed_from_previous;
   s.residual_tol = r.residual_tol;
   s.step_tol = r.step_tol;
+}
+
+// Cell-sized device buffers of a context (its slab when decomposed).
+void alloc_cell_buffers(perrk_ctx* c) {
+  const size_t bytes = sizeof(double) * c->ndofs_();
+  for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK}) {
+    CK(cudaMalloc(p, bytes));
+    CK(cudaMemsetAsync(*p, 0, bytes, c->stream));
+  }
+  CK(cudaMalloc(&c->dlevel, c->ncells));
+  CK(cudaMemset(c->dlevel, 1, c->ncells));
+  CK(cudaMalloc(&c->dlist_tmp, sizeof(int) * c->ncells));
+  CK(cudaMalloc(&c->dnu, sizeof(double) * c->ncells));
+  if (c->slab) {
+    const size_t tb = sizeof(double) * c->trace_doubles();
+    for (double** p : {&c->ghost_lo, &c->ghost_hi, &c->send_lo, &c->send_hi}) {
+      CK(cudaMalloc(p, tb));
+      CK(cudaMemsetAsync(*p, 0, tb, c->stream));
+    }
+    CK(cudaMalloc(&c->red_all, sizeof(double) * dev::NRED * c->nranks));
+  }
+}
+
+void free_cell_buffers(perrk_ctx* c) {
+  for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK, &c->dnu, &c->ghost_lo,
+                     &c->ghost_hi, &c->send_lo, &c->send_hi, &c->red_all}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+  }
+  if (c->dlevel) cudaFree(c->dlevel);
+  if (c->dlist_tmp) cudaFree(c->dlist_tmp);
+  c->dlevel = nullptr;
+  c->dlist_tmp = nullptr;
+}
+
+double* red_local_ptr(perrk_ctx* c) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(c->st) + offsetof(StepState, red_local));
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Fail(PERRK_ECOMM, std::string(what) + ": " + ncclGetErrorString(r));
+}
+#define NK(x) nccl_check((x), #x)
+
+// One rank per process (GPU): grouped send/recv of the boundary traces to the
+// slab neighbours (periodic ring) and an all-gather of the reduction partials,
+// all on the context's stream.
+struct NcclExchange : Exchange {
+  ncclComm_t comm = nullptr;
+  ~NcclExchange() override {
+    if (comm) ncclCommDestroy(comm);
+  }
+  void halo(std::vector<perrk_ctx*>& g) override {
+    perrk_ctx* c = g[0];
+    const int up = (c->rank + 1) % c->nranks, dn = (c->rank - 1 + c->nranks) % c->nranks;
+    const size_t n = c->trace_doubles();
+    // matched in order per peer, so nranks == 2 (up == dn) pairs correctly
+    NK(ncclGroupStart());
+    NK(ncclSend(c->send_hi, n, ncclDouble, up, comm, c->stream));
+    NK(ncclRecv(c->ghost_lo, n, ncclDouble, dn, comm, c->stream));
+    NK(ncclSend(c->send_lo, n, ncclDouble, dn, comm, c->stream));
+    NK(ncclRecv(c->ghost_hi, n, ncclDouble, up, comm, c->stream));
+    NK(ncclGroupEnd());
+  }
+  void gather(std::vector<perrk_ctx*>& g) override {
+    perrk_ctx* c = g[0];
+    NK(ncclAllGather(red_local_ptr(c), c->red_all, dev::NRED, ncclDouble, comm, c->stream));
+  }
+};
+
+// Several slabs on one device and one stream: the same data movement as
+// device-to-device copies, stream-ordered (no kernel waits on another).
+struct LoopbackExchange : Exchange {
+  void halo(std::vector<perrk_ctx*>& g) override {
+    const int P = static_cast<int>(g.size());
+    for (int r = 0; r < P; ++r) {
+      perrk_ctx* c = g[r];
+      const size_t bytes = sizeof(double) * c->trace_doubles();
+      CK(cudaMemcpyAsync(g[(r + 1) % P]->ghost_lo, c->send_hi, bytes, cudaMemcpyDeviceToDevice,
+                         c->stream));
+      CK(cudaMemcpyAsync(g[(r - 1 + P) % P]->ghost_hi, c->send_lo, bytes,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+  void gather(std::vector<perrk_ctx*>& g) override {
+    const int P = static_cast<int>(g.size());
+    for (int r = 0; r < P; ++r)
+      for (int q = 0; q < P; ++q)
+        CK(cudaMemcpyAsync(g[q]->red_all + static_cast<size_t>(r) * dev::NRED, red_local_ptr(g[r]),
+                           sizeof(double) * dev::NRED, cudaMemcpyDeviceToDevice, g[r]->stream));
+  }
+};
+
+// Restrict a context to its slab of last-axis layers [cuts[rank], cuts[rank+1]).
+void make_slab(perrk_ctx* c, int rank, int nranks, const int* cuts) {
+  REQUIRE(!c->slab, "context is already decomposed");
+  REQUIRE(!c->has_family, "decompose before perrk_set_family");
+  REQUIRE(nranks >= 2 && rank >= 0 && rank < nranks, "bad rank / rank count");
+  const int L = c->dim - 1, nl = c->nlast;
+  REQUIRE(nranks <= nl, "more ranks than cell layers along the last axis");
+  int b = rank * nl / nranks, e = (rank + 1) * nl / nranks;
+  if (cuts) {
+    REQUIRE(cuts[0] == 0 && cuts[nranks] == nl, "layer cuts must span 0..n_last");
+    for (int q = 0; q < nranks; ++q) REQUIRE(cuts[q + 1] > cuts[q], "layer cuts must increase");
+    b = cuts[rank];
+    e = cuts[rank + 1];
+  }
+  set_device(c);
+  CK(cudaStreamSynchronize(c->stream));
+  free_cell_buffers(c);
+  c->slab = true;
+  c->rank = rank;
+  c->nranks = nranks;
+  c->layer0 = b;
+  c->nc[L] = e - b;
+  c->ncells = c->layer_cells * (e - b);
+  c->nnodes = c->ncells * c->npc;
+  c->ndofs = c->nnodes * c->V;
+  alloc_cell_buffers(c);
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+void no_slab(const perrk_ctx* c, const char* what) {
+  if (c->slab)
+    throw Fail(PERRK_EUNSUP, std::string(what) + " is not available on a slab-decomposed context");
+}
+
+// per-member copy of the step state: the slab flag and rank count
+StepState slab_state(const perrk_ctx* c, StepState s) {
+  s.slab = c->slab ? 1 : 0;
+  s.nranks = c->nranks;
+  return s;
 }
 
 bool needs_h(bool relax, const perrk_relax_cfg& r, double h_ref) {
@@ -503,8 +729,8 @@ void fill_result(const perrk_ctx* c, const StepState& s, bool relax, double gamm
   r->delta_h = s.dh_hi + s.dh_lo;
   r->aborted = s.aborted;
   if (s.aborted && s.bad_code != std::numeric_limits<long long>::max()) {
-    r->bad_stage = static_cast<int>(s.bad_code / c->ncells);
-    r->bad_cell = static_cast<int>(s.bad_code % c->ncells);
+    r->bad_stage = static_cast<int>(s.bad_code / c->ncells_global);
+    r->bad_cell = static_cast<int>(s.bad_code % c->ncells_global);  // global cell id
   } else {
     r->bad_stage = r->bad_cell = -1;
   }
@@ -585,6 +811,10 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     REQUIRE(c->ncells < (1ll << 31) / 64, "mesh too large for 32-bit cell ids");
     c->nnodes = c->ncells * c->npc;
     c->ndofs = c->nnodes * c->V;
+    for (int a = 0; a < 3; ++a) c->ncg[a] = c->nc[a];
+    c->ncells_global = c->ncells;
+    c->nlast = c->nc[c->dim - 1];
+    c->layer_cells = c->ncells / c->nlast;
     set_device(c);
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     int sms = 148;
@@ -595,11 +825,7 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     const int occ = stage_blocks_per_sm(c->dim, sf);
     c->grid_stage = sms * (occ > 0 ? occ : 1);
     c->grid_flat = 8 * sms;
-    const size_t bytes = sizeof(double) * c->ndofs;
-    for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK}) {
-      CK(cudaMalloc(p, bytes));
-      CK(cudaMemsetAsync(*p, 0, bytes, c->stream));
-    }
+    alloc_cell_buffers(c);
     const double w0 = c->basis.w[0];
     for (int a = 0; a < 3; ++a) {
       std::vector<double> jac(c->nc[a]), lift(c->nc[a]);
@@ -614,16 +840,14 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
       CK(cudaMemcpy(c->djac[a], jac.data(), sizeof(double) * c->nc[a], cudaMemcpyHostToDevice));
       CK(cudaMemcpy(c->dlift[a], lift.data(), sizeof(double) * c->nc[a], cudaMemcpyHostToDevice));
     }
-    CK(cudaMalloc(&c->dlevel, c->ncells));
-    CK(cudaMemset(c->dlevel, 1, c->ncells));
     CK(cudaMalloc(&c->st, sizeof(StepState)));
     CK(cudaMalloc(&c->partials, sizeof(double) * 2 * 8 * 4096));
     CK(cudaMalloc(&c->counter, sizeof(unsigned)));
     CK(cudaMemset(c->counter, 0, sizeof(unsigned)));
     CK(cudaMalloc(&c->dout, sizeof(double) * 8));
     CK(cudaMalloc(&c->dint, sizeof(int) * 4));
-    CK(cudaMalloc(&c->dlist_tmp, sizeof(int) * c->ncells));
-    CK(cudaMalloc(&c->dnu, sizeof(double) * c->ncells));
+    c->group = std::make_shared<Group>();
+    c->group->members = {c};
     CK(upload_basis(c->basis.D.data(), c->basis.w.data()));
     CK(cudaStreamSynchronize(c->stream));
     *out = c;
@@ -636,20 +860,27 @@ int perrk_destroy(perrk_ctx* c) {
   if (!c) return PERRK_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (double* p : {c->U, c->K1, c->Ka, c->Kb, c->d, c->tU, c->tK, c->partials, c->dout, c->records,
-                    c->dnu})
+  free_cell_buffers(c);
+  for (double* p : {c->partials, c->dout, c->records})
     if (p) cudaFree(p);
   for (int a = 0; a < 3; ++a)
     for (double* p : {c->dh[a], c->djac[a], c->dlift[a]})
       if (p) cudaFree(p);
   for (auto& p : c->plan)
     if (p.dlist) cudaFree(p.dlist);
-  if (c->dlevel) cudaFree(c->dlevel);
   if (c->st) cudaFree(c->st);
   if (c->counter) cudaFree(c->counter);
   if (c->dint) cudaFree(c->dint);
-  if (c->dlist_tmp) cudaFree(c->dlist_tmp);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->group) {  // leave the group (the exchange dies with its last member)
+    auto& mem = c->group->members;
+    for (size_t i = 0; i < mem.size(); ++i)
+      if (mem[i] == c) {
+        mem.erase(mem.begin() + static_cast<long>(i));
+        break;
+      }
+    c->group.reset();
+  }
   if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return PERRK_OK;
@@ -674,15 +905,18 @@ int perrk_node_geometry(const perrk_ctx* c, double* x, double* y, double* z, dou
     for (long long cell = 0; cell < c->ncells; ++cell) {
       const int ci = static_cast<int>(cell % c->nc[0]);
       const int cj = static_cast<int>((cell / c->nc[0]) % c->nc[1]);
-      const int ck = static_cast<int>(cell / (static_cast<long long>(c->nc[0]) * c->nc[1]));
+      int ck = static_cast<int>(cell / (static_cast<long long>(c->nc[0]) * c->nc[1]));
+      int cj2 = cj;
+      if (c->dim == 3) ck += c->layer0;
+      else cj2 += c->layer0;
       for (int l = 0; l < c->npc; ++l) {
         const int ix = l % 4, iy = (l / 4) % 4, iz = l / 16;
         const long long n = cell * c->npc + l;
         if (x) x[n] = c->edges[0][ci] + 0.5 * c->h[0][ci] * (B.x[ix] + 1.0);
-        if (y) y[n] = c->edges[1][cj] + 0.5 * c->h[1][cj] * (B.x[iy] + 1.0);
+        if (y) y[n] = c->edges[1][cj2] + 0.5 * c->h[1][cj2] * (B.x[iy] + 1.0);
         if (z && c->dim == 3) z[n] = c->edges[2][ck] + 0.5 * c->h[2][ck] * (B.x[iz] + 1.0);
         if (measure)
-          measure[n] = c->dim == 2 ? 0.25 * c->h[0][ci] * c->h[1][cj] * B.w[ix] * B.w[iy]
+          measure[n] = c->dim == 2 ? 0.25 * c->h[0][ci] * c->h[1][cj2] * B.w[ix] * B.w[iy]
                                    : 0.125 * c->h[0][ci] * c->h[1][cj] * c->h[2][ck] * B.w[ix] *
                                          B.w[iy] * B.w[iz];
       }
@@ -701,12 +935,13 @@ int perrk_set_family(perrk_ctx* c, const perrk_family_desc* f, const int* eff) {
     c->A.assign(f->A, f->A + static_cast<size_t>(f->R) * f->S * f->S);
     c->b.assign(f->b, f->b + f->S);
     c->c.assign(f->c, f->c + f->S);
-    c->eff.assign(eff, eff + c->ncells);
-    std::vector<int8_t> lv(c->ncells);
-    for (long long i = 0; i < c->ncells; ++i) {
+    // the level map is global; the context keeps its slab's part
+    const long long off = static_cast<long long>(c->layer0) * c->layer_cells;
+    for (long long i = 0; i < c->ncells_global; ++i)
       REQUIRE(eff[i] >= 1 && eff[i] <= f->R, "level out of range");
-      lv[i] = static_cast<int8_t>(eff[i]);
-    }
+    c->eff.assign(eff + off, eff + off + c->ncells);
+    std::vector<int8_t> lv(c->ncells);
+    for (long long i = 0; i < c->ncells; ++i) lv[i] = static_cast<int8_t>(c->eff[i]);
     CK(cudaMemcpy(c->dlevel, lv.data(), c->ncells, cudaMemcpyHostToDevice));
     build_plan(c);
     c->has_family = true;
@@ -751,6 +986,7 @@ int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const
   (void)t;  // the periodic 2D/3D RHS is autonomous (semidisc.cpp:411)
   return guarded([&] {
     REQUIRE(c && U && out, "null argument");
+    no_slab(c, "rhs_masked");
     set_device(c);
     std::vector<int> list;
     for (long long i = 0; i < c->ncells; ++i)
@@ -770,7 +1006,8 @@ int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const
       a.list = mask ? c->dlist_tmp : nullptr;
       a.n = static_cast<int>(list.size());
       a.write_k = 1;
-      a.ncells = c->ncells;
+      a.ncells = c->ncells_global;
+      a.cell_offset = 0;
       CK(launch_stage(c->dim, c->surface, a, c->mesh(), c->ph, c->st, c->partials, c->counter,
                       c->grid_stage, c->stream));
       const StepState r = get_state(c);
@@ -789,6 +1026,7 @@ int perrk_br1_gradients(perrk_ctx*, double, const double*, double*) {
 int perrk_total_entropy(perrk_ctx* c, const double* U, double* out) {
   return guarded([&] {
     REQUIRE(c && out, "null argument");
+    no_slab(c, "total_entropy");
     set_device(c);
     *out = quad(c, stage_input(c, U), nullptr, 0, nullptr);
   });
@@ -797,6 +1035,7 @@ int perrk_total_entropy(perrk_ctx* c, const double* U, double* out) {
 int perrk_entropy_inner_product(perrk_ctx* c, const double* U, const double* K, double* out) {
   return guarded([&] {
     REQUIRE(c && K && out, "null argument");
+    no_slab(c, "entropy_inner_product");
     set_device(c);
     const double* dU = stage_input(c, U);
     upload(c, c->tK, K);
@@ -807,6 +1046,7 @@ int perrk_entropy_inner_product(perrk_ctx* c, const double* U, const double* K, 
 int perrk_integral_per_variable(perrk_ctx* c, const double* U, double* out) {
   return guarded([&] {
     REQUIRE(c && out, "null argument");
+    no_slab(c, "integral_per_variable");
     set_device(c);
     quad(c, stage_input(c, U), nullptr, 2, out);
   });
@@ -815,6 +1055,7 @@ int perrk_integral_per_variable(perrk_ctx* c, const double* U, double* out) {
 int perrk_admissible(perrk_ctx* c, const double* U, int* ok, int* first_bad) {
   return guarded([&] {
     REQUIRE(c && ok, "null argument");
+    no_slab(c, "admissible");
     set_device(c);
     const double* dU = stage_input(c, U);
     const int init = std::numeric_limits<int>::max();
@@ -848,11 +1089,16 @@ int perrk_compute_dt(perrk_ctx* c, const double* U, int fixed, double dt_or_cfl,
       return;
     }
     set_device(c);
+    Group& g = *c->group;
+    REQUIRE(g.members.size() == 1 || !U, "a loopback group takes the resident state (U = NULL)");
     StepState s = fresh_state();
     s.numax_bits = 0;
-    put_state(c, s);
-    CK(launch_numax(c->dim, stage_input(c, U), c->mesh(), c->ph, c->st, c->nnodes, c->grid_flat,
-                    c->stream));
+    for (perrk_ctx* m : g.members) {
+      put_state(m, slab_state(m, s));
+      CK(launch_numax(m->dim, m == c ? stage_input(c, U) : m->U, m->mesh(), m->ph, m->st,
+                      m->nnodes, m->grid_flat, m->stream));
+    }
+    if (g.ex) reduce_point(g, RED_NUMAX, true);  // global max over the slabs
     const StepState r = get_state(c);
     double best;
     std::memcpy(&best, &r.numax_bits, sizeof best);
@@ -869,6 +1115,8 @@ static int step_common(perrk_ctx* c, double* t, double dt, const perrk_step_opts
     REQUIRE(c->has_family, "no family set (perrk_set_family)");
     REQUIRE(dt > 0.0, "dt must be positive");
     if (o->relax_enabled) check_relax_cfg(o->relax);
+    Group& g = *c->group;
+    for (perrk_ctx* m : g.members) REQUIRE(m->has_family, "no family set on a group member");
     set_device(c);
     StepState s = fresh_state();
     s.t = *t;
@@ -879,14 +1127,14 @@ static int step_common(perrk_ctx* c, double* t, double dt, const perrk_step_opts
     s.h_ref = o->h_ref;
     s.idt = o->idt;
     configure_relax(s, o->relax_enabled != 0, o->relax);
-    put_state(c, s);
+    for (perrk_ctx* m : g.members) put_state(m, slab_state(m, s));
     StepMode mode;
     mode.relax = o->relax_enabled != 0;
     mode.cfg = o->relax;
-    enqueue_step(c, mode, needs_h(mode.relax, o->relax, o->h_ref));
+    enqueue_step(g, mode, needs_h(mode.relax, o->relax, o->h_ref));
     const StepState r = get_state(c);
     if (r.error == 1) throw Fail(PERRK_ENUMERIC, "non-finite update direction");
-    c->evals += evals_per_step(c);
+    for (perrk_ctx* m : g.members) m->evals += evals_per_step(m);
     fill_result(c, r, mode.relax, o->gamma_override, res);
     if (!r.aborted) *t = r.t;
   });
@@ -932,13 +1180,20 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
     configure_relax(s, cfg->relax_enabled != 0, cfg->relax);
     if (cfg->relax_enabled && cfg->anchor_initial)
       s.h_ref = quad(c, c->U, nullptr, 0, nullptr);  // H(U_0)
-    put_state(c, s);
-    const bool rec = cfg->records && log;
-    if (rec && c->records_cap < nsteps) {
-      if (c->records) cudaFree(c->records);
-      CK(cudaMalloc(&c->records, sizeof(double) * 11 * nsteps));
-      c->records_cap = nsteps;
+    Group& g = *c->group;
+    REQUIRE(!(g.ex && cfg->relax_enabled && cfg->anchor_initial),
+            "anchored relaxation is not supported with the slab decomposition");
+    for (perrk_ctx* m : g.members) {
+      REQUIRE(m->has_family, "no family set on a group member");
+      put_state(m, slab_state(m, s));
     }
+    const bool rec = cfg->records && log;
+    for (perrk_ctx* m : g.members)
+      if (rec && m->records_cap < nsteps) {
+        if (m->records) cudaFree(m->records);
+        CK(cudaMalloc(&m->records, sizeof(double) * 11 * nsteps));
+        m->records_cap = nsteps;
+      }
     StepMode mode;
     mode.relax = cfg->relax_enabled != 0;
     mode.cfg = cfg->relax;
@@ -946,18 +1201,23 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
     mode.want_record = rec;
     mode.records = rec ? c->records : nullptr;
     if (!cfg->fixed_dt) {
-      CK(launch_numax(c->dim, c->U, c->mesh(), c->ph, c->st, c->nnodes, c->grid_flat, c->stream));
-      c->launches += 1;
+      for (perrk_ctx* m : g.members) {
+        CK(launch_numax(m->dim, m->U, m->mesh(), m->ph, m->st, m->nnodes, m->grid_flat,
+                        m->stream));
+        m->launches += 1;
+      }
+      if (g.ex) reduce_point(g, RED_NUMAX, true);
     }
     const bool want_h = needs_h(mode.relax, cfg->relax, s.h_ref);
-    for (int k = 0; k < nsteps; ++k) enqueue_step(c, mode, want_h);
+    for (int k = 0; k < nsteps; ++k) enqueue_step(g, mode, want_h);
     const StepState r = get_state(c);
     if (r.error == 1) throw Fail(PERRK_ENUMERIC, "non-finite update direction");
     if (r.error == 2) throw Fail(PERRK_EINVAL, "vanishing characteristic speed");
     *t = r.t;
     if (steps_taken) *steps_taken = r.steps_taken;
     if (aborted) *aborted = r.aborted;
-    c->evals += evals_per_step(c) * static_cast<uint64_t>(r.steps_taken + (r.aborted ? 1 : 0));
+    for (perrk_ctx* m : g.members)
+      m->evals += evals_per_step(m) * static_cast<uint64_t>(r.steps_taken + (r.aborted ? 1 : 0));
     if (rec && r.steps_taken > 0) {
       std::vector<double> raw(static_cast<size_t>(11) * r.steps_taken);
       CK(cudaMemcpy(raw.data(), c->records, sizeof(double) * raw.size(), cudaMemcpyDeviceToHost));
@@ -1148,16 +1408,86 @@ int perrk_fp64_peak(int device, double* gflops) {
   });
 }
 
-int perrk_comm_init(perrk_ctx*, const void*, int, int) {
-  g_last_error = "multi-GPU slab decomposition not built yet";
-  return PERRK_EUNSUP;
+int perrk_nccl_id(void* out) {
+  return guarded([&] {
+    REQUIRE(out, "null argument");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof id);
+  });
+}
+
+int perrk_comm_init(perrk_ctx* c, const void* nccl_id, int rank, int nranks, const int* cuts) {
+  return guarded([&] {
+    REQUIRE(c && nccl_id, "null argument");
+    if (nranks == 1) return;  // the whole periodic mesh: nothing to exchange
+    make_slab(c, rank, nranks, cuts);
+    auto ex = std::make_unique<NcclExchange>();
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    set_device(c);
+    NK(ncclCommInitRank(&ex->comm, nranks, id, rank));
+    c->group->ex = std::move(ex);
+  });
+}
+
+int perrk_loopback_group(perrk_ctx** ctxs, int n, const int* cuts) {
+  return guarded([&] {
+    REQUIRE(ctxs && n >= 2, "need at least two contexts");
+    for (int r = 0; r < n; ++r) {
+      REQUIRE(ctxs[r], "null context");
+      REQUIRE(ctxs[r]->device == ctxs[0]->device, "loopback contexts share one device");
+      REQUIRE(ctxs[r]->ncells_global == ctxs[0]->ncells_global, "contexts of different meshes");
+    }
+    auto g = std::make_shared<Group>();
+    g->ex = std::make_unique<LoopbackExchange>();
+    for (int r = 0; r < n; ++r) {
+      perrk_ctx* c = ctxs[r];
+      make_slab(c, r, n, cuts);
+      if (r > 0) {  // one stream orders every member's work
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->own_stream) CK(cudaStreamDestroy(c->stream));
+        c->stream = ctxs[0]->stream;
+        c->own_stream = false;
+      }
+      g->members.push_back(c);
+      c->group = g;
+    }
+  });
 }
 
 int perrk_slab_range(const perrk_ctx* c, int* b, int* e) {
   return guarded([&] {
     REQUIRE(c && b && e, "null argument");
-    *b = 0;
-    *e = c->dim == 2 ? c->nc[1] : c->nc[2];
+    *b = c->layer0;
+    *e = c->layer0 + c->nc[c->dim - 1];
+  });
+}
+
+int perrk_slab_cuts(int nlast, const double* layer_work, int nranks, int* cuts) {
+  return guarded([&] {
+    REQUIRE(nlast >= 1 && nranks >= 1 && nranks <= nlast && cuts, "bad arguments");
+    // contiguous layers, cut where the running work crosses r / nranks of the
+    // total (uniform layers when layer_work is NULL), every slab >= 1 layer
+    std::vector<double> pre(nlast + 1, 0.0);
+    for (int l = 0; l < nlast; ++l) pre[l + 1] = pre[l] + (layer_work ? layer_work[l] : 1.0);
+    cuts[0] = 0;
+    for (int r = 1; r < nranks; ++r) {
+      const double target = pre[nlast] * r / nranks;
+      int l = cuts[r - 1] + 1;
+      while (l < nlast - (nranks - r) && pre[l] + 0.5 * (pre[l + 1] - pre[l]) < target) ++l;
+      cuts[r] = l;
+    }
+    cuts[nranks] = nlast;
+  });
+}
+
+int perrk_slab_trace_nodes(int dim, int side, int* nodes) {
+  return guarded([&] {
+    REQUIRE((dim == 2 || dim == 3) && (side == 0 || side == 1) && nodes, "bad arguments");
+    // face of the last axis, points in (t1 + 4 t2) order (pack_traces_kernel)
+    const int fp = dim == 3 ? 16 : 4, stride = dim == 3 ? 16 : 4;
+    for (int pt = 0; pt < fp; ++pt) nodes[pt] = pt + (side ? 3 * stride : 0);
   });
 }
 

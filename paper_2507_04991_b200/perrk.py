@@ -293,6 +293,33 @@ class Semidiscretization:
     def sync(self):
         check(lib().perrk_sync(self._h))
 
+    # element-slab decomposition (perrk_comm_init, include/perrk_b200.h)
+    def _refresh_sizes(self):
+        dofs, nodes, cells = C.c_int64(), C.c_int64(), C.c_int64()
+        v, npc = C.c_int(), C.c_int()
+        check(lib().perrk_sizes(self._h, C.byref(dofs), C.byref(nodes), C.byref(cells), C.byref(v),
+                                C.byref(npc)))
+        self._n = (dofs.value, nodes.value, cells.value, v.value, npc.value)
+        self._geom = None
+        self._family_key = None
+
+    def comm_init(self, nccl_id: bytes, rank: int, nranks: int, cuts=None):
+        """Own the slab of last-axis layers of `rank` (one process per GPU)."""
+        cu = None if cuts is None else np.ascontiguousarray(cuts, dtype=np.int32)
+        buf = C.create_string_buffer(bytes(nccl_id), 128)
+        check(lib().perrk_comm_init(self._h, buf, int(rank), int(nranks),
+                                    None if cu is None else _ip(cu)))
+        self._cuts_keep = cu
+        self._refresh_sizes()
+
+    def slab_range(self):
+        b, e = C.c_int(), C.c_int()
+        check(lib().perrk_slab_range(self._h, C.byref(b), C.byref(e)))
+        return b.value, e.value
+
+    def global_num_cells(self):
+        return self.spec.mesh.num_cells()
+
     # instrumentation (perrk_set_stream / perrk_profile*, include/perrk_b200.h)
     def set_stream(self, cuda_stream):
         """Order this context's work on a caller CUDA stream (int handle, 0/None:
@@ -335,6 +362,73 @@ class Semidiscretization:
                              _dp(c))
         check(lib().perrk_set_family(self._h, C.byref(fd), _ip(eff)))
         self._family_key = key
+
+
+def nccl_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for perrk_comm_init."""
+    buf = C.create_string_buffer(128)
+    check(lib().perrk_nccl_id(buf))
+    return buf.raw
+
+
+def slab_cuts(n_last, nranks, layer_work=None):
+    """Contiguous layer cuts [0, ..., n_last] balancing layer_work."""
+    cuts = np.zeros(nranks + 1, dtype=np.int32)
+    w = None if layer_work is None else _f64(layer_work)
+    check(lib().perrk_slab_cuts(int(n_last), None if w is None else _dp(w), int(nranks), _ip(cuts)))
+    return cuts
+
+
+def slab_trace_nodes(dim, side):
+    """Cell-local node indices of the last-axis face traces, exchange order."""
+    out = np.zeros(16 if dim == 3 else 4, dtype=np.int32)
+    check(lib().perrk_slab_trace_nodes(int(dim), int(side), _ip(out)))
+    return out
+
+
+def layer_work(mesh, pmap, family, npc):
+    """DOF-stage work per last-axis layer (cells x active stages x nodes)."""
+    shape = mesh.shape()
+    lv = np.asarray(pmap.effective_level).reshape(tuple(reversed(shape)))  # [z, y, x] / [y, x]
+    E = np.array([len(family.active_sets[family.member_index_for_level(l)])
+                  for l in range(1, family.R + 1)], dtype=np.float64)
+    per_cell = E[lv - 1] * npc
+    return per_cell.reshape(per_cell.shape[0], -1).sum(axis=1)
+
+
+def slab_pmap(semi, pmap):
+    """The rank's part of a global partition map (for work accounting)."""
+    b, e = semi.slab_range()
+    lc = semi.global_num_cells() // semi.spec.mesh.shape()[-1]
+    eff = np.asarray(pmap.effective_level)[b * lc:e * lc]
+    raw = np.asarray(pmap.raw_level)[b * lc:e * lc]
+    return PartitionMap(pmap.R, raw.copy(), eff.copy())
+
+
+def init_slabs(semi, rank, nranks, cuts=None):
+    """Decompose `semi` over torch.distributed ranks (NCCL id broadcast from
+    rank 0 over the default process group)."""
+    import torch
+    import torch.distributed as dist
+    ident = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        ident = torch.frombuffer(bytearray(nccl_id()), dtype=torch.uint8).clone()
+    if dist.get_backend() == "nccl":
+        ident = ident.cuda()
+    dist.broadcast(ident, 0)
+    semi.comm_init(bytes(ident.cpu().numpy().tobytes()), rank, nranks, cuts)
+
+
+def loopback_group(semis, cuts=None):
+    """Ranks 0..n-1 of a slab decomposition as contexts on one device (test
+    harness of the multi-rank logic; stepping any member steps all)."""
+    arr = (C.c_void_p * len(semis))(*[s._h.value if isinstance(s._h, C.c_void_p) else s._h
+                                       for s in semis])
+    cu = None if cuts is None else np.ascontiguousarray(cuts, dtype=np.int32)
+    check(lib().perrk_loopback_group(arr, len(semis), None if cu is None else _ip(cu)))
+    for s in semis:
+        s._refresh_sizes()
+        s._group = semis
 
 
 def fp64_peak(device=0):

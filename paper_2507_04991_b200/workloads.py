@@ -294,7 +294,9 @@ class ConfigRun:
         self.semi = P.Semidiscretization(cfg.spec(device))
         self.pmap = cfg.partition_map()
         if world > 1:
-            P.init_slabs(self.semi, rank, world, comm)
+            work = P.layer_work(cfg.mesh, self.pmap, cfg.family, cfg.nodes_per_cell())
+            self.cuts = P.slab_cuts(len(work), world, work)
+            P.init_slabs(self.semi, rank, world, self.cuts)
 
     def initial_state(self):
         s = self.semi
