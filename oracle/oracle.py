@@ -99,6 +99,8 @@ def ref_lib():
             "ref_create": (C.c_void_p, [C.c_int, _D, C.c_int, _D, C.c_int, C.c_int, C.c_int,
                                         C.c_double, _D, C.c_int, C.c_int, C.c_int]),
             "ref_destroy": (None, [C.c_void_p]),
+            "ref_create_nsf1d": (C.c_void_p, [_D, C.c_int, C.c_int, C.c_double, C.c_double,
+                                              C.c_double, C.c_int, C.c_int, C.c_int]),
             "ref_num_dofs": (C.c_int, [C.c_void_p]),
             "ref_num_cells": (C.c_int, [C.c_void_p]),
             "ref_set_threads": (None, [C.c_void_p, C.c_int]),
@@ -305,6 +307,40 @@ class Ref(_Base):
 
     def rhs_cell_evaluations(self):
         return self.L.ref_rhs_cell_evaluations(self.h)
+
+
+class RefNSF1D:
+    """The reference's own 1D NSF + BR1 semidiscretization (the oracle's 2D
+    NSF extension reduces to it on y-independent data with v = 0)."""
+
+    def __init__(self, x_edges, gamma=1.4, mu=1e-2, prandtl=0.72, surface_flux="rusanov",
+                 volume_flux="ec"):
+        self.L = ref_lib()
+        xe = np.ascontiguousarray(x_edges, dtype=np.float64)
+        self.h = self.L.ref_create_nsf1d(dp(xe), xe.size, 3, gamma, mu, prandtl,
+                                         FLUX[surface_flux], 1, FLUX[volume_flux])
+        if not self.h:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        self.V = 3
+        self.ndofs = self.L.ref_num_dofs(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.ref_destroy(self.h)
+            self.h = None
+
+    def node_coords(self):
+        n = self.ndofs // self.V
+        x, y, m = np.zeros(n), np.zeros(n), np.zeros(n)
+        self.L.ref_node_coords(self.h, dp(x), dp(y), dp(m))
+        return x
+
+    def rhs(self, t, U):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.empty_like(U)
+        if self.L.ref_rhs_masked(self.h, t, dp(U), dp(out), None):
+            raise RuntimeError(self.L.ref_last_error().decode())
+        return out
 
 
 class Orc(_Base):

@@ -159,6 +159,28 @@ ref_ctx* ref_create(int dim, const double* xe, int nxe, const double* ye, int ny
   return rc ? nullptr : ctx;
 }
 
+// 1D compressible Navier-Stokes-Fourier with BR1 (NSFPhysics, physics.hpp:127-146;
+// the reference's only viscous path, semidisc.cpp:245-395), periodic
+ref_ctx* ref_create_nsf1d(const double* xe, int nxe, int k, double gamma, double mu,
+                          double prandtl, int surface_flux, int volume_mode, int volume_flux) {
+  ref_ctx* ctx = nullptr;
+  int rc = guarded([&] {
+    SemidiscretizationSpec spec;
+    Mesh1D m;
+    m.edges.assign(xe, xe + nxe);
+    m.periodic = true;
+    spec.mesh = m;
+    spec.polydeg = k;
+    spec.physics = std::make_shared<NSFPhysics>(gamma, mu, prandtl);
+    spec.viscous = true;
+    spec.surface_flux = tag_of(surface_flux);
+    spec.volume_mode = volume_mode ? VolumeMode::flux_differencing : VolumeMode::weak;
+    spec.volume_flux = tag_of(volume_flux);
+    ctx = new ref_ctx{std::make_unique<Semidiscretization>(std::move(spec))};
+  });
+  return rc ? nullptr : ctx;
+}
+
 void ref_destroy(ref_ctx* ctx) { delete ctx; }
 int ref_num_dofs(ref_ctx* ctx) { return ctx->semi->num_dofs(); }
 int ref_num_cells(ref_ctx* ctx) { return ctx->semi->num_cells(); }

@@ -67,6 +67,7 @@ __device__ __forceinline__ void report_bad(StepState* st, int stage, long long n
 }  // namespace perrk
 
 #include "dg_stage.cuh"
+#include "dg_visc.cuh"
 
 namespace perrk {
 namespace dev {
@@ -442,49 +443,55 @@ __global__ void admissible_kernel(const double* __restrict__ U, Phys ph, int* fi
 // launchers
 // ---------------------------------------------------------------------------
 
-template <int DIM, int SURF>
+template <int DIM, int SURF, bool VISC>
+static size_t stage_smem() {
+  return sizeof(double) * (StageGeo<DIM>::SM_TOTAL + (VISC ? StageGeo<DIM>::SM_VISC : 0));
+}
+
+template <int DIM, int SURF, bool VISC>
 static void configure_stage() {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(stage_kernel<DIM, SURF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(double) * StageGeo<DIM>::SM_TOTAL));
+    cudaFuncSetAttribute(stage_kernel<DIM, SURF, VISC>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(stage_smem<DIM, SURF, VISC>()));
     configured = true;
   }
 }
 
 template <int DIM, int SURF>
 static int stage_occ_t() {
-  configure_stage<DIM, SURF>();
+  configure_stage<DIM, SURF, false>();
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, stage_kernel<DIM, SURF>, StageGeo<DIM>::T,
-                                                sizeof(double) * StageGeo<DIM>::SM_TOTAL);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, stage_kernel<DIM, SURF, false>,
+                                                StageGeo<DIM>::T, stage_smem<DIM, SURF, false>());
   return n;
 }
 
-template <int DIM, int SURF>
+template <int DIM, int SURF, bool VISC>
 static cudaError_t launch_stage_t(const StageArgs& a, const MeshDev& m, const Phys& ph,
                                   StepState* st, double* partials, unsigned* counter, int grid,
                                   cudaStream_t s) {
   using G = StageGeo<DIM>;
-  configure_stage<DIM, SURF>();
-  const size_t shm = sizeof(double) * G::SM_TOTAL;
+  configure_stage<DIM, SURF, VISC>();
   const int groups = (a.n + G::CPB - 1) / G::CPB;
   const int g = groups < grid ? groups : grid;
   if (g <= 0) return cudaSuccess;
-  stage_kernel<DIM, SURF><<<g, G::T, shm, s>>>(a, m, ph, st, partials, counter);
+  stage_kernel<DIM, SURF, VISC><<<g, G::T, stage_smem<DIM, SURF, VISC>(), s>>>(a, m, ph, st,
+                                                                            partials, counter);
   return cudaGetLastError();
 }
 
-template <int DIM>
+template <int DIM, bool VISC>
 static cudaError_t launch_stage_d(int surf, const StageArgs& a, const MeshDev& m, const Phys& ph,
                                   StepState* st, double* partials, unsigned* counter, int grid,
                                   cudaStream_t s) {
   switch (surf) {
-    case 0: return launch_stage_t<DIM, 0>(a, m, ph, st, partials, counter, grid, s);
-    case 2: return launch_stage_t<DIM, 2>(a, m, ph, st, partials, counter, grid, s);
-    case 3: return launch_stage_t<DIM, 3>(a, m, ph, st, partials, counter, grid, s);
-    case 4: return launch_stage_t<DIM, 4>(a, m, ph, st, partials, counter, grid, s);
-    case 5: return launch_stage_t<DIM, 5>(a, m, ph, st, partials, counter, grid, s);
+    case 0: return launch_stage_t<DIM, 0, VISC>(a, m, ph, st, partials, counter, grid, s);
+    case 2: return launch_stage_t<DIM, 2, VISC>(a, m, ph, st, partials, counter, grid, s);
+    case 3: return launch_stage_t<DIM, 3, VISC>(a, m, ph, st, partials, counter, grid, s);
+    case 4: return launch_stage_t<DIM, 4, VISC>(a, m, ph, st, partials, counter, grid, s);
+    case 5: return launch_stage_t<DIM, 5, VISC>(a, m, ph, st, partials, counter, grid, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -669,8 +676,21 @@ int stage_cells_per_block(int dim) { return dim == 2 ? StageGeo<2>::CPB : StageG
 cudaError_t launch_stage(int dim, int surf, const StageArgs& a, const MeshDev& m, const Phys& ph,
                          StepState* st, double* partials, unsigned* counter, int grid,
                          cudaStream_t s) {
-  return dim == 2 ? launch_stage_d<2>(surf, a, m, ph, st, partials, counter, grid, s)
-                  : launch_stage_d<3>(surf, a, m, ph, st, partials, counter, grid, s);
+  if (a.G) {
+    if (dim != 2) return cudaErrorInvalidValue;
+    return launch_stage_d<2, true>(surf, a, m, ph, st, partials, counter, grid, s);
+  }
+  return dim == 2 ? launch_stage_d<2, false>(surf, a, m, ph, st, partials, counter, grid, s)
+                  : launch_stage_d<3, false>(surf, a, m, ph, st, partials, counter, grid, s);
+}
+
+cudaError_t launch_grad(const StageArgs& a, const MeshDev& m, const Phys& ph, StepState* st,
+                        double* out, long long ndofs, int mode, int grid, cudaStream_t s) {
+  const int groups = (a.n + 7) / 8;
+  const int g = groups < grid ? groups : grid;
+  if (g <= 0) return cudaSuccess;
+  grad_kernel<<<g, 128, 0, s>>>(a, m, ph, st, out, ndofs, mode);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_begin_step(StepState* st, cudaStream_t s) {

@@ -28,6 +28,8 @@ struct StageArgs {
   int stage;
   long long ncells;      // GLOBAL cells (positivity codes are stage * ncells + global cell)
   long long cell_offset; // global id of local cell 0
+  const double* G;       // BR1 viscous fluxes [2][ndofs] (nullptr: inviscid)
+  long long ndofs;
 };
 
 double measure_fp64_peak();  // GFLOP/s on the current device (DFMA loop)
@@ -39,6 +41,9 @@ int stage_blocks_per_sm(int dim, int surf);  // resident stage blocks per SM
 cudaError_t launch_stage(int dim, int surf, const StageArgs& a, const dev::MeshDev& m,
                          const dev::Phys& ph, dev::StepState* st, double* partials,
                          unsigned* counter, int grid, cudaStream_t s);
+cudaError_t launch_grad(const StageArgs& a, const dev::MeshDev& m, const dev::Phys& ph,
+                        dev::StepState* st, double* out, long long ndofs, int mode, int grid,
+                        cudaStream_t s);
 cudaError_t launch_begin_step(dev::StepState* st, cudaStream_t s);
 cudaError_t launch_relax_pass(int dim, const double* U, const double* d, const dev::MeshDev& m,
                               const dev::Phys& ph, dev::StepState* st, double* partials,

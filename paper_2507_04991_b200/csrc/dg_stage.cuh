@@ -64,6 +64,8 @@ struct StageGeo {
   static constexpr int SM_PR = NPR * T;           // primitives, SoA [slot][cell*NPC+node]
   static constexpr int SM_NB = CPB * NFP * V;     // neighbour traces [cell][face][pt][var]
   static constexpr int SM_TOTAL = SM_PR + SM_NB;
+  // BR1 (2D NSF): own viscous fluxes [2][T][V] and neighbour face values [CPB][NFP][V]
+  static constexpr int SM_VISC = 2 * T * V + CPB * NFP * V;
 };
 
 // primitive slots: rho, v[DIM], p, E, log rho, beta, log beta
@@ -353,7 +355,7 @@ __device__ __forceinline__ void direction_terms(const Phys& ph, const MeshDev& m
   }
 }
 
-template <int DIM, int SURF>
+template <int DIM, int SURF, bool VISC>
 __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
     stage_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
                  unsigned* counter) {
@@ -363,6 +365,8 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
   extern __shared__ double smem[];
   double* pr = smem;            // [NPR][T]
   double* nb = pr + G::SM_PR;   // [CPB][NFP][V]
+  double* vg = nb + G::SM_NB;   // VISC: own G [2][T][V], then neighbour G_d [CPB][NFP][V]
+  double* vn = vg + 2 * T * V;
   __shared__ int s_cell[CPB];
   __shared__ int s_coord[CPB][3];
   __shared__ double s_ca1[CPB], s_cap[CPB];
@@ -505,6 +509,27 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
 #pragma unroll
       for (int v = 0; v < V; ++v) o[v] = u[v];
     }
+    if constexpr (VISC) {  // BR1 viscous fluxes from grad_kernel (2D)
+      const size_t nd = static_cast<size_t>(a.ndofs);
+      if (cell >= 0) {
+        const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          vg[tid * V + v] = a.G[gi + v];
+          vg[(T + tid) * V + v] = a.G[nd + gi + v];
+        }
+      }
+      for (int q = tid; q < CPB * NFP; q += T) {
+        const int c2 = q / NFP, r = q % NFP, f = r / FP, pt = r % FP;
+        if (s_cell[c2] < 0) continue;
+        const int d = f >> 1, side = f & 1;
+        const int node =
+            line_base<DIM>(d, pt % N1, pt / N1) + (side ? 0 : N1 - 1) * line_stride(d);
+        const size_t gi = (static_cast<size_t>(s_nbc[c2][f]) * NPC + node) * V + d * nd;
+#pragma unroll
+        for (int v = 0; v < V; ++v) vn[q * V + v] = a.G[gi + v];
+      }
+    }
     __syncthreads();
 
     double K[V];
@@ -515,6 +540,36 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
       direction_terms<DIM, SURF, 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][1], &s_nbg[cs][2 * (1)], own, lr, be, lb, K);
       if constexpr (DIM == 3)
         direction_terms<DIM, SURF, DIM - 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][DIM - 1], &s_nbg[cs][2 * (DIM - 1)], own, lr, be, lb, K);
+      if constexpr (VISC) {
+        // weak-form divergence of the viscous flux with the central interface
+        // flux (add_viscous_1d, semidisc.cpp:341-394, per direction)
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          const int stride = d == 0 ? 1 : N1;
+          const int j = il[d];
+          const int cd = s_coord[cs][d];
+          const double jac = m.jac[d][cd];
+#pragma unroll
+          for (int k = 0; k < N1; ++k) {
+            const double coef = jac * c_D[k * N1 + j] * c_w[k] / c_w[j];
+            const double* gk = vg + (d * T + tid + (k - j) * stride) * V;
+#pragma unroll
+            for (int v = 0; v < V; ++v) K[v] -= coef * gk[v];
+          }
+          if (j == 0 || j == N1 - 1) {
+            const int e = j == 0 ? 0 : 1;
+            const int pt = d == 0 ? il[1] : il[0];
+            const double* gn = vn + ((cs * 2 * DIM + 2 * d + e) * FP + pt) * V;
+            const double* go = vg + (d * T + tid) * V;
+            const double coef = m.lift[d][cd];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const double gs = 0.5 * (e ? go[v] + gn[v] : gn[v] + go[v]);
+              K[v] += (e ? coef : -coef) * gs;
+            }
+          }
+        }
+      }
 
       // ---- epilogue: entropy products, K and d stores (coalesced) -------------
       if (a.want_dh || a.want_h) {

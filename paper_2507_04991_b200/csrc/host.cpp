@@ -240,6 +240,8 @@ void build_member(int kind, int S, int E, const double* fr, const std::vector<do
 struct StagePlan {
   int* dlist = nullptr;  // nullptr: all cells
   int n = 0;
+  int* glist = nullptr;  // BR1: active cells and their face neighbours (nullptr: all)
+  int gn = 0;
   double bytes = 0.0;    // compulsory HBM bytes of the launch (roofline)
   StageArgs args{};
   int kin = -1, kout = -1;  // buffer ids: 0 K1, 1 Ka, 2 Kb
@@ -287,6 +289,7 @@ struct perrk_ctx {
   // device buffers
   double *U = nullptr, *K1 = nullptr, *Ka = nullptr, *Kb = nullptr, *d = nullptr;
   double *tU = nullptr, *tK = nullptr;  // scratch for host-buffer queries
+  double* G = nullptr;                   // BR1 viscous fluxes [2][ndofs] (NSF only)
   double *dh[3] = {}, *djac[3] = {}, *dlift[3] = {};
   int8_t* dlevel = nullptr;
   StepState* st = nullptr;
@@ -384,9 +387,29 @@ void download(perrk_ctx* c, double* dst, const double* src) {
 }
 
 // Build per-stage launch plans from the family and the effective levels.
+// cells of a mask plus their periodic face neighbours (2D), ascending
+std::vector<int> with_neighbours_2d(const perrk_ctx* c, const std::vector<char>& on) {
+  const int nx = c->nc[0], ny = c->nc[1];
+  std::vector<char> g(on);
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i)
+      if (on[i + nx * j]) {
+        g[(i + 1) % nx + nx * j] = 1;
+        g[(i + nx - 1) % nx + nx * j] = 1;
+        g[i + nx * ((j + 1) % ny)] = 1;
+        g[i + nx * ((j + ny - 1) % ny)] = 1;
+      }
+  std::vector<int> out;
+  for (long long q = 0; q < c->ncells; ++q)
+    if (g[q]) out.push_back(static_cast<int>(q));
+  return out;
+}
+
 void build_plan(perrk_ctx* c) {
-  for (auto& p : c->plan)
+  for (auto& p : c->plan) {
     if (p.dlist) cudaFree(p.dlist);
+    if (p.glist) cudaFree(p.glist);
+  }
   c->plan.clear();
   const int S = c->S, R = c->R;
   std::vector<std::vector<char>> active(R);  // by level-1
@@ -415,6 +438,16 @@ void build_plan(perrk_ctx* c) {
     if (!all && p.n > 0) {
       CK(cudaMalloc(&p.dlist, sizeof(int) * list.size()));
       CK(cudaMemcpy(p.dlist, list.data(), sizeof(int) * list.size(), cudaMemcpyHostToDevice));
+    }
+    if (c->physics == 1) {  // BR1: gradients on the active cells and their neighbours
+      std::vector<char> on(c->ncells, 0);
+      for (int q : list) on[q] = 1;
+      const std::vector<int> gl = with_neighbours_2d(c, on);
+      p.gn = static_cast<int>(gl.size());
+      if (p.gn < c->ncells && p.gn > 0) {
+        CK(cudaMalloc(&p.glist, sizeof(int) * gl.size()));
+        CK(cudaMemcpy(p.glist, gl.data(), sizeof(int) * gl.size(), cudaMemcpyHostToDevice));
+      }
     }
     for (int lvl = 0; lvl <= dev::MAXR; ++lvl) a.a1[lvl] = a.ap[lvl] = 0.0;
     for (int lvl = 1; lvl <= R; ++lvl) {
@@ -477,6 +510,15 @@ void enqueue_stage(perrk_ctx* c, int i, bool want_h) {
   a.Kout = c->kbuf(p.kout);
   a.d = c->d;
   a.want_h = (i == 0 && want_h) ? 1 : 0;
+  a.ndofs = c->ndofs;
+  if (c->physics == 1) {  // BR1: viscous fluxes of the stage state first
+    StageArgs ga = a;
+    ga.list = p.glist;
+    ga.n = p.gn;
+    CK(launch_grad(ga, c->mesh(), c->ph, c->st, c->G, c->ndofs, 0, c->grid_stage, c->stream));
+    c->launches += 1;
+    a.G = c->G;
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->profiling) {
     if (c->ev_used + 2 > c->ev_pool.size()) {
@@ -584,6 +626,7 @@ void alloc_cell_buffers(perrk_ctx* c) {
     CK(cudaMalloc(p, bytes));
     CK(cudaMemsetAsync(*p, 0, bytes, c->stream));
   }
+  if (c->physics == 1) CK(cudaMalloc(&c->G, 2 * bytes));
   CK(cudaMalloc(&c->dlevel, c->ncells));
   CK(cudaMemset(c->dlevel, 1, c->ncells));
   CK(cudaMalloc(&c->dlist_tmp, sizeof(int) * c->ncells));
@@ -599,7 +642,7 @@ void alloc_cell_buffers(perrk_ctx* c) {
 }
 
 void free_cell_buffers(perrk_ctx* c) {
-  for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK, &c->dnu, &c->ghost_lo,
+  for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK, &c->dnu, &c->G, &c->ghost_lo,
                      &c->ghost_hi, &c->send_lo, &c->send_hi, &c->red_all}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
@@ -671,6 +714,8 @@ struct LoopbackExchange : Exchange {
 // Restrict a context to its slab of last-axis layers [cuts[rank], cuts[rank+1]).
 void make_slab(perrk_ctx* c, int rank, int nranks, const int* cuts) {
   REQUIRE(!c->slab, "context is already decomposed");
+  if (c->physics == 1)
+    throw Fail(PERRK_EUNSUP, "the slab decomposition runs the Euler configurations");
   REQUIRE(!c->has_family, "decompose before perrk_set_family");
   REQUIRE(nranks >= 2 && rank >= 0 && rank < nranks, "bad rank / rank count");
   const int L = c->dim - 1, nl = c->nlast;
@@ -769,7 +814,10 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     REQUIRE(dsc && out, "null argument");
     REQUIRE(dsc->dim == 2 || dsc->dim == 3, "dim must be 2 or 3");
     if (dsc->polydeg != 3) throw Fail(PERRK_EUNSUP, "the device path is built for polydeg 3");
-    if (dsc->physics != 0) throw Fail(PERRK_EUNSUP, "Navier-Stokes/BR1 not built yet");
+    REQUIRE(dsc->physics == 0 || dsc->physics == 1, "physics must be 0 (Euler) or 1 (NSF)");
+    if (dsc->physics == 1 && dsc->dim != 2)
+      throw Fail(PERRK_EUNSUP, "Navier-Stokes/BR1 runs in 2D on the device");
+    if (dsc->physics == 1) REQUIRE(dsc->mu >= 0.0 && dsc->prandtl > 0.0, "need mu >= 0 and Pr > 0");
     if (dsc->volume_mode != 1) throw Fail(PERRK_EUNSUP, "weak-form volume integral not on the device path");
     if (dsc->volume_flux != PERRK_FLUX_EC)
       throw Fail(PERRK_EUNSUP, "device flux differencing uses the Ranocha EC volume flux");
@@ -791,6 +839,8 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     c->ph.gamma = dsc->gamma;
     c->ph.gm1 = dsc->gamma - 1.0;
     c->ph.inv_gm1 = 1.0 / (dsc->gamma - 1.0);
+    c->ph.mu = dsc->physics == 1 ? dsc->mu : 0.0;
+    c->ph.kappa = dsc->physics == 1 ? dsc->gamma / (dsc->gamma - 1.0) * dsc->mu / dsc->prandtl : 0.0;
     c->basis = make_basis(3);
     for (int a = 0; a < 3; ++a) {
       c->nc[a] = a < dsc->dim ? dsc->n[a] : 1;
@@ -866,8 +916,10 @@ int perrk_destroy(perrk_ctx* c) {
   for (int a = 0; a < 3; ++a)
     for (double* p : {c->dh[a], c->djac[a], c->dlift[a]})
       if (p) cudaFree(p);
-  for (auto& p : c->plan)
+  for (auto& p : c->plan) {
     if (p.dlist) cudaFree(p.dlist);
+    if (p.glist) cudaFree(p.glist);
+  }
   if (c->st) cudaFree(c->st);
   if (c->counter) cudaFree(c->counter);
   if (c->dint) cudaFree(c->dint);
@@ -1008,8 +1060,27 @@ int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const
       a.write_k = 1;
       a.ncells = c->ncells_global;
       a.cell_offset = 0;
+      a.ndofs = c->ndofs;
+      int* gl_dev = nullptr;
+      if (c->physics == 1) {  // BR1 viscous fluxes on the cells and their neighbours
+        std::vector<char> on(c->ncells, 0);
+        for (int q : list) on[q] = 1;
+        const std::vector<int> gl = with_neighbours_2d(c, on);
+        CK(cudaMalloc(&gl_dev, sizeof(int) * gl.size()));
+        CK(cudaMemcpyAsync(gl_dev, gl.data(), sizeof(int) * gl.size(), cudaMemcpyHostToDevice,
+                           c->stream));
+        StageArgs ga = a;
+        ga.list = gl_dev;
+        ga.n = static_cast<int>(gl.size());
+        CK(launch_grad(ga, c->mesh(), c->ph, c->st, c->G, c->ndofs, 0, c->grid_stage, c->stream));
+        a.G = c->G;
+      }
       CK(launch_stage(c->dim, c->surface, a, c->mesh(), c->ph, c->st, c->partials, c->counter,
                       c->grid_stage, c->stream));
+      if (gl_dev) {
+        CK(cudaStreamSynchronize(c->stream));
+        cudaFree(gl_dev);
+      }
       const StepState r = get_state(c);
       if (r.bad_code != std::numeric_limits<long long>::max())
         throw Fail(PERRK_ENUMERIC, "inadmissible state passed to numerical flux");
@@ -1018,9 +1089,24 @@ int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const
   });
 }
 
-int perrk_br1_gradients(perrk_ctx*, double, const double*, double*) {
-  g_last_error = "Navier-Stokes/BR1 not built yet";
-  return PERRK_EUNSUP;
+int perrk_br1_gradients(perrk_ctx* c, double t, const double* U, double* grads) {
+  (void)t;
+  return guarded([&] {
+    REQUIRE(c && U && grads, "null argument");
+    no_slab(c, "br1_gradients");
+    if (c->physics != 1) throw Fail(PERRK_EUNSUP, "BR1 gradients need NSF physics");
+    set_device(c);
+    upload(c, c->tU, U);
+    StepState s = fresh_state();
+    put_state(c, s);
+    StageArgs a{};
+    a.U = a.K1 = a.Kp = c->tU;
+    a.n = static_cast<int>(c->ncells);
+    CK(launch_grad(a, c->mesh(), c->ph, c->st, c->G, c->ndofs, 1, c->grid_stage, c->stream));
+    CK(cudaMemcpyAsync(grads, c->G, sizeof(double) * 2 * c->ndofs, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
 }
 
 int perrk_total_entropy(perrk_ctx* c, const double* U, double* out) {

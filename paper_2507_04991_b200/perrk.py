@@ -229,6 +229,13 @@ class Semidiscretization:
         check(lib().perrk_rhs_masked(self._h, float(t), _dp(U), _dp(out), mb))
         return out
 
+    def br1_gradients(self, t, U):
+        """BR1 auxiliary gradients (semidisc.hpp:75), NSF physics: [dim][dofs]."""
+        U = self._state(U)
+        g = np.empty(2 * U.size)
+        check(lib().perrk_br1_gradients(self._h, float(t), _dp(U), _dp(g)))
+        return g.reshape(2, -1)
+
     def rhs_partition_restricted(self, t, U, pmap, level):
         mask = (np.asarray(pmap.effective_level) == level).astype(np.int8)
         return self.rhs_masked(t, U, mask)

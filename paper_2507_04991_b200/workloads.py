@@ -11,7 +11,9 @@ Appendix A) are fixed here and recorded in DESIGN.md:
       EC + HLLE, p3 {4,7}, 500 steps
   C3  256^2 three-level "+" mesh on [0,2pi]^2, seeded random Fourier state,
       EC + Rusanov, p4 {5,9,16}, 200 steps
-  C4  (2D Navier-Stokes double shear layer) -- pending on the device path
+  C4  512^2 two-level "+" mesh on [0,1]^2 (64 h | 128 h/2 | 128 h | 128 h/2 |
+      64 h per axis, h = 1/384), double shear layer (delta 1/30, eps 0.05,
+      Ma 0.1), NSF mu = 1e-4, Pr = 0.72, BR1, EC + HLLE, p3 {4,8}, 200 steps
   C5  64^3 three-level "+" mesh on [0,2pi]^3, Taylor-Green vortex Ma 0.1,
       EC + Rusanov, p4 {5,8,14}, 100 steps
 Free coefficients of the C2-C5 families come from configs/make_families.py
@@ -104,6 +106,17 @@ def random_fourier_state(x, y, seed=20250704, modes=8, kmax=4, gamma=1.4, length
     return np.stack([rho, rho * vx, rho * vy, p / (gamma - 1.0) + 0.5 * rho * (vx * vx + vy * vy)])
 
 
+def double_shear_layer(x, y, mach=0.1, gamma=1.4, delta=1.0 / 30.0, eps=0.05):
+    """C4: periodic double shear layer on [0,1]^2 (Bell-Colella-Glaz form):
+    u = tanh((y - 1/4)/delta) for y <= 1/2, tanh((3/4 - y)/delta) above,
+    v = eps sin(2 pi (x + 1/4)), rho = 1, p = 1/(gamma Ma^2) (Ma on |u| = 1)."""
+    vx = np.where(y <= 0.5, np.tanh((y - 0.25) / delta), np.tanh((0.75 - y) / delta))
+    vy = eps * np.sin(2 * math.pi * (x + 0.25))
+    rho = np.ones_like(x)
+    p = np.full_like(x, 1.0 / (gamma * mach * mach))
+    return np.stack([rho, rho * vx, rho * vy, p / (gamma - 1.0) + 0.5 * rho * (vx * vx + vy * vy)])
+
+
 def taylor_green(x, y, z, mach=0.1, gamma=1.4, rho0=1.0, u0=1.0):
     """C5: 3D Taylor-Green vortex on [0, 2pi]^3 at Mach `mach`:
     p0 = rho0 u0^2 / (gamma Ma^2),
@@ -189,6 +202,8 @@ class Config:
             return random_fourier_state(x, y)
         if self.ic == "tgv":
             return taylor_green(x, y, z)
+        if self.ic == "shear":
+            return double_shear_layer(x, y)
         raise ValueError(self.ic)
 
     def nodes_per_cell(self):
@@ -235,6 +250,16 @@ def make_config(name: str, family=None, cfl=None, steps=None) -> Config:
         return Config("c3", "2D Euler random Fourier state, 256^2 3-level mesh, p4 {5,9,16}",
                       mesh, "rusanov", fam, geometric_levels([al, al], fam.R), cfl or 1.5,
                       steps or 200, "random")
+    if name == "c4":
+        h = 1.0 / 384.0
+        bands = [(64, h), (128, h / 2), (128, h), (128, h / 2), (64, h)]
+        e = banded_edges(0.0, bands)
+        mesh = P.Mesh2DRect(e, list(e))
+        al = axis_levels(bands)
+        fam = family or load_config_family("c4_p3_4_8")
+        return Config("c4", "2D Navier-Stokes double shear layer, 512^2 2-level mesh, p3 {4,8}",
+                      mesh, "hlle", fam, geometric_levels([al, al], fam.R), cfl or 1.1,
+                      steps or 200, "shear", physics="nsf", mu=1e-4, prandtl=0.72)
     if name == "c5":
         h = 2 * math.pi / 54.0
         bands = [(24, h), (4, h / 2), (8, h / 4), (4, h / 2), (24, h)]

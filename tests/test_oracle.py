@@ -324,3 +324,32 @@ def test_reference_own_suite_passes(name):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "failed: 0" in r.stdout
+
+
+@need_ref
+@pytest.mark.parametrize("surface", ["rusanov", "hlle"])
+def test_orc_nsf2d_reduces_to_reference_nsf1d(surface):
+    """Oracle extension pin (2D NSF + BR1): on y-independent data with v = 0
+    the 2D RHS equals the reference's own 1D NSF + BR1 RHS (NSFPhysics,
+    semidisc.cpp:245-395) in (rho, m_x, E), with a zero y-momentum RHS."""
+    xe = nonuniform = np.cumsum(np.r_[0.0, np.random.default_rng(4).uniform(0.5, 1.5, 9)])
+    xe = list(xe / xe[-1] * 2.0 - 1.0)
+    ref = O.RefNSF1D(xe, mu=2e-2, surface_flux=surface)
+    x1 = ref.node_coords()
+    rho = 1.0 + 0.2 * np.sin(np.pi * x1)
+    vx = 0.3 * np.cos(np.pi * x1)
+    p = 1.0 + 0.25 * np.sin(2 * np.pi * x1 + 0.3)
+    U1 = np.stack([rho, rho * vx, p / 0.4 + 0.5 * rho * vx * vx]).T.reshape(-1)
+    r1 = ref.rhs(0.0, U1).reshape(-1, 4, 3)            # [cell][node][var]
+    m2 = P.Mesh2DRect(xe, [0.0, 0.5, 1.2, 2.0])
+    orc = O.Orc(m2, surface_flux=surface, viscous=True, mu=2e-2, prandtl=0.72)
+    nx, ny = 9, 3
+    u1 = U1.reshape(nx, 4, 3)
+    U2 = np.zeros((ny, nx, 4, 4, 4))                   # [cj][ci][iy][ix][v]
+    for v, v2 in ((0, 0), (1, 1), (2, 3)):
+        U2[..., v2] = u1[None, :, None, :, v]
+    r2 = orc.rhs(0.0, U2.reshape(-1)).reshape(U2.shape)
+    scale = np.abs(r1).max()
+    for v, v2 in ((0, 0), (1, 1), (2, 3)):
+        assert np.abs(r2[..., v2] - r1.reshape(nx, 4, 3)[None, :, None, :, v]).max() < 1e-12 * scale
+    assert np.abs(r2[..., 2]).max() < 1e-12 * scale
