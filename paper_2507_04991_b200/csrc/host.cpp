@@ -271,6 +271,10 @@ struct Exchange {
 struct Group {
   std::vector<perrk_ctx*> members;
   std::unique_ptr<Exchange> ex;  // null: a single context on the whole mesh
+  cudaStream_t shared_stream = nullptr;  // loopback: owned by the group, not a member
+  ~Group() {
+    if (shared_stream) cudaStreamDestroy(shared_stream);
+  }
 };
 
 }  // namespace perrk
@@ -1527,15 +1531,17 @@ int perrk_loopback_group(perrk_ctx** ctxs, int n, const int* cuts) {
     }
     auto g = std::make_shared<Group>();
     g->ex = std::make_unique<LoopbackExchange>();
+    set_device(ctxs[0]);
+    CK(cudaStreamCreateWithFlags(&g->shared_stream, cudaStreamNonBlocking));
     for (int r = 0; r < n; ++r) {
       perrk_ctx* c = ctxs[r];
       make_slab(c, r, n, cuts);
-      if (r > 0) {  // one stream orders every member's work
-        CK(cudaStreamSynchronize(c->stream));
-        if (c->own_stream) CK(cudaStreamDestroy(c->stream));
-        c->stream = ctxs[0]->stream;
-        c->own_stream = false;
-      }
+      // one stream, owned by the group (it outlives every member), orders
+      // every member's work
+      CK(cudaStreamSynchronize(c->stream));
+      if (c->own_stream) CK(cudaStreamDestroy(c->stream));
+      c->stream = g->shared_stream;
+      c->own_stream = false;
       g->members.push_back(c);
       c->group = g;
     }

@@ -363,7 +363,7 @@ class Semidiscretization:
         A = _f64(family.A)
         b, c = _f64(family.b), _f64(family.c)
         eff = np.ascontiguousarray(pmap.effective_level, dtype=np.int32)
-        if eff.size != self.num_cells():
+        if eff.size != self.global_num_cells():
             raise Error(capi.PERRK_EINVAL, "partition map does not match semidiscretization")
         fd = capi.FamilyDesc(capi.FAMILY[family.kind], family.S, family.R, _ip(E), _dp(A), _dp(b),
                              _dp(c))
