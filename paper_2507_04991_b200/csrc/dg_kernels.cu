@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(256)
   }
   const double gamma = st->gamma;
   const double gdt = gamma * st->dt;
+  const int numerics = st->numerics;
   dd A = dd_zero(), B = dd_zero();
   for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < nnodes;
        n += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -229,17 +230,17 @@ __global__ void __launch_bounds__(256)
       dv[v] = __ldg(d + n * V + v);
       T[v] = u[v] + gdt * dv[v];
     }
-    double a;
-    if (st->numerics == 1) {
-      double du[V];
+    if (numerics == 1) {
+      double du[V], a, b;
 #pragma unroll
       for (int v = 0; v < V; ++v) du[v] = gdt * dv[v];
-      a = entropy_difference<DIM>(ph, u, du);
-    } else {
-      a = entropy<DIM>(ph, T);
+      relax_terms<DIM>(ph, u, du, dv, a, b);
+      A = dd_add_prod(A, om, a);
+      B = dd_add_prod(B, om, b);
+    } else {  // the reference's residual / derivative on the rounded trial state
+      A = dd_add_prod(A, om, entropy<DIM>(ph, T));
+      B = dd_add_prod(B, om, entropy_dot<DIM>(ph, T, dv));
     }
-    A = dd_add_prod(A, om, a);
-    B = dd_add_prod(B, om, entropy_dot<DIM>(ph, T, dv));
   }
   dd v[2] = {A, B}, tot[2];
   block_reduce_dd<2>(v, s_red);

@@ -19,6 +19,7 @@ struct StageArgs {
   double a1[dev::MAXR + 1];  // a_{i,1} by effective level
   double ap[dev::MAXR + 1];  // a_{i,i-1} by effective level
   int form;              // 0: stage state = U_n; 1: U_n + dt (a1 K1 [+ ap K_{i-1}])
+  int kp_used;           // some level reads K_{i-1} at this stage
   int write_k;
   int d_mode;            // 0 none, 1 d = b K, 2 d += b K
   double b;

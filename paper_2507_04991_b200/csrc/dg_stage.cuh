@@ -33,22 +33,9 @@
 namespace perrk {
 namespace dev {
 
-// 1/x to full double precision: MUFU seed, two Newton steps (rel. error of
-// the seed squared twice), no slow path (x is a finite positive/negative
-// normal number wherever it is used).
-__device__ __forceinline__ double frcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-
-__device__ __forceinline__ double fdiv(double a, double b) {
-  const double r = frcp(b);
-  const double q = a * r;
-  return fma(fma(-b, q, a), r, q);
+// cp.async.bulk.prefetch.L2 (sm_90+): bytes a multiple of 16, 16-byte aligned
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 template <int DIM>
@@ -293,65 +280,59 @@ __device__ __forceinline__ int pick_int3(const int (&a)[3], int i) {
   return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]);
 }
 
-// Volume, diagonal and surface terms of one node along direction D
-// (compile-time, so velocity components, strides and flux slots resolve
-// statically).  cd: the cell's index along D; nbc: neighbour cells across
-// the -D / +D faces (for the positivity report).
-template <int DIM, int SURF, int D>
-__device__ __forceinline__ void direction_terms(const Phys& ph, const MeshDev& m, StepState* st,
-                                                const StageArgs& a, const double* pr,
-                                                const double* nb, int tid, int cs,
-                                                const int (&il)[3], int cd,
-                                                const long long* nbc,
-                                                const Prim<DIM>& own, double lr, double be,
-                                                double lb, double* K) {
+// Flux-differencing volume term of one node along direction D (compile-time,
+// so velocity components, strides and flux slots resolve statically).
+template <int DIM, int D>
+__device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, int tid,
+                                             const int (&il)[3], double J2, const Prim<DIM>& own,
+                                             double lr, double be, double lb, double* K) {
   using G = StageGeo<DIM>;
   using S = Slot<DIM>;
-  constexpr int V = G::V, FP = G::FP, T = G::T;
+  constexpr int V = G::V, T = G::T;
   constexpr int stride = D == 0 ? 1 : (D == 1 ? N1 : N1 * N1);
   const int j = il[D];
-  const double J2 = 2.0 * m.jac[D][cd];
-  // ---- volume: the three partners on this node's D-line (semidisc.cpp:455-464;
-  // the EC flux is symmetric, so f(l, m) here is the reference's f(min, max)
-  // up to the order of commutative operations)
-#pragma unroll
-  for (int s = 1; s < N1; ++s) {
-    const int k = (j + s) & (N1 - 1);
+  // ---- volume: the three partners on this node's D-line (semidisc.cpp:455-464).
+  // Lines along x and y lie inside a warp (node = ix + 4 iy + 16 iz), so each
+  // symmetric pair is evaluated once: lane j computes f(j, j+1 mod 4) and
+  // receives f(j-1, j) from its neighbour by shuffle; the distance-2 pair is
+  // evaluated by both ends.  Along z the lines cross warps: every lane
+  // evaluates its three pairs.  The EC flux is symmetric in its arguments up
+  // to the order of commutative operations.
+  auto ec_with = [&](int k, double* f) {
     const int qk = tid + (k - j) * stride;
     double vk[DIM];
 #pragma unroll
     for (int i = 0; i < DIM; ++i) vk[i] = pr[(S::V0 + i) * T + qk];
-    double f[V];
     ec2<DIM>(ph, D, own.rho, own.v, own.p, lr, be, lb, pr[S::RHO * T + qk], vk,
              pr[S::P * T + qk], pr[S::LRHO * T + qk], pr[S::BETA * T + qk],
              pr[S::LBETA * T + qk], f);
-    const double cjk = J2 * c_D[j * N1 + k];
+  };
+  constexpr bool kInWarp = D < 2;
+  if constexpr (kInWarp) {
+    const int kn = (j + 1) & (N1 - 1), kp = (j + N1 - 1) & (N1 - 1), k2 = (j + 2) & (N1 - 1);
+    double f1[V], f2[V], fp[V];
+    ec_with(kn, f1);
+    const int src = (threadIdx.x & 31) + (kp - j) * stride;
 #pragma unroll
-    for (int v = 0; v < V; ++v) K[v] = fma(-cjk, f[v], K[v]);
-  }
-  // ---- endpoints: diagonal physical flux (D_ll != 0 only there,
-  // basis.cpp:80-81) and surface flux + strong-form lift (semidisc.cpp:492-556)
-  if (j == 0 || j == N1 - 1) {
-    const int e = j == 0 ? 0 : 1;
-    double fo[V];
-    pflux<DIM>(own, D, fo);
-    const int pt = D == 0 ? il[1] + N1 * il[2] : (D == 1 ? il[0] + N1 * il[2] : il[0] + N1 * il[1]);
-    const double* un = nb + ((cs * 2 * DIM + 2 * D + e) * FP + pt) * V;
-    double uu[V];
+    for (int v = 0; v < V; ++v) fp[v] = __shfl_sync(0xffffffffu, f1[v], src);
+    ec_with(k2, f2);
+    const double cn = J2 * c_D[j * N1 + kn], cp = J2 * c_D[j * N1 + kp], c2 = J2 * c_D[j * N1 + k2];
 #pragma unroll
-    for (int v = 0; v < V; ++v) uu[v] = un[v];
-    const Prim<DIM> nbp = prim_of<DIM>(ph, uu);
-    if (!prim_ok<DIM>(nbp)) report_bad(st, a.stage, a.ncells, nbc[e]);
-    double fs[V];
-    if (e)
-      sflux<DIM, SURF>(ph, own, nbp, D, fs);
-    else
-      sflux<DIM, SURF>(ph, nbp, own, D, fs);
-    const double lift = m.lift[D][cd];
-    const double cll = J2 * c_D[j * N1 + j];
-    const double sg = e ? -lift : lift;
+    for (int v = 0; v < V; ++v) {
+      K[v] = fma(-cn, f1[v], K[v]);
+      K[v] = fma(-cp, fp[v], K[v]);
+      K[v] = fma(-c2, f2[v], K[v]);
+    }
+  } else {
 #pragma unroll
-    for (int v = 0; v < V; ++v) K[v] = fma(sg, fs[v] - fo[v], fma(-cll, fo[v], K[v]));
+    for (int s = 1; s < N1; ++s) {
+      const int k = (j + s) & (N1 - 1);
+      double f[V];
+      ec_with(k, f);
+      const double cjk = J2 * c_D[j * N1 + k];
+#pragma unroll
+      for (int v = 0; v < V; ++v) K[v] = fma(-cjk, f[v], K[v]);
+    }
   }
 }
 
@@ -362,17 +343,21 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
   using G = StageGeo<DIM>;
   using S = Slot<DIM>;
   constexpr int V = G::V, NPC = G::NPC, FP = G::FP, NFP = G::NFP, CPB = G::CPB, T = G::T;
+  constexpr int NQ = (CPB * NFP + T - 1) / T;  // face points per thread
   extern __shared__ double smem[];
-  double* pr = smem;            // [NPR][T]
-  double* nb = pr + G::SM_PR;   // [CPB][NFP][V]
-  double* vg = nb + G::SM_NB;   // VISC: own G [2][T][V], then neighbour G_d [CPB][NFP][V]
+  double* pr = smem;            // [NPR][T] per-node primitives
+  double* sf = pr + G::SM_PR;   // [CPB][NFP][V] surface + diagonal terms per face point
+  double* vg = sf + G::SM_NB;   // VISC: own G [2][T][V], then neighbour G_d [CPB][NFP][V]
   double* vn = vg + 2 * T * V;
-  __shared__ int s_cell[CPB];
-  __shared__ int s_coord[CPB][3];
-  __shared__ double s_ca1[CPB], s_cap[CPB];
-  __shared__ int s_nbc[CPB][2 * DIM];          // local neighbour, or -1 - face cell (ghost)
-  __shared__ long long s_nbg[CPB][2 * DIM];    // global id (positivity reports)
-  __shared__ double s_na1[CPB][2 * DIM], s_nap[CPB][2 * DIM];
+  // group descriptors, double-buffered: the next group's are written while
+  // the current one computes
+  __shared__ int s_cell_[2][CPB];
+  __shared__ int s_coord_[2][CPB][3];
+  __shared__ double s_ca1_[2][CPB], s_cap_[2][CPB];
+  __shared__ double s_J2_[2][CPB][DIM], s_lift_[2][CPB][DIM];
+  __shared__ int s_nbc_[2][CPB][2 * DIM];        // local neighbour, or -1 - face cell (ghost)
+  __shared__ long long s_nbg_[2][CPB][2 * DIM];  // global id (positivity reports)
+  __shared__ double s_na1_[2][CPB][2 * DIM], s_nap_[2][CPB][2 * DIM];
   __shared__ double s_red[2 * 2 * (T / 32)];
 
   if (st->aborted || st->finished) return;  // uniform across the grid
@@ -385,27 +370,22 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
   bool dbad = false;
   const int ngroups = (a.n + CPB - 1) / CPB;
 
-  // group descriptor of the first group, loaded by threads < CPB and
-  // thereafter prefetched one group ahead (the list -> cell -> level chain
-  // resolves while the current group computes)
-  int nx_cell = -1;
-  if (tid < CPB) {
-    const int slot = blockIdx.x * CPB + tid;
-    nx_cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
-  }
-
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    if (tid < CPB) {
-      const int cell = nx_cell;
-      s_cell[tid] = cell;
+  // descriptor of one group (threads < CPB, one cell each) into buffer b
+  auto describe = [&](int b, int t, int cell) {
+      s_cell_[b][t] = cell;
       const int cc = cell < 0 ? 0 : cell;
       int co[3] = {cc % m.nc[0], (cc / m.nc[0]) % m.nc[1], cc / (m.nc[0] * m.nc[1])};
-      s_coord[tid][0] = co[0];
-      s_coord[tid][1] = co[1];
-      s_coord[tid][2] = co[2];
+      s_coord_[b][t][0] = co[0];
+      s_coord_[b][t][1] = co[1];
+      s_coord_[b][t][2] = co[2];
       const int lev = m.level[cc];
-      s_ca1[tid] = dt * a.a1[lev];
-      s_cap[tid] = dt * a.ap[lev];
+      s_ca1_[b][t] = dt * a.a1[lev];
+      s_cap_[b][t] = dt * a.ap[lev];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        s_J2_[b][t][d] = 2.0 * m.jac[d][co[d]];
+        s_lift_[b][t][d] = m.lift[d][co[d]];
+      }
 #pragma unroll
       for (int f = 0; f < 2 * DIM; ++f) {  // face neighbours (periodic / ghost), their rows
         const int d = f >> 1, side = f & 1;
@@ -419,28 +399,68 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
           // traces received from the neighbouring slab; no formation here
           const int fc = DIM == 3 ? co[0] + m.nc[0] * co[1] : co[0];
           const int gl = side ? (m.layer0 + nd) % m.nlast : (m.layer0 - 1 + m.nlast) % m.nlast;
-          s_nbc[tid][f] = -1 - fc;
-          s_nbg[tid][f] = fc + layer_cells * gl;
-          s_na1[tid][f] = 0.0;
-          s_nap[tid][f] = 0.0;
+          s_nbc_[b][t][f] = -1 - fc;
+          s_nbg_[b][t][f] = fc + layer_cells * gl;
+          s_na1_[b][t][f] = 0.0;
+          s_nap_[b][t][f] = 0.0;
         } else {
           const int l2 = m.level[nbc];
-          s_nbc[tid][f] = nbc;
-          s_nbg[tid][f] = nbc + a.cell_offset;
-          s_na1[tid][f] = dt * a.a1[l2];
-          s_nap[tid][f] = dt * a.ap[l2];
+          s_nbc_[b][t][f] = nbc;
+          s_nbg_[b][t][f] = nbc + a.cell_offset;
+          s_na1_[b][t][f] = dt * a.a1[l2];
+          s_nap_[b][t][f] = dt * a.ap[l2];
         }
       }
-      const int slot = (grp + gridDim.x) * CPB + tid;  // prefetch the next group
+  };
+
+  // first group's descriptors; afterwards each group describes the next one
+  // while it computes (list -> cell -> level chains resolve off the critical path)
+  if (tid < CPB) {
+    const int slot = blockIdx.x * CPB + tid;
+    describe(0, tid, slot < a.n ? (a.list ? a.list[slot] : slot) : -1);
+  }
+  __syncthreads();
+  int buf = 0;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf ^= 1) {
+    auto& s_cell = s_cell_[buf];
+    auto& s_coord = s_coord_[buf];
+    auto& s_ca1 = s_ca1_[buf];
+    auto& s_cap = s_cap_[buf];
+    auto& s_J2 = s_J2_[buf];
+    auto& s_lift = s_lift_[buf];
+    auto& s_nbc = s_nbc_[buf];
+    auto& s_nbg = s_nbg_[buf];
+    auto& s_na1 = s_na1_[buf];
+    auto& s_nap = s_nap_[buf];
+    // the last CPB threads fetch and describe the next group
+    const int dt_t = tid - (T - CPB);
+    int nx_cell = -1;
+    if (dt_t >= 0) {
+      const int slot = (grp + gridDim.x) * CPB + dt_t;
       nx_cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
     }
-    __syncthreads();
     const int cell = s_cell[cs];
+    // the next group's own cells go to L2 now (bulk prefetch, contiguous
+    // NPC*V doubles per array), so its loads hit L2 instead of HBM
+    if (dt_t >= 0 && nx_cell >= 0) {
+      constexpr unsigned kBytes = NPC * V * sizeof(double);
+      const size_t off = static_cast<size_t>(nx_cell) * NPC * V;
+      l2_prefetch(a.U + off, kBytes);
+      if (a.form) {
+        l2_prefetch(a.K1 + off, kBytes);
+        if (a.kp_used) l2_prefetch(a.Kp + off, kBytes);
+      }
+    }
 
-    // ---- load: own node (coalesced: consecutive threads, consecutive nodes)
-    // and this thread's share of the cells' neighbour face traces ------------
+    // ---- load: own node (coalesced: consecutive threads, consecutive nodes),
+    // formed with the cell's member row (stepper.cpp:60-72) ------------------
     Prim<DIM> own;
-    double lr = 0.0, be = 0.0, lb = 0.0;
+    own.rho = 1.0;  // padding lanes (tail group) compute on a dummy state
+    own.p = 1.0;
+    own.E = 2.5;
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) own.v[i] = 0.0;
+    double lr = 0.0, be = 1.0, lb = 0.0;
     if (cell >= 0) {
       const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
       double u[V];
@@ -473,26 +493,30 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
       pr[S::BETA * T + tid] = be;
       pr[S::LBETA * T + tid] = lb;
     }
+    // ---- this thread's face points: the neighbour's trace, formed with the
+    // neighbour's row (or received from the neighbouring slab), kept in
+    // registers across the barrier --------------------------------------------
+    double nbu[NQ][V];
 #pragma unroll
-    for (int q = tid; q < CPB * NFP; q += T) {
+    for (int k = 0; k < NQ; ++k) {
+      const int q = tid + k * T;
+      if (q >= CPB * NFP) break;
       const int c2 = q / NFP, r = q % NFP, f = r / FP, pt = r % FP;
       const int d = f >> 1, side = f & 1;
       if (s_cell[c2] < 0) continue;
       const int nbc = s_nbc[c2][f];
-      double* o = nb + q * V;
-      if (nbc < 0) {  // slab boundary: formed trace from the neighbouring rank
+      if (nbc < 0) {
         const double* g = (side ? m.ghost_hi : m.ghost_lo) + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
 #pragma unroll
-        for (int v = 0; v < V; ++v) o[v] = g[v];
+        for (int v = 0; v < V; ++v) nbu[k][v] = g[v];
         continue;
       }
       // the neighbour's node on the shared face: far end of the same line
       const int node =
           line_base<DIM>(d, pt % N1, pt / N1) + (side ? 0 : N1 - 1) * line_stride(d);
       const size_t gi = (static_cast<size_t>(nbc) * NPC + node) * V;
-      double u[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
+      for (int v = 0; v < V; ++v) nbu[k][v] = __ldg(a.U + gi + v);
       if (a.form) {
         const double b1 = s_na1[c2][f], bp = s_nap[c2][f];
         double k1[V];
@@ -500,14 +524,12 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
         for (int v = 0; v < V; ++v) k1[v] = __ldg(a.K1 + gi + v);
         if (bp != 0.0) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) u[v] = u[v] + fma(b1, k1[v], bp * __ldg(a.Kp + gi + v));
+          for (int v = 0; v < V; ++v) nbu[k][v] = nbu[k][v] + fma(b1, k1[v], bp * __ldg(a.Kp + gi + v));
         } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v) u[v] = fma(b1, k1[v], u[v]);
+          for (int v = 0; v < V; ++v) nbu[k][v] = fma(b1, k1[v], nbu[k][v]);
         }
       }
-#pragma unroll
-      for (int v = 0; v < V; ++v) o[v] = u[v];
     }
     if constexpr (VISC) {  // BR1 viscous fluxes from grad_kernel (2D)
       const size_t nd = static_cast<size_t>(a.ndofs);
@@ -532,14 +554,69 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
     }
     __syncthreads();
 
+    // ---- surface flux + strong-form lift and the endpoint diagonal term, one
+    // face point per thread (semidisc.cpp:489-556, diagonal :450-454) ----------
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int q = tid + k * T;
+      if (q >= CPB * NFP) break;
+      const int c2 = q / NFP, r = q % NFP, f = r / FP, pt = r % FP;
+      const int d = f >> 1, side = f & 1;
+      if (s_cell[c2] < 0) continue;
+      const int own_q = c2 * NPC + line_base<DIM>(d, pt % N1, pt / N1) +
+                        (side ? N1 - 1 : 0) * line_stride(d);
+      Prim<DIM> o;
+      o.rho = pr[S::RHO * T + own_q];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) o.v[i] = pr[(S::V0 + i) * T + own_q];
+      o.p = pr[S::P * T + own_q];
+      o.E = pr[S::E * T + own_q];
+      const Prim<DIM> nbp = prim_of<DIM>(ph, nbu[k]);
+      if (!prim_ok<DIM>(nbp)) report_bad(st, a.stage, a.ncells, s_nbg[c2][f]);
+      double fs[V], fo[V];
+      const double J2 = s_J2[c2][d], lift = s_lift[c2][d];
+      const int j = side ? N1 - 1 : 0;
+      const double cll = J2 * c_D[j * N1 + j];
+      const double sg = side ? -lift : lift;
+      // compile-time direction for the flux kernels
+      if (d == 0) {
+        pflux<DIM>(o, 0, fo);
+        if (side) sflux<DIM, SURF>(ph, o, nbp, 0, fs); else sflux<DIM, SURF>(ph, nbp, o, 0, fs);
+      } else if (d == 1) {
+        pflux<DIM>(o, 1, fo);
+        if (side) sflux<DIM, SURF>(ph, o, nbp, 1, fs); else sflux<DIM, SURF>(ph, nbp, o, 1, fs);
+      } else {
+        pflux<DIM>(o, DIM - 1, fo);
+        if (side) sflux<DIM, SURF>(ph, o, nbp, DIM - 1, fs);
+        else sflux<DIM, SURF>(ph, nbp, o, DIM - 1, fs);
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) sf[q * V + v] = fma(sg, fs[v] - fo[v], -cll * fo[v]);
+    }
+
+    // ---- flux-differencing volume terms (every lane: the in-warp pair
+    // exchange needs the whole warp; padding lanes are discarded) ------------
     double K[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) K[v] = 0.0;
+    volume_terms<DIM, 0>(ph, pr, tid, il, s_J2[cs][0], own, lr, be, lb, K);
+    volume_terms<DIM, 1>(ph, pr, tid, il, s_J2[cs][1], own, lr, be, lb, K);
+    if constexpr (DIM == 3) volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, lr, be, lb, K);
+    if (dt_t >= 0) describe(buf ^ 1, dt_t, nx_cell);  // the next group, off the critical path
+    __syncthreads();  // surface terms of every face point visible
+
     if (cell >= 0) {
-      direction_terms<DIM, SURF, 0>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][0], &s_nbg[cs][2 * (0)], own, lr, be, lb, K);
-      direction_terms<DIM, SURF, 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][1], &s_nbg[cs][2 * (1)], own, lr, be, lb, K);
-      if constexpr (DIM == 3)
-        direction_terms<DIM, SURF, DIM - 1>(ph, m, st, a, pr, nb, tid, cs, il, s_coord[cs][DIM - 1], &s_nbg[cs][2 * (DIM - 1)], own, lr, be, lb, K);
+      // gather the node's face contributions (one per direction it ends)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        const int j = il[d];
+        if (j == 0 || j == N1 - 1) {
+          const int pt = d == 0 ? il[1] + N1 * il[2] : (d == 1 ? il[0] + N1 * il[2] : il[0] + N1 * il[1]);
+          const double* c = sf + ((cs * 2 * DIM + 2 * d + (j ? 1 : 0)) * FP + pt) * V;
+#pragma unroll
+          for (int v = 0; v < V; ++v) K[v] += c[v];
+        }
+      }
       if constexpr (VISC) {
         // weak-form divergence of the viscous flux with the central interface
         // flux (add_viscous_1d, semidisc.cpp:341-394, per direction)
@@ -547,8 +624,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
         for (int d = 0; d < DIM; ++d) {
           const int stride = d == 0 ? 1 : N1;
           const int j = il[d];
-          const int cd = s_coord[cs][d];
-          const double jac = m.jac[d][cd];
+          const double jac = 0.5 * s_J2[cs][d];
 #pragma unroll
           for (int k = 0; k < N1; ++k) {
             const double coef = jac * c_D[k * N1 + j] * c_w[k] / c_w[j];
@@ -561,7 +637,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
             const int pt = d == 0 ? il[1] : il[0];
             const double* gn = vn + ((cs * 2 * DIM + 2 * d + e) * FP + pt) * V;
             const double* go = vg + (d * T + tid) * V;
-            const double coef = m.lift[d][cd];
+            const double coef = s_lift[cs][d];
 #pragma unroll
             for (int v = 0; v < V; ++v) {
               const double gs = 0.5 * (e ? go[v] + gn[v] : gn[v] + go[v]);
@@ -605,7 +681,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
         }
       }
     }
-    __syncthreads();  // smem of this group consumed
+    __syncthreads();  // smem of this group consumed; next descriptors visible
   }
 
   // ---- grid epilogue --------------------------------------------------------

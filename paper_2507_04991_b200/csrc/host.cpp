@@ -460,6 +460,8 @@ void build_plan(perrk_ctx* c) {
       a.ap[lvl] = i >= 2 ? Am[i * S + i - 1] : 0.0;
     }
     a.form = i > 0 ? 1 : 0;
+    a.kp_used = 0;
+    for (int lvl = 1; lvl <= R; ++lvl) a.kp_used |= a.ap[lvl] != 0.0 ? 1 : 0;
     bool needed_next = false;
     if (i + 1 < S)
       for (int r = 0; r < R; ++r)
