@@ -53,6 +53,7 @@ struct StageGeo {
   static constexpr int SM_TOTAL = SM_PR + SM_NB;
   // BR1 (2D NSF): own viscous fluxes [2][T][V] and neighbour face values [CPB][NFP][V]
   static constexpr int SM_VISC = 2 * T * V + CPB * NFP * V;
+  static constexpr int SM_ZF = DIM == 3 ? T * V : 0;  // published z-pair fluxes
 };
 
 // primitive slots: rho, v[DIM], p, E, log rho, beta, log beta
@@ -285,7 +286,8 @@ __device__ __forceinline__ int pick_int3(const int (&a)[3], int i) {
 template <int DIM, int D>
 __device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, int tid,
                                              const int (&il)[3], double J2, const Prim<DIM>& own,
-                                             double lr, double be, double lb, double* K) {
+                                             double lr, double be, double lb, double* K,
+                                             double* zf = nullptr) {
   using G = StageGeo<DIM>;
   using S = Slot<DIM>;
   constexpr int V = G::V, T = G::T;
@@ -324,16 +326,34 @@ __device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, i
       K[v] = fma(-c2, f2[v], K[v]);
     }
   } else {
+    // z-lines cross warps: f(j, j+1) is published in shared memory and the
+    // partner's f(j-1, j) is picked up after the block's next barrier
+    // (zf_gather); the distance-2 pair is evaluated by both ends
+    const int kn = (j + 1) & (N1 - 1), k2 = (j + 2) & (N1 - 1);
+    double f1[V], f2[V];
+    ec_with(kn, f1);
 #pragma unroll
-    for (int s = 1; s < N1; ++s) {
-      const int k = (j + s) & (N1 - 1);
-      double f[V];
-      ec_with(k, f);
-      const double cjk = J2 * c_D[j * N1 + k];
+    for (int v = 0; v < V; ++v) zf[tid * V + v] = f1[v];
+    ec_with(k2, f2);
+    const double cn = J2 * c_D[j * N1 + kn], c2 = J2 * c_D[j * N1 + k2];
 #pragma unroll
-      for (int v = 0; v < V; ++v) K[v] = fma(-cjk, f[v], K[v]);
+    for (int v = 0; v < V; ++v) {
+      K[v] = fma(-cn, f1[v], K[v]);
+      K[v] = fma(-c2, f2[v], K[v]);
     }
   }
+}
+
+// the z-partner's published pair flux f(j-1, j) (after a block barrier)
+template <int DIM>
+__device__ __forceinline__ void zf_gather(const double* zf, int tid, const int (&il)[3],
+                                          double J2, double* K) {
+  constexpr int V = DIM + 2, stride = N1 * N1;
+  const int j = il[2], kp = (j + N1 - 1) & (N1 - 1);
+  const double cp = J2 * c_D[j * N1 + kp];
+  const double* f = zf + (tid + (kp - j) * stride) * V;
+#pragma unroll
+  for (int v = 0; v < V; ++v) K[v] = fma(-cp, f[v], K[v]);
 }
 
 template <int DIM, int SURF, bool VISC>
@@ -347,7 +367,8 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
   extern __shared__ double smem[];
   double* pr = smem;            // [NPR][T] per-node primitives
   double* sf = pr + G::SM_PR;   // [CPB][NFP][V] surface + diagonal terms per face point
-  double* vg = sf + G::SM_NB;   // VISC: own G [2][T][V], then neighbour G_d [CPB][NFP][V]
+  double* zf = sf + G::SM_NB;   // 3D: published z-pair fluxes [T][V]
+  double* vg = zf + G::SM_ZF;   // VISC: own G [2][T][V], then neighbour G_d [CPB][NFP][V]
   double* vn = vg + 2 * T * V;
   // group descriptors, double-buffered: the next group's are written while
   // the current one computes
@@ -601,10 +622,12 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
     for (int v = 0; v < V; ++v) K[v] = 0.0;
     volume_terms<DIM, 0>(ph, pr, tid, il, s_J2[cs][0], own, lr, be, lb, K);
     volume_terms<DIM, 1>(ph, pr, tid, il, s_J2[cs][1], own, lr, be, lb, K);
-    if constexpr (DIM == 3) volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, lr, be, lb, K);
+    if constexpr (DIM == 3)
+      volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, lr, be, lb, K, zf);
     if (dt_t >= 0) describe(buf ^ 1, dt_t, nx_cell);  // the next group, off the critical path
     __syncthreads();  // surface terms of every face point visible
 
+    if constexpr (DIM == 3) zf_gather<DIM>(zf, tid, il, s_J2[cs][DIM - 1], K);
     if (cell >= 0) {
       // gather the node's face contributions (one per direction it ends)
 #pragma unroll
