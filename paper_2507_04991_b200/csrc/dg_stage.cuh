@@ -44,7 +44,7 @@ struct StageGeo {
   static constexpr int NPC = DIM == 2 ? 16 : 64;  // nodes per cell
   static constexpr int FP = DIM == 2 ? 4 : 16;    // points per face
   static constexpr int NFP = 2 * DIM * FP;        // face points per cell
-  static constexpr int T = 128;                   // threads per block
+  static constexpr int T = 64;                    // threads per block
   static constexpr int CPB = T / NPC;             // cells per block (one node per thread)
   static constexpr int NPR = DIM + 6;             // primitives per node (see slots)
   // shared memory (doubles)
@@ -357,7 +357,7 @@ __device__ __forceinline__ void zf_gather(const double* zf, int tid, const int (
 }
 
 template <int DIM, int SURF, bool VISC>
-__global__ void __launch_bounds__(StageGeo<DIM>::T, 4)
+__global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     stage_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
                  unsigned* counter) {
   using G = StageGeo<DIM>;
