@@ -11,15 +11,18 @@ namespace perrk {
 struct StageArgs {
   const double* U;       // U_n
   const double* K1;      // K_1 (stage 0 RHS)
-  const double* Kp;      // K_{i-1}
-  double* Kout;          // K_i (written when write_k)
+  const double* Us;      // formed stage state U_i (cells of levels with formed[lev])
+  double* Usn;           // U_{i+1} of the processed cells (write_next)
+  double* Kout;          // K_i (written when write_k: stage 0 -> K1, rhs queries)
   double* d;             // update direction
   const int* list;       // active cells of the stage (nullptr: all cells 0..n-1)
   int n;                 // number of cells processed
-  double a1[dev::MAXR + 1];  // a_{i,1} by effective level
-  double ap[dev::MAXR + 1];  // a_{i,i-1} by effective level
-  int form;              // 0: stage state = U_n; 1: U_n + dt (a1 K1 [+ ap K_{i-1}])
-  int kp_used;           // some level reads K_{i-1} at this stage
+  double a1[dev::MAXR + 1];   // a_{i,1} by level: fallback formation U + dt a1 K1
+  double a1n[dev::MAXR + 1];  // a_{i+1,1} by level (epilogue formation of U_{i+1})
+  double apn[dev::MAXR + 1];  // a_{i+1,i} by level
+  signed char formed[dev::MAXR + 1];  // U_i of this level's cells is in Us (active at i-1)
+  int form;              // 0: the stage state is U_n (stage 0, RHS queries)
+  int write_next;        // U_{i+1} = U + dt (a_{i+1,1} K1 + a_{i+1,i} K_i) for processed cells
   int write_k;
   int d_mode;            // 0 none, 1 d = b K, 2 d += b K
   double b;

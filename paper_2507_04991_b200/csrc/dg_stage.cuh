@@ -374,11 +374,14 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   // the current one computes
   __shared__ int s_cell_[2][CPB];
   __shared__ int s_coord_[2][CPB][3];
-  __shared__ double s_ca1_[2][CPB], s_cap_[2][CPB];
+  __shared__ double s_ca1_[2][CPB];
+  __shared__ signed char s_cform_[2][CPB];
+  __shared__ int s_lev_[2][CPB];
   __shared__ double s_J2_[2][CPB][DIM], s_lift_[2][CPB][DIM];
   __shared__ int s_nbc_[2][CPB][2 * DIM];        // local neighbour, or -1 - face cell (ghost)
   __shared__ long long s_nbg_[2][CPB][2 * DIM];  // global id (positivity reports)
-  __shared__ double s_na1_[2][CPB][2 * DIM], s_nap_[2][CPB][2 * DIM];
+  __shared__ double s_na1_[2][CPB][2 * DIM];
+  __shared__ signed char s_nform_[2][CPB][2 * DIM];
   __shared__ double s_red[2 * 2 * (T / 32)];
 
   if (st->aborted || st->finished) return;  // uniform across the grid
@@ -401,7 +404,8 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       s_coord_[b][t][2] = co[2];
       const int lev = m.level[cc];
       s_ca1_[b][t] = dt * a.a1[lev];
-      s_cap_[b][t] = dt * a.ap[lev];
+      s_cform_[b][t] = a.formed[lev];
+      s_lev_[b][t] = lev;
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         s_J2_[b][t][d] = 2.0 * m.jac[d][co[d]];
@@ -423,13 +427,13 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
           s_nbc_[b][t][f] = -1 - fc;
           s_nbg_[b][t][f] = fc + layer_cells * gl;
           s_na1_[b][t][f] = 0.0;
-          s_nap_[b][t][f] = 0.0;
+          s_nform_[b][t][f] = 1;
         } else {
           const int l2 = m.level[nbc];
           s_nbc_[b][t][f] = nbc;
           s_nbg_[b][t][f] = nbc + a.cell_offset;
           s_na1_[b][t][f] = dt * a.a1[l2];
-          s_nap_[b][t][f] = dt * a.ap[l2];
+          s_nform_[b][t][f] = a.formed[l2];
         }
       }
   };
@@ -446,13 +450,14 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     auto& s_cell = s_cell_[buf];
     auto& s_coord = s_coord_[buf];
     auto& s_ca1 = s_ca1_[buf];
-    auto& s_cap = s_cap_[buf];
+    auto& s_cform = s_cform_[buf];
+    auto& s_lev = s_lev_[buf];
     auto& s_J2 = s_J2_[buf];
     auto& s_lift = s_lift_[buf];
     auto& s_nbc = s_nbc_[buf];
     auto& s_nbg = s_nbg_[buf];
     auto& s_na1 = s_na1_[buf];
-    auto& s_nap = s_nap_[buf];
+    auto& s_nform = s_nform_[buf];
     // the last CPB threads fetch and describe the next group
     const int dt_t = tid - (T - CPB);
     int nx_cell = -1;
@@ -466,13 +471,10 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     if (dt_t >= 0 && nx_cell >= 0) {
       constexpr unsigned kBytes = NPC * V * sizeof(double);
       const size_t off = static_cast<size_t>(nx_cell) * NPC * V;
-      l2_prefetch(a.U + off, kBytes);
-      if (a.form) {
-        l2_prefetch(a.K1 + off, kBytes);
-        if (a.kp_used) l2_prefetch(a.Kp + off, kBytes);
-      }
+      if (a.form) l2_prefetch(a.Us + off, kBytes);
+      l2_prefetch(a.U + off, kBytes);                       // stage 0 state / epilogue
+      if (a.write_next && a.form) l2_prefetch(a.K1 + off, kBytes);  // epilogue formation
     }
-
     // ---- load: own node (coalesced: consecutive threads, consecutive nodes),
     // formed with the cell's member row (stepper.cpp:60-72) ------------------
     Prim<DIM> own;
@@ -485,20 +487,18 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     if (cell >= 0) {
       const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
       double u[V];
+      // U_i: from the previous stage's epilogue, or formed here from the first
+      // column (cells that were inactive at i-1, whose a_{i,i-1} = 0)
+      if (!a.form) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
-      if (a.form) {
-        const double a1 = s_ca1[cs], ap = s_cap[cs];
-        double k1[V];
+        for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
+      } else if (s_cform[cs]) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) k1[v] = __ldg(a.K1 + gi + v);
-        if (ap != 0.0) {
+        for (int v = 0; v < V; ++v) u[v] = __ldg(a.Us + gi + v);
+      } else {
+        const double a1 = s_ca1[cs];
 #pragma unroll
-          for (int v = 0; v < V; ++v) u[v] = u[v] + fma(a1, k1[v], ap * __ldg(a.Kp + gi + v));
-        } else {
-#pragma unroll
-          for (int v = 0; v < V; ++v) u[v] = fma(a1, k1[v], u[v]);
-        }
+        for (int v = 0; v < V; ++v) u[v] = fma(a1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
       }
       own = prim_of<DIM>(ph, u);
       if (!prim_ok<DIM>(own)) report_bad(st, a.stage, a.ncells, cell + a.cell_offset);
@@ -536,20 +536,16 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       const int node =
           line_base<DIM>(d, pt % N1, pt / N1) + (side ? 0 : N1 - 1) * line_stride(d);
       const size_t gi = (static_cast<size_t>(nbc) * NPC + node) * V;
+      if (!a.form) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) nbu[k][v] = __ldg(a.U + gi + v);
-      if (a.form) {
-        const double b1 = s_na1[c2][f], bp = s_nap[c2][f];
-        double k1[V];
+        for (int v = 0; v < V; ++v) nbu[k][v] = __ldg(a.U + gi + v);
+      } else if (s_nform[c2][f]) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) k1[v] = __ldg(a.K1 + gi + v);
-        if (bp != 0.0) {
+        for (int v = 0; v < V; ++v) nbu[k][v] = __ldg(a.Us + gi + v);
+      } else {
+        const double b1 = s_na1[c2][f];
 #pragma unroll
-          for (int v = 0; v < V; ++v) nbu[k][v] = nbu[k][v] + fma(b1, k1[v], bp * __ldg(a.Kp + gi + v));
-        } else {
-#pragma unroll
-          for (int v = 0; v < V; ++v) nbu[k][v] = fma(b1, k1[v], nbu[k][v]);
-        }
+        for (int v = 0; v < V; ++v) nbu[k][v] = fma(b1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
       }
     }
     if constexpr (VISC) {  // BR1 viscous fluxes from grad_kernel (2D)
@@ -692,6 +688,20 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       if (a.write_k)
 #pragma unroll
         for (int v = 0; v < V; ++v) a.Kout[gi + v] = K[v];
+      if (a.write_next) {
+        // U_{i+1} = U + dt (a_{i+1,1} K1 + a_{i+1,i} K_i) with the cell's row
+        // (stepper.cpp:60-72, one stage ahead); at stage 0, K1 = K_0 = K
+        const int lev = s_lev[cs];
+        const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
+        if (!a.form) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) a.Usn[gi + v] = fma(an, K[v], __ldg(a.U + gi + v));
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            a.Usn[gi + v] = __ldg(a.U + gi + v) + fma(an, __ldg(a.K1 + gi + v), pn * K[v]);
+        }
+      }
       if (a.d_mode) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -753,18 +763,17 @@ __global__ void __launch_bounds__(256)
     const int node = line_base<DIM>(D, pt % N1, pt / N1) + (side ? N1 - 1 : 0) * line_stride(D);
     const size_t gi = (static_cast<size_t>(cell) * NPC + node) * V;
     double u[V];
+    const int lev = m.level[cell];
+    if (!a.form) {
 #pragma unroll
-    for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
-    if (a.form) {
-      const int lev = m.level[cell];
-      const double b1 = dt * a.a1[lev], bp = dt * a.ap[lev];
-      if (bp != 0.0) {
+      for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
+    } else if (a.formed[lev]) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) u[v] = u[v] + fma(b1, __ldg(a.K1 + gi + v), bp * __ldg(a.Kp + gi + v));
-      } else {
+      for (int v = 0; v < V; ++v) u[v] = __ldg(a.Us + gi + v);
+    } else {
+      const double b1 = dt * a.a1[lev];
 #pragma unroll
-        for (int v = 0; v < V; ++v) u[v] = fma(b1, __ldg(a.K1 + gi + v), u[v]);
-      }
+      for (int v = 0; v < V; ++v) u[v] = fma(b1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
     }
     double* o = (side ? send_hi : send_lo) + (static_cast<size_t>(fc) * FP + pt) * V;
 #pragma unroll

@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(128)
   __shared__ double su[CPB * NPC * V];      // formed stage state
   __shared__ double sn[CPB * NFP * V];      // neighbour traces [cell][face][pt][V]
   __shared__ int s_cell[CPB], s_coord[CPB][2], s_nbc[CPB][4];
-  __shared__ double s_ca1[CPB], s_cap[CPB], s_na1[CPB][4], s_nap[CPB][4];
+  __shared__ double s_ca1[CPB], s_na1[CPB][4];
+  __shared__ signed char s_cform[CPB], s_nform[CPB][4];
   if (st->aborted || st->finished) return;
   const int tid = threadIdx.x;
   const int cs = tid / NPC, l = tid % NPC;
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(128)
       s_coord[tid][1] = co[1];
       const int lev = m.level[cc];
       s_ca1[tid] = dt * a.a1[lev];
-      s_cap[tid] = dt * a.ap[lev];
+      s_cform[tid] = a.formed[lev];
       for (int f = 0; f < 4; ++f) {
         const int d = f >> 1, side = f & 1;
         int c2[2] = {co[0], co[1]};
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(128)
         const int l2 = m.level[nbc];
         s_nbc[tid][f] = nbc;
         s_na1[tid][f] = dt * a.a1[l2];
-        s_nap[tid][f] = dt * a.ap[l2];
+        s_nform[tid][f] = a.formed[l2];
       }
     }
     __syncthreads();
@@ -86,12 +87,10 @@ __global__ void __launch_bounds__(128)
       const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        double u = __ldg(a.U + gi + v);
-        if (a.form) {
-          const double k1 = __ldg(a.K1 + gi + v);
-          u = s_cap[cs] != 0.0 ? u + fma(s_ca1[cs], k1, s_cap[cs] * __ldg(a.Kp + gi + v))
-                               : fma(s_ca1[cs], k1, u);
-        }
+        double u;
+        if (!a.form) u = __ldg(a.U + gi + v);
+        else if (s_cform[cs]) u = __ldg(a.Us + gi + v);
+        else u = fma(s_ca1[cs], __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
         su[tid * V + v] = u;
       }
     }
@@ -104,12 +103,10 @@ __global__ void __launch_bounds__(128)
       const size_t gi = (static_cast<size_t>(nbc) * NPC + node) * V;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        double u = __ldg(a.U + gi + v);
-        if (a.form) {
-          const double k1 = __ldg(a.K1 + gi + v);
-          u = s_nap[c2][f] != 0.0 ? u + fma(s_na1[c2][f], k1, s_nap[c2][f] * __ldg(a.Kp + gi + v))
-                                  : fma(s_na1[c2][f], k1, u);
-        }
+        double u;
+        if (!a.form) u = __ldg(a.U + gi + v);
+        else if (s_nform[c2][f]) u = __ldg(a.Us + gi + v);
+        else u = fma(s_na1[c2][f], __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
         sn[q * V + v] = u;
       }
     }

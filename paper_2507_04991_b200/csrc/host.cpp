@@ -244,7 +244,6 @@ struct StagePlan {
   int gn = 0;
   double bytes = 0.0;    // compulsory HBM bytes of the launch (roofline)
   StageArgs args{};
-  int kin = -1, kout = -1;  // buffer ids: 0 K1, 1 Ka, 2 Kb
 };
 
 }  // namespace
@@ -291,7 +290,8 @@ struct perrk_ctx {
   int physics = 0, surface = 2, volume_mode = 1, volume_flux = 5;
   double mu = 0.0, prandtl = 1.0;
   // device buffers
-  double *U = nullptr, *K1 = nullptr, *Ka = nullptr, *Kb = nullptr, *d = nullptr;
+  double *U = nullptr, *K1 = nullptr, *d = nullptr;
+  double *Ka = nullptr, *Kb = nullptr;  // formed stage states U_i, ping-pong by stage parity
   double *tU = nullptr, *tK = nullptr;  // scratch for host-buffer queries
   double* G = nullptr;                   // BR1 viscous fluxes [2][ndofs] (NSF only)
   double *dh[3] = {}, *djac[3] = {}, *dlift[3] = {};
@@ -353,7 +353,7 @@ struct perrk_ctx {
   }
   size_t ndofs_() const { return static_cast<size_t>(ndofs); }
   size_t trace_doubles() const { return static_cast<size_t>(layer_cells) * (dim == 3 ? 16 : 4) * V; }
-  double* kbuf(int id) { return id == 0 ? K1 : (id == 1 ? Ka : Kb); }
+  double* sbuf(int parity) { return parity ? Kb : Ka; }  // formed stage states (ping-pong)
 };
 
 namespace perrk {
@@ -453,22 +453,30 @@ void build_plan(perrk_ctx* c) {
         CK(cudaMemcpy(p.glist, gl.data(), sizeof(int) * gl.size(), cudaMemcpyHostToDevice));
       }
     }
-    for (int lvl = 0; lvl <= dev::MAXR; ++lvl) a.a1[lvl] = a.ap[lvl] = 0.0;
+    // stage-state data flow ("K4 folded into the loads"): the
+    // epilogue of stage i writes U_{i+1} = U + dt (a_{i+1,1} K1 + a_{i+1,i} K_i)
+    // for its cells, so stage i+1 reads one formed array for every cell that
+    // was active at i; cells that were not are formed from the first column
+    // (their a_{i+1,i} is zero: chain rows follow active stages,
+    // butcher.cpp:67-77).  Only K1 is ever stored.
+    for (int lvl = 0; lvl <= dev::MAXR; ++lvl) {
+      a.a1[lvl] = a.a1n[lvl] = a.apn[lvl] = 0.0;
+      a.formed[lvl] = 0;
+    }
     for (int lvl = 1; lvl <= R; ++lvl) {
       const double* Am = &c->A[static_cast<size_t>(R - lvl) * S * S];
       a.a1[lvl] = i > 0 ? Am[i * S] : 0.0;
-      a.ap[lvl] = i >= 2 ? Am[i * S + i - 1] : 0.0;
+      a.formed[lvl] = i == 0 || active[lvl - 1][i - 1] ? 1 : 0;
+      if (i >= 1 && !a.formed[lvl])
+        REQUIRE(Am[i * S + i - 1] == 0.0, "chain coefficient on a stage following an inactive one");
+      if (i + 1 < S) {
+        a.a1n[lvl] = Am[(i + 1) * S];
+        a.apn[lvl] = i >= 1 ? Am[(i + 1) * S + i] : 0.0;
+      }
     }
     a.form = i > 0 ? 1 : 0;
-    a.kp_used = 0;
-    for (int lvl = 1; lvl <= R; ++lvl) a.kp_used |= a.ap[lvl] != 0.0 ? 1 : 0;
-    bool needed_next = false;
-    if (i + 1 < S)
-      for (int r = 0; r < R; ++r)
-        if (c->A[static_cast<size_t>(r) * S * S + (i + 1) * S + i] != 0.0) needed_next = true;
-    a.write_k = (i == 0) || needed_next;
-    p.kout = i == 0 ? 0 : (i % 2 == 1 ? 1 : 2);
-    p.kin = i >= 2 ? (i % 2 == 1 ? 2 : 1) : -1;
+    a.write_next = i + 1 < S ? 1 : 0;
+    a.write_k = i == 0 ? 1 : 0;  // K1
     a.b = c->b[i];
     a.d_mode = c->b[i] != 0.0 ? (i == first_b ? 1 : 2) : 0;
     a.want_dh = c->b[i] != 0.0;
@@ -479,16 +487,17 @@ void build_plan(perrk_ctx* c) {
     a.cell_offset = static_cast<long long>(c->layer0) * c->layer_cells;
     a.list = p.dlist;
     a.n = p.n;
-    // compulsory traffic per active cell, in node-vectors of 8V bytes:
-    // read U (+K1 when the state is formed, +K_{i-1} on chain rows),
-    // write K_i, and d (write at the first b-stage, read-modify-write after)
+    // compulsory traffic per active cell, in node-vectors of 8V bytes: the
+    // stage state (U_i, or U and K1 where formed from the first column),
+    // K1 written at stage 0, U_{i+1} written (its formation reads U and K1),
+    // and d (write at the first b-stage, read-modify-write after)
     double vecs = 0.0;
     for (long long cell = 0; cell < c->ncells; ++cell) {
       const int lv = c->eff[cell];
       if (!(i == 0 || active[lv - 1][i])) continue;
-      double v = 1.0;
-      if (a.form) v += 1.0 + (a.ap[lv] != 0.0 ? 1.0 : 0.0);
+      double v = (a.form && !a.formed[lv]) ? 2.0 : 1.0;
       if (a.write_k) v += 1.0;
+      if (a.write_next) v += 1.0 + (a.form && a.formed[lv] ? 2.0 : 0.0);
       v += a.d_mode == 1 ? 1.0 : (a.d_mode == 2 ? 2.0 : 0.0);
       vecs += v;
     }
@@ -512,8 +521,9 @@ void enqueue_stage(perrk_ctx* c, int i, bool want_h) {
   StageArgs a = p.args;
   a.U = c->U;
   a.K1 = c->K1;
-  a.Kp = p.kin >= 0 ? c->kbuf(p.kin) : c->K1;
-  a.Kout = c->kbuf(p.kout);
+  a.Us = i > 0 ? c->sbuf(i & 1) : nullptr;
+  a.Usn = c->sbuf((i + 1) & 1);
+  a.Kout = c->K1;
   a.d = c->d;
   a.want_h = (i == 0 && want_h) ? 1 : 0;
   a.ndofs = c->ndofs;
@@ -549,7 +559,7 @@ void enqueue_pack(perrk_ctx* c, int i) {
   StageArgs a = c->plan[i].args;
   a.U = c->U;
   a.K1 = c->K1;
-  a.Kp = c->plan[i].kin >= 0 ? c->kbuf(c->plan[i].kin) : c->K1;
+  a.Us = i > 0 ? c->sbuf(i & 1) : nullptr;
   CK(launch_pack_traces(c->dim, a, c->mesh(), c->st, c->send_lo, c->send_hi, c->stream));
   c->launches += 1;
 }
@@ -1059,7 +1069,7 @@ int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const
       put_state(c, s);
       StageArgs a{};
       a.U = c->tU;
-      a.K1 = a.Kp = c->tU;
+      a.K1 = c->tU;
       a.Kout = c->tK;
       a.list = mask ? c->dlist_tmp : nullptr;
       a.n = static_cast<int>(list.size());
@@ -1106,7 +1116,7 @@ int perrk_br1_gradients(perrk_ctx* c, double t, const double* U, double* grads) 
     StepState s = fresh_state();
     put_state(c, s);
     StageArgs a{};
-    a.U = a.K1 = a.Kp = c->tU;
+    a.U = a.K1 = c->tU;
     a.n = static_cast<int>(c->ncells);
     CK(launch_grad(a, c->mesh(), c->ph, c->st, c->G, c->ndofs, 1, c->grid_stage, c->stream));
     CK(cudaMemcpyAsync(grads, c->G, sizeof(double) * 2 * c->ndofs, cudaMemcpyDeviceToHost,
