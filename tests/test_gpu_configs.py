@@ -1,0 +1,115 @@
+"""GPU: BASELINE configurations C2-C5 at their full sizes.
+
+Parity against the oracle where a CPU run finishes in seconds to a minute
+(a few steps at full size), and size-independent properties over the full
+step counts:
+  * the quadrature totals of every conserved variable stay constant
+    (conservative scheme on a periodic domain; the relaxed update
+    U + gamma dt d keeps linear invariants, PAPER.md 1104);
+  * the total entropy never increases (entropy-conservative volume flux with
+    dissipative surface fluxes plus relaxation: H_{n+1} = H_n + gamma dH_n,
+    dH_n <= 0);
+  * no positivity abort and no relaxation fallback; gamma stays near 1.
+Tolerances: states 1e-11 relative L2 per variable after the stated steps,
+gamma 1e-12 (same relaxation numerics), invariants 1e-12 relative to
+their scale."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import rel_err
+from paper_2507_04991_b200 import perrk as P
+from paper_2507_04991_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+THREADS = os.cpu_count() or 1
+
+
+def _setup(name):
+    cfg = W.make_config(name)
+    semi = P.Semidiscretization(cfg.spec())
+    coords = (semi.node_x(), semi.node_y(), semi.node_z() if cfg.dim == 3 else None)
+    U0 = W.initial_state_for(cfg, coords)
+    return cfg, semi, U0
+
+
+def _orc(cfg):
+    kw = dict(surface_flux=cfg.surface_flux, threads=THREADS)
+    if cfg.physics == "nsf":
+        kw.update(viscous=True, mu=cfg.mu, prandtl=cfg.prandtl)
+    return O.Orc(cfg.mesh, **kw)
+
+
+def _gpu_run(cfg, semi, U0, steps):
+    semi.upload(U0)
+    rc = P.IntegratorConfig(tf=1e30, time=P.TimeControl(False, 0.0, P.CflRamp(cfg.cfl, cfg.cfl)),
+                            relaxation=cfg.relaxation)
+    t, taken, aborted, recs = P.advance(semi, cfg.family, cfg.partition_map(), rc, 0.0, steps)
+    assert taken == steps and not aborted
+    return semi.download(), recs
+
+
+def _parity(name, steps):
+    cfg, semi, U0 = _setup(name)
+    Ug, recs = _gpu_run(cfg, semi, U0, steps)
+    Uo = U0.copy()
+    _, taken, log, _ = _orc(cfg).run_steps(Uo, 0.0, steps, cfg.family,
+                                           cfg.partition_map().effective_level, cfg.relaxation,
+                                           False, cfg.cfl)
+    assert taken == steps
+    assert rel_err(Ug, Uo, semi.num_vars()) < 1e-11
+    assert np.abs(np.array([r.gamma for r in recs]) - log[:, 2]).max() < 1e-12
+    assert np.abs(np.array([r.t for r in recs]) - log[:, 0]).max() < 1e-12 * max(1.0, log[-1, 0])
+
+
+def _properties(name, steps=None):
+    cfg, semi, U0 = _setup(name)
+    steps = steps or cfg.steps
+    inv0 = semi.integral_per_variable(U0)
+    H0 = semi.total_entropy(U0)
+    _, recs = _gpu_run(cfg, semi, U0, steps)
+    inv = np.array([r.invariants[: semi.num_vars()] for r in recs])
+    scale = np.maximum(np.abs(inv0), 1e-300)
+    # momenta of symmetric states sit at ~0: measure against the energy scale
+    ref = np.maximum(scale, 1e-12 * np.abs(inv0).max())
+    assert np.all(np.abs(inv - inv0) <= 1e-12 * np.maximum(ref, np.abs(inv0).max() * 1e-3))
+    H = np.array([H0] + [r.entropy for r in recs])
+    assert np.all(np.diff(H) <= 1e-12 * max(1.0, np.abs(H).max()))
+    g = np.array([r.gamma for r in recs])
+    assert not any(r.fell_back for r in recs)
+    assert np.abs(g - 1.0).max() < 1e-2
+    return recs
+
+
+def test_c2_parity_20_steps():
+    _parity("c2", 20)
+
+
+def test_c2_full_500_steps_properties():
+    _properties("c2")
+
+
+def test_c3_parity_3_steps_full_size():
+    _parity("c3", 3)
+
+
+def test_c3_full_200_steps_properties():
+    _properties("c3")
+
+
+def test_c4_parity_1_step_full_size():
+    _parity("c4", 1)
+
+
+def test_c4_full_200_steps_properties():
+    _properties("c4")
+
+
+def test_c5_parity_1_step_full_size():
+    _parity("c5", 1)
+
+
+def test_c5_full_100_steps_properties():
+    _properties("c5")
