@@ -51,6 +51,22 @@ def _gpu_run(cfg, semi, U0, steps):
     return semi.download(), recs
 
 
+def state_err(Ug, Uo, U0, V):
+    """Per conserved variable ||Ug_v - Uo_v|| / ||Uo_v||, with the momentum
+    components measured against the norm of the momentum field: a
+    per-component ratio is not rotation invariant, and a component that is
+    small by symmetry (the TGV's z-momentum, ~1e-4 of the others after a
+    step) would be judged against its own size instead of the flux terms
+    (pressure scale) it is resolved from."""
+    a, b = Ug.reshape(-1, V), Uo.reshape(-1, V)
+    mom = np.linalg.norm(b[:, 1:V - 1])
+    errs = []
+    for v in range(V):
+        den = mom if 0 < v < V - 1 else np.linalg.norm(b[:, v])
+        errs.append(np.linalg.norm(a[:, v] - b[:, v]) / den)
+    return max(errs), errs
+
+
 def _parity(name, steps):
     cfg, semi, U0 = _setup(name)
     Ug, recs = _gpu_run(cfg, semi, U0, steps)
@@ -59,7 +75,10 @@ def _parity(name, steps):
                                            cfg.partition_map().effective_level, cfg.relaxation,
                                            False, cfg.cfl)
     assert taken == steps
-    assert rel_err(Ug, Uo, semi.num_vars()) < 1e-11
+    worst, errs = state_err(Ug, Uo, U0, semi.num_vars())
+    V = semi.num_vars()
+    norms = [np.linalg.norm(Uo.reshape(-1, V)[:, v]) for v in range(V)]
+    assert worst < 1e-11, (errs, norms)
     assert np.abs(np.array([r.gamma for r in recs]) - log[:, 2]).max() < 1e-12
     assert np.abs(np.array([r.t for r in recs]) - log[:, 0]).max() < 1e-12 * max(1.0, log[-1, 0])
 
