@@ -313,11 +313,13 @@ __device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, i
   if constexpr (kInWarp) {
     const int kn = (j + 1) & (N1 - 1), kp = (j + N1 - 1) & (N1 - 1), k2 = (j + 2) & (N1 - 1);
     double f1[V], f2[V], fp[V];
+    // both pair fluxes first (independent chains the scheduler can overlap),
+    // then the exchange
     ec_with(kn, f1);
+    ec_with(k2, f2);
     const int src = (threadIdx.x & 31) + (kp - j) * stride;
 #pragma unroll
     for (int v = 0; v < V; ++v) fp[v] = __shfl_sync(0xffffffffu, f1[v], src);
-    ec_with(k2, f2);
     const double cn = J2 * c_D[j * N1 + kn], cp = J2 * c_D[j * N1 + kp], c2 = J2 * c_D[j * N1 + k2];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -332,9 +334,9 @@ __device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, i
     const int kn = (j + 1) & (N1 - 1), k2 = (j + 2) & (N1 - 1);
     double f1[V], f2[V];
     ec_with(kn, f1);
+    ec_with(k2, f2);
 #pragma unroll
     for (int v = 0; v < V; ++v) zf[tid * V + v] = f1[v];
-    ec_with(k2, f2);
     const double cn = J2 * c_D[j * N1 + kn], c2 = J2 * c_D[j * N1 + k2];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
