@@ -240,6 +240,10 @@ void build_member(int kind, int S, int E, const double* fr, const std::vector<do
 struct StagePlan {
   int* dlist = nullptr;  // nullptr: all cells
   int n = 0;
+  // slab decomposition: the stage's cells off the slab boundary (computed
+  // while the halo is in flight) and on it (after the halo arrives)
+  int *ilist = nullptr, *blist = nullptr;
+  int in = 0, bn = 0;
   int* glist = nullptr;  // BR1: active cells and their face neighbours (nullptr: all)
   int gn = 0;
   double bytes = 0.0;    // compulsory HBM bytes of the launch (roofline)
@@ -263,6 +267,10 @@ struct Exchange {
   virtual ~Exchange() = default;
   // send_lo / send_hi of every rank -> ghost_hi of the rank below / ghost_lo above
   virtual void halo(std::vector<perrk_ctx*>& g) = 0;
+  // the same, overlapped: started after the packing on the compute stream,
+  // waited for before the boundary cells' stage launch
+  virtual void halo_begin(std::vector<perrk_ctx*>& g) { halo(g); }
+  virtual void halo_end(std::vector<perrk_ctx*>&) {}
   // StepState::red_local of every rank -> red_all[rank][NRED] on every rank
   virtual void gather(std::vector<perrk_ctx*>& g) = 0;
 };
@@ -410,10 +418,9 @@ std::vector<int> with_neighbours_2d(const perrk_ctx* c, const std::vector<char>&
 }
 
 void build_plan(perrk_ctx* c) {
-  for (auto& p : c->plan) {
-    if (p.dlist) cudaFree(p.dlist);
-    if (p.glist) cudaFree(p.glist);
-  }
+  for (auto& p : c->plan)
+    for (int* q : {p.dlist, p.glist, p.ilist, p.blist})
+      if (q) cudaFree(q);
   c->plan.clear();
   const int S = c->S, R = c->R;
   std::vector<std::vector<char>> active(R);  // by level-1
@@ -442,6 +449,24 @@ void build_plan(perrk_ctx* c) {
     if (!all && p.n > 0) {
       CK(cudaMalloc(&p.dlist, sizeof(int) * list.size()));
       CK(cudaMemcpy(p.dlist, list.data(), sizeof(int) * list.size(), cudaMemcpyHostToDevice));
+    }
+    if (c->slab) {  // interior / boundary split of the stage's cells
+      const int nloc = c->nc[c->dim - 1];
+      std::vector<int> il, bl;
+      for (int q : list) {
+        const long long layer = q / c->layer_cells;
+        (layer == 0 || layer == nloc - 1 ? bl : il).push_back(q);
+      }
+      p.in = static_cast<int>(il.size());
+      p.bn = static_cast<int>(bl.size());
+      if (p.in > 0) {
+        CK(cudaMalloc(&p.ilist, sizeof(int) * il.size()));
+        CK(cudaMemcpy(p.ilist, il.data(), sizeof(int) * il.size(), cudaMemcpyHostToDevice));
+      }
+      if (p.bn > 0) {
+        CK(cudaMalloc(&p.blist, sizeof(int) * bl.size()));
+        CK(cudaMemcpy(p.blist, bl.data(), sizeof(int) * bl.size(), cudaMemcpyHostToDevice));
+      }
     }
     if (c->physics == 1) {  // BR1: gradients on the active cells and their neighbours
       std::vector<char> on(c->ncells, 0);
@@ -515,10 +540,19 @@ struct StepMode {
   double* records_of(perrk_ctx* c) const { return records ? c->records : nullptr; }
 };
 
-// Enqueue the stage launches of stage i of one context.
-void enqueue_stage(perrk_ctx* c, int i, bool want_h) {
+// Enqueue the stage launch of stage i of one context; part 0: all the
+// stage's cells, 1: those off the slab boundary, 2: those on it.
+void enqueue_stage(perrk_ctx* c, int i, bool want_h, int part = 0) {
   StagePlan& p = c->plan[i];
   StageArgs a = p.args;
+  if (part == 1) {
+    a.list = p.ilist;
+    a.n = p.in;
+  } else if (part == 2) {
+    a.list = p.blist;
+    a.n = p.bn;
+  }
+  if (a.n == 0) return;
   a.U = c->U;
   a.K1 = c->K1;
   a.Us = i > 0 ? c->sbuf(i & 1) : nullptr;
@@ -546,7 +580,7 @@ void enqueue_stage(perrk_ctx* c, int i, bool want_h) {
     }
     e0 = c->ev_pool[c->ev_used++];
     e1 = c->ev_pool[c->ev_used++];
-    c->ev_bytes.push_back(p.bytes);
+    c->ev_bytes.push_back(p.n > 0 ? p.bytes * a.n / p.n : 0.0);
     CK(cudaEventRecord(e0, c->stream));
   }
   CK(launch_stage(c->dim, c->surface, a, c->mesh(), c->ph, c->st, c->partials, c->counter,
@@ -592,10 +626,17 @@ void enqueue_step(Group& g, const StepMode& mode, bool want_h) {
   const int S = g.members[0]->S;
   for (int i = 0; i < S; ++i) {
     if (slab) {
+      // boundary traces out, interior cells while they travel, boundary
+      // cells once they are in (north_star item 5: halo overlapped with the
+      // interior volume work)
       for (perrk_ctx* c : g.members) enqueue_pack(c, i);
-      g.ex->halo(g.members);
+      g.ex->halo_begin(g.members);
+      for (perrk_ctx* c : g.members) enqueue_stage(c, i, want_h, 1);
+      g.ex->halo_end(g.members);
+      for (perrk_ctx* c : g.members) enqueue_stage(c, i, want_h, 2);
+    } else {
+      for (perrk_ctx* c : g.members) enqueue_stage(c, i, want_h);
     }
-    for (perrk_ctx* c : g.members) enqueue_stage(c, i, want_h);
   }
   if (slab) reduce_point(g, RED_STAGES, true);
   if (mode.relax) {
@@ -683,21 +724,42 @@ void nccl_check(ncclResult_t r, const char* what) {
 // all on the context's stream.
 struct NcclExchange : Exchange {
   ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t packed = nullptr, arrived = nullptr;
   ~NcclExchange() override {
     if (comm) ncclCommDestroy(comm);
+    if (packed) cudaEventDestroy(packed);
+    if (arrived) cudaEventDestroy(arrived);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
   }
-  void halo(std::vector<perrk_ctx*>& g) override {
-    perrk_ctx* c = g[0];
+  void setup() {
+    CK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&packed, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&arrived, cudaEventDisableTiming));
+  }
+  void sendrecv(perrk_ctx* c, cudaStream_t s) {
     const int up = (c->rank + 1) % c->nranks, dn = (c->rank - 1 + c->nranks) % c->nranks;
     const size_t n = c->trace_doubles();
-    // matched in order per peer, so nranks == 2 (up == dn) pairs correctly
     NK(ncclGroupStart());
-    NK(ncclSend(c->send_hi, n, ncclDouble, up, comm, c->stream));
-    NK(ncclRecv(c->ghost_lo, n, ncclDouble, dn, comm, c->stream));
-    NK(ncclSend(c->send_lo, n, ncclDouble, dn, comm, c->stream));
-    NK(ncclRecv(c->ghost_hi, n, ncclDouble, up, comm, c->stream));
+    NK(ncclSend(c->send_hi, n, ncclDouble, up, comm, s));
+    NK(ncclRecv(c->ghost_lo, n, ncclDouble, dn, comm, s));
+    NK(ncclSend(c->send_lo, n, ncclDouble, dn, comm, s));
+    NK(ncclRecv(c->ghost_hi, n, ncclDouble, up, comm, s));
     NK(ncclGroupEnd());
   }
+  void halo_begin(std::vector<perrk_ctx*>& g) override {
+    perrk_ctx* c = g[0];
+    CK(cudaEventRecord(packed, c->stream));
+    CK(cudaStreamWaitEvent(comm_stream, packed, 0));
+    sendrecv(c, comm_stream);
+    CK(cudaEventRecord(arrived, comm_stream));
+  }
+  void halo_end(std::vector<perrk_ctx*>& g) override {
+    CK(cudaStreamWaitEvent(g[0]->stream, arrived, 0));
+  }
+  // grouped send/recv, matched in order per peer, so nranks == 2 (up == dn)
+  // pairs correctly
+  void halo(std::vector<perrk_ctx*>& g) override { sendrecv(g[0], g[0]->stream); }
   void gather(std::vector<perrk_ctx*>& g) override {
     perrk_ctx* c = g[0];
     NK(ncclAllGather(red_local_ptr(c), c->red_all, dev::NRED, ncclDouble, comm, c->stream));
@@ -932,10 +994,9 @@ int perrk_destroy(perrk_ctx* c) {
   for (int a = 0; a < 3; ++a)
     for (double* p : {c->dh[a], c->djac[a], c->dlift[a]})
       if (p) cudaFree(p);
-  for (auto& p : c->plan) {
-    if (p.dlist) cudaFree(p.dlist);
-    if (p.glist) cudaFree(p.glist);
-  }
+  for (auto& p : c->plan)
+    for (int* q : {p.dlist, p.glist, p.ilist, p.blist})
+      if (q) cudaFree(q);
   if (c->st) cudaFree(c->st);
   if (c->counter) cudaFree(c->counter);
   if (c->dint) cudaFree(c->dint);
@@ -1525,6 +1586,7 @@ int perrk_comm_init(perrk_ctx* c, const void* nccl_id, int rank, int nranks, con
     if (nranks == 1) return;  // the whole periodic mesh: nothing to exchange
     make_slab(c, rank, nranks, cuts);
     auto ex = std::make_unique<NcclExchange>();
+    ex->setup();
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof id);
     set_device(c);
