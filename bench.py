@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-profile", action="store_true",
+                    help="no per-launch events in the timed region (steps replay as one CUDA "
+                         "graph); the roofline block is then omitted")
     return ap.parse_args()
 
 
@@ -245,7 +248,7 @@ def perrk_arm(args):
 
     clocks = Clocks(local)
     clocks.start()
-    semi.profile(True)
+    semi.profile(not args.no_profile)
     l0 = semi.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -308,25 +311,29 @@ def perrk_arm(args):
 
     # ---- roofline of the dominant kernel ------------------------------------
     hbm, hbm_kind = peaks()
-    achieved = (stage_bytes / stage_launches) / ((stage_ms / stage_launches) * 1e-3) / 1e9
+    if args.no_profile:
+        stage_launches = 0
+    achieved = ((stage_bytes / stage_launches) / ((stage_ms / stage_launches) * 1e-3) / 1e9
+                if stage_launches else None)
     traffic = traffic_fixture(args.config)
-    fp64_peak = P.fp64_peak(local)
-    dof_stage_per_launch = per_step / len([p for p in range(fam.S)])
-    flops = FLOPS_PER_DOF_STAGE[cfg.dim] * per_step * args.steps
-    fp64_achieved = flops / (stage_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic,
-                "kernel": "stage_kernel<3,2> (volume + surface + lift + stage formation)",
-                "peak_kind": f"{hbm_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                "stage_kernel_share": stage_ms / ms,
-                "launches": stage_launches, "ms_per_launch": stage_ms / stage_launches,
-                "algorithmic_bytes_per_launch": stage_bytes / stage_launches,
-                "fp64": {"achieved_gflops": fp64_achieved, "peak_gflops": fp64_peak,
-                         "frac": fp64_achieved / fp64_peak,
-                         "flops_per_dof_stage": FLOPS_PER_DOF_STAGE[cfg.dim],
-                         "logs_per_dof_stage_not_counted": LOGS_PER_DOF_STAGE[cfg.dim],
-                         "peak_kind": "measured DFMA loop (perrk_fp64_peak)"}}
-    del dof_stage_per_launch
+    roofline = None
+    if stage_launches:
+        fp64_peak = P.fp64_peak(local)
+        flops = FLOPS_PER_DOF_STAGE[cfg.dim] * per_step * args.steps
+        fp64_achieved = flops / (stage_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": traffic,
+                    "kernel": f"stage_kernel<{cfg.dim},{cfg.surface_flux}> (volume + surface + "
+                              "lift + stage formation)",
+                    "peak_kind": f"{hbm_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                    "stage_kernel_share": stage_ms / ms,
+                    "launches": stage_launches, "ms_per_launch": stage_ms / stage_launches,
+                    "algorithmic_bytes_per_launch": stage_bytes / stage_launches,
+                    "fp64": {"achieved_gflops": fp64_achieved, "peak_gflops": fp64_peak,
+                             "frac": fp64_achieved / fp64_peak,
+                             "flops_per_dof_stage": FLOPS_PER_DOF_STAGE[cfg.dim],
+                             "logs_per_dof_stage_not_counted": LOGS_PER_DOF_STAGE[cfg.dim],
+                             "peak_kind": "measured DFMA loop (perrk_fp64_peak)"}}
 
     # ---- CPU baseline (rank 0, N = 1) ----------------------------------------
     cpu = None

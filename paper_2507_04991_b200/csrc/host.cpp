@@ -330,6 +330,13 @@ struct perrk_ctx {
   double *ghost_lo = nullptr, *ghost_hi = nullptr, *send_lo = nullptr, *send_hi = nullptr;
   double* red_all = nullptr;  // [nranks][NRED]
   std::shared_ptr<perrk::Group> group;
+  // CUDA graph of one run() step (perrk_advance): launch latency matters for
+  // the small configurations (C1 is 4096 nodes, ~20 kernels per step)
+  bool use_graphs = true;
+  cudaGraphExec_t graph_exec = nullptr;
+  std::string graph_key;
+  int64_t graph_launches = 0;  // kernels per graph launch
+  uint64_t plan_version = 0;
   // instrumentation: launch counter and per-stage-launch event pairs
   bool own_stream = true;
   int64_t launches = 0;
@@ -1001,6 +1008,7 @@ int perrk_destroy(perrk_ctx* c) {
   if (c->counter) cudaFree(c->counter);
   if (c->dint) cudaFree(c->dint);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->group) {  // leave the group (the exchange dies with its last member)
     auto& mem = c->group->members;
     for (size_t i = 0; i < mem.size(); ++i)
@@ -1074,6 +1082,7 @@ int perrk_set_family(perrk_ctx* c, const perrk_family_desc* f, const int* eff) {
     CK(cudaMemcpy(c->dlevel, lv.data(), c->ncells, cudaMemcpyHostToDevice));
     build_plan(c);
     c->has_family = true;
+    c->plan_version += 1;
   });
 }
 
@@ -1372,7 +1381,41 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
       if (g.ex) reduce_point(g, RED_NUMAX, true);
     }
     const bool want_h = needs_h(mode.relax, cfg->relax, s.h_ref);
-    for (int k = 0; k < nsteps; ++k) enqueue_step(g, mode, want_h);
+    bool graphs = c->use_graphs && nsteps > 1;
+    for (perrk_ctx* m : g.members) graphs = graphs && !m->profiling;
+    if (graphs) {
+      // every step enqueues the same launches with the same arguments (the
+      // step-to-step state lives in the device StepState), so one captured
+      // step is replayed nsteps times
+      std::string key;
+      for (perrk_ctx* m : g.members) key += std::to_string(m->plan_version) + ":" +
+                                           std::to_string(reinterpret_cast<uintptr_t>(m->records)) + ";";
+      key += std::to_string(mode.relax) + std::to_string(mode.cfg.numerics) + ":" +
+             std::to_string(mode.cfg.max_iter) + std::to_string(mode.want_nu) +
+             std::to_string(mode.want_record) + std::to_string(want_h);
+      if (!c->graph_exec || c->graph_key != key) {
+        if (c->graph_exec) {
+          cudaGraphExecDestroy(c->graph_exec);
+          c->graph_exec = nullptr;
+        }
+        const int64_t l0 = c->launches;
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+        enqueue_step(g, mode, want_h);
+        CK(cudaStreamEndCapture(c->stream, &graph));
+        CK(cudaGraphInstantiate(&c->graph_exec, graph, 0));
+        cudaGraphDestroy(graph);
+        c->graph_key = key;
+        c->graph_launches = c->launches - l0;
+        c->launches = l0;
+      }
+      for (int k = 0; k < nsteps; ++k) {
+        CK(cudaGraphLaunch(c->graph_exec, c->stream));
+        c->launches += c->graph_launches;
+      }
+    } else {
+      for (int k = 0; k < nsteps; ++k) enqueue_step(g, mode, want_h);
+    }
     const StepState r = get_state(c);
     if (r.error == 1) throw Fail(PERRK_ENUMERIC, "non-finite update direction");
     if (r.error == 2) throw Fail(PERRK_EINVAL, "vanishing characteristic speed");
