@@ -101,7 +101,8 @@ __global__ void begin_step_kernel(StepState* st) {
   st->dh_hi = st->dh_lo = 0.0;
   st->dmax_bits = 0ull;
   st->d_nonfinite = 0;
-  st->gamma = st->seed_from_previous ? st->gamma_seed : 1.0;
+  st->gamma = st->method == 1 ? st->bracket_min
+                              : (st->seed_from_previous ? st->gamma_seed : 1.0);
   st->residual = 0.0;
   st->pending_step = st->prev_step = 0.0;
   st->iters = 0;
@@ -191,6 +192,88 @@ __device__ void relax_newton_update(StepState* st, dd A, dd B) {
   st->pass = it;
 }
 
+// Bisection (relax.cpp:105-127) and secant (relax.cpp:128-148) on the device:
+// each launch evaluates the residual at st->gamma; this single-thread step
+// consumes it and sets the next evaluation point, or finishes.
+__device__ double relax_residual(const StepState* st, dd A) {
+  const dd dh = {st->dh_hi, st->dh_lo};
+  const double gamma = st->gamma;
+  if (st->numerics == 1) {
+    dd rr = A;
+    if (!isnan(st->h_ref)) rr = dd_add(rr, dd_add(dd{st->h_hi, st->h_lo}, dd{-st->h_ref, 0.0}));
+    rr = dd_add(rr, dd_mul_d(dh, -gamma));
+    return rr.hi + rr.lo;
+  }
+  const double h_ref = isnan(st->h_ref) ? st->h_hi + st->h_lo : st->h_ref;
+  return (A.hi + A.lo) - h_ref - gamma * (dh.hi + dh.lo);
+}
+
+__device__ void relax_done_at(StepState* st, double g, int iters, double r) {
+  st->gamma = g;
+  st->iters = iters;
+  st->residual = r;
+  st->relax_done = 1;
+  if (!(g > 0.0)) relax_fallback(st, iters, r);
+}
+
+__device__ void relax_update(StepState* st, dd A, dd B) {
+  if (st->method == 0) return relax_newton_update(st, A, B);
+  const double r = relax_residual(st, A);
+  const int pass = st->pass;
+  st->pass = pass + 1;
+  if (st->method == 1) {  // bisection
+    if (pass == 0) {  // r(lo)
+      st->lo = st->bracket_min;
+      st->hi = st->bracket_max;
+      st->rlo = r;
+      st->gamma = st->hi;
+      return;
+    }
+    if (pass == 1) {  // r(hi): a sign change is required
+      if (signbit(st->rlo) == signbit(r)) return relax_fallback(st, 0, st->rlo);
+      st->gamma = 0.5 * (st->lo + st->hi);
+      return;
+    }
+    const int it = pass - 1;  // r(mid), iteration it
+    const double mid = st->gamma;
+    st->iters = it;
+    const bool conv = fabs(r) <= st->residual_tol || (st->hi - st->lo) <= st->step_tol;
+    if (conv) return relax_done_at(st, mid, it, r);
+    if (it >= st->max_iter) return relax_fallback(st, it, r);
+    if (signbit(r) == signbit(st->rlo)) {
+      st->lo = mid;
+      st->rlo = r;
+    } else {
+      st->hi = mid;
+    }
+    st->gamma = 0.5 * (st->lo + st->hi);
+    return;
+  }
+  // secant
+  if (pass == 0) {  // r(g0)
+    st->g0 = st->gamma;
+    st->r0 = r;
+    st->gamma = st->g0 - 1e-6;
+    return;
+  }
+  if (pass >= 2) {  // r(g1) of iteration pass-1: converged?
+    const int it = pass - 1;
+    if (fabs(r) <= st->residual_tol || fabs(st->gamma - st->g0) <= st->step_tol)
+      return relax_done_at(st, st->gamma, it, r);
+    if (it >= st->max_iter) return relax_fallback(st, st->max_iter, r);
+  }
+  // next secant point from (g0, r0), (g1, r1)
+  const int it = pass;  // iteration about to be taken
+  const double g1 = st->gamma, r1 = r;
+  if (r1 == st->r0) return relax_fallback(st, it, r1);
+  const double g2 = g1 - r1 * (g1 - st->g0) / (r1 - st->r0);
+  if (!isfinite(g2)) return relax_fallback(st, it, r1);
+  st->g0 = g1;
+  st->r0 = r1;
+  st->gamma = g2;
+  st->iters = it;
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(256)
     relax_pass_kernel(const double* __restrict__ U, const double* __restrict__ d, MeshDev m,
@@ -251,7 +334,7 @@ __global__ void __launch_bounds__(256)
       st->red_local[R_B_HI] = tot[1].hi;
       st->red_local[R_B_LO] = tot[1].lo;
     } else {
-      relax_newton_update(st, tot[0], tot[1]);
+      relax_update(st, tot[0], tot[1]);
     }
   }
 }
@@ -568,7 +651,7 @@ __global__ void combine_kernel(StepState* st, const double* all, int nranks, int
     st->aborted = bad != kNoBad ? 1 : st->aborted;
   } else if (mode == COMBINE_RELAX) {
     if (st->aborted || st->finished || st->relax_done) return;
-    relax_newton_update(st, sum(R_A_HI, R_A_LO), sum(R_B_HI, R_B_LO));
+    relax_update(st, sum(R_A_HI, R_A_LO), sum(R_B_HI, R_B_LO));
   } else if (mode == COMBINE_UPDATE) {
     if (st->aborted || st->finished) return;
     const double gamma = st->relax_enabled ? st->gamma : st->gamma_override;

@@ -647,7 +647,7 @@ void enqueue_step(Group& g, const StepMode& mode, bool want_h) {
   }
   if (slab) reduce_point(g, RED_STAGES, true);
   if (mode.relax) {
-    const int passes = mode.cfg.numerics == 1 ? mode.cfg.max_iter : mode.cfg.max_iter + 1;
+    const int passes = relax_passes(mode.cfg);
     for (int p = 0; p < passes; ++p) {
       for (perrk_ctx* c : g.members) {
         CK(launch_relax_pass(c->dim, c->U, c->d, c->mesh(), c->ph, c->st, c->partials,
@@ -666,9 +666,15 @@ void enqueue_step(Group& g, const StepMode& mode, bool want_h) {
   if (slab) reduce_point(g, RED_UPDATE, true, mode.want_record ? mode.records : nullptr);
 }
 
+// residual evaluations one step may need (each pass is one fused launch)
+int relax_passes(const perrk_relax_cfg& r) {
+  if (r.method == 0) return r.numerics == 1 ? r.max_iter : r.max_iter + 1;
+  return r.max_iter + 2;  // bisection: r(lo), r(hi) + max_iter; secant: r(g0), r(g1) + ...
+}
+
 void check_relax_cfg(const perrk_relax_cfg& r) {
-  if (r.method != 0)
-    throw Fail(PERRK_EUNSUP, "only Newton relaxation (method 0) runs on the device");
+  REQUIRE(r.method >= 0 && r.method <= 2, "relaxation method must be 0 newton, 1 bisection, 2 secant");
+  if (r.method == 1) REQUIRE(r.bracket_max > r.bracket_min, "empty bisection bracket");
   REQUIRE(r.max_iter >= 1, "relaxation max_iter must be >= 1");
   REQUIRE(r.numerics == 0 || r.numerics == 1, "relaxation numerics must be 0 or 1");
 }
@@ -681,6 +687,9 @@ void configure_relax(StepState& s, bool enabled, const perrk_relax_cfg& r) {
   s.seed_from_previous = r.seed_from_previous;
   s.residual_tol = r.residual_tol;
   s.step_tol = r.step_tol;
+  s.method = r.method;
+  s.bracket_min = r.bracket_min;
+  s.bracket_max = r.bracket_max;
 }
 
 // Cell-sized device buffers of a context (its slab when decomposed).
