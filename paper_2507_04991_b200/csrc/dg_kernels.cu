@@ -237,14 +237,17 @@ __device__ void relax_update(StepState* st, dd A, dd B) {
     const int it = pass - 1;  // r(mid), iteration it
     const double mid = st->gamma;
     st->iters = it;
-    const bool conv = fabs(r) <= st->residual_tol || (st->hi - st->lo) <= st->step_tol;
-    if (conv) return relax_done_at(st, mid, it, r);
-    if (it >= st->max_iter) return relax_fallback(st, it, r);
+    if (fabs(r) <= st->residual_tol || (st->hi - st->lo) <= st->step_tol)
+      return relax_done_at(st, mid, it, r);
     if (signbit(r) == signbit(st->rlo)) {
       st->lo = mid;
       st->rlo = r;
     } else {
       st->hi = mid;
+    }
+    if (it >= st->max_iter) {  // the reference re-tests with the halved bracket
+      if ((st->hi - st->lo) <= st->step_tol) return relax_done_at(st, mid, it, r);
+      return relax_fallback(st, it, r);
     }
     st->gamma = 0.5 * (st->lo + st->hi);
     return;

@@ -285,3 +285,44 @@ def test_cpp_adapter_drop_in_parity():
         pytest.skip("adapter_parity not built")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("method", ["bisection", "secant"])
+def test_bisection_secant_relaxation_vs_reference(method):
+    """relax.cpp:105-148 on the device: the same residual sequence as the
+    unmodified reference (reference numerics, C1 vortex; a bracket around 1)."""
+    cfg, semi, U0 = c1_setup()
+    ref = O.Ref(cfg.mesh)
+    dt = ref.compute_dt(U0, False, 0.9)
+    rx = P.RelaxationConfig(method=method, max_iter=30, bracket_min=0.9, bracket_max=1.1,
+                            residual_tol=1e-14, step_tol=1e-12)
+    Ug, Ur = U0.copy(), U0.copy()
+    tg = tr = 0.0
+    for _ in range(5):
+        tg, rg = P.perk_step(Ug, tg, dt, cfg.family, cfg.partition_map(), semi,
+                             P.PerkStepOptions(relaxation=rx))
+        tr, rr = ref.perk_step(Ur, tr, dt, cfg.family, cfg.partition_map().effective_level, rx)
+        assert rg.fell_back == bool(rr.fell_back)
+        assert rg.iterations == rr.iterations
+        assert abs(rg.gamma - rr.gamma) < 1e-12
+    assert rel_err(Ug, Ur, 4) < 1e-12
+
+
+@pytest.mark.parametrize("method", ["bisection", "secant"])
+def test_bisection_secant_accurate_vs_oracle(method):
+    mesh = mesh2d(10, 8, seed=91)
+    fam = P.build_perk4(14, [5, 8, 14], [[], [0.5] * 3, [0.7] * 9])
+    pm = _multilevel(mesh, fam.R, 9)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh))
+    orc = O.Orc(mesh)
+    U0 = smooth_state((semi.node_x(), semi.node_y()), 2, seed=23, amp=0.3)
+    dt = 0.3 * orc.compute_dt(U0, False, 1.0)
+    rx = P.RelaxationConfig(method=method, numerics="accurate", max_iter=40, bracket_min=0.95,
+                            bracket_max=1.05, residual_tol=1e-15, step_tol=1e-13)
+    Ug, Uo = U0.copy(), U0.copy()
+    for _ in range(3):
+        _, rg = P.perk_step(Ug, 0.0, dt, fam, pm, semi, P.PerkStepOptions(relaxation=rx))
+        _, ro = orc.perk_step(Uo, 0.0, dt, fam, pm.effective_level, rx)
+        assert rg.fell_back == bool(ro.fell_back)
+        assert abs(rg.gamma - ro.gamma) < 1e-12
+    assert rel_err(Ug, Uo, 4) < 1e-11
