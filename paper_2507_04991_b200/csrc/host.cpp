@@ -538,6 +538,12 @@ void build_plan(perrk_ctx* c) {
   }
 }
 
+// residual evaluations one step may need (each pass is one fused launch)
+int relax_passes(const perrk_relax_cfg& r) {
+  if (r.method == 0) return r.numerics == 1 ? r.max_iter : r.max_iter + 1;
+  return r.max_iter + 2;  // bisection: r(lo), r(hi) + max_iter; secant: r(g0), r(g1) + ...
+}
+
 struct StepMode {
   bool relax = false;
   perrk_relax_cfg cfg{};
@@ -664,12 +670,6 @@ void enqueue_step(Group& g, const StepMode& mode, bool want_h) {
     c->launches += 1;
   }
   if (slab) reduce_point(g, RED_UPDATE, true, mode.want_record ? mode.records : nullptr);
-}
-
-// residual evaluations one step may need (each pass is one fused launch)
-int relax_passes(const perrk_relax_cfg& r) {
-  if (r.method == 0) return r.numerics == 1 ? r.max_iter : r.max_iter + 1;
-  return r.max_iter + 2;  // bisection: r(lo), r(hi) + max_iter; secant: r(g0), r(g1) + ...
 }
 
 void check_relax_cfg(const perrk_relax_cfg& r) {
