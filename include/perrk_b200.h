@@ -117,16 +117,19 @@ typedef struct {
 } perrk_step_result;
 
 /* Replaces IntegratorConfig/TimeControl/CflRamp for the loop of run()
- * (stepper.hpp:13-41).  The CFL ramp is constant (cfl0 == cfl_max). */
+ * (stepper.hpp:13-41).  CFL mode: dt = cfl(t - t0) / nu_max with the ramp
+ * cfl(s) = min(cfl_max, cfl0 + (cfl_max - cfl0) s / t_ramp) (stepper.cpp:13-15);
+ * dt_or_cfl is cfl_max, and cfl0 == cfl_max (or t_ramp <= 0) is constant. */
 typedef struct {
   int fixed_dt;              /* 1: dt fixed (truncated to tf), 0: CFL */
-  double dt_or_cfl;
+  double dt_or_cfl;          /* fixed dt, or cfl_max */
   double tf;                 /* stop when t >= tf - 1e-12 max(1,|tf|) */
   int relax_enabled;
   perrk_relax_cfg relax;
   int anchor_initial;        /* EntropyAnchor::initial: h_ref = H(U_0) */
   int idt;
   int records;               /* fill the per-step log */
+  double cfl0, t_ramp, t0;   /* CflRamp and IntegratorConfig::t0 */
 } perrk_run_cfg;
 
 /* One row of the step log; replaces StepRecord (stepper.hpp:43-52). */

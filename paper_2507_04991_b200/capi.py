@@ -53,7 +53,8 @@ class StepResult(C.Structure):
 class RunCfg(C.Structure):
     _fields_ = [("fixed_dt", C.c_int), ("dt_or_cfl", C.c_double), ("tf", C.c_double),
                 ("relax_enabled", C.c_int), ("relax", RelaxCfg), ("anchor_initial", C.c_int),
-                ("idt", C.c_int), ("records", C.c_int)]
+                ("idt", C.c_int), ("records", C.c_int), ("cfl0", C.c_double),
+                ("t_ramp", C.c_double), ("t0", C.c_double)]
 
 
 class StepRecord(C.Structure):

@@ -94,7 +94,12 @@ __global__ void begin_step_kernel(StepState* st) {
       st->finished = 1;
       return;
     }
-    dt = st->dt_or_cfl / numax;
+    // CflRamp::operator() (stepper.cpp:13-15) at t - t0
+    const double cfl = st->t_ramp > 0.0
+                           ? fmin(st->dt_or_cfl, st->cfl0 + (st->dt_or_cfl - st->cfl0) *
+                                                                (st->t - st->t0) / st->t_ramp)
+                           : st->dt_or_cfl;
+    dt = cfl / numax;
     st->numax_bits = 0ull;  // re-accumulated by this step's update kernel
   }
   st->dt = dt;

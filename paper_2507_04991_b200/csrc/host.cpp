@@ -1356,6 +1356,9 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
     s.t_eps = 1e-12 * std::fmax(1.0, std::fabs(cfg->tf));
     s.dt_mode = cfg->fixed_dt ? 1 : 2;
     s.dt_or_cfl = cfg->dt_or_cfl;
+    s.cfl0 = cfg->cfl0;
+    s.t_ramp = cfg->cfl0 == cfg->dt_or_cfl ? 0.0 : cfg->t_ramp;
+    s.t0 = cfg->t0;
     s.idt = cfg->idt;
     s.gamma_seed = 1.0;
     configure_relax(s, cfg->relax_enabled != 0, cfg->relax);

@@ -739,12 +739,17 @@ class IntegratorConfig:
     max_steps: int = 10_000_000
 
 
+def cfl_at(ramp: CflRamp, s):
+    """CflRamp::operator() (stepper.cpp:13-15)."""
+    if ramp.cfl0 == ramp.cfl_max:
+        return ramp.cfl_max
+    return min(ramp.cfl_max, ramp.cfl0 + (ramp.cfl_max - ramp.cfl0) * s / ramp.t_ramp)
+
+
 def compute_dt(U, semi, config: IntegratorConfig, t):
-    """stepper.cpp:116-127 (constant CFL ramp only on the device)."""
+    """stepper.cpp:116-127."""
     r = config.time.ramp
-    if not config.time.fixed and r.cfl0 != r.cfl_max:
-        raise Error(capi.PERRK_EUNSUP, "CFL ramps are not on the device path")
-    val = config.time.dt if config.time.fixed else r.cfl_max
+    val = config.time.dt if config.time.fixed else cfl_at(r, t - config.t0)
     out = C.c_double()
     check(lib().perrk_compute_dt(semi._h, _dp(semi._state(U)), int(config.time.fixed), float(val),
                                  float(t), float(config.tf), C.byref(out)))
@@ -775,9 +780,10 @@ class RunResult:
 
 def _run_cfg(config: IntegratorConfig, records=True):
     r = config.time.ramp
-    if not config.time.fixed and r.cfl0 != r.cfl_max:
-        raise Error(capi.PERRK_EUNSUP, "CFL ramps are not on the device path")
     rc = capi.RunCfg()
+    rc.cfl0 = r.cfl0
+    rc.t_ramp = r.t_ramp
+    rc.t0 = config.t0
     rc.fixed_dt = int(config.time.fixed)
     rc.dt_or_cfl = config.time.dt if config.time.fixed else r.cfl_max
     rc.tf = config.tf

@@ -326,3 +326,26 @@ def test_bisection_secant_accurate_vs_oracle(method):
         assert rg.fell_back == bool(ro.fell_back)
         assert abs(rg.gamma - ro.gamma) < 1e-12
     assert rel_err(Ug, Uo, 4) < 1e-11
+
+
+def test_cfl_ramp_on_device_matches_stepwise_compute_dt():
+    """CflRamp (stepper.cpp:13-15) evaluated in begin_step equals compute_dt
+    with the ramp evaluated on the host, step by step (gamma seed carried as
+    run() does, stepper.cpp:153,170)."""
+    cfg, semi, U0 = c1_setup()
+    ramp = P.CflRamp(0.3, 0.9, 0.5)
+    ic = P.IntegratorConfig(t0=0.1, tf=1e9, time=P.TimeControl(False, 0.0, ramp),
+                            relaxation=P.RelaxationConfig(numerics="accurate"))
+    semi.upload(U0)
+    t, taken, aborted, recs = P.advance(semi, cfg.family, cfg.partition_map(), ic, 0.1, 12)
+    assert taken == 12 and not aborted
+    Uh = U0.copy()
+    th, seed = 0.1, 1.0
+    for r in recs:
+        dt = P.compute_dt(Uh, semi, ic, th)
+        assert abs(dt - r.dt) <= 1e-13 * dt
+        th, res = P.perk_step(Uh, th, dt, cfg.family, cfg.partition_map(), semi,
+                              P.PerkStepOptions(relaxation=ic.relaxation, gamma_seed=seed))
+        seed = 1.0 if res.fell_back else res.gamma
+    dts = [r.dt for r in recs]
+    assert dts[-1] > 1.5 * dts[0]  # the ramp raises the step
