@@ -378,15 +378,23 @@ __global__ void __launch_bounds__(256)
       int ci, cj, ck;
       cell_coords(m, cell, ci, cj, ck);
       const int cc[3] = {ci, cj, ck};
+      // one pressure / sound speed per node (mesh.cpp:97-129 takes
+      // |v_dir| + c per direction; 1/h_dir = jac_dir / 2 exactly)
+      const double ir = frcp(u[0]);
+      double m2 = 0.0;
+#pragma unroll
+      for (int dir = 0; dir < DIM; ++dir) m2 = fma(u[1 + dir], u[1 + dir], m2);
+      const double p = ph.gm1 * (u[DIM + 1] - 0.5 * m2 * ir);
       if (want_nu) {
-        const double p = pressure<DIM>(ph, u);
+        const double c = sqrt(ph.gamma * p * ir);
 #pragma unroll
         for (int dir = 0; dir < DIM; ++dir)
-          numax = fmax(numax, max_wave_speed<DIM>(ph, u, p, dir) / m.h[dir][cc[dir]]);
+          numax = fmax(numax, (fabs(u[1 + dir]) * ir + c) * (0.5 * m.jac[dir][cc[dir]]));
       }
       if (want_record) {
         const double om = node_measure<DIM>(m, ci, cj, ck, l);
-        acc[0] = dd_add_prod(acc[0], om, entropy<DIM>(ph, u));
+        // s = -rho log(p / rho^gamma) (physics.cpp:130-132) as -rho (log p - gamma log rho)
+        acc[0] = dd_add_prod(acc[0], om, -u[0] * (log(p) - ph.gamma * log(u[0])));
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[1 + v] = dd_add_prod(acc[1 + v], om, u[v]);
       }
