@@ -546,7 +546,8 @@ __global__ void admissible_kernel(const double* __restrict__ U, Phys ph, int* fi
 template <int DIM, int SURF, bool VISC>
 static size_t stage_smem() {
   return sizeof(double) *
-         (StageGeo<DIM>::SM_TOTAL + StageGeo<DIM>::SM_ZF + (VISC ? StageGeo<DIM>::SM_VISC : 0));
+         (StageGeo<DIM>::SM_TOTAL + StageGeo<DIM>::SM_ZF + StageGeo<DIM>::SM_PF +
+          (VISC ? StageGeo<DIM>::SM_VISC : 0));
 }
 
 template <int DIM, int SURF, bool VISC>

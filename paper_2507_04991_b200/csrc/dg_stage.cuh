@@ -30,6 +30,8 @@
 // logmean (physics.cpp:30-38) is kept with the reference's threshold.
 #pragma once
 
+#include <type_traits>
+
 namespace perrk {
 namespace dev {
 
@@ -54,6 +56,7 @@ struct StageGeo {
   // BR1 (2D NSF): own viscous fluxes [2][T][V] and neighbour face values [CPB][NFP][V]
   static constexpr int SM_VISC = 2 * T * V + CPB * NFP * V;
   static constexpr int SM_ZF = DIM == 3 ? T * V : 0;  // published z-pair fluxes
+  static constexpr int SM_PF = DIM * CPB * FP * 2 * V;  // distance-2 pair fluxes
 };
 
 // primitive slots: rho, v[DIM], p, E, log rho, beta, log beta
@@ -309,40 +312,83 @@ __device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, i
              pr[S::P * T + qk], pr[S::LRHO * T + qk], pr[S::BETA * T + qk],
              pr[S::LBETA * T + qk], f);
   };
-  constexpr bool kInWarp = D < 2;
-  if constexpr (kInWarp) {
-    const int kn = (j + 1) & (N1 - 1), kp = (j + N1 - 1) & (N1 - 1), k2 = (j + 2) & (N1 - 1);
-    double f1[V], f2[V], fp[V];
-    // both pair fluxes first (independent chains the scheduler can overlap),
-    // then the exchange
-    ec_with(kn, f1);
-    ec_with(k2, f2);
+  // the distance-2 pair (j, j+2) is evaluated once per pair by dist2_pairs
+  // and gathered after the block's next barrier (dist2_gather)
+  const int kn = (j + 1) & (N1 - 1);
+  double f1[V];
+  ec_with(kn, f1);
+  const double cn = J2 * c_D[j * N1 + kn];
+#pragma unroll
+  for (int v = 0; v < V; ++v) K[v] = fma(-cn, f1[v], K[v]);
+  if constexpr (D < 2) {
+    const int kp = (j + N1 - 1) & (N1 - 1);
     const int src = (threadIdx.x & 31) + (kp - j) * stride;
+    const double cp = J2 * c_D[j * N1 + kp];
 #pragma unroll
-    for (int v = 0; v < V; ++v) fp[v] = __shfl_sync(0xffffffffu, f1[v], src);
-    const double cn = J2 * c_D[j * N1 + kn], cp = J2 * c_D[j * N1 + kp], c2 = J2 * c_D[j * N1 + k2];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      K[v] = fma(-cn, f1[v], K[v]);
-      K[v] = fma(-cp, fp[v], K[v]);
-      K[v] = fma(-c2, f2[v], K[v]);
-    }
+    for (int v = 0; v < V; ++v) K[v] = fma(-cp, __shfl_sync(0xffffffffu, f1[v], src), K[v]);
   } else {
     // z-lines cross warps: f(j, j+1) is published in shared memory and the
-    // partner's f(j-1, j) is picked up after the block's next barrier
-    // (zf_gather); the distance-2 pair is evaluated by both ends
-    const int kn = (j + 1) & (N1 - 1), k2 = (j + 2) & (N1 - 1);
-    double f1[V], f2[V];
-    ec_with(kn, f1);
-    ec_with(k2, f2);
+    // partner's f(j-1, j) is picked up after the block's next barrier (zf_gather)
 #pragma unroll
     for (int v = 0; v < V; ++v) zf[tid * V + v] = f1[v];
-    const double cn = J2 * c_D[j * N1 + kn], c2 = J2 * c_D[j * N1 + k2];
+  }
+}
+
+// Distance-2 pairs (0,2) and (1,3) of every LGL line, each evaluated once:
+// pair p = ((d * CPB + cell) * FP + line) * 2 + lower end; a warp's 32 pairs
+// share the direction, so the flux kernel is selected per warp.
+template <int DIM>
+__device__ __forceinline__ void dist2_pairs(const Phys& ph, const double* pr, double* pf, int tid) {
+  using G = StageGeo<DIM>;
+  using S = Slot<DIM>;
+  constexpr int V = G::V, T = G::T, FP = G::FP, CPB = G::CPB, NPC = G::NPC;
+  constexpr int NP = DIM * CPB * FP * 2;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      K[v] = fma(-cn, f1[v], K[v]);
-      K[v] = fma(-c2, f2[v], K[v]);
+  for (int r = 0; r < (NP + T - 1) / T; ++r) {
+    const int p = tid + r * T;
+    if (p >= NP) break;
+    const int d = p / (CPB * FP * 2), rem = p % (CPB * FP * 2);
+    const int c2 = rem / (FP * 2), li = (rem / 2) % FP, which = rem & 1;
+    const int lo = c2 * NPC + line_base<DIM>(d, li % N1, li / N1) + which * line_stride(d);
+    const int hi = lo + 2 * line_stride(d);
+    double vl[DIM], vr[DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      vl[i] = pr[(S::V0 + i) * T + lo];
+      vr[i] = pr[(S::V0 + i) * T + hi];
     }
+    double f[V];
+    auto run = [&](auto dc) {
+      constexpr int Dd = decltype(dc)::value;
+      ec2<DIM>(ph, Dd, pr[S::RHO * T + lo], vl, pr[S::P * T + lo], pr[S::LRHO * T + lo],
+               pr[S::BETA * T + lo], pr[S::LBETA * T + lo], pr[S::RHO * T + hi], vr,
+               pr[S::P * T + hi], pr[S::LRHO * T + hi], pr[S::BETA * T + hi],
+               pr[S::LBETA * T + hi], f);
+    };
+    if (d == 0)
+      run(std::integral_constant<int, 0>{});
+    else if (d == 1)
+      run(std::integral_constant<int, 1>{});
+    else
+      run(std::integral_constant<int, DIM - 1>{});
+#pragma unroll
+    for (int v = 0; v < V; ++v) pf[p * V + v] = f[v];
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ void dist2_gather(const double* pf, int cs, const int (&il)[3],
+                                             const double* J2, double* K) {
+  using G = StageGeo<DIM>;
+  constexpr int V = G::V, FP = G::FP, CPB = G::CPB;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    const int j = il[d], k2 = j ^ 2;
+    const int li = d == 0 ? il[1] + N1 * il[2] : (d == 1 ? il[0] + N1 * il[2] : il[0] + N1 * il[1]);
+    const int p = ((d * CPB + cs) * FP + li) * 2 + (j & 1);
+    const double c2 = J2[d] * c_D[j * N1 + k2];
+#pragma unroll
+    for (int v = 0; v < V; ++v) K[v] = fma(-c2, pf[p * V + v], K[v]);
   }
 }
 
@@ -370,7 +416,8 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   double* pr = smem;            // [NPR][T] per-node primitives
   double* sf = pr + G::SM_PR;   // [CPB][NFP][V] surface + diagonal terms per face point
   double* zf = sf + G::SM_NB;   // 3D: published z-pair fluxes [T][V]
-  double* vg = zf + G::SM_ZF;   // VISC: own G [2][T][V], then neighbour G_d [CPB][NFP][V]
+  double* pf = zf + G::SM_ZF;   // distance-2 pair fluxes [DIM*CPB*FP*2][V]
+  double* vg = pf + G::SM_PF;   // VISC: own G [2][T][V], then neighbour G_d [CPB][NFP][V]
   double* vn = vg + 2 * T * V;
   // group descriptors, double-buffered: the next group's are written while
   // the current one computes
@@ -622,10 +669,12 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     volume_terms<DIM, 1>(ph, pr, tid, il, s_J2[cs][1], own, lr, be, lb, K);
     if constexpr (DIM == 3)
       volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, lr, be, lb, K, zf);
+    dist2_pairs<DIM>(ph, pr, pf, tid);
     if (dt_t >= 0) describe(buf ^ 1, dt_t, nx_cell);  // the next group, off the critical path
     __syncthreads();  // surface terms of every face point visible
 
     if constexpr (DIM == 3) zf_gather<DIM>(zf, tid, il, s_J2[cs][DIM - 1], K);
+    dist2_gather<DIM>(pf, cs, il, s_J2[cs], K);
     if (cell >= 0) {
       // gather the node's face contributions (one per direction it ends)
 #pragma unroll
