@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   __shared__ signed char s_cform_[2][CPB];
   __shared__ int s_lev_[2][CPB];
   __shared__ double s_J2_[2][CPB][DIM], s_lift_[2][CPB][DIM];
+  __shared__ double s_meas_[2][CPB];  // h_x h_y (h_z) / 2^DIM of the cell
   __shared__ int s_nbc_[2][CPB][2 * DIM];        // local neighbour, or -1 - face cell (ghost)
   __shared__ long long s_nbg_[2][CPB][2 * DIM];  // global id (positivity reports)
   __shared__ double s_na1_[2][CPB][2 * DIM];
@@ -455,6 +456,8 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       s_ca1_[b][t] = dt * a.a1[lev];
       s_cform_[b][t] = a.formed[lev];
       s_lev_[b][t] = lev;
+      s_meas_[b][t] = DIM == 2 ? 0.25 * m.h[0][co[0]] * m.h[1][co[1]]
+                               : 0.125 * m.h[0][co[0]] * m.h[1][co[1]] * m.h[2][co[2]];
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         s_J2_[b][t][d] = 2.0 * m.jac[d][co[d]];
@@ -501,6 +504,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     auto& s_ca1 = s_ca1_[buf];
     auto& s_cform = s_cform_[buf];
     auto& s_lev = s_lev_[buf];
+    auto& s_meas = s_meas_[buf];
     auto& s_J2 = s_J2_[buf];
     auto& s_lift = s_lift_[buf];
     auto& s_nbc = s_nbc_[buf];
@@ -523,6 +527,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       if (a.form) l2_prefetch(a.Us + off, kBytes);
       l2_prefetch(a.U + off, kBytes);                       // stage 0 state / epilogue
       if (a.write_next && a.form) l2_prefetch(a.K1 + off, kBytes);  // epilogue formation
+      if (a.d_mode == 2) l2_prefetch(a.d + off, kBytes);              // d read-modify-write
     }
     // ---- load: own node (coalesced: consecutive threads, consecutive nodes),
     // formed with the cell's member row (stepper.cpp:60-72) ------------------
@@ -721,7 +726,9 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       if (a.want_dh || a.want_h) {
         // log(p / rho^gamma) = -(log beta + (gamma - 1) log rho)
         const double s_therm = -(lb + ph.gm1 * lr);
-        const double om = node_measure<DIM>(m, s_coord[cs][0], s_coord[cs][1], s_coord[cs][2], l);
+        // node_measure (semidisc.cpp:67) with the cell factor from the descriptor
+        const double om = DIM == 2 ? s_meas[cs] * c_w[il[0]] * c_w[il[1]]
+                                   : s_meas[cs] * c_w[il[0]] * c_w[il[1]] * c_w[il[2]];
         if (a.want_dh) {
           double v2 = 0.0, dot = 0.0;
 #pragma unroll
