@@ -830,3 +830,113 @@ def run(config: IntegratorConfig, family, pmap, semi, U0, chunk=64):
         if taken == 0 and not aborted:
             break
     return RunResult(semi.download(), log, t, aborted, semi.rhs_cell_evaluations(), h0)
+
+
+# ---------------------------------------------------------------------------
+# spectrum probing for family design (reference:
+# probe_jacobian / eigenvalues_dense / clean_spectrum, specopt.cpp:18-60)
+# ---------------------------------------------------------------------------
+def _color_period(n, radius):
+    """Smallest period k >= 2 radius + 1 dividing n (periodic wrap keeps the
+    colouring proper), else n (no compression along that axis)."""
+    for k in range(2 * radius + 1, n + 1):
+        if n % k == 0:
+            return k
+    return n
+
+
+def probe_jacobian(semi, U, t=0.0, epsilon=1e-7, colored=True):
+    """Dense Jacobian of the device RHS by central differences, column j with
+    h_j = epsilon (1 + |U_j|) as specopt.cpp:18-35.  With `colored`, the
+    columns of cells that are far enough apart are probed in one RHS pair
+    (compressed Jacobian): a cell's RHS depends on its face neighbours (BR1:
+    on their neighbours too), so cells whose footprints do not overlap share
+    an evaluation; 2 x colours x (nodes per cell x V) RHS calls instead of
+    2 M."""
+    U = semi._state(U)
+    M, npc, V = U.size, semi.nodes_per_cell(), semi.num_vars()
+    if M > 5000 and not colored:
+        raise Error(capi.PERRK_EINVAL, "dense Jacobian probing guarded to M <= 5000")
+    shape = semi.spec.mesh.shape()
+    dim = len(shape)
+    cells = np.arange(semi.num_cells())
+    coords = [cells % shape[0], (cells // shape[0]) % shape[1]]
+    if dim == 3:
+        coords.append(cells // (shape[0] * shape[1]))
+    radius = 2 if semi.spec.physics == "nsf" else 1
+    if colored:
+        periods = [_color_period(n, radius) for n in shape]
+    else:
+        periods = list(shape)
+    color = np.zeros(cells.size, dtype=np.int64)
+    mult = 1
+    for a in range(dim):
+        color += (coords[a] % periods[a]) * mult
+        mult *= periods[a]
+    ncolors = mult
+    # footprint rows of each cell: itself and its neighbours within `radius`
+    def footprint(c):
+        out = set()
+        base = [coords[a][c] for a in range(dim)]
+        rng = range(-radius, radius + 1)
+        offs = [(dx, dy) for dx in rng for dy in rng] if dim == 2 else \
+               [(dx, dy, dz) for dx in rng for dy in rng for dz in rng]
+        for o in offs:
+            if sum(abs(x) > 0 for x in o) > 1 and radius == 1:
+                continue  # face neighbours only for the inviscid footprint
+            q = [(base[a] + o[a]) % shape[a] for a in range(dim)]
+            cid = q[0] + shape[0] * (q[1] + (shape[1] * q[2] if dim == 3 else 0))
+            out.add(int(cid))
+        return sorted(out)
+    J = np.zeros((M, M))
+    for col in range(ncolors):
+        members = cells[color == col]
+        if members.size == 0:
+            continue
+        feet = {int(c): footprint(int(c)) for c in members}
+        for q in range(npc * V):
+            idx = members * npc * V + q
+            h = epsilon * (1.0 + np.abs(U[idx]))
+            up, um = U.copy(), U.copy()
+            up[idx] += h
+            um[idx] -= h
+            diff = semi.rhs(t, up) - semi.rhs(t, um)
+            for c, hc in zip(members, h):
+                rows = np.concatenate([np.arange(f * npc * V, (f + 1) * npc * V) for f in feet[int(c)]])
+                J[rows, c * npc * V + q] = diff[rows] / (2.0 * hc)
+    return J
+
+
+def clean_spectrum(eigs, relative_tol=1e-10):
+    """specopt.cpp:48-54: clip tiny positive real parts and imaginary parts."""
+    eigs = np.array(eigs, dtype=complex)
+    rho = np.abs(eigs).max()
+    re, im = eigs.real.copy(), eigs.imag.copy()
+    re[(re > 0.0) & (re <= relative_tol * rho)] = 0.0
+    im[np.abs(im) <= 1e-14 * rho] = 0.0
+    return re + 1j * im
+
+
+def probe_spectrum(semi, U, t=0.0, colored=True):
+    """probe_spectrum (specopt.cpp:56-60) on the device RHS."""
+    return clean_spectrum(np.linalg.eigvals(probe_jacobian(semi, U, t, colored=colored)))
+
+
+def stability_margin(family, eigs, dt):
+    """max |P_r(dt lambda)| over the spectrum for every member r (P from the
+    tableau, butcher.cpp stability_function): <= 1 means stable at dt."""
+    out = []
+    for r in range(family.R):
+        A, b = family.A[r], family.b
+        S = family.S
+        z = dt * np.asarray(eigs, dtype=complex)
+        k = np.zeros((S, z.size), dtype=complex)
+        for i in range(S):
+            acc = np.zeros(z.size, dtype=complex)
+            for j in range(i):
+                if A[i, j] != 0.0:
+                    acc += A[i, j] * k[j]
+            k[i] = 1.0 + z * acc
+        R_ = 1.0 + z * sum(b[i] * k[i] for i in range(S) if b[i] != 0.0)
+        out.append(float(np.abs(R_).max()))
+    return out

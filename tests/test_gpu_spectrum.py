@@ -1,0 +1,58 @@
+"""GPU: spectrum probing for family design: the
+device RHS's Jacobian by central differences, compressed by cell colouring,
+against the reference's own procedure (specopt.cpp:18-35, dense column by
+column) on the unmodified reference RHS."""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import mesh2d, smooth_state
+from paper_2507_04991_b200 import perrk as P
+from paper_2507_04991_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref_jacobian(ref, U, eps=1e-7):
+    M = U.size
+    J = np.zeros((M, M))
+    u = U.copy()
+    for j in range(M):
+        h = eps * (1.0 + abs(U[j]))
+        u[j] = U[j] + h
+        fp = ref.rhs(0.0, u)
+        u[j] = U[j] - h
+        fm = ref.rhs(0.0, u)
+        u[j] = U[j]
+        J[:, j] = (fp - fm) / (2.0 * h)
+    return J
+
+
+def test_colored_device_jacobian_vs_reference_probe():
+    mesh = mesh2d(6, 6, seed=101)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux="hlle"))
+    U = smooth_state((semi.node_x(), semi.node_y()), 2, seed=5, amp=0.2)
+    Jg = P.probe_jacobian(semi, U)                  # 2 x 4 colours x 64 RHS pairs
+    Jr = _ref_jacobian(O.Ref(mesh, surface_flux="hlle"), U)
+    scale = np.abs(Jr).max()
+    assert np.abs(Jg - Jr).max() < 1e-6 * scale    # central differences at eps 1e-7
+    eg = P.clean_spectrum(np.linalg.eigvals(Jg))
+    er = P.clean_spectrum(np.linalg.eigvals(Jr))
+    assert abs(np.abs(eg).max() - np.abs(er).max()) < 1e-6 * np.abs(er).max()
+    assert abs(eg.real.min() - er.real.min()) < 1e-6 * np.abs(er).max()
+    assert abs(np.abs(eg.imag).max() - np.abs(er.imag).max()) < 1e-6 * np.abs(er).max()
+
+
+def test_probed_spectrum_supports_the_c1_family_at_its_cfl():
+    """The probed C1 spectrum with the C1 family: |P(dt lambda)| ~ 1 at the
+    CFL step the config uses (the isentropic vortex runs 100 steps stably)."""
+    cfg = W.make_config("c1")
+    mesh = P.build_uniform_mesh2d(10.0, 6)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh))
+    U = np.ascontiguousarray(W.isentropic_vortex(W.VortexParams(), semi.node_x(),
+                                                 semi.node_y()).T).reshape(-1)
+    eigs = P.probe_spectrum(semi, U)
+    dt = P.compute_dt(U, semi, P.IntegratorConfig(time=P.TimeControl(False, 0.0,
+                                                                      P.CflRamp(0.9, 0.9))), 0.0)
+    margin = P.stability_margin(cfg.family, eigs, dt)
+    assert margin[0] < 1.0 + 1e-2
