@@ -200,6 +200,14 @@ int perrk_perk_step_resident(perrk_ctx* ctx, double* t, double dt, const perrk_s
 int perrk_advance(perrk_ctx* ctx, const perrk_run_cfg* cfg, double* t, int nsteps,
                   perrk_step_record* log, int* steps_taken, int* aborted);
 
+/* error_norms (stepper.cpp:195-265): L1 (domain-normalised) and Linf of the
+ * DG solution interpolated to the degree-2k GLL points against an exact
+ * solution; exact = 0: the 2D isentropic vortex (isentropic_vortex_state,
+ * physics.cpp:301-328) with params = {gamma, mach, radius, intensity,
+ * rho_inf, v_inf_x, v_inf_y, half_width} at time t.  U == NULL: resident. */
+int perrk_error_norms(perrk_ctx* ctx, const double* U, int exact, const double* params, double t,
+                      double* l1, double* linf);
+
 /* scalar RHS evaluation counter (semidisc.hpp:81-82): n_active*nodes*V per
  * evaluated stage */
 int perrk_rhs_cell_evaluations(const perrk_ctx* ctx, uint64_t* out);

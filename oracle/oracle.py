@@ -115,6 +115,9 @@ def ref_lib():
             "ref_characteristic_speed": (C.c_int, [C.c_void_p, _D, _D]),
             "ref_project_vortex": (C.c_int, [C.c_void_p, _D, C.c_double, _D]),
             "ref_gll": (None, [C.c_int, _D, _D, _D]),
+            "ref_error_norms_vortex": (C.c_int, [C.c_void_p, _D, _D, C.c_double, _D, _D]),
+            "ref_write_step_log": (C.c_int, [C.c_void_p, C.c_int, _D, C.c_char_p]),
+            "ref_write_snapshot": (C.c_int, [C.c_void_p, _D, C.c_char_p]),
             "ref_logmean": (C.c_double, [C.c_double, C.c_double]),
             "ref_numerical_flux": (C.c_int, [C.c_int, C.c_double, C.c_int, _D, _D, C.c_int, _D]),
             "ref_physics_eval": (C.c_int, [C.c_int, C.c_double, _D, C.c_int, _D, _D, _D, _D]),
@@ -307,6 +310,13 @@ class Ref(_Base):
 
     def rhs_cell_evaluations(self):
         return self.L.ref_rhs_cell_evaluations(self.h)
+
+    def error_norms_vortex(self, U, params, t):
+        pv = np.ascontiguousarray(params, dtype=np.float64)
+        l1, li = np.zeros(4), np.zeros(4)
+        self._check(self.L.ref_error_norms_vortex(self.h, dp(np.ascontiguousarray(U)), dp(pv), t,
+                                                  dp(l1), dp(li)))
+        return l1, li
 
 
 class RefNSF1D:

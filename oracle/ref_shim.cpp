@@ -263,6 +263,57 @@ int ref_project_vortex(ref_ctx* ctx, const double* p, double t, double* U) {
   });
 }
 
+// error_norms (stepper.cpp:195-265) against the isentropic vortex
+int ref_error_norms_vortex(ref_ctx* ctx, const double* U, const double* p, double t, double* l1,
+                           double* linf) {
+  return guarded([&] {
+    VortexParams vp;
+    vp.gamma = p[0];
+    vp.mach = p[1];
+    vp.radius = p[2];
+    vp.intensity = p[3];
+    vp.rho_inf = p[4];
+    vp.v_inf[0] = p[5];
+    vp.v_inf[1] = p[6];
+    vp.half_width = p[7];
+    const auto& s = *ctx->semi;
+    StateVector u(U, U + s.num_dofs());
+    const auto e = error_norms(
+        u, [&](double x, double y, double tt, double* out) { isentropic_vortex_state(vp, x, y, tt, out); },
+        t, s);
+    std::memcpy(l1, e.l1.data(), sizeof(double) * e.l1.size());
+    std::memcpy(linf, e.linf.data(), sizeof(double) * e.linf.size());
+  });
+}
+
+// the reference's CSV writers (stepper.cpp:267-301, semidisc.cpp:609-632);
+// rows: [step, t, dt, gamma, iters, H, fell_back, invariants...]
+int ref_write_step_log(ref_ctx* ctx, int n, const double* rows, const char* path) {
+  return guarded([&] {
+    const int V = ctx->semi->num_vars();
+    std::vector<StepRecord> log(n);
+    for (int k = 0; k < n; ++k) {
+      const double* r = rows + static_cast<std::size_t>(k) * (7 + V);
+      log[k].step = static_cast<int>(r[0]);
+      log[k].t = r[1];
+      log[k].dt = r[2];
+      log[k].gamma = r[3];
+      log[k].newton_iters = static_cast<int>(r[4]);
+      log[k].entropy = r[5];
+      log[k].fell_back = r[6] != 0.0;
+      log[k].invariants.assign(r + 7, r + 7 + V);
+    }
+    write_step_log_csv(log, *ctx->semi, path);
+  });
+}
+
+int ref_write_snapshot(ref_ctx* ctx, const double* U, const char* path) {
+  return guarded([&] {
+    StateVector u(U, U + ctx->semi->num_dofs());
+    write_snapshot_csv(*ctx->semi, u, path);
+  });
+}
+
 // ---- basis / physics pins ------------------------------------------------
 void ref_gll(int k, double* nodes, double* weights, double* D) {
   const auto b = gll_basis(k);

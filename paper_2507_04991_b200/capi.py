@@ -93,6 +93,7 @@ _PROTOS = {
                                            C.POINTER(StepResult)]),
     "perrk_advance": (C.c_int, [_P, C.POINTER(RunCfg), _D, C.c_int, C.POINTER(StepRecord),
                                 _I, _I]),
+    "perrk_error_norms": (C.c_int, [_P, _D, C.c_int, _D, C.c_double, _D, _D]),
     "perrk_rhs_cell_evaluations": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "perrk_reset_counter": (C.c_int, [_P]),
     "perrk_family_build": (C.c_int, [C.c_int, C.c_int, C.c_int, _I, _D, C.c_double, _D, _D, _D,

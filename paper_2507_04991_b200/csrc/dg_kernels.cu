@@ -697,9 +697,107 @@ __global__ void record_kernel(StepState* st, const double* all, int nranks, int 
   }
 }
 
+// ---------------------------------------------------------------------------
+// error_norms (stepper.cpp:195-265), 2D, isentropic-vortex exact solution
+// (isentropic_vortex_state, physics.cpp:301-328): the DG solution
+// interpolated to the degree-2k GLL points of each cell, L1 (quadrature, later
+// divided by the domain measure) and Linf of the pointwise difference.
+// fine: [nf nodes][nf weights][nf x 4 interpolation matrix]
+// ---------------------------------------------------------------------------
+__device__ void vortex_state(const double* p, double x, double y, double t, double* u) {
+  const double gamma = p[0], mach = p[1], radius = p[2], intensity = p[3], rho_inf = p[4];
+  const double vix = p[5], viy = p[6], hw = p[7];
+  auto wrap = [&](double d) {
+    const double span = 2.0 * hw;
+    d = fmod(d + hw, span);
+    if (d < 0.0) d += span;
+    return d - hw;
+  };
+  const double cx = wrap(x - vix * t), cy = wrap(y - viy * t);
+  const double r2 = cx * cx + cy * cy;
+  const double g = exp((1.0 - r2) / (2.0 * radius * radius));
+  const double gm1 = gamma - 1.0;
+  const double rho = rho_inf * pow(1.0 - intensity * intensity * mach * mach * gm1 * g * g /
+                                             (8.0 * M_PI * M_PI),
+                                   1.0 / gm1);
+  const double coef = intensity * g / (2.0 * M_PI * radius);
+  const double vx = vix - coef * cy, vy = viy + coef * cx;
+  const double pres = pow(rho, gamma) / (gamma * mach * mach);
+  u[0] = rho;
+  u[1] = rho * vx;
+  u[2] = rho * vy;
+  u[3] = pres / gm1 + 0.5 * rho * (vx * vx + vy * vy);
+}
+
+__global__ void __launch_bounds__(256)
+    error_norms_kernel(const double* __restrict__ U, MeshDev m, const double* x0,
+                       const double* y0, const double* fine, int nf, const double* vp, double t,
+                       double* partials, unsigned* counter, double* out, unsigned long long* linf,
+                       long long npts) {
+  constexpr int V = 4, NPC = 16;
+  __shared__ double s_red[2 * 4 * 8];
+  dd acc[4];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = dd_zero();
+  double mx[V] = {0.0, 0.0, 0.0, 0.0};
+  const double* fx = fine;
+  const double* fw = fine + nf;
+  const double* L = fine + 2 * nf;
+  for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < npts;
+       n += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int cell = static_cast<int>(n / (nf * nf)), q = static_cast<int>(n % (nf * nf));
+    const int qx = q / nf, qy = q % nf;
+    const int ci = cell % m.nc[0], cj = cell / m.nc[0];
+    const double hx = m.h[0][ci], hy = m.h[1][cj];
+    double val[V] = {0.0, 0.0, 0.0, 0.0};
+    // interpolate along x per original row, then along y (stepper.cpp:231-251)
+#pragma unroll
+    for (int iy = 0; iy < N1; ++iy) {
+      double row[V] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int l = 0; l < N1; ++l)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          row[v] += L[qx * N1 + l] * __ldg(U + (static_cast<size_t>(cell) * NPC + l + N1 * iy) * V + v);
+#pragma unroll
+      for (int v = 0; v < V; ++v) val[v] += L[qy * N1 + iy] * row[v];
+    }
+    const double x = x0[ci] + 0.5 * hx * (fx[qx] + 1.0);
+    const double y = y0[cj] + 0.5 * hy * (fx[qy] + 1.0);
+    double ue[V];
+    vortex_state(vp, x, y, t, ue);
+    const double w = 0.25 * hx * hy * fw[qx] * fw[qy];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double diff = fabs(val[v] - ue[v]);
+      acc[v] = dd_add_prod(acc[v], w, diff);
+      mx[v] = fmax(mx[v], diff);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double w = warp_max(mx[v]);
+    if ((threadIdx.x & 31) == 0) atomic_max_pos(&linf[v], w);
+  }
+  dd tot[4];
+  block_reduce_dd<4>(acc, s_red);
+  if (grid_reduce_dd<4>(acc, partials, counter, s_red, tot) && threadIdx.x == 0)
+    for (int v = 0; v < V; ++v) out[v] = tot[v].hi + tot[v].lo;
+}
+
 }  // namespace dev
 
 using namespace dev;
+
+cudaError_t launch_error_norms(const double* U, const MeshDev& m, const double* x0,
+                               const double* y0, const double* fine, int nf, const double* vp,
+                               double t, double* partials, unsigned* counter, double* out,
+                               unsigned long long* linf, long long ncells, int grid,
+                               cudaStream_t s) {
+  error_norms_kernel<<<grid, 256, 0, s>>>(U, m, x0, y0, fine, nf, vp, t, partials, counter, out,
+                                          linf, ncells * nf * nf);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_pack_traces(int dim, const StageArgs& a, const MeshDev& m, StepState* st,
                                double* send_lo, double* send_hi, cudaStream_t s) {

@@ -63,6 +63,12 @@ cudaError_t launch_nu_cell(int dim, const double* U, const dev::MeshDev& m, cons
 cudaError_t launch_quad(int dim, const double* U, const double* K, const dev::MeshDev& m,
                         const dev::Phys& ph, int mode, double* partials, unsigned* counter,
                         double* out, long long nnodes, int grid, cudaStream_t s);
+cudaError_t launch_error_norms(const double* U, const dev::MeshDev& m, const double* x0,
+                               const double* y0, const double* fine, int nf, const double* vp,
+                               double t, double* partials, unsigned* counter, double* out,
+                               unsigned long long* linf, long long ncells, int grid,
+                               cudaStream_t s);
+
 // element-slab decomposition
 enum { RED_STAGES = 0, RED_RELAX = 1, RED_UPDATE = 2, RED_NUMAX = 3 };
 cudaError_t launch_pack_traces(int dim, const StageArgs& a, const dev::MeshDev& m,

@@ -1454,6 +1454,66 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
   });
 }
 
+int perrk_error_norms(perrk_ctx* c, const double* U, int exact, const double* params, double t,
+                      double* l1, double* linf) {
+  return guarded([&] {
+    REQUIRE(c && params && l1 && linf, "null argument");
+    no_slab(c, "error_norms");
+    if (c->dim != 2 || exact != 0)
+      throw Fail(PERRK_EUNSUP, "device error norms: 2D isentropic vortex (exact = 0)");
+    set_device(c);
+    // degree-2k GLL points and the interpolation matrix (basis.cpp:35-110)
+    const Basis fine = make_basis(2 * c->basis.k);
+    const int nf = static_cast<int>(fine.x.size()), n1 = c->basis.k + 1;
+    std::vector<double> buf(2 * nf + nf * n1 + 8 + c->nc[0] + c->nc[1] + 4);
+    std::copy(fine.x.begin(), fine.x.end(), buf.begin());
+    std::copy(fine.w.begin(), fine.w.end(), buf.begin() + nf);
+    std::vector<double> bw(n1, 1.0);
+    for (int j = 0; j < n1; ++j)
+      for (int q = 0; q < n1; ++q)
+        if (q != j) bw[j] /= (c->basis.x[j] - c->basis.x[q]);
+    for (int i = 0; i < nf; ++i) {
+      double* row = &buf[2 * nf + i * n1];
+      int hit = -1;
+      for (int j = 0; j < n1; ++j)
+        if (fine.x[i] == c->basis.x[j]) hit = j;
+      if (hit >= 0) {
+        for (int j = 0; j < n1; ++j) row[j] = j == hit ? 1.0 : 0.0;
+        continue;
+      }
+      double den = 0.0;
+      for (int j = 0; j < n1; ++j) den += bw[j] / (fine.x[i] - c->basis.x[j]);
+      for (int j = 0; j < n1; ++j) row[j] = (bw[j] / (fine.x[i] - c->basis.x[j])) / den;
+    }
+    const size_t off_vp = 2 * nf + nf * n1, off_x = off_vp + 8, off_y = off_x + c->nc[0];
+    std::copy(params, params + 8, buf.begin() + off_vp);
+    for (int i = 0; i < c->nc[0]; ++i) buf[off_x + i] = c->edges[0][i];
+    for (int j = 0; j < c->nc[1]; ++j) buf[off_y + j] = c->edges[1][j];
+    double* dbuf = nullptr;
+    unsigned long long* dmax = nullptr;
+    CK(cudaMalloc(&dbuf, sizeof(double) * buf.size()));
+    CK(cudaMalloc(&dmax, sizeof(unsigned long long) * 4));
+    CK(cudaMemcpyAsync(dbuf, buf.data(), sizeof(double) * buf.size(), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long) * 4, c->stream));
+    CK(launch_error_norms(stage_input(c, U), c->mesh(), dbuf + off_x, dbuf + off_y, dbuf, nf,
+                          dbuf + off_vp, t, c->partials, c->counter, c->dout, dmax, c->ncells,
+                          c->grid_flat, c->stream));
+    unsigned long long mx[4];
+    CK(cudaMemcpyAsync(l1, c->dout, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(mx, dmax, sizeof mx, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(dbuf);
+    cudaFree(dmax);
+    double dom = 1.0;
+    for (int a = 0; a < 2; ++a) dom *= c->edges[a].back() - c->edges[a].front();
+    for (int v = 0; v < 4; ++v) {
+      l1[v] /= dom;  // domain_measure (semidisc.cpp:71-72)
+      std::memcpy(&linf[v], &mx[v], sizeof(double));
+    }
+  });
+}
+
 int perrk_rhs_cell_evaluations(const perrk_ctx* c, uint64_t* out) {
   return guarded([&] {
     REQUIRE(c && out, "null argument");

@@ -236,6 +236,16 @@ class Semidiscretization:
         check(lib().perrk_br1_gradients(self._h, float(t), _dp(U), _dp(g)))
         return g.reshape(2, -1)
 
+    def error_norms_vortex(self, U, params, t):
+        """error_norms (stepper.cpp:195-265) against the isentropic vortex
+        (physics.cpp:301-328); params: workloads.VortexParams.  U None: the
+        resident state.  Returns (l1[V], linf[V])."""
+        pv = _f64(params.as_array())
+        l1, li = np.zeros(4), np.zeros(4)
+        Up = None if U is None else _dp(self._state(U))
+        check(lib().perrk_error_norms(self._h, Up, 0, _dp(pv), float(t), _dp(l1), _dp(li)))
+        return l1, li
+
     def rhs_partition_restricted(self, t, U, pmap, level):
         mask = (np.asarray(pmap.effective_level) == level).astype(np.int8)
         return self.rhs_masked(t, U, mask)
@@ -940,3 +950,32 @@ def stability_margin(family, eigs, dt):
         R_ = 1.0 + z * sum(b[i] * k[i] for i in range(S) if b[i] != 0.0)
         out.append(float(np.abs(R_).max()))
     return out
+
+
+# ---------------------------------------------------------------------------
+# CSV writers (write_step_log_csv, stepper.cpp:267-301; write_snapshot_csv,
+# semidisc.cpp:609-632): the reference's headers and %.17g formatting
+# ---------------------------------------------------------------------------
+def write_step_log_csv(log, semi, path):
+    V = semi.num_vars()
+    names = ["mass", "momentum_x", "momentum_y", "momentum_z"][: semi.dim() + 1] + ["energy"]
+    with open(path, "w") as f:
+        f.write("step,t,dt,gamma,newton_iters,H," + ",".join(names[:V]) + ",fell_back\n")
+        for r in log:
+            vals = [r.t, r.dt, r.gamma]
+            f.write(f"{r.step}," + ",".join("%.17g" % v for v in vals) + f",{r.newton_iters},"
+                    + "%.17g" % r.entropy + "," + ",".join("%.17g" % v for v in r.invariants[:V])
+                    + f",{1 if r.fell_back else 0}\n")
+
+
+def write_snapshot_csv(semi, U, path):
+    V = semi.num_vars()
+    # EulerPhysics::variable_name (physics.cpp:90-95), z extended
+    names = ["rho", "rho_v_x", "rho_v_y", "rho_v_z"][: semi.dim() + 1] + ["rho_e"]
+    x, y, z = semi.node_x(), semi.node_y(), semi.node_z()
+    U = np.asarray(U).reshape(-1, V)
+    with open(path, "w") as f:
+        f.write("x,y" + (",z" if semi.dim() == 3 else "") + "," + ",".join(names[:V]) + "\n")
+        for n in range(U.shape[0]):
+            cols = [x[n], y[n]] + ([z[n]] if semi.dim() == 3 else []) + list(U[n])
+            f.write(",".join("%.17g" % v for v in cols) + "\n")

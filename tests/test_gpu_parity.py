@@ -349,3 +349,29 @@ def test_cfl_ramp_on_device_matches_stepwise_compute_dt():
         seed = 1.0 if res.fell_back else res.gamma
     dts = [r.dt for r in recs]
     assert dts[-1] > 1.5 * dts[0]  # the ramp raises the step
+
+
+def test_error_norms_vortex_vs_reference():
+    """error_norms (stepper.cpp:195-265) on the device against the reference,
+    for the C1 vortex at t = 0 and after 20 device steps."""
+    cfg, semi, U0 = c1_setup()
+    ref = O.Ref(cfg.mesh)
+    vp = W.VortexParams()
+    l1, li = semi.error_norms_vortex(U0, vp, 0.0)
+    r1, ri = ref.error_norms_vortex(U0, vp.as_array(), 0.0)
+    assert np.allclose(l1, r1, rtol=1e-11, atol=1e-16) and np.allclose(li, ri, rtol=1e-11, atol=1e-16)
+    Ug, recs = _run_c1(semi, cfg, U0, "accurate", steps=20)
+    t = recs[-1].t
+    l1, li = semi.error_norms_vortex(Ug, vp, t)
+    r1, ri = ref.error_norms_vortex(Ug, vp.as_array(), t)
+    assert np.allclose(l1, r1, rtol=1e-11) and np.allclose(li, ri, rtol=1e-11)
+    assert l1.max() < 1e-2  # the vortex is resolved: small discretisation error
+
+
+def test_snapshot_csv_matches_reference_writer(tmp_path):
+    cfg, semi, U0 = c1_setup()
+    ref = O.Ref(cfg.mesh)
+    ours, theirs = tmp_path / "ours.csv", tmp_path / "ref.csv"
+    P.write_snapshot_csv(semi, U0, str(ours))
+    assert ref.L.ref_write_snapshot(ref.h, O.dp(U0), str(theirs).encode()) == 0
+    assert ours.read_bytes() == theirs.read_bytes()

@@ -353,3 +353,23 @@ def test_orc_nsf2d_reduces_to_reference_nsf1d(surface):
     for v, v2 in ((0, 0), (1, 1), (2, 3)):
         assert np.abs(r2[..., v2] - r1.reshape(nx, 4, 3)[None, :, None, :, v]).max() < 1e-12 * scale
     assert np.abs(r2[..., 2]).max() < 1e-12 * scale
+
+
+@need_ref
+def test_step_log_csv_matches_reference_writer(tmp_path):
+    """write_step_log_csv (stepper.cpp:267-301): the same file bytes."""
+    import types
+    rng = np.random.default_rng(2)
+    log = [P.StepRecord(k + 1, *rng.standard_normal(3), int(rng.integers(0, 5)),
+                        float(rng.standard_normal()), rng.standard_normal(4), bool(k % 2))
+           for k in range(7)]
+    semi = types.SimpleNamespace(num_vars=lambda: 4, dim=lambda: 2)
+    ours = tmp_path / "ours.csv"
+    P.write_step_log_csv(log, semi, str(ours))
+    ref = O.Ref(mesh2d(3, 3, seed=1))
+    rows = np.array([[r.step, r.t, r.dt, r.gamma, r.newton_iters, r.entropy, float(r.fell_back),
+                      *r.invariants] for r in log])
+    theirs = tmp_path / "ref.csv"
+    assert ref.L.ref_write_step_log(ref.h, len(log), O.dp(np.ascontiguousarray(rows)),
+                                    str(theirs).encode()) == 0
+    assert ours.read_bytes() == theirs.read_bytes()
