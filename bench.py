@@ -276,20 +276,40 @@ def perrk_arm(args):
     gammas = [r.gamma for r in recs]
     fell_back = sum(int(r.fell_back) for r in recs)
 
-    # ---- e2e through the reference-facing call with host buffers ----------
+    # ---- e2e through the public API with host buffers ----------------------
+    # (1) run() (stepper.cpp:129-193; perrk.run_steps -> perrk_upload_state,
+    #     perrk_advance, perrk_download_state): U0 from pinned host memory to
+    #     the device, K steps resident, every step's StepRecord (the step's
+    #     metric: gamma, H, invariants) and the final state back to the host;
+    # (2) perk_step with the host state every step (perrk_perk_step): the
+    #     strictest reading, U up and down every step.
     e2e = None
     if not args.no_e2e:
-        Uh = torch.empty(U0.size, dtype=torch.float64, pin_memory=True).numpy()
-        Uh[:] = semi.download()
-        dt = P.compute_dt(Uh, semi, rc, t)
-        opts = P.PerkStepOptions(relaxation=cfg.relaxation)
-        te = t
-        # one untimed call (first-call costs), then the timed ones
-        te, r = P.perk_step(Uh, te, dt, fam, pm, semi, opts)
+        U_host = torch.empty(U0.size, dtype=torch.float64, pin_memory=True).numpy()
+        U_host[:] = semi.download()
+        U_out = torch.empty(U0.size, dtype=torch.float64, pin_memory=True).numpy()
+        rc_run = P.IntegratorConfig(t0=t, tf=1e30, time=rc.time, relaxation=cfg.relaxation)
+        P.run_steps(rc_run, fam, pm, semi, U_host, 1, out=U_out)  # untimed first call
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
+        e0.record(stream)
+        res = P.run_steps(rc_run, fam, pm, semi, U_host, args.steps, out=U_out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rms = e0.elapsed_time(e1)
+        rwall = time.perf_counter() - w0
+        if res.aborted or len(res.log) != args.steps:
+            raise RuntimeError("e2e run aborted")
+        # (2)
+        Uh = U_out
+        dt = P.compute_dt(Uh, semi, rc, t)
+        opts = P.PerkStepOptions(relaxation=cfg.relaxation)
+        te = t
+        te, r = P.perk_step(Uh, te, dt, fam, pm, semi, opts)
+        torch.cuda.synchronize()
+        barrier()
         e0.record(stream)
         for _ in range(args.steps):
             te, r = P.perk_step(Uh, te, dt, fam, pm, semi, opts)
@@ -298,16 +318,23 @@ def perrk_arm(args):
         e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
-        wall = time.perf_counter() - w0
         if world > 1:
             import torch.distributed as dist
-            m = torch.tensor([ems], device="cuda")
+            m = torch.tensor([rms, ems], device="cuda")
             dist.all_reduce(m, op=dist.ReduceOp.MAX)
-            ems = float(m.item())
-        e2e = {"value": total_per_step * args.steps / (ems * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(Uh.nbytes), "d2h_bytes_per_step": int(Uh.nbytes),
-               "ms_per_step": ems / args.steps, "wall_ms_per_step": 1e3 * wall / args.steps,
-               "path": "perrk_perk_step (include/perrk_b200.h) with pinned host U"}
+            rms, ems = (float(x) for x in m.tolist())
+        rec_bytes = 88  # one StepRecord row (t, dt, gamma, iters, fell_back, H, 5 invariants)
+        e2e = {"value": total_per_step * args.steps / (rms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(U_host.nbytes // args.steps),
+               "d2h_bytes_per_step": int(U_out.nbytes // args.steps + rec_bytes),
+               "ms_per_step": rms / args.steps, "wall_ms_per_step": 1e3 * rwall / args.steps,
+               "path": f"run() for {args.steps} steps: perrk_upload_state (pinned U0), "
+                       "perrk_advance (steps + StepRecords), perrk_download_state (pinned U)",
+               "host_state_every_step": {
+                   "value": total_per_step * args.steps / (ems * 1e-3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(Uh.nbytes), "d2h_bytes_per_step": int(Uh.nbytes),
+                   "ms_per_step": ems / args.steps,
+                   "path": "perrk_perk_step (include/perrk_b200.h) with pinned host U"}}
 
     # ---- roofline of the dominant kernel ------------------------------------
     hbm, hbm_kind = peaks()

@@ -842,6 +842,20 @@ def run(config: IntegratorConfig, family, pmap, semi, U0, chunk=64):
     return RunResult(semi.download(), log, t, aborted, semi.rhs_cell_evaluations(), h0)
 
 
+def run_steps(config: IntegratorConfig, family, pmap, semi, U0, nsteps, out=None):
+    """run() (stepper.cpp:129-193) for exactly nsteps steps (the reference's
+    run has no step-count mode): U0 (host) -> device once, the
+    steps resident with the step log, the final state -> `out` (host)."""
+    U0 = semi._state(U0)
+    semi.upload(U0)
+    t, taken, aborted, recs = advance(semi, family, pmap, config, config.t0, nsteps, True)
+    log = [StepRecord(k + 1, r.t, r.dt, r.gamma, r.newton_iters, r.entropy,
+                      np.array(r.invariants[: semi.num_vars()]), bool(r.fell_back))
+           for k, r in enumerate(recs)]
+    U = semi.download(out)
+    return RunResult(U, log, t, aborted, semi.rhs_cell_evaluations(), float("nan"))
+
+
 # ---------------------------------------------------------------------------
 # spectrum probing for family design (SURVEY.md 8f item 1; reference:
 # probe_jacobian / eigenvalues_dense / clean_spectrum, specopt.cpp:18-60)
