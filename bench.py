@@ -373,14 +373,16 @@ def perrk_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.description, "nodes": int(run.total_nodes()),
                        "dof_stage_per_step": int(total_per_step), "cfl": cfg.cfl,
                        "family": f"{fam.kind} S={fam.S} E={fam.E}",
                        "relaxation": "newton, accurate numerics (SURVEY 7.3 H1)",
                        "l2": "inputs larger than L2 (state 5 x 640 MiB)",
-                       "parallelism": f"slab{world}" if world > 1 else "single"},
+                       "parallelism": (f"{run.partition}-partition x{world} (NCCL halo)"
+                                       if world > 1 else "single"),
+                       "halo_traces": run.halo_traces() if world > 1 else 0},
             "gpu_launches": int(launches), "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu, "clocks": clk,
             "run": {"gamma_min": min(gammas), "gamma_max": max(gammas), "fell_back": fell_back,

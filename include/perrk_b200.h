@@ -241,36 +241,58 @@ int perrk_step_traffic(const perrk_ctx* ctx, double* stage_bytes, double* pass_b
                        double* update_bytes);
 int perrk_fp64_peak(int device, double* gflops);
 
-/* ---- multi-GPU: element-slab decomposition ---------------
- * No reference counterpart (the reference is single-process).  The mesh is
- * cut into contiguous slabs of last-axis cell layers (z in 3D, y in 2D), one
- * per rank (one process per GPU).  Per stage each rank packs the formed stage
- * traces of its two boundary layers and exchanges them with the slab
- * neighbours (periodic ring: ncclSend/ncclRecv); the reductions (dH, the
- * Newton residual/derivative, max |d|, the CFL speed, H and invariants) are
- * per-rank double-double partials all-gathered and summed in rank order.
+/* ---- multi-GPU: element partition ------------------------
+ * No reference counterpart (the reference is single-process).  Every global
+ * cell is owned by one rank (one process per GPU); `owner` is the global
+ * ownership map (global cell id -> rank, the reference's cell order; NULL:
+ * uniform slabs of last-axis cell layers).  Per stage each rank packs the
+ * formed stage traces of its faces that border another rank and exchanges
+ * them with those peers (grouped ncclSend/ncclRecv on a comm stream while the
+ * interior cells run); the reductions (dH, the Newton residual/derivative,
+ * max |d|, the CFL speed, H and invariants) are per-rank double-double
+ * partials all-gathered and summed in rank order.
  *
  * nccl_id: the 128-byte ncclUniqueId from perrk_nccl_id on rank 0 (broadcast
- * by the caller, e.g. through torch.distributed).  layer_cuts: nranks+1
- * increasing layer indices (NULL: uniform).  Call before perrk_set_family;
- * afterwards upload/download/geometry refer to the rank's slab, while
- * perrk_set_family still takes the GLOBAL effective-level array and
- * positivity reports carry global cell ids.  nranks == 1 is a no-op. */
+ * by the caller, e.g. through torch.distributed).  Call before
+ * perrk_set_family; afterwards upload/download/geometry refer to the rank's
+ * cells in ascending global id (perrk_local_cells), while perrk_set_family
+ * still takes the GLOBAL effective-level array and positivity reports carry
+ * global cell ids.  nranks == 1 is a no-op. */
 int perrk_nccl_id(void* nccl_id_out);
 int perrk_comm_init(perrk_ctx* ctx, const void* nccl_id, int rank, int nranks,
-                    const int* layer_cuts);
-int perrk_slab_range(const perrk_ctx* ctx, int* layer_begin, int* layer_end);
+                    const int* owner);
+/* the context's cells (global ids, ascending); gids may be NULL to query n */
+int perrk_local_cells(const perrk_ctx* ctx, int* gids, int64_t* n);
 /* Test harness for the multi-rank logic on ONE device: the n contexts (same
  * global mesh) become ranks 0..n-1 of a group sharing one stream; the halo
  * and the gathers are stream-ordered device copies.  perrk_advance /
  * perrk_perk_step_resident / perrk_compute_dt(U = NULL) on any member then
  * step every member. */
-int perrk_loopback_group(perrk_ctx** ctxs, int n, const int* layer_cuts);
-/* Host helpers (no device work): balanced contiguous cuts from per-layer work
- * (NULL: uniform), and the cell-local node indices of the last-axis face
- * traces (side 0: bottom, 1: top) in exchange order. */
-int perrk_slab_cuts(int n_last, const double* layer_work, int nranks, int* cuts);
-int perrk_slab_trace_nodes(int dim, int side, int* nodes);
+int perrk_loopback_group(perrk_ctx** ctxs, int n, const int* owner);
+/* Host helpers (no device work).
+ * perrk_partition_slabs: contiguous last-axis layers balanced by per-cell
+ *   work (NULL: uniform).
+ * perrk_partition_levels: every level's cells cut into nranks equal runs in
+ *   global order, so each rank holds 1/nranks of every level and every P-ERK
+ *   stage is balanced (the stage loop synchronises ranks once per stage).
+ * perrk_halo_plan: the plan perrk_comm_init builds for `rank`.  counts[4] =
+ *   {local cells, ghost traces, sent traces, peers}; any array may be NULL
+ *   (call once with NULLs for the sizes).  gid[local]; nbr[local*2dim + f] =
+ *   local neighbour or -1-ghost slot; ghost_gid[slot] = the neighbour's
+ *   global id; peers ascending; a peer k's ghost slots are
+ *   [recv_off[k], recv_off[k+1]) and the traces we send it are the
+ *   (local cell, face) pairs send[2 j], send[2 j + 1] for j in
+ *   [send_off[k], send_off[k+1]).  Both sides order a peer's traces by the
+ *   sender's (global cell, face).
+ * perrk_face_nodes: cell-local node index of trace point pt of face f
+ *   (2 d + side), the point order of the exchanged traces. */
+int perrk_partition_slabs(int dim, const int* n, const double* cell_work, int nranks, int* owner);
+int perrk_partition_levels(int dim, const int* n, const int* level, int nlevels, int nranks,
+                           int* owner);
+int perrk_halo_plan(int dim, const int* n, const int* owner, int rank, int64_t* counts, int* gid,
+                    int* nbr, int64_t* ghost_gid, int* peers, int64_t* recv_off,
+                    int64_t* send_off, int* send);
+int perrk_face_nodes(int dim, int face, int* nodes);
 
 #ifdef __cplusplus
 }

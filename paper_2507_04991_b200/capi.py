@@ -108,10 +108,14 @@ _PROTOS = {
     "perrk_fp64_peak": (C.c_int, [C.c_int, _D]),
     "perrk_nccl_id": (C.c_int, [C.c_void_p]),
     "perrk_comm_init": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int, _I]),
-    "perrk_slab_range": (C.c_int, [_P, _I, _I]),
+    "perrk_local_cells": (C.c_int, [_P, _I, C.POINTER(C.c_int64)]),
     "perrk_loopback_group": (C.c_int, [C.POINTER(_P), C.c_int, _I]),
-    "perrk_slab_cuts": (C.c_int, [C.c_int, _D, C.c_int, _I]),
-    "perrk_slab_trace_nodes": (C.c_int, [C.c_int, C.c_int, _I]),
+    "perrk_partition_slabs": (C.c_int, [C.c_int, _I, _D, C.c_int, _I]),
+    "perrk_partition_levels": (C.c_int, [C.c_int, _I, _I, C.c_int, C.c_int, _I]),
+    "perrk_halo_plan": (C.c_int, [C.c_int, _I, _I, C.c_int, C.POINTER(C.c_int64), _I, _I,
+                                  C.POINTER(C.c_int64), _I, C.POINTER(C.c_int64),
+                                  C.POINTER(C.c_int64), _I]),
+    "perrk_face_nodes": (C.c_int, [C.c_int, C.c_int, _I]),
 }
 EXPORTED = tuple(_PROTOS)
 

@@ -37,6 +37,7 @@ __device__ __forceinline__ T pick3(const T (&a)[3], int i) {
 }
 
 __device__ __forceinline__ void cell_coords(const MeshDev& m, int cell, int& ci, int& cj, int& ck) {
+  if (m.gid) cell = m.gid[cell];  // a local cell of a decomposed context
   ci = cell % m.nc[0];
   const int r = cell / m.nc[0];
   cj = r % m.nc[1];
@@ -800,14 +801,14 @@ cudaError_t launch_error_norms(const double* U, const MeshDev& m, const double* 
 }
 
 cudaError_t launch_pack_traces(int dim, const StageArgs& a, const MeshDev& m, StepState* st,
-                               double* send_lo, double* send_hi, cudaStream_t s) {
-  const int lc = dim == 3 ? m.nc[0] * m.nc[1] : m.nc[0];
+                               const int* send, int nsend, double* out, cudaStream_t s) {
+  if (nsend <= 0) return cudaSuccess;
   const int fp = dim == 3 ? 16 : 4;
-  const int grid = (2 * lc * fp + 255) / 256;
+  const int grid = (nsend * fp + 255) / 256;
   if (dim == 2)
-    pack_traces_kernel<2><<<grid, 256, 0, s>>>(a, m, st, send_lo, send_hi);
+    pack_traces_kernel<2><<<grid, 256, 0, s>>>(a, m, st, send, nsend, out);
   else
-    pack_traces_kernel<3><<<grid, 256, 0, s>>>(a, m, st, send_lo, send_hi);
+    pack_traces_kernel<3><<<grid, 256, 0, s>>>(a, m, st, send, nsend, out);
   return cudaGetLastError();
 }
 

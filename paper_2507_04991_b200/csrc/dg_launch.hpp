@@ -31,7 +31,6 @@ struct StageArgs {
   int want_dmax;         // max |d| (last b-stage)
   int stage;
   long long ncells;      // GLOBAL cells (positivity codes are stage * ncells + global cell)
-  long long cell_offset; // global id of local cell 0
   const double* G;       // BR1 viscous fluxes [2][ndofs] (nullptr: inviscid)
   long long ndofs;
 };
@@ -72,7 +71,7 @@ cudaError_t launch_error_norms(const double* U, const dev::MeshDev& m, const dou
 // element-slab decomposition
 enum { RED_STAGES = 0, RED_RELAX = 1, RED_UPDATE = 2, RED_NUMAX = 3 };
 cudaError_t launch_pack_traces(int dim, const StageArgs& a, const dev::MeshDev& m,
-                               dev::StepState* st, double* send_lo, double* send_hi,
+                               dev::StepState* st, const int* send, int nsend, double* out,
                                cudaStream_t s);
 cudaError_t launch_stash(dev::StepState* st, int mode, cudaStream_t s);
 cudaError_t launch_combine(dev::StepState* st, const double* all, int nranks, int mode, int V,

@@ -429,7 +429,6 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   __shared__ double s_J2_[2][CPB][DIM], s_lift_[2][CPB][DIM];
   __shared__ double s_meas_[2][CPB];  // h_x h_y (h_z) / 2^DIM of the cell
   __shared__ int s_nbc_[2][CPB][2 * DIM];        // local neighbour, or -1 - face cell (ghost)
-  __shared__ long long s_nbg_[2][CPB][2 * DIM];  // global id (positivity reports)
   __shared__ double s_na1_[2][CPB][2 * DIM];
   __shared__ signed char s_nform_[2][CPB][2 * DIM];
   __shared__ double s_red[2 * 2 * (T / 32)];
@@ -447,8 +446,9 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   // descriptor of one group (threads < CPB, one cell each) into buffer b
   auto describe = [&](int b, int t, int cell) {
       s_cell_[b][t] = cell;
-      const int cc = cell < 0 ? 0 : cell;
-      int co[3] = {cc % m.nc[0], (cc / m.nc[0]) % m.nc[1], cc / (m.nc[0] * m.nc[1])};
+      const int cc = cell < 0 ? 0 : cell;               // local cell
+      const int g = m.gid ? m.gid[cc] : cc;             // global cell
+      int co[3] = {g % m.nc[0], (g / m.nc[0]) % m.nc[1], g / (m.nc[0] * m.nc[1])};
       s_coord_[b][t][0] = co[0];
       s_coord_[b][t][1] = co[1];
       s_coord_[b][t][2] = co[2];
@@ -464,26 +464,24 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
         s_lift_[b][t][d] = m.lift[d][co[d]];
       }
 #pragma unroll
-      for (int f = 0; f < 2 * DIM; ++f) {  // face neighbours (periodic / ghost), their rows
-        const int d = f >> 1, side = f & 1;
-        int c3[3] = {co[0], co[1], co[2]};
-        const int nd = m.nc[d];
-        const bool ghost = m.slab && d == DIM - 1 && (side ? c3[d] + 1 == nd : c3[d] == 0);
-        c3[d] = side ? (c3[d] + 1 == nd ? 0 : c3[d] + 1) : (c3[d] == 0 ? nd - 1 : c3[d] - 1);
-        const int nbc = c3[0] + m.nc[0] * (c3[1] + m.nc[1] * c3[2]);
-        const long long layer_cells = DIM == 3 ? static_cast<long long>(m.nc[0]) * m.nc[1] : m.nc[0];
-        if (ghost) {
-          // traces received from the neighbouring slab; no formation here
-          const int fc = DIM == 3 ? co[0] + m.nc[0] * co[1] : co[0];
-          const int gl = side ? (m.layer0 + nd) % m.nlast : (m.layer0 - 1 + m.nlast) % m.nlast;
-          s_nbc_[b][t][f] = -1 - fc;
-          s_nbg_[b][t][f] = fc + layer_cells * gl;
+      for (int f = 0; f < 2 * DIM; ++f) {  // face neighbours (periodic / table / ghost), rows
+        int nbc;
+        if (m.nbr) {
+          nbc = m.nbr[static_cast<size_t>(cc) * 2 * DIM + f];
+        } else {
+          const int d = f >> 1, side = f & 1;
+          int c3[3] = {co[0], co[1], co[2]};
+          const int nd = m.nc[d];
+          c3[d] = side ? (c3[d] + 1 == nd ? 0 : c3[d] + 1) : (c3[d] == 0 ? nd - 1 : c3[d] - 1);
+          nbc = c3[0] + m.nc[0] * (c3[1] + m.nc[1] * c3[2]);
+        }
+        if (nbc < 0) {  // trace formed and sent by the neighbour's owner
+          s_nbc_[b][t][f] = nbc;
           s_na1_[b][t][f] = 0.0;
           s_nform_[b][t][f] = 1;
         } else {
           const int l2 = m.level[nbc];
           s_nbc_[b][t][f] = nbc;
-          s_nbg_[b][t][f] = nbc + a.cell_offset;
           s_na1_[b][t][f] = dt * a.a1[l2];
           s_nform_[b][t][f] = a.formed[l2];
         }
@@ -508,7 +506,6 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     auto& s_J2 = s_J2_[buf];
     auto& s_lift = s_lift_[buf];
     auto& s_nbc = s_nbc_[buf];
-    auto& s_nbg = s_nbg_[buf];
     auto& s_na1 = s_na1_[buf];
     auto& s_nform = s_nform_[buf];
     // the last CPB threads fetch and describe the next group
@@ -555,7 +552,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
         for (int v = 0; v < V; ++v) u[v] = fma(a1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
       }
       own = prim_of<DIM>(ph, u);
-      if (!prim_ok<DIM>(own)) report_bad(st, a.stage, a.ncells, cell + a.cell_offset);
+      if (!prim_ok<DIM>(own)) report_bad(st, a.stage, a.ncells, m.gid ? m.gid[cell] : cell);
       be = own.rho * frcp(own.p);
       lr = log(own.rho);
       lb = log(be);
@@ -581,7 +578,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       if (s_cell[c2] < 0) continue;
       const int nbc = s_nbc[c2][f];
       if (nbc < 0) {
-        const double* g = (side ? m.ghost_hi : m.ghost_lo) + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
+        const double* g = m.ghost + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
 #pragma unroll
         for (int v = 0; v < V; ++v) nbu[k][v] = g[v];
         continue;
@@ -643,7 +640,11 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       o.p = pr[S::P * T + own_q];
       o.E = pr[S::E * T + own_q];
       const Prim<DIM> nbp = prim_of<DIM>(ph, nbu[k]);
-      if (!prim_ok<DIM>(nbp)) report_bad(st, a.stage, a.ncells, s_nbg[c2][f]);
+      if (!prim_ok<DIM>(nbp)) {
+        const int nb = s_nbc[c2][f];  // global id of the neighbour, only on failure
+        report_bad(st, a.stage, a.ncells,
+                   nb < 0 ? m.ghost_gid[-1 - nb] : (m.gid ? m.gid[nb] : nb));
+      }
       double fs[V], fo[V];
       const double J2 = s_J2[c2][d], lift = s_lift[c2][d];
       const int j = side ? N1 - 1 : 0;
@@ -799,26 +800,24 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   }
 }
 
-// Slab decomposition: formed stage traces of the slab's boundary layers,
-// packed for the neighbouring ranks (stepper.cpp:60-72 restricted to the
-// face nodes the neighbour's stage kernel reads).  send_lo: bottom face of
-// local layer 0 (-> the rank below, its ghost_hi); send_hi: top face of the
-// last local layer (-> the rank above, its ghost_lo).  [face cell][FP][V].
+// Domain decomposition: the formed stage traces a neighbouring rank reads
+// (stepper.cpp:60-72 restricted to those face nodes).  send: [entry] =
+// (local cell, face) in peer order; out: [entry][FP][V], points in the
+// (t1 + 4 t2) order of the face (line_base), so the receiver indexes them as
+// its own face points.
 template <int DIM>
 __global__ void __launch_bounds__(256)
-    pack_traces_kernel(StageArgs a, MeshDev m, StepState* st, double* send_lo, double* send_hi) {
+    pack_traces_kernel(StageArgs a, MeshDev m, StepState* st, const int* send, int nsend,
+                       double* out) {
   using G = StageGeo<DIM>;
-  constexpr int V = G::V, NPC = G::NPC, FP = G::FP, D = DIM - 1;
+  constexpr int V = G::V, NPC = G::NPC, FP = G::FP;
   if (st->aborted || st->finished) return;
-  const int layer_cells = DIM == 3 ? m.nc[0] * m.nc[1] : m.nc[0];
-  const int nloc = m.nc[D];
   const double dt = st->dt;
-  const int total = 2 * layer_cells * FP;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
-    const int side = q / (layer_cells * FP), r = q % (layer_cells * FP);
-    const int fc = r / FP, pt = r % FP;
-    const int cell = fc + layer_cells * (side ? nloc - 1 : 0);
-    const int node = line_base<DIM>(D, pt % N1, pt / N1) + (side ? N1 - 1 : 0) * line_stride(D);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nsend * FP; q += gridDim.x * blockDim.x) {
+    const int e = q / FP, pt = q % FP;
+    const int cell = send[2 * e], f = send[2 * e + 1];
+    const int d = f >> 1, side = f & 1;
+    const int node = line_base<DIM>(d, pt % N1, pt / N1) + (side ? N1 - 1 : 0) * line_stride(d);
     const size_t gi = (static_cast<size_t>(cell) * NPC + node) * V;
     double u[V];
     const int lev = m.level[cell];
@@ -833,7 +832,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int v = 0; v < V; ++v) u[v] = fma(b1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
     }
-    double* o = (side ? send_hi : send_lo) + (static_cast<size_t>(fc) * FP + pt) * V;
+    double* o = out + (static_cast<size_t>(e) * FP + pt) * V;
 #pragma unroll
     for (int v = 0; v < V; ++v) o[v] = u[v];
   }

@@ -10,6 +10,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include <memory>
@@ -265,7 +266,7 @@ namespace perrk {
 // multi-rank logic on a single GPU).
 struct Exchange {
   virtual ~Exchange() = default;
-  // send_lo / send_hi of every rank -> ghost_hi of the rank below / ghost_lo above
+  // every rank's packed traces (sendbuf, per peer) -> the peers' ghost slots
   virtual void halo(std::vector<perrk_ctx*>& g) = 0;
   // the same, overlapped: started after the packing on the compute stream,
   // waited for before the boundary cells' stage launch
@@ -321,13 +322,21 @@ struct perrk_ctx {
   std::vector<int> E, eff;
   std::vector<StagePlan> plan;
   uint64_t evals = 0;
-  // element-slab decomposition: this context owns global
-  // layers [layer0, layer0 + nc[last]) of the last axis
-  bool slab = false;
-  int rank = 0, nranks = 1, layer0 = 0, nlast = 1;
+  // domain decomposition: this context owns the cells g of the
+  // global mesh with owner[g] == rank, in increasing global id; face
+  // neighbours owned elsewhere are ghost trace slots filled by the halo
+  bool slab = false;  // decomposed
+  int rank = 0, nranks = 1;
   int ncg[3] = {1, 1, 1};
-  long long ncells_global = 0, layer_cells = 0;
-  double *ghost_lo = nullptr, *ghost_hi = nullptr, *send_lo = nullptr, *send_hi = nullptr;
+  long long ncells_global = 0;
+  std::vector<int> gid;    // local -> global cell
+  std::vector<int> nbr_h;  // [local][2 dim]: local neighbour or -1 - ghost slot
+  int *d_gid = nullptr, *d_nbr = nullptr, *d_send = nullptr;
+  long long* d_ghost_gid = nullptr;
+  double *ghost = nullptr, *sendbuf = nullptr;  // [slot][FP][V], [entry][FP][V]
+  std::vector<int> peers;                       // ascending
+  std::vector<long long> recv_off, send_off;    // per peer, in traces
+  long long nghost = 0, nsend = 0;
   double* red_all = nullptr;  // [nranks][NRED]
   std::shared_ptr<perrk::Group> group;
   // CUDA graph of one run() step (perrk_advance): launch latency matters for
@@ -348,26 +357,23 @@ struct perrk_ctx {
   dev::MeshDev mesh() const {
     dev::MeshDev m{};
     for (int a = 0; a < 3; ++a) {
-      m.nc[a] = nc[a];
+      m.nc[a] = nc[a];  // global
       m.h[a] = dh[a];
       m.jac[a] = djac[a];
       m.lift[a] = dlift[a];
     }
     m.dim = dim;
     m.level = dlevel;
-    const int L = dim - 1;
-    m.slab = slab ? 1 : 0;
-    m.layer0 = layer0;
-    m.nlast = nlast;
-    m.h[L] = dh[L] + layer0;
-    m.jac[L] = djac[L] + layer0;
-    m.lift[L] = dlift[L] + layer0;
-    m.ghost_lo = ghost_lo;
-    m.ghost_hi = ghost_hi;
+    if (slab) {
+      m.gid = d_gid;
+      m.nbr = d_nbr;
+      m.ghost = ghost;
+      m.ghost_gid = d_ghost_gid;
+    }
     return m;
   }
   size_t ndofs_() const { return static_cast<size_t>(ndofs); }
-  size_t trace_doubles() const { return static_cast<size_t>(layer_cells) * (dim == 3 ? 16 : 4) * V; }
+  size_t trace_doubles() const { return static_cast<size_t>(dim == 3 ? 16 : 4) * V; }  // one face trace
   double* sbuf(int parity) { return parity ? Kb : Ka; }  // formed stage states (ping-pong)
 };
 
@@ -457,12 +463,12 @@ void build_plan(perrk_ctx* c) {
       CK(cudaMalloc(&p.dlist, sizeof(int) * list.size()));
       CK(cudaMemcpy(p.dlist, list.data(), sizeof(int) * list.size(), cudaMemcpyHostToDevice));
     }
-    if (c->slab) {  // interior / boundary split of the stage's cells
-      const int nloc = c->nc[c->dim - 1];
+    if (c->slab) {  // interior / boundary (some neighbour is a ghost) split
       std::vector<int> il, bl;
       for (int q : list) {
-        const long long layer = q / c->layer_cells;
-        (layer == 0 || layer == nloc - 1 ? bl : il).push_back(q);
+        bool boundary = false;
+        for (int f = 0; f < 2 * c->dim; ++f) boundary |= c->nbr_h[static_cast<size_t>(q) * 2 * c->dim + f] < 0;
+        (boundary ? bl : il).push_back(q);
       }
       p.in = static_cast<int>(il.size());
       p.bn = static_cast<int>(bl.size());
@@ -516,7 +522,6 @@ void build_plan(perrk_ctx* c) {
     a.want_h = 0;
     a.stage = i;
     a.ncells = c->ncells_global;
-    a.cell_offset = static_cast<long long>(c->layer0) * c->layer_cells;
     a.list = p.dlist;
     a.n = p.n;
     // compulsory traffic per active cell, in node-vectors of 8V bytes: the
@@ -607,7 +612,8 @@ void enqueue_pack(perrk_ctx* c, int i) {
   a.U = c->U;
   a.K1 = c->K1;
   a.Us = i > 0 ? c->sbuf(i & 1) : nullptr;
-  CK(launch_pack_traces(c->dim, a, c->mesh(), c->st, c->send_lo, c->send_hi, c->stream));
+  CK(launch_pack_traces(c->dim, a, c->mesh(), c->st, c->d_send, static_cast<int>(c->nsend),
+                        c->sendbuf, c->stream));
   c->launches += 1;
 }
 
@@ -706,17 +712,16 @@ void alloc_cell_buffers(perrk_ctx* c) {
   CK(cudaMalloc(&c->dnu, sizeof(double) * c->ncells));
   if (c->slab) {
     const size_t tb = sizeof(double) * c->trace_doubles();
-    for (double** p : {&c->ghost_lo, &c->ghost_hi, &c->send_lo, &c->send_hi}) {
-      CK(cudaMalloc(p, tb));
-      CK(cudaMemsetAsync(*p, 0, tb, c->stream));
-    }
+    CK(cudaMalloc(&c->ghost, tb * std::max<long long>(c->nghost, 1)));
+    CK(cudaMalloc(&c->sendbuf, tb * std::max<long long>(c->nsend, 1)));
+    CK(cudaMemsetAsync(c->ghost, 0, tb * std::max<long long>(c->nghost, 1), c->stream));
     CK(cudaMalloc(&c->red_all, sizeof(double) * dev::NRED * c->nranks));
   }
 }
 
 void free_cell_buffers(perrk_ctx* c) {
-  for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK, &c->dnu, &c->G, &c->ghost_lo,
-                     &c->ghost_hi, &c->send_lo, &c->send_hi, &c->red_all}) {
+  for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK, &c->dnu, &c->G,
+                     &c->ghost, &c->sendbuf, &c->red_all}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -754,13 +759,14 @@ struct NcclExchange : Exchange {
     CK(cudaEventCreateWithFlags(&arrived, cudaEventDisableTiming));
   }
   void sendrecv(perrk_ctx* c, cudaStream_t s) {
-    const int up = (c->rank + 1) % c->nranks, dn = (c->rank - 1 + c->nranks) % c->nranks;
-    const size_t n = c->trace_doubles();
+    const size_t tu = c->trace_doubles();
     NK(ncclGroupStart());
-    NK(ncclSend(c->send_hi, n, ncclDouble, up, comm, s));
-    NK(ncclRecv(c->ghost_lo, n, ncclDouble, dn, comm, s));
-    NK(ncclSend(c->send_lo, n, ncclDouble, dn, comm, s));
-    NK(ncclRecv(c->ghost_hi, n, ncclDouble, up, comm, s));
+    for (size_t k = 0; k < c->peers.size(); ++k) {
+      const size_t ns = c->send_off[k + 1] - c->send_off[k];
+      const size_t nr = c->recv_off[k + 1] - c->recv_off[k];
+      if (ns) NK(ncclSend(c->sendbuf + c->send_off[k] * tu, ns * tu, ncclDouble, c->peers[k], comm, s));
+      if (nr) NK(ncclRecv(c->ghost + c->recv_off[k] * tu, nr * tu, ncclDouble, c->peers[k], comm, s));
+    }
     NK(ncclGroupEnd());
   }
   void halo_begin(std::vector<perrk_ctx*>& g) override {
@@ -786,14 +792,17 @@ struct NcclExchange : Exchange {
 // device-to-device copies, stream-ordered (no kernel waits on another).
 struct LoopbackExchange : Exchange {
   void halo(std::vector<perrk_ctx*>& g) override {
-    const int P = static_cast<int>(g.size());
-    for (int r = 0; r < P; ++r) {
-      perrk_ctx* c = g[r];
-      const size_t bytes = sizeof(double) * c->trace_doubles();
-      CK(cudaMemcpyAsync(g[(r + 1) % P]->ghost_lo, c->send_hi, bytes, cudaMemcpyDeviceToDevice,
-                         c->stream));
-      CK(cudaMemcpyAsync(g[(r - 1 + P) % P]->ghost_hi, c->send_lo, bytes,
-                         cudaMemcpyDeviceToDevice, c->stream));
+    for (perrk_ctx* c : g) {
+      const size_t tb = sizeof(double) * c->trace_doubles();
+      for (size_t k = 0; k < c->peers.size(); ++k) {
+        perrk_ctx* p = g[c->peers[k]];
+        const size_t kk = std::lower_bound(p->peers.begin(), p->peers.end(), c->rank) - p->peers.begin();
+        const size_t n = c->send_off[k + 1] - c->send_off[k];
+        if (n)
+          CK(cudaMemcpyAsync(p->ghost + p->recv_off[kk] * c->trace_doubles(),
+                             c->sendbuf + c->send_off[k] * c->trace_doubles(), n * tb,
+                             cudaMemcpyDeviceToDevice, c->stream));
+      }
     }
   }
   void gather(std::vector<perrk_ctx*>& g) override {
@@ -805,34 +814,141 @@ struct LoopbackExchange : Exchange {
   }
 };
 
-// Restrict a context to its slab of last-axis layers [cuts[rank], cuts[rank+1]).
-void make_slab(perrk_ctx* c, int rank, int nranks, const int* cuts) {
-  REQUIRE(!c->slab, "context is already decomposed");
-  if (c->physics == 1)
-    throw Fail(PERRK_EUNSUP, "the slab decomposition runs the Euler configurations");
-  REQUIRE(!c->has_family, "decompose before perrk_set_family");
-  REQUIRE(nranks >= 2 && rank >= 0 && rank < nranks, "bad rank / rank count");
-  const int L = c->dim - 1, nl = c->nlast;
-  REQUIRE(nranks <= nl, "more ranks than cell layers along the last axis");
-  int b = rank * nl / nranks, e = (rank + 1) * nl / nranks;
-  if (cuts) {
-    REQUIRE(cuts[0] == 0 && cuts[nranks] == nl, "layer cuts must span 0..n_last");
-    for (int q = 0; q < nranks; ++q) REQUIRE(cuts[q + 1] > cuts[q], "layer cuts must increase");
-    b = cuts[rank];
-    e = cuts[rank + 1];
+// Periodic face neighbour of global cell g across face f (2 d + side).
+long long face_neighbour(int dim, const int* n, long long g, int f) {
+  long long co[3] = {g % n[0], (g / n[0]) % n[1], g / (static_cast<long long>(n[0]) * n[1])};
+  const int d = f >> 1, side = f & 1;
+  co[d] = side ? (co[d] + 1 == n[d] ? 0 : co[d] + 1) : (co[d] == 0 ? n[d] - 1 : co[d] - 1);
+  (void)dim;
+  return co[0] + n[0] * (co[1] + static_cast<long long>(n[1]) * co[2]);
+}
+
+// Halo plan of one rank for an ownership map: the local cells (ascending
+// global id), per local cell and face the local neighbour or a ghost slot, and
+// per peer (ascending) the ghost slots it fills and the (local cell, face)
+// traces it receives from us.  Both sides order a peer's entries by the
+// sender's (global cell, face), so slot k of the receiver is entry k of the
+// sender.
+struct HaloPlan {
+  std::vector<int> gid, nbr, peers, send;  // send: (local cell, face) pairs
+  std::vector<long long> ghost_gid, recv_off, send_off;
+};
+
+HaloPlan halo_plan(int dim, const int* n, const int* owner, int rank) {
+  HaloPlan h;
+  const long long NG = static_cast<long long>(n[0]) * n[1] * (dim == 3 ? n[2] : 1);
+  std::vector<int> loc(NG, -1);
+  for (long long g = 0; g < NG; ++g)
+    if (owner[g] == rank) {
+      loc[g] = static_cast<int>(h.gid.size());
+      h.gid.push_back(static_cast<int>(g));
+    }
+  REQUIRE(!h.gid.empty(), "a rank owns no cells");
+  const int nf = 2 * dim;
+  struct Key {
+    int peer;
+    long long g;  // sender's cell
+    int f;        // sender's face
+    int local, lf;  // our (receiver) cell and face, or our (sender) cell and face
+  };
+  std::vector<Key> recv, send;
+  h.nbr.assign(h.gid.size() * nf, 0);
+  for (size_t c = 0; c < h.gid.size(); ++c)
+    for (int f = 0; f < nf; ++f) {
+      const long long ng = face_neighbour(dim, n, h.gid[c], f);
+      if (owner[ng] == rank) {
+        h.nbr[c * nf + f] = loc[ng];
+      } else {
+        recv.push_back({owner[ng], ng, f ^ 1, static_cast<int>(c), f});
+        send.push_back({owner[ng], h.gid[c], f, static_cast<int>(c), f});
+      }
+    }
+  auto by_key = [](const Key& x, const Key& y) {
+    return x.peer != y.peer ? x.peer < y.peer : (x.g != y.g ? x.g < y.g : x.f < y.f);
+  };
+  std::sort(recv.begin(), recv.end(), by_key);
+  std::sort(send.begin(), send.end(), by_key);
+  for (size_t k = 0; k < recv.size(); ++k) {
+    h.nbr[static_cast<size_t>(recv[k].local) * nf + recv[k].lf] = -1 - static_cast<int>(k);
+    h.ghost_gid.push_back(recv[k].g);
+    if (h.peers.empty() || h.peers.back() != recv[k].peer) {
+      h.peers.push_back(recv[k].peer);
+      h.recv_off.push_back(static_cast<long long>(k));
+    }
   }
+  h.recv_off.push_back(static_cast<long long>(recv.size()));
+  size_t k = 0;
+  for (int p : h.peers) {
+    h.send_off.push_back(static_cast<long long>(k));
+    while (k < send.size() && send[k].peer == p) {
+      h.send.push_back(send[k].local);
+      h.send.push_back(send[k].lf);
+      ++k;
+    }
+  }
+  h.send_off.push_back(static_cast<long long>(k));
+  REQUIRE(k == send.size(), "asymmetric halo");
+  return h;
+}
+
+// Restrict a context to the cells it owns (owner: global cell -> rank; NULL:
+// uniform slabs of last-axis layers).
+void make_partition(perrk_ctx* c, int rank, int nranks, const int* owner) {
+  REQUIRE(!c->slab, "context is already decomposed");
+  REQUIRE(!c->has_family, "decompose before perrk_set_family");
+  if (c->physics == 1)
+    throw Fail(PERRK_EUNSUP, "the multi-GPU decomposition runs the Euler configurations");
+  REQUIRE(nranks >= 2 && rank >= 0 && rank < nranks, "bad rank / rank count");
+  const long long NG = c->ncells_global;
+  std::vector<int> own(NG);
+  if (owner) {
+    for (long long g = 0; g < NG; ++g) {
+      REQUIRE(owner[g] >= 0 && owner[g] < nranks, "owner out of range");
+      own[g] = owner[g];
+    }
+  } else {
+    const int L = c->dim - 1, nl = c->nc[L];
+    const long long lc = NG / nl;
+    REQUIRE(nranks <= nl, "more ranks than cell layers along the last axis");
+    for (long long g = 0; g < NG; ++g) {
+      const int layer = static_cast<int>(g / lc);
+      int r = 0;
+      while (r + 1 < nranks && layer >= (r + 1) * nl / nranks) ++r;
+      own[g] = r;
+    }
+  }
+  HaloPlan h = halo_plan(c->dim, c->nc, own.data(), rank);
   set_device(c);
   CK(cudaStreamSynchronize(c->stream));
   free_cell_buffers(c);
   c->slab = true;
   c->rank = rank;
   c->nranks = nranks;
-  c->layer0 = b;
-  c->nc[L] = e - b;
-  c->ncells = c->layer_cells * (e - b);
+  c->gid = h.gid;
+  c->nbr_h = h.nbr;
+  c->peers = h.peers;
+  c->recv_off = h.recv_off;
+  c->send_off = h.send_off;
+  c->nghost = static_cast<long long>(h.ghost_gid.size());
+  c->nsend = static_cast<long long>(h.send.size() / 2);
+  c->ncells = static_cast<long long>(h.gid.size());
   c->nnodes = c->ncells * c->npc;
   c->ndofs = c->nnodes * c->V;
   alloc_cell_buffers(c);
+  for (int** p : {&c->d_gid, &c->d_nbr, &c->d_send})
+    if (*p) cudaFree(*p);
+  if (c->d_ghost_gid) cudaFree(c->d_ghost_gid);
+  CK(cudaMalloc(&c->d_gid, sizeof(int) * h.gid.size()));
+  CK(cudaMalloc(&c->d_nbr, sizeof(int) * h.nbr.size()));
+  CK(cudaMalloc(&c->d_send, sizeof(int) * std::max<size_t>(h.send.size(), 1)));
+  CK(cudaMalloc(&c->d_ghost_gid, sizeof(long long) * std::max<size_t>(h.ghost_gid.size(), 1)));
+  CK(cudaMemcpy(c->d_gid, h.gid.data(), sizeof(int) * h.gid.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_nbr, h.nbr.data(), sizeof(int) * h.nbr.size(), cudaMemcpyHostToDevice));
+  if (!h.send.empty())
+    CK(cudaMemcpy(c->d_send, h.send.data(), sizeof(int) * h.send.size(), cudaMemcpyHostToDevice));
+  if (!h.ghost_gid.empty())
+    CK(cudaMemcpy(c->d_ghost_gid, h.ghost_gid.data(), sizeof(long long) * h.ghost_gid.size(),
+                  cudaMemcpyHostToDevice));
   CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -957,8 +1073,6 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     c->ndofs = c->nnodes * c->V;
     for (int a = 0; a < 3; ++a) c->ncg[a] = c->nc[a];
     c->ncells_global = c->ncells;
-    c->nlast = c->nc[c->dim - 1];
-    c->layer_cells = c->ncells / c->nlast;
     set_device(c);
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     int sms = 148;
@@ -1014,6 +1128,9 @@ int perrk_destroy(perrk_ctx* c) {
     for (int* q : {p.dlist, p.glist, p.ilist, p.blist})
       if (q) cudaFree(q);
   if (c->st) cudaFree(c->st);
+  for (int* p : {c->d_gid, c->d_nbr, c->d_send})
+    if (p) cudaFree(p);
+  if (c->d_ghost_gid) cudaFree(c->d_ghost_gid);
   if (c->counter) cudaFree(c->counter);
   if (c->dint) cudaFree(c->dint);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -1049,12 +1166,11 @@ int perrk_node_geometry(const perrk_ctx* c, double* x, double* y, double* z, dou
     REQUIRE(c, "null context");
     const auto& B = c->basis;
     for (long long cell = 0; cell < c->ncells; ++cell) {
-      const int ci = static_cast<int>(cell % c->nc[0]);
-      const int cj = static_cast<int>((cell / c->nc[0]) % c->nc[1]);
-      int ck = static_cast<int>(cell / (static_cast<long long>(c->nc[0]) * c->nc[1]));
-      int cj2 = cj;
-      if (c->dim == 3) ck += c->layer0;
-      else cj2 += c->layer0;
+      const long long g = c->slab ? c->gid[cell] : cell;
+      const int ci = static_cast<int>(g % c->nc[0]);
+      const int cj = static_cast<int>((g / c->nc[0]) % c->nc[1]);
+      const int ck = static_cast<int>(g / (static_cast<long long>(c->nc[0]) * c->nc[1]));
+      const int cj2 = cj;
       for (int l = 0; l < c->npc; ++l) {
         const int ix = l % 4, iy = (l / 4) % 4, iz = l / 16;
         const long long n = cell * c->npc + l;
@@ -1081,11 +1197,11 @@ int perrk_set_family(perrk_ctx* c, const perrk_family_desc* f, const int* eff) {
     c->A.assign(f->A, f->A + static_cast<size_t>(f->R) * f->S * f->S);
     c->b.assign(f->b, f->b + f->S);
     c->c.assign(f->c, f->c + f->S);
-    // the level map is global; the context keeps its slab's part
-    const long long off = static_cast<long long>(c->layer0) * c->layer_cells;
+    // the level map is global; the context keeps its own cells' part
     for (long long i = 0; i < c->ncells_global; ++i)
       REQUIRE(eff[i] >= 1 && eff[i] <= f->R, "level out of range");
-    c->eff.assign(eff + off, eff + off + c->ncells);
+    c->eff.resize(c->ncells);
+    for (long long i = 0; i < c->ncells; ++i) c->eff[i] = eff[c->slab ? c->gid[i] : i];
     std::vector<int8_t> lv(c->ncells);
     for (long long i = 0; i < c->ncells; ++i) lv[i] = static_cast<int8_t>(c->eff[i]);
     CK(cudaMemcpy(c->dlevel, lv.data(), c->ncells, cudaMemcpyHostToDevice));
@@ -1154,7 +1270,6 @@ int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const
       a.n = static_cast<int>(list.size());
       a.write_k = 1;
       a.ncells = c->ncells_global;
-      a.cell_offset = 0;
       a.ndofs = c->ndofs;
       int* gl_dev = nullptr;
       if (c->physics == 1) {  // BR1 viscous fluxes on the cells and their neighbours
@@ -1695,11 +1810,11 @@ int perrk_nccl_id(void* out) {
   });
 }
 
-int perrk_comm_init(perrk_ctx* c, const void* nccl_id, int rank, int nranks, const int* cuts) {
+int perrk_comm_init(perrk_ctx* c, const void* nccl_id, int rank, int nranks, const int* owner) {
   return guarded([&] {
     REQUIRE(c && nccl_id, "null argument");
     if (nranks == 1) return;  // the whole periodic mesh: nothing to exchange
-    make_slab(c, rank, nranks, cuts);
+    make_partition(c, rank, nranks, owner);
     auto ex = std::make_unique<NcclExchange>();
     ex->setup();
     ncclUniqueId id;
@@ -1710,7 +1825,7 @@ int perrk_comm_init(perrk_ctx* c, const void* nccl_id, int rank, int nranks, con
   });
 }
 
-int perrk_loopback_group(perrk_ctx** ctxs, int n, const int* cuts) {
+int perrk_loopback_group(perrk_ctx** ctxs, int n, const int* owner) {
   return guarded([&] {
     REQUIRE(ctxs && n >= 2, "need at least two contexts");
     for (int r = 0; r < n; ++r) {
@@ -1724,7 +1839,7 @@ int perrk_loopback_group(perrk_ctx** ctxs, int n, const int* cuts) {
     CK(cudaStreamCreateWithFlags(&g->shared_stream, cudaStreamNonBlocking));
     for (int r = 0; r < n; ++r) {
       perrk_ctx* c = ctxs[r];
-      make_slab(c, r, n, cuts);
+      make_partition(c, r, n, owner);
       // one stream, owned by the group (it outlives every member), orders
       // every member's work
       CK(cudaStreamSynchronize(c->stream));
@@ -1737,38 +1852,110 @@ int perrk_loopback_group(perrk_ctx** ctxs, int n, const int* cuts) {
   });
 }
 
-int perrk_slab_range(const perrk_ctx* c, int* b, int* e) {
+int perrk_local_cells(const perrk_ctx* c, int* gids, int64_t* n) {
   return guarded([&] {
-    REQUIRE(c && b && e, "null argument");
-    *b = c->layer0;
-    *e = c->layer0 + c->nc[c->dim - 1];
+    REQUIRE(c && n, "null argument");
+    *n = c->ncells;
+    if (gids)
+      for (long long i = 0; i < c->ncells; ++i) gids[i] = c->slab ? c->gid[i] : static_cast<int>(i);
   });
 }
 
-int perrk_slab_cuts(int nlast, const double* layer_work, int nranks, int* cuts) {
+namespace {
+long long global_cells(int dim, const int* n) {
+  REQUIRE((dim == 2 || dim == 3) && n && n[0] >= 1 && n[1] >= 1 && (dim == 2 || n[2] >= 1),
+          "bad mesh shape");
+  return static_cast<long long>(n[0]) * n[1] * (dim == 3 ? n[2] : 1);
+}
+}  // namespace
+
+int perrk_partition_slabs(int dim, const int* n, const double* cell_work, int nranks, int* owner) {
   return guarded([&] {
-    REQUIRE(nlast >= 1 && nranks >= 1 && nranks <= nlast && cuts, "bad arguments");
-    // contiguous layers, cut where the running work crosses r / nranks of the
-    // total (uniform layers when layer_work is NULL), every slab >= 1 layer
-    std::vector<double> pre(nlast + 1, 0.0);
-    for (int l = 0; l < nlast; ++l) pre[l + 1] = pre[l] + (layer_work ? layer_work[l] : 1.0);
-    cuts[0] = 0;
+    const long long NG = global_cells(dim, n);
+    const int nl = n[dim - 1];
+    const long long lc = NG / nl;
+    REQUIRE(owner && nranks >= 1 && nranks <= nl, "bad arguments");
+    // contiguous last-axis layers, cut where the running work crosses
+    // r / nranks of the total, every rank >= 1 layer
+    std::vector<double> pre(nl + 1, 0.0);
+    for (int l = 0; l < nl; ++l) {
+      double w = 0.0;
+      for (long long i = 0; i < lc; ++i) w += cell_work ? cell_work[l * lc + i] : 1.0;
+      pre[l + 1] = pre[l] + w;
+    }
+    std::vector<int> cuts(nranks + 1, 0);
     for (int r = 1; r < nranks; ++r) {
-      const double target = pre[nlast] * r / nranks;
+      const double target = pre[nl] * r / nranks;
       int l = cuts[r - 1] + 1;
-      while (l < nlast - (nranks - r) && pre[l] + 0.5 * (pre[l + 1] - pre[l]) < target) ++l;
+      while (l < nl - (nranks - r) && pre[l] + 0.5 * (pre[l + 1] - pre[l]) < target) ++l;
       cuts[r] = l;
     }
-    cuts[nranks] = nlast;
+    cuts[nranks] = nl;
+    for (int r = 0; r < nranks; ++r)
+      for (long long g = cuts[r] * lc; g < cuts[r + 1] * lc; ++g) owner[g] = r;
   });
 }
 
-int perrk_slab_trace_nodes(int dim, int side, int* nodes) {
+int perrk_partition_levels(int dim, const int* n, const int* level, int nlevels, int nranks,
+                           int* owner) {
   return guarded([&] {
-    REQUIRE((dim == 2 || dim == 3) && (side == 0 || side == 1) && nodes, "bad arguments");
-    // face of the last axis, points in (t1 + 4 t2) order (pack_traces_kernel)
-    const int fp = dim == 3 ? 16 : 4, stride = dim == 3 ? 16 : 4;
-    for (int pt = 0; pt < fp; ++pt) nodes[pt] = pt + (side ? 3 * stride : 0);
+    const long long NG = global_cells(dim, n);
+    REQUIRE(level && owner && nlevels >= 1 && nranks >= 1, "bad arguments");
+    // every level's cells, in global (last-axis-major) order, cut into nranks
+    // contiguous runs of equal size: each rank holds 1/nranks of every level,
+    // so every stage's active set is balanced, and a run is a band of layers
+    std::vector<long long> cnt(nlevels + 1, 0), seen(nlevels + 1, 0);
+    for (long long g = 0; g < NG; ++g) {
+      REQUIRE(level[g] >= 1 && level[g] <= nlevels, "level out of range");
+      ++cnt[level[g]];
+    }
+    for (long long g = 0; g < NG; ++g) {
+      const int l = level[g];
+      owner[g] = static_cast<int>(seen[l]++ * nranks / cnt[l]);
+    }
+    std::vector<char> has(nranks, 0);
+    for (long long g = 0; g < NG; ++g) has[owner[g]] = 1;
+    for (int r = 0; r < nranks; ++r) REQUIRE(has[r], "more ranks than cells");
+  });
+}
+
+int perrk_halo_plan(int dim, const int* n, const int* owner, int rank, int64_t* counts, int* gid,
+                    int* nbr, int64_t* ghost_gid, int* peers, int64_t* recv_off,
+                    int64_t* send_off, int* send) {
+  return guarded([&] {
+    const long long NG = global_cells(dim, n);
+    REQUIRE(owner && counts, "null argument");
+    for (long long g = 0; g < NG; ++g) REQUIRE(owner[g] >= 0, "negative owner");
+    HaloPlan h = halo_plan(dim, n, owner, rank);
+    counts[0] = static_cast<int64_t>(h.gid.size());
+    counts[1] = static_cast<int64_t>(h.ghost_gid.size());
+    counts[2] = static_cast<int64_t>(h.send.size() / 2);
+    counts[3] = static_cast<int64_t>(h.peers.size());
+    auto put = [](auto* dst, const auto& src) {
+      if (dst) std::copy(src.begin(), src.end(), dst);
+    };
+    put(gid, h.gid);
+    put(nbr, h.nbr);
+    put(ghost_gid, h.ghost_gid);
+    put(peers, h.peers);
+    put(recv_off, h.recv_off);
+    put(send_off, h.send_off);
+    put(send, h.send);
+  });
+}
+
+int perrk_face_nodes(int dim, int face, int* nodes) {
+  return guarded([&] {
+    REQUIRE((dim == 2 || dim == 3) && face >= 0 && face < 2 * dim && nodes, "bad arguments");
+    // trace point pt of face f (pack_traces_kernel / the stage kernel's ghost read)
+    const int d = face >> 1, side = face & 1, fp = dim == 3 ? 16 : 4;
+    const int stride = d == 0 ? 1 : (d == 1 ? 4 : 16);
+    for (int pt = 0; pt < fp; ++pt) {
+      const int t1 = pt % 4, t2 = pt / 4;
+      const int base = dim == 2 ? (d == 0 ? 4 * t1 : t1)
+                                : (d == 0 ? 4 * t1 + 16 * t2 : (d == 1 ? t1 + 16 * t2 : t1 + 4 * t2));
+      nodes[pt] = base + (side ? 3 : 0) * stride;
+    }
   });
 }
 

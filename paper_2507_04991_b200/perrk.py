@@ -310,7 +310,7 @@ class Semidiscretization:
     def sync(self):
         check(lib().perrk_sync(self._h))
 
-    # element-slab decomposition (perrk_comm_init, include/perrk_b200.h)
+    # element partition (perrk_comm_init, include/perrk_b200.h)
     def _refresh_sizes(self):
         dofs, nodes, cells = C.c_int64(), C.c_int64(), C.c_int64()
         v, npc = C.c_int(), C.c_int()
@@ -319,20 +319,26 @@ class Semidiscretization:
         self._n = (dofs.value, nodes.value, cells.value, v.value, npc.value)
         self._geom = None
         self._family_key = None
+        self._cells = None
 
-    def comm_init(self, nccl_id: bytes, rank: int, nranks: int, cuts=None):
-        """Own the slab of last-axis layers of `rank` (one process per GPU)."""
-        cu = None if cuts is None else np.ascontiguousarray(cuts, dtype=np.int32)
+    def comm_init(self, nccl_id: bytes, rank: int, nranks: int, owner=None):
+        """Own the cells `owner` (global cell -> rank; None: uniform last-axis
+        slabs) gives `rank` (one process per GPU)."""
+        ow = None if owner is None else np.ascontiguousarray(owner, dtype=np.int32)
         buf = C.create_string_buffer(bytes(nccl_id), 128)
         check(lib().perrk_comm_init(self._h, buf, int(rank), int(nranks),
-                                    None if cu is None else _ip(cu)))
-        self._cuts_keep = cu
+                                    None if ow is None else _ip(ow)))
         self._refresh_sizes()
 
-    def slab_range(self):
-        b, e = C.c_int(), C.c_int()
-        check(lib().perrk_slab_range(self._h, C.byref(b), C.byref(e)))
-        return b.value, e.value
+    def local_cells(self):
+        """Global ids of this context's cells (ascending; the local cell order)."""
+        if getattr(self, "_cells", None) is None:
+            n = C.c_int64()
+            check(lib().perrk_local_cells(self._h, None, C.byref(n)))
+            out = np.zeros(n.value, dtype=np.int32)
+            check(lib().perrk_local_cells(self._h, _ip(out), C.byref(n)))
+            self._cells = out
+        return self._cells
 
     def global_num_cells(self):
         return self.spec.mesh.num_cells()
@@ -388,41 +394,75 @@ def nccl_id() -> bytes:
     return buf.raw
 
 
-def slab_cuts(n_last, nranks, layer_work=None):
-    """Contiguous layer cuts [0, ..., n_last] balancing layer_work."""
-    cuts = np.zeros(nranks + 1, dtype=np.int32)
-    w = None if layer_work is None else _f64(layer_work)
-    check(lib().perrk_slab_cuts(int(n_last), None if w is None else _dp(w), int(nranks), _ip(cuts)))
-    return cuts
+def _shape3(mesh):
+    sh = list(mesh.shape()) + [1]
+    return np.ascontiguousarray(sh[:3], dtype=np.int32), len(mesh.shape())
 
 
-def slab_trace_nodes(dim, side):
-    """Cell-local node indices of the last-axis face traces, exchange order."""
+def cell_work(pmap, family, npc):
+    """DOF-stage work per cell of one step (active stages x nodes)."""
+    E = np.array([len(family.active_sets[family.member_index_for_level(l)])
+                  for l in range(1, family.R + 1)], dtype=np.float64)
+    return E[np.asarray(pmap.effective_level) - 1] * npc
+
+
+def partition_slabs(mesh, nranks, work=None):
+    """Ownership map: contiguous last-axis layers balanced by per-cell work."""
+    n, dim = _shape3(mesh)
+    owner = np.zeros(mesh.num_cells(), dtype=np.int32)
+    w = None if work is None else _f64(work)
+    check(lib().perrk_partition_slabs(dim, _ip(n), None if w is None else _dp(w), int(nranks),
+                                      _ip(owner)))
+    return owner
+
+
+def partition_levels(mesh, pmap, nranks):
+    """Ownership map: 1/nranks of every level per rank (balanced stages)."""
+    n, dim = _shape3(mesh)
+    owner = np.zeros(mesh.num_cells(), dtype=np.int32)
+    lv = np.ascontiguousarray(pmap.effective_level, dtype=np.int32)
+    check(lib().perrk_partition_levels(dim, _ip(n), _ip(lv), int(pmap.R), int(nranks),
+                                       _ip(owner)))
+    return owner
+
+
+def halo_plan(mesh, owner, rank):
+    """The halo plan perrk_comm_init builds for `rank` (dict of arrays)."""
+    n, dim = _shape3(mesh)
+    ow = np.ascontiguousarray(owner, dtype=np.int32)
+    cnt = np.zeros(4, dtype=np.int64)
+    i64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))
+    check(lib().perrk_halo_plan(dim, _ip(n), _ip(ow), int(rank), i64(cnt), None, None, None, None,
+                                None, None, None))
+    nl, ng, ns, npe = (int(x) for x in cnt)
+    h = dict(gid=np.zeros(nl, np.int32), nbr=np.zeros(nl * 2 * dim, np.int32),
+             ghost_gid=np.zeros(max(ng, 1), np.int64), peers=np.zeros(max(npe, 1), np.int32),
+             recv_off=np.zeros(npe + 1, np.int64), send_off=np.zeros(npe + 1, np.int64),
+             send=np.zeros(max(2 * ns, 1), np.int32))
+    check(lib().perrk_halo_plan(dim, _ip(n), _ip(ow), int(rank), i64(cnt), _ip(h["gid"]),
+                                _ip(h["nbr"]), i64(h["ghost_gid"]), _ip(h["peers"]),
+                                i64(h["recv_off"]), i64(h["send_off"]), _ip(h["send"])))
+    h["ghost_gid"], h["peers"], h["send"] = h["ghost_gid"][:ng], h["peers"][:npe], h["send"][:2 * ns]
+    h["send"] = h["send"].reshape(-1, 2)
+    return h
+
+
+def face_nodes(dim, face):
+    """Cell-local node indices of face `face` (2 d + side), exchange point order."""
     out = np.zeros(16 if dim == 3 else 4, dtype=np.int32)
-    check(lib().perrk_slab_trace_nodes(int(dim), int(side), _ip(out)))
+    check(lib().perrk_face_nodes(int(dim), int(face), _ip(out)))
     return out
 
 
-def layer_work(mesh, pmap, family, npc):
-    """DOF-stage work per last-axis layer (cells x active stages x nodes)."""
-    shape = mesh.shape()
-    lv = np.asarray(pmap.effective_level).reshape(tuple(reversed(shape)))  # [z, y, x] / [y, x]
-    E = np.array([len(family.active_sets[family.member_index_for_level(l)])
-                  for l in range(1, family.R + 1)], dtype=np.float64)
-    per_cell = E[lv - 1] * npc
-    return per_cell.reshape(per_cell.shape[0], -1).sum(axis=1)
-
-
-def slab_pmap(semi, pmap):
+def local_pmap(semi, pmap):
     """The rank's part of a global partition map (for work accounting)."""
-    b, e = semi.slab_range()
-    lc = semi.global_num_cells() // semi.spec.mesh.shape()[-1]
-    eff = np.asarray(pmap.effective_level)[b * lc:e * lc]
-    raw = np.asarray(pmap.raw_level)[b * lc:e * lc]
+    g = semi.local_cells()
+    eff = np.asarray(pmap.effective_level)[g]
+    raw = np.asarray(pmap.raw_level)[g]
     return PartitionMap(pmap.R, raw.copy(), eff.copy())
 
 
-def init_slabs(semi, rank, nranks, cuts=None):
+def init_partition(semi, rank, nranks, owner=None):
     """Decompose `semi` over torch.distributed ranks (NCCL id broadcast from
     rank 0 over the default process group)."""
     import torch
@@ -433,16 +473,16 @@ def init_slabs(semi, rank, nranks, cuts=None):
     if dist.get_backend() == "nccl":
         ident = ident.cuda()
     dist.broadcast(ident, 0)
-    semi.comm_init(bytes(ident.cpu().numpy().tobytes()), rank, nranks, cuts)
+    semi.comm_init(bytes(ident.cpu().numpy().tobytes()), rank, nranks, owner)
 
 
-def loopback_group(semis, cuts=None):
-    """Ranks 0..n-1 of a slab decomposition as contexts on one device (test
-    harness of the multi-rank logic; stepping any member steps all)."""
+def loopback_group(semis, owner=None):
+    """Ranks 0..n-1 of a partition as contexts on one device (test harness of
+    the multi-rank logic; stepping any member steps all)."""
     arr = (C.c_void_p * len(semis))(*[s._h.value if isinstance(s._h, C.c_void_p) else s._h
                                        for s in semis])
-    cu = None if cuts is None else np.ascontiguousarray(cuts, dtype=np.int32)
-    check(lib().perrk_loopback_group(arr, len(semis), None if cu is None else _ip(cu)))
+    ow = None if owner is None else np.ascontiguousarray(owner, dtype=np.int32)
+    check(lib().perrk_loopback_group(arr, len(semis), None if ow is None else _ip(ow)))
     for s in semis:
         s._refresh_sizes()
         s._group = semis

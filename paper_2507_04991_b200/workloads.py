@@ -311,17 +311,19 @@ def sample_config(cfg: Config) -> Config:
 class ConfigRun:
     """A configuration instantiated on one device: semidiscretization,
     partition map, initial state.  With world > 1 the context owns the
-    rank's element slab (perrk_comm_init)."""
+    rank's cells (perrk_comm_init) of a per-level balanced partition
+    ("levels", the default: every stage balanced) or of work-balanced
+    last-axis slabs ("slabs": least halo)."""
 
-    def __init__(self, cfg: Config, device=0, rank=0, world=1, comm=None):
+    def __init__(self, cfg: Config, device=0, rank=0, world=1, comm=None, partition="levels"):
         self.cfg = cfg
         self.rank, self.world = rank, world
+        self.partition = partition
         self.semi = P.Semidiscretization(cfg.spec(device))
         self.pmap = cfg.partition_map()
         if world > 1:
-            work = P.layer_work(cfg.mesh, self.pmap, cfg.family, cfg.nodes_per_cell())
-            self.cuts = P.slab_cuts(len(work), world, work)
-            P.init_slabs(self.semi, rank, world, self.cuts)
+            self.owner = make_owner(cfg, self.pmap, world, partition)
+            P.init_partition(self.semi, rank, world, self.owner)
 
     def initial_state(self):
         s = self.semi
@@ -333,11 +335,26 @@ class ConfigRun:
         return dof_stage_updates_per_step(self.cfg.family, self.local_pmap(),
                                           self.cfg.nodes_per_cell())
 
+    def halo_traces(self):
+        """Face traces all ranks exchange per stage."""
+        return int(sum(P.halo_plan(self.cfg.mesh, self.owner, r)["send"].shape[0]
+                       for r in range(self.world)))
+
     def local_pmap(self):
-        return self.pmap if self.world == 1 else P.slab_pmap(self.semi, self.pmap)
+        return self.pmap if self.world == 1 else P.local_pmap(self.semi, self.pmap)
 
     def total_nodes(self):
         return self.cfg.mesh.num_cells() * self.cfg.nodes_per_cell()
+
+
+def make_owner(cfg: Config, pmap, world, partition="levels"):
+    """Global ownership map (cell -> rank) of a decomposition over `world` ranks."""
+    if partition == "levels":
+        return P.partition_levels(cfg.mesh, pmap, world)
+    if partition == "slabs":
+        return P.partition_slabs(cfg.mesh, world,
+                                 P.cell_work(pmap, cfg.family, cfg.nodes_per_cell()))
+    raise ValueError(f"unknown partition {partition!r}")
 
 
 def initial_state_for(cfg: Config, semi_or_coords):

@@ -1,13 +1,15 @@
-"""GPU: the element-slab decomposition's device path on ONE GPU.
+"""GPU: the element partition's device path on ONE GPU.
 
-perrk_loopback_group makes n contexts on one device ranks 0..n-1 of a slab
-decomposition sharing one stream: per stage every rank packs its boundary
+perrk_loopback_group makes n contexts on one device ranks 0..n-1 of a
+partition (uniform slabs, per-level balanced, or scattered cells) sharing one
+stream: per stage every rank packs its boundary
 traces, the halo and the reduction gathers are stream-ordered device copies
 (the data movement NcclExchange does with ncclSend/Recv and ncclAllGather),
 and every kernel of the multi-rank path runs (ghost traces in the stage
 kernel, stash/combine reductions, global positivity codes).  The
-concatenated slabs must reproduce the single-context run.  Tolerance: the
-reductions are regrouped by slab, so 1e-13 relative (not bitwise)."""
+ranks' cells, scattered back by their global ids, must reproduce the
+single-context run.  Tolerance: the reductions are regrouped by rank, so
+1e-13 relative (not bitwise)."""
 import numpy as np
 import pytest
 
@@ -17,25 +19,47 @@ from paper_2507_04991_b200 import perrk as P
 pytestmark = pytest.mark.gpu
 
 
-def _run(semis, fam, pm, U0, steps, cfl, relax, cuts=None):
+def _scatter(semis, U0):
+    npc, V = semis[0].nodes_per_cell(), semis[0].num_vars()
+    cells = U0.reshape(-1, npc, V)
+    for s in semis:
+        s.upload(np.ascontiguousarray(cells[s.local_cells()]).reshape(-1))
+
+
+def _gather(semis, like):
+    npc, V = semis[0].nodes_per_cell(), semis[0].num_vars()
+    out = np.full(like.size, np.nan).reshape(-1, npc, V)
+    for s in semis:
+        out[s.local_cells()] = s.download().reshape(-1, npc, V)
+    return out.reshape(-1)
+
+
+def _run(semis, fam, pm, U0, steps, cfl, relax):
     for s in semis:
         s._use_family(fam, pm)
     rc = P.IntegratorConfig(tf=1e30, time=P.TimeControl(False, 0.0, P.CflRamp(cfl, cfl)),
                             relaxation=relax)
-    npc, V = semis[0].nodes_per_cell(), semis[0].num_vars()
-    lc = semis[0].global_num_cells() // semis[0].spec.mesh.shape()[-1]
-    cells = U0.reshape(-1, npc, V)
-    for s in semis:
-        b, e = s.slab_range()
-        s.upload(np.ascontiguousarray(cells[b * lc:e * lc]).reshape(-1))
+    _scatter(semis, U0)
     t, taken, aborted, recs = P.advance(semis[0], fam, pm, rc, 0.0, steps)
     assert taken == steps and not aborted
-    U = np.concatenate([s.download() for s in semis])
-    return U, recs
+    return _gather(semis, U0), recs
 
 
-@pytest.mark.parametrize("dim,nranks", [(2, 2), (2, 3), (3, 2), (3, 4)])
-def test_loopback_slabs_reproduce_single_domain(dim, nranks):
+def _owner(kind, mesh, pm, nranks):
+    if kind == "slabs":
+        return None
+    if kind == "levels":
+        return P.partition_levels(mesh, pm, nranks)
+    rng = np.random.default_rng(17)
+    own = rng.integers(0, nranks, mesh.num_cells()).astype(np.int32)
+    own[:nranks] = np.arange(nranks)
+    return own
+
+
+@pytest.mark.parametrize("dim,nranks,kind", [(2, 2, "slabs"), (2, 3, "slabs"), (3, 2, "slabs"),
+                                             (3, 4, "slabs"), (2, 3, "levels"), (3, 4, "levels"),
+                                             (2, 2, "scattered"), (3, 3, "scattered")])
+def test_loopback_partition_reproduces_single_domain(dim, nranks, kind):
     if dim == 2:
         mesh = mesh2d(10, 12, seed=71)
         fam = P.build_perk3_variant(7, [4, 7], [[0.3], [0.2, 0.25, 0.3, 0.35]])
@@ -52,13 +76,20 @@ def test_loopback_slabs_reproduce_single_domain(dim, nranks):
     relax = P.RelaxationConfig(numerics="accurate")
     U1, r1 = _run([one], fam, pm, U0, 6, 0.3, relax)
     semis = [P.Semidiscretization(spec) for _ in range(nranks)]
-    P.loopback_group(semis)
-    # the slab geometry is the global geometry's layers
+    owner = _owner(kind, mesh, pm, nranks)
+    P.loopback_group(semis, owner)
+    # every rank's geometry is the global geometry of its cells
     gx = one.node_x().reshape(-1, one.nodes_per_cell())
-    lc = mesh.num_cells() // mesh.shape()[-1]
-    for s in semis:
-        b, e = s.slab_range()
-        assert np.array_equal(s.node_x(), gx[b * lc:e * lc].reshape(-1))
+    gz = (one.node_z() if dim == 3 else one.node_y()).reshape(-1, one.nodes_per_cell())
+    seen = np.zeros(mesh.num_cells(), int)
+    for r, s in enumerate(semis):
+        g = s.local_cells()
+        seen[g] += 1
+        if owner is not None:
+            assert np.array_equal(g, np.flatnonzero(owner == r))
+        assert np.array_equal(s.node_x(), gx[g].reshape(-1))
+        assert np.array_equal(s.node_z() if dim == 3 else s.node_y(), gz[g].reshape(-1))
+    assert np.all(seen == 1)
     Un, rn = _run(semis, fam, pm, U0, 6, 0.3, relax)
     assert rel_err(Un, U1, dim + 2) < 1e-13
     g1 = np.array([r.gamma for r in r1])
@@ -80,12 +111,9 @@ def test_loopback_slab_positivity_reports_global_cell():
     U0.reshape(-1, 64, 5)[bad, 7, 0] = -1.0
     semis = [P.Semidiscretization(spec) for _ in range(2)]
     P.loopback_group(semis)
-    lc = 16
     for s in semis:
         s._use_family(fam, pm)
-        b, e = s.slab_range()
-        s.upload(np.ascontiguousarray(U0.reshape(-1, 64, 5)[b * lc:e * lc]).reshape(-1))
+    _scatter(semis, U0)
     t, res = P.perk_step_resident(0.0, 0.01, fam, pm, semis[0], P.PerkStepOptions())
     assert res.aborted and res.bad_cell == bad and res.bad_stage == 0
-    Ud = np.concatenate([s.download() for s in semis])
-    assert np.array_equal(Ud, U0)  # untouched on abort
+    assert np.array_equal(_gather(semis, U0), U0)  # untouched on abort
