@@ -65,8 +65,9 @@ typedef struct {
   double gamma;              /* ratio of specific heats (> 1) */
   double mu, prandtl;        /* NSF only */
   int surface_flux;          /* PERRK_FLUX_* */
-  int volume_mode;           /* 1 flux differencing (0 weak form: unsupported) */
-  int volume_flux;           /* PERRK_FLUX_EC */
+  int volume_mode;           /* 1 flux differencing, 0 weak form (semidisc.cpp:429-445) */
+  int volume_flux;           /* flux differencing: PERRK_FLUX_EC or PERRK_FLUX_CENTRAL
+                                (NSF: EC only) */
   int device;                /* CUDA device ordinal */
 } perrk_semi_desc;
 
@@ -86,8 +87,8 @@ typedef struct {
  * residual: 0 = the reference's form r = H(U+g dt d) - h_ref - g dH with its
  * stopping rule (relax.cpp:79-104); 1 = the accurate form:
  * compensated reductions, per-node cancellation-free entropy differences,
- * Newton stop on |dg| <= 1e-13 g or stagnation.  Only method 0 (Newton) runs
- * on the device. */
+ * Newton stop on |dg| <= 1e-13 g or stagnation.  Methods: Newton
+ * (relax.cpp:51-104), bisection and secant (relax.cpp:105-148). */
 typedef struct {
   int method;                /* 0 newton, 1 bisection, 2 secant */
   int max_iter;
@@ -220,7 +221,7 @@ int perrk_family_build(int kind, int S, int R, const int* E, const double* free_
                        double c_sm3, double* A, double* b, double* c, int* active);
 /* assign_levels (mesh.cpp:73-95) */
 int perrk_assign_levels(const double* nu, int64_t n, int R, int* levels);
-/* make_partition_map (mesh.cpp:56-71) on a periodic rectilinear mesh */
+/* make_partition_map (mesh.cpp:56-71) on a periodic rectilinear mesh, dim 1-3 */
 int perrk_make_partition_map(int dim, const int* ncells, const int* levels, int R, int* effective);
 
 /* ---- instrumentation (bench.py / profiling; no reference counterpart) ---
@@ -240,6 +241,30 @@ int perrk_launch_count(const perrk_ctx* ctx, int64_t* launches);
 int perrk_step_traffic(const perrk_ctx* ctx, double* stage_bytes, double* pass_bytes,
                        double* update_bytes);
 int perrk_fp64_peak(int device, double* gflops);
+
+/* ---- linear advection: the update matrix of one step --------------------
+ * Replaces analysis::assemble_update_matrix (analysis.cpp:11-32): for every
+ * unit vector e_j, perk_step (stepper.cpp:17-114) with relaxation off and
+ * gamma fixed, on AdvectionPhysics (physics.hpp:54-85) over a periodic 1D
+ * mesh (Mesh1D) or a periodic 2D rectilinear mesh.  All M = cells * 4^dim
+ * columns advance together on the device, in column chunks sized to free
+ * memory.  D is written column-major: D(i, j) = D[j * M + i] (Eigen's layout
+ * of UpdateMatrix::D).  HLLE/HLLC surface fluxes are rejected as in the
+ * reference (physics.cpp:73-78). */
+typedef struct {
+  int dim;                   /* 1 or 2 */
+  int n[2];                  /* cells per axis */
+  const double* edges[2];    /* n[a]+1 strictly increasing edges per axis */
+  double velocity[2];        /* AdvectionPhysics velocity */
+  int surface_flux;          /* PERRK_FLUX_CENTRAL / _UPWIND / _RUSANOV / _EC */
+  int volume_mode;           /* 1 flux differencing, 0 weak form */
+  int volume_flux;           /* flux differencing: PERRK_FLUX_CENTRAL or _EC */
+  int device;
+} perrk_advection_desc;
+/* M: out, number of dofs (D has M*M entries); D may be NULL to query M. */
+int perrk_update_matrix(const perrk_advection_desc* desc, const perrk_family_desc* fam,
+                        const int* effective_level, double dt, double gamma, double* D,
+                        int64_t* M);
 
 /* ---- multi-GPU: element partition ------------------------
  * No reference counterpart (the reference is single-process).  Every global

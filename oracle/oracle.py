@@ -126,6 +126,8 @@ def ref_lib():
             "ref_family_to_text": (C.c_int, [C.POINTER(RefFamily), C.c_char_p, C.c_int]),
             "ref_assign_levels": (C.c_int, [_D, C.c_int, C.c_int, _I]),
             "ref_make_partition_map": (C.c_int, [C.c_void_p, _I, C.c_int, _I]),
+            "ref_update_matrix": (C.c_int, [C.c_void_p, C.POINTER(RefFamily), _I, C.c_double,
+                                            C.c_double, _D]),
             "ref_perk_step": (C.c_int, [C.c_void_p, _D, _D, C.c_double, C.POINTER(RefFamily),
                                         _I, C.POINTER(RefRelax), C.c_double, C.c_double,
                                         C.c_int, C.c_double, C.POINTER(StepResult)]),
@@ -317,6 +319,38 @@ class Ref(_Base):
         self._check(self.L.ref_error_norms_vortex(self.h, dp(np.ascontiguousarray(U)), dp(pv), t,
                                                   dp(l1), dp(li)))
         return l1, li
+
+
+class RefAdvection(Ref):
+    """The reference on AdvectionPhysics (physics.hpp:54-85), periodic 1D
+    (Mesh1D) or 2D meshes: RHS, perk_step and the update matrix
+    (analysis.cpp:11-32, looped in ref_shim.cpp)."""
+
+    def __init__(self, mesh, velocity, surface_flux="upwind", volume_flux="ec",
+                 volume_mode="flux_differencing", k=3, threads=1):
+        self.L = ref_lib()
+        xe = np.ascontiguousarray(mesh.edges[0], dtype=np.float64)
+        ye = np.ascontiguousarray(mesh.edges[1] if mesh.dim == 2 else [0.0, 1.0],
+                                  dtype=np.float64)
+        vel = np.ascontiguousarray(velocity, dtype=np.float64)
+        self.h = self.L.ref_create(mesh.dim, dp(xe), xe.size, dp(ye), ye.size, k, 1, 1.4,
+                                   dp(vel), FLUX[surface_flux],
+                                   int(volume_mode == "flux_differencing"), FLUX[volume_flux])
+        if not self.h:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        self.V = 1
+        self.ndofs = self.L.ref_num_dofs(self.h)
+        self.ncells = self.L.ref_num_cells(self.h)
+        self.L.ref_set_threads(self.h, threads)
+
+    def update_matrix(self, fam, eff, dt, gamma):
+        """D (M x M) of one step, D[:, j] = perk_step(e_j)."""
+        f = self._fam(fam)
+        eff = np.ascontiguousarray(eff, dtype=np.int32)
+        M = self.ndofs
+        D = np.zeros(M * M)
+        self._check(self.L.ref_update_matrix(self.h, C.byref(f), ip(eff), dt, gamma, dp(D)))
+        return D.reshape(M, M).T  # column-major -> D[i, j]
 
 
 class RefNSF1D:

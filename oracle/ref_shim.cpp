@@ -14,6 +14,7 @@
 //   make_partition_map etc.   proj/core/src/mesh.cpp:56-129
 #include <chrono>
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -419,6 +420,31 @@ int ref_perk_step(ref_ctx* ctx, double* U, double* t, double dt, const ref_famil
     out->aborted = r.aborted;
     out->bad_cell = r.bad_cell;
     out->bad_stage = r.bad_stage;
+  });
+}
+
+// analysis::assemble_update_matrix (analysis.cpp:11-32) without its Eigen
+// container: column j = perk_step(e_j) with relaxation off and gamma fixed;
+// D column-major (D(i, j) = D[j * M + i]).
+int ref_update_matrix(ref_ctx* ctx, const ref_family* f, const int* eff, double dt, double gamma,
+                      double* D) {
+  return guarded([&] {
+    const auto& s = *ctx->semi;
+    PERRK_REQUIRE(s.physics().name() == "advection", "update matrix needs linear physics");
+    const auto fam = make_family(f);
+    const auto map = make_map(s, eff, f->R);
+    const int M = s.num_dofs();
+    PerkStepOptions opts;
+    opts.relaxation = nullptr;
+    opts.gamma_override = gamma;
+    StateVector unit(static_cast<std::size_t>(M));
+    for (int j = 0; j < M; ++j) {
+      std::fill(unit.begin(), unit.end(), 0.0);
+      unit[j] = 1.0;
+      double t = 0.0;
+      perk_step(unit, t, dt, fam, map, s, opts);
+      std::memcpy(D + static_cast<std::size_t>(j) * M, unit.data(), sizeof(double) * M);
+    }
   });
 }
 

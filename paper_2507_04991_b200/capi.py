@@ -32,6 +32,12 @@ class FamilyDesc(C.Structure):
                 ("c", C.POINTER(C.c_double))]
 
 
+class AdvectionDesc(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n", C.c_int * 2), ("edges", C.POINTER(C.c_double) * 2),
+                ("velocity", C.c_double * 2), ("surface_flux", C.c_int),
+                ("volume_mode", C.c_int), ("volume_flux", C.c_int), ("device", C.c_int)]
+
+
 class RelaxCfg(C.Structure):
     _fields_ = [("method", C.c_int), ("max_iter", C.c_int), ("residual_tol", C.c_double),
                 ("step_tol", C.c_double), ("bracket_min", C.c_double),
@@ -106,6 +112,8 @@ _PROTOS = {
     "perrk_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "perrk_step_traffic": (C.c_int, [_P, _D, _D, _D]),
     "perrk_fp64_peak": (C.c_int, [C.c_int, _D]),
+    "perrk_update_matrix": (C.c_int, [C.POINTER(AdvectionDesc), C.POINTER(FamilyDesc), _I,
+                                      C.c_double, C.c_double, _D, C.POINTER(C.c_int64)]),
     "perrk_nccl_id": (C.c_int, [C.c_void_p]),
     "perrk_comm_init": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int, _I]),
     "perrk_local_cells": (C.c_int, [_P, _I, C.POINTER(C.c_int64)]),

@@ -69,6 +69,7 @@ __device__ __forceinline__ void report_bad(StepState* st, int stage, long long n
 
 #include "dg_stage.cuh"
 #include "dg_visc.cuh"
+#include "dg_advection.cuh"
 
 namespace perrk {
 namespace dev {
@@ -544,57 +545,57 @@ __global__ void admissible_kernel(const double* __restrict__ U, Phys ph, int* fi
 // launchers
 // ---------------------------------------------------------------------------
 
-template <int DIM, int SURF, bool VISC>
+template <int DIM, bool VISC>
 static size_t stage_smem() {
   return sizeof(double) *
          (StageGeo<DIM>::SM_TOTAL + StageGeo<DIM>::SM_ZF + StageGeo<DIM>::SM_PF +
           (VISC ? StageGeo<DIM>::SM_VISC : 0));
 }
 
-template <int DIM, int SURF, bool VISC>
+template <int DIM, int SURF, bool VISC, bool SIMPLE>
 static void configure_stage() {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(stage_kernel<DIM, SURF, VISC>,
+    cudaFuncSetAttribute(stage_kernel<DIM, SURF, VISC, SIMPLE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(stage_smem<DIM, SURF, VISC>()));
+                         static_cast<int>(stage_smem<DIM, VISC>()));
     configured = true;
   }
 }
 
-template <int DIM, int SURF>
+template <int DIM, int SURF, bool SIMPLE>
 static int stage_occ_t() {
-  configure_stage<DIM, SURF, false>();
+  configure_stage<DIM, SURF, false, SIMPLE>();
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, stage_kernel<DIM, SURF, false>,
-                                                StageGeo<DIM>::T, stage_smem<DIM, SURF, false>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, stage_kernel<DIM, SURF, false, SIMPLE>,
+                                                StageGeo<DIM>::T, stage_smem<DIM, false>());
   return n;
 }
 
-template <int DIM, int SURF, bool VISC>
+template <int DIM, int SURF, bool VISC, bool SIMPLE>
 static cudaError_t launch_stage_t(const StageArgs& a, const MeshDev& m, const Phys& ph,
                                   StepState* st, double* partials, unsigned* counter, int grid,
                                   cudaStream_t s) {
   using G = StageGeo<DIM>;
-  configure_stage<DIM, SURF, VISC>();
+  configure_stage<DIM, SURF, VISC, SIMPLE>();
   const int groups = (a.n + G::CPB - 1) / G::CPB;
   const int g = groups < grid ? groups : grid;
   if (g <= 0) return cudaSuccess;
-  stage_kernel<DIM, SURF, VISC><<<g, G::T, stage_smem<DIM, SURF, VISC>(), s>>>(a, m, ph, st,
-                                                                            partials, counter);
+  stage_kernel<DIM, SURF, VISC, SIMPLE><<<g, G::T, stage_smem<DIM, VISC>(), s>>>(
+      a, m, ph, st, partials, counter);
   return cudaGetLastError();
 }
 
-template <int DIM, bool VISC>
+template <int DIM, bool VISC, bool SIMPLE>
 static cudaError_t launch_stage_d(int surf, const StageArgs& a, const MeshDev& m, const Phys& ph,
                                   StepState* st, double* partials, unsigned* counter, int grid,
                                   cudaStream_t s) {
   switch (surf) {
-    case 0: return launch_stage_t<DIM, 0, VISC>(a, m, ph, st, partials, counter, grid, s);
-    case 2: return launch_stage_t<DIM, 2, VISC>(a, m, ph, st, partials, counter, grid, s);
-    case 3: return launch_stage_t<DIM, 3, VISC>(a, m, ph, st, partials, counter, grid, s);
-    case 4: return launch_stage_t<DIM, 4, VISC>(a, m, ph, st, partials, counter, grid, s);
-    case 5: return launch_stage_t<DIM, 5, VISC>(a, m, ph, st, partials, counter, grid, s);
+    case 0: return launch_stage_t<DIM, 0, VISC, SIMPLE>(a, m, ph, st, partials, counter, grid, s);
+    case 2: return launch_stage_t<DIM, 2, VISC, SIMPLE>(a, m, ph, st, partials, counter, grid, s);
+    case 3: return launch_stage_t<DIM, 3, VISC, SIMPLE>(a, m, ph, st, partials, counter, grid, s);
+    case 4: return launch_stage_t<DIM, 4, VISC, SIMPLE>(a, m, ph, st, partials, counter, grid, s);
+    case 5: return launch_stage_t<DIM, 5, VISC, SIMPLE>(a, m, ph, st, partials, counter, grid, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -861,28 +862,51 @@ size_t stage_smem_bytes(int dim) {
   return dim == 2 ? sizeof(double) * StageGeo<2>::SM_TOTAL : sizeof(double) * StageGeo<3>::SM_TOTAL;
 }
 
-int stage_blocks_per_sm(int dim, int surf) {
+template <int DIM, bool SIMPLE>
+static int stage_occ_d(int surf) {
   switch (surf) {
-    case 0: return dim == 2 ? stage_occ_t<2, 0>() : stage_occ_t<3, 0>();
-    case 2: return dim == 2 ? stage_occ_t<2, 2>() : stage_occ_t<3, 2>();
-    case 3: return dim == 2 ? stage_occ_t<2, 3>() : stage_occ_t<3, 3>();
-    case 4: return dim == 2 ? stage_occ_t<2, 4>() : stage_occ_t<3, 4>();
-    case 5: return dim == 2 ? stage_occ_t<2, 5>() : stage_occ_t<3, 5>();
+    case 0: return stage_occ_t<DIM, 0, SIMPLE>();
+    case 2: return stage_occ_t<DIM, 2, SIMPLE>();
+    case 3: return stage_occ_t<DIM, 3, SIMPLE>();
+    case 4: return stage_occ_t<DIM, 4, SIMPLE>();
+    case 5: return stage_occ_t<DIM, 5, SIMPLE>();
   }
   return 1;
 }
 
+int stage_blocks_per_sm(int dim, int surf, int vol) {
+  const bool simple = vol != VOL_EC;
+  if (dim == 2) return simple ? stage_occ_d<2, true>(surf) : stage_occ_d<2, false>(surf);
+  return simple ? stage_occ_d<3, true>(surf) : stage_occ_d<3, false>(surf);
+}
+
 int stage_cells_per_block(int dim) { return dim == 2 ? StageGeo<2>::CPB : StageGeo<3>::CPB; }
 
-cudaError_t launch_stage(int dim, int surf, const StageArgs& a, const MeshDev& m, const Phys& ph,
-                         StepState* st, double* partials, unsigned* counter, int grid,
-                         cudaStream_t s) {
-  if (a.G) {
-    if (dim != 2) return cudaErrorInvalidValue;
-    return launch_stage_d<2, true>(surf, a, m, ph, st, partials, counter, grid, s);
+cudaError_t launch_stage(int dim, int surf, int vol, const StageArgs& a0, const MeshDev& m,
+                         const Phys& ph, StepState* st, double* partials, unsigned* counter,
+                         int grid, cudaStream_t s) {
+  StageArgs a = a0;
+  a.weak = vol == VOL_WEAK;
+  if (a.G) {  // BR1 (2D Navier-Stokes) runs with the EC volume flux only
+    if (dim != 2 || vol != VOL_EC) return cudaErrorInvalidValue;
+    return launch_stage_d<2, true, false>(surf, a, m, ph, st, partials, counter, grid, s);
   }
-  return dim == 2 ? launch_stage_d<2, false>(surf, a, m, ph, st, partials, counter, grid, s)
-                  : launch_stage_d<3, false>(surf, a, m, ph, st, partials, counter, grid, s);
+  if (vol == VOL_EC)
+    return dim == 2 ? launch_stage_d<2, false, false>(surf, a, m, ph, st, partials, counter, grid, s)
+                    : launch_stage_d<3, false, false>(surf, a, m, ph, st, partials, counter, grid, s);
+  return dim == 2 ? launch_stage_d<2, false, true>(surf, a, m, ph, st, partials, counter, grid, s)
+                  : launch_stage_d<3, false, true>(surf, a, m, ph, st, partials, counter, grid, s);
+}
+
+cudaError_t launch_adv_stage(const AdvArgs& a, int grid, cudaStream_t s) {
+  adv_stage_kernel<<<grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adv_final(const double* d, long long M, long long col0, int ncols, double scale,
+                             double* D, int grid, cudaStream_t s) {
+  adv_final_kernel<<<grid, 256, 0, s>>>(d, M, col0, ncols, scale, D);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_grad(const StageArgs& a, const MeshDev& m, const Phys& ph, StepState* st,

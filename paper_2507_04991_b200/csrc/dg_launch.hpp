@@ -33,17 +33,49 @@ struct StageArgs {
   long long ncells;      // GLOBAL cells (positivity codes are stage * ncells + global cell)
   const double* G;       // BR1 viscous fluxes [2][ndofs] (nullptr: inviscid)
   long long ndofs;
+  int weak;              // volume: set by launch_stage from its vol argument
 };
+
+// one stage of the batched advection update-matrix step (dg_advection.cuh)
+struct AdvArgs {
+  int dim;          // 1 or 2
+  int nc[2];        // cells per axis
+  const double* h[2];  // cell sizes per axis
+  const int8_t* level;  // effective level per cell
+  double a[2];      // advection velocity
+  int surface;      // PERRK_FLUX_* (central, upwind, rusanov, ec)
+  int volume_flux;  // flux differencing: central or ec (both 1/2 a (ul + ur) up to rounding)
+  int weak;         // weak-form volume integral
+  long long M;      // dofs per column
+  long long col0;   // first column of the chunk
+  int ncols;        // columns in the chunk
+  const double* K1;
+  const double* Kp;  // K_{i-1}
+  double* Kout;      // K_i (stage 0: K1)
+  double* d;
+  double dt;
+  int stage;
+  double a1[dev::MAXR + 1], ap[dev::MAXR + 1];  // by level: a_{i,1}, a_{i,i-1} (0 at i = 1)
+  double b;                           // b_i
+  const int* list;                    // active cells (nullptr: all)
+  int nlist;
+};
+
+// volume integral of the stage kernel (SemidiscretizationSpec::volume_mode/_flux)
+enum { VOL_WEAK = 0, VOL_CENTRAL = 1, VOL_EC = 2 };
 
 double measure_fp64_peak();  // GFLOP/s on the current device (DFMA loop)
 cudaError_t upload_basis(const double* D, const double* w);
 size_t stage_smem_bytes(int dim);
 int stage_cells_per_block(int dim);
-int stage_blocks_per_sm(int dim, int surf);  // resident stage blocks per SM
+int stage_blocks_per_sm(int dim, int surf, int vol);  // resident stage blocks per SM
 
-cudaError_t launch_stage(int dim, int surf, const StageArgs& a, const dev::MeshDev& m,
+cudaError_t launch_stage(int dim, int surf, int vol, const StageArgs& a, const dev::MeshDev& m,
                          const dev::Phys& ph, dev::StepState* st, double* partials,
                          unsigned* counter, int grid, cudaStream_t s);
+cudaError_t launch_adv_stage(const AdvArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_adv_final(const double* d, long long M, long long col0, int ncols, double scale,
+                             double* D, int grid, cudaStream_t s);
 cudaError_t launch_grad(const StageArgs& a, const dev::MeshDev& m, const dev::Phys& ph,
                         dev::StepState* st, double* out, long long ndofs, int mode, int grid,
                         cudaStream_t s);

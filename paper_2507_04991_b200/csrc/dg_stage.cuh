@@ -404,7 +404,52 @@ __device__ __forceinline__ void zf_gather(const double* zf, int tid, const int (
   for (int v = 0; v < V; ++v) K[v] = fma(-cp, f[v], K[v]);
 }
 
-template <int DIM, int SURF, bool VISC>
+// Volume term without the EC flux (SIMPLE kernels), along direction D:
+//   weak form (semidisc.cpp:429-445):  K += J sum_m D_mj w_m / w_j f(u_m);
+//   flux differencing with the central two-point flux 1/2 (f_j + f_m)
+//   (semidisc.cpp:446-485 with FluxTag::central): K -= 2 J sum_{m != j} D_jm f*,
+//   the diagonal -2 J D_jj f(u_j) being added by the surface phase as for EC.
+// The physical fluxes of the line's nodes come from the primitives in smem.
+template <int DIM, int D>
+__device__ __forceinline__ void simple_volume(const double* pr, int tid, const int (&il)[3],
+                                              double J2, const Prim<DIM>& own, bool weak,
+                                              double* K) {
+  using G = StageGeo<DIM>;
+  using S = Slot<DIM>;
+  constexpr int V = G::V, T = G::T;
+  constexpr int stride = D == 0 ? 1 : (D == 1 ? N1 : N1 * N1);
+  const int j = il[D];
+  double fj[V];
+  pflux<DIM>(own, D, fj);
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    double f[V];
+    if (m == j) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) f[v] = fj[v];
+    } else {
+      const int q = tid + (m - j) * stride;
+      Prim<DIM> pm;
+      pm.rho = pr[S::RHO * T + q];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) pm.v[i] = pr[(S::V0 + i) * T + q];
+      pm.p = pr[S::P * T + q];
+      pm.E = pr[S::E * T + q];
+      pflux<DIM>(pm, D, f);
+    }
+    if (weak) {
+      const double coef = 0.5 * J2 * c_D[m * N1 + j] * c_w[m] / c_w[j];
+#pragma unroll
+      for (int v = 0; v < V; ++v) K[v] = fma(coef, f[v], K[v]);
+    } else if (m != j) {
+      const double coef = J2 * c_D[j * N1 + m];
+#pragma unroll
+      for (int v = 0; v < V; ++v) K[v] = fma(-coef, 0.5 * (fj[v] + f[v]), K[v]);
+    }
+  }
+}
+
+template <int DIM, int SURF, bool VISC, bool SIMPLE>
 __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     stage_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
                  unsigned* counter) {
@@ -662,8 +707,13 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
         if (side) sflux<DIM, SURF>(ph, o, nbp, DIM - 1, fs);
         else sflux<DIM, SURF>(ph, nbp, o, DIM - 1, fs);
       }
+      if (SIMPLE && a.weak) {  // weak form: the lift of f* alone (semidisc.cpp:505,548)
 #pragma unroll
-      for (int v = 0; v < V; ++v) sf[q * V + v] = fma(sg, fs[v] - fo[v], -cll * fo[v]);
+        for (int v = 0; v < V; ++v) sf[q * V + v] = sg * fs[v];
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) sf[q * V + v] = fma(sg, fs[v] - fo[v], -cll * fo[v]);
+      }
     }
 
     // ---- flux-differencing volume terms (every lane: the in-warp pair
@@ -671,16 +721,24 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     double K[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) K[v] = 0.0;
-    volume_terms<DIM, 0>(ph, pr, tid, il, s_J2[cs][0], own, lr, be, lb, K);
-    volume_terms<DIM, 1>(ph, pr, tid, il, s_J2[cs][1], own, lr, be, lb, K);
-    if constexpr (DIM == 3)
-      volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, lr, be, lb, K, zf);
-    dist2_pairs<DIM>(ph, pr, pf, tid);
+    if constexpr (SIMPLE) {
+      simple_volume<DIM, 0>(pr, tid, il, s_J2[cs][0], own, a.weak, K);
+      simple_volume<DIM, 1>(pr, tid, il, s_J2[cs][1], own, a.weak, K);
+      if constexpr (DIM == 3) simple_volume<DIM, DIM - 1>(pr, tid, il, s_J2[cs][DIM - 1], own, a.weak, K);
+    } else {
+      volume_terms<DIM, 0>(ph, pr, tid, il, s_J2[cs][0], own, lr, be, lb, K);
+      volume_terms<DIM, 1>(ph, pr, tid, il, s_J2[cs][1], own, lr, be, lb, K);
+      if constexpr (DIM == 3)
+        volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, lr, be, lb, K, zf);
+      dist2_pairs<DIM>(ph, pr, pf, tid);
+    }
     if (dt_t >= 0) describe(buf ^ 1, dt_t, nx_cell);  // the next group, off the critical path
     __syncthreads();  // surface terms of every face point visible
 
-    if constexpr (DIM == 3) zf_gather<DIM>(zf, tid, il, s_J2[cs][DIM - 1], K);
-    dist2_gather<DIM>(pf, cs, il, s_J2[cs], K);
+    if constexpr (!SIMPLE) {
+      if constexpr (DIM == 3) zf_gather<DIM>(zf, tid, il, s_J2[cs][DIM - 1], K);
+      dist2_gather<DIM>(pf, cs, il, s_J2[cs], K);
+    }
     if (cell >= 0) {
       // gather the node's face contributions (one per direction it ends)
 #pragma unroll

@@ -297,6 +297,9 @@ struct perrk_ctx {
   Basis basis;
   dev::Phys ph{};
   int physics = 0, surface = 2, volume_mode = 1, volume_flux = 5;
+  int vol() const {  // the stage kernel's volume variant (dg_launch.hpp)
+    return volume_mode == 0 ? VOL_WEAK : (volume_flux == PERRK_FLUX_EC ? VOL_EC : VOL_CENTRAL);
+  }
   double mu = 0.0, prandtl = 1.0;
   // device buffers
   double *U = nullptr, *K1 = nullptr, *d = nullptr;
@@ -601,7 +604,7 @@ void enqueue_stage(perrk_ctx* c, int i, bool want_h, int part = 0) {
     c->ev_bytes.push_back(p.n > 0 ? p.bytes * a.n / p.n : 0.0);
     CK(cudaEventRecord(e0, c->stream));
   }
-  CK(launch_stage(c->dim, c->surface, a, c->mesh(), c->ph, c->st, c->partials, c->counter,
+  CK(launch_stage(c->dim, c->surface, c->vol(), a, c->mesh(), c->ph, c->st, c->partials, c->counter,
                   c->grid_stage, c->stream));
   if (c->profiling) CK(cudaEventRecord(e1, c->stream));
   c->launches += p.n > 0 ? 1 : 0;
@@ -811,6 +814,21 @@ struct LoopbackExchange : Exchange {
       for (int q = 0; q < P; ++q)
         CK(cudaMemcpyAsync(g[q]->red_all + static_cast<size_t>(r) * dev::NRED, red_local_ptr(g[r]),
                            sizeof(double) * dev::NRED, cudaMemcpyDeviceToDevice, g[r]->stream));
+  }
+};
+
+// device allocations released on every exit path
+struct DeviceBuffers {
+  std::vector<void*> p;
+  ~DeviceBuffers() {
+    for (void* q : p) cudaFree(q);
+  }
+  template <class T>
+  T* get(size_t n) {
+    void* q = nullptr;
+    CK(cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T)));
+    p.push_back(q);
+    return static_cast<T*>(q);
   }
 };
 
@@ -1028,9 +1046,13 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     if (dsc->physics == 1 && dsc->dim != 2)
       throw Fail(PERRK_EUNSUP, "Navier-Stokes/BR1 runs in 2D on the device");
     if (dsc->physics == 1) REQUIRE(dsc->mu >= 0.0 && dsc->prandtl > 0.0, "need mu >= 0 and Pr > 0");
-    if (dsc->volume_mode != 1) throw Fail(PERRK_EUNSUP, "weak-form volume integral not on the device path");
-    if (dsc->volume_flux != PERRK_FLUX_EC)
-      throw Fail(PERRK_EUNSUP, "device flux differencing uses the Ranocha EC volume flux");
+    REQUIRE(dsc->volume_mode == 0 || dsc->volume_mode == 1, "volume_mode must be 0 (weak) or 1");
+    // semidisc.cpp:25-28: flux differencing takes the central or the EC two-point flux
+    if (dsc->volume_mode == 1 && dsc->volume_flux != PERRK_FLUX_EC &&
+        dsc->volume_flux != PERRK_FLUX_CENTRAL)
+      throw Fail(PERRK_EINVAL, "flux differencing needs a symmetric consistent volume flux");
+    if (dsc->physics == 1 && !(dsc->volume_mode == 1 && dsc->volume_flux == PERRK_FLUX_EC))
+      throw Fail(PERRK_EUNSUP, "the 2D Navier-Stokes path runs EC flux differencing");
     const int sf = dsc->surface_flux;
     if (sf == PERRK_FLUX_UPWIND) throw Fail(PERRK_EINVAL, "upwind flux only available for advection");
     REQUIRE(sf >= 0 && sf <= 5, "unknown surface flux");
@@ -1080,7 +1102,7 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     // persistent stage grid: exactly the resident capacity, so the active
     // cells are swept in order and neighbour traces are L2 hits; a function
     // of the device only, so block partials (and the sums) are reproducible
-    const int occ = stage_blocks_per_sm(c->dim, sf);
+    const int occ = stage_blocks_per_sm(c->dim, sf, c->vol());
     c->grid_stage = sms * (occ > 0 ? occ : 1);
     c->grid_flat = 8 * sms;
     alloc_cell_buffers(c);
@@ -1285,7 +1307,7 @@ int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const
         CK(launch_grad(ga, c->mesh(), c->ph, c->st, c->G, c->ndofs, 0, c->grid_stage, c->stream));
         a.G = c->G;
       }
-      CK(launch_stage(c->dim, c->surface, a, c->mesh(), c->ph, c->st, c->partials, c->counter,
+      CK(launch_stage(c->dim, c->surface, c->vol(), a, c->mesh(), c->ph, c->st, c->partials, c->counter,
                       c->grid_stage, c->stream));
       if (gl_dev) {
         CK(cudaStreamSynchronize(c->stream));
@@ -1698,8 +1720,8 @@ int perrk_assign_levels(const double* nu, int64_t n, int R, int* levels) {
 int perrk_make_partition_map(int dim, const int* n, const int* levels, int R, int* eff) {
   return guarded([&] {
     REQUIRE(R >= 1, "R must be at least 1");
-    REQUIRE((dim == 2 || dim == 3) && n && levels && eff, "bad arguments");
-    const int nx = n[0], ny = n[1], nz = dim == 3 ? n[2] : 1;
+    REQUIRE(dim >= 1 && dim <= 3 && n && levels && eff, "bad arguments");
+    const int nx = n[0], ny = dim >= 2 ? n[1] : 1, nz = dim == 3 ? n[2] : 1;
     const long long N = static_cast<long long>(nx) * ny * nz;
     for (long long i = 0; i < N; ++i)
       REQUIRE(levels[i] >= 1 && levels[i] <= R, "level out of range");
@@ -1790,6 +1812,130 @@ int perrk_step_traffic(const perrk_ctx* c, double* stage_bytes, double* pass_byt
     if (stage_bytes) *stage_bytes = s;
     if (pass_bytes) *pass_bytes = 16.0 * c->V * c->nnodes;    // read U, d
     if (update_bytes) *update_bytes = 24.0 * c->V * c->nnodes;  // read U, d; write U
+  });
+}
+
+int perrk_update_matrix(const perrk_advection_desc* ad, const perrk_family_desc* f,
+                        const int* eff, double dt, double gamma, double* D, int64_t* Mout) {
+  return guarded([&] {
+    REQUIRE(ad && Mout, "null argument");
+    REQUIRE(ad->dim == 1 || ad->dim == 2, "advection runs on 1D or 2D meshes");
+    const int sf = ad->surface_flux;
+    if (sf == PERRK_FLUX_HLLE) throw Fail(PERRK_EINVAL, "HLLE flux not available for this physics");
+    if (sf == PERRK_FLUX_HLLC) throw Fail(PERRK_EINVAL, "HLLC flux not available for this physics");
+    REQUIRE(sf == PERRK_FLUX_CENTRAL || sf == PERRK_FLUX_UPWIND || sf == PERRK_FLUX_RUSANOV ||
+                sf == PERRK_FLUX_EC,
+            "unknown surface flux");
+    REQUIRE(ad->volume_mode == 0 || ad->volume_mode == 1, "volume_mode must be 0 (weak) or 1");
+    if (ad->volume_mode == 1 && ad->volume_flux != PERRK_FLUX_EC &&
+        ad->volume_flux != PERRK_FLUX_CENTRAL)
+      throw Fail(PERRK_EINVAL, "flux differencing needs a symmetric consistent volume flux");
+    const int npc = ad->dim == 1 ? 4 : 16;
+    long long ncells = 1;
+    std::vector<double> hs[2];
+    for (int a = 0; a < ad->dim; ++a) {
+      REQUIRE(ad->n[a] >= 1 && ad->edges[a], "bad mesh");
+      ncells *= ad->n[a];
+      for (int i = 0; i < ad->n[a]; ++i) {
+        const double h = ad->edges[a][i + 1] - ad->edges[a][i];
+        REQUIRE(h > 0.0, "edges must be strictly increasing");
+        hs[a].push_back(h);
+      }
+    }
+    const long long M = ncells * npc;
+    *Mout = M;
+    if (!D) return;
+    REQUIRE(f && eff, "null argument");
+    REQUIRE(dt > 0.0, "dt must be positive");
+    REQUIRE(f->S >= 1 && f->R >= 1 && f->R <= dev::MAXR, "family size out of range");
+    const int S = f->S, R = f->R;
+    std::vector<double> A(f->A, f->A + static_cast<size_t>(R) * S * S), b(f->b, f->b + S);
+    for (long long i = 0; i < ncells; ++i) REQUIRE(eff[i] >= 1 && eff[i] <= R, "level out of range");
+    CK(cudaSetDevice(ad->device));
+    const Basis B = make_basis(3);
+    CK(upload_basis(B.D.data(), B.w.data()));
+    // per-level rows and activity (member R - level, butcher.hpp:47)
+    std::vector<std::vector<char>> active(R);
+    for (int lvl = 1; lvl <= R; ++lvl)
+      active[lvl - 1] = reachable_stages(S, &A[static_cast<size_t>(R - lvl) * S * S], b);
+    DeviceBuffers buf;
+    AdvArgs base{};
+    base.dim = ad->dim;
+    for (int a = 0; a < 2; ++a) {
+      base.nc[a] = a < ad->dim ? ad->n[a] : 1;
+      base.a[a] = a < ad->dim ? ad->velocity[a] : 0.0;
+      if (a < ad->dim) {
+        double* h = buf.get<double>(hs[a].size());
+        CK(cudaMemcpy(h, hs[a].data(), sizeof(double) * hs[a].size(), cudaMemcpyHostToDevice));
+        base.h[a] = h;
+      }
+    }
+    std::vector<int8_t> lv(eff, eff + ncells);
+    int8_t* dl = buf.get<int8_t>(ncells);
+    CK(cudaMemcpy(dl, lv.data(), ncells, cudaMemcpyHostToDevice));
+    base.level = dl;
+    base.surface = sf;
+    base.volume_flux = ad->volume_flux;
+    base.weak = ad->volume_mode == 0;
+    base.M = M;
+    base.dt = dt;
+    std::vector<int*> lists(S, nullptr);
+    std::vector<int> nlist(S, 0);
+    for (int i = 0; i < S; ++i) {
+      std::vector<int> l;
+      for (long long cell = 0; cell < ncells; ++cell)
+        if (i == 0 || active[eff[cell] - 1][i]) l.push_back(static_cast<int>(cell));
+      nlist[i] = static_cast<int>(l.size());
+      if (nlist[i] > 0 && nlist[i] < ncells) {
+        lists[i] = buf.get<int>(l.size());
+        CK(cudaMemcpy(lists[i], l.data(), sizeof(int) * l.size(), cudaMemcpyHostToDevice));
+      }
+    }
+    // column chunk: K1, two K buffers, d and the output chunk (5 x B x M doubles)
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const double budget = std::min(0.5 * static_cast<double>(free_b), 16.0e9);
+    long long Bc = static_cast<long long>(budget / (5.0 * 8.0 * static_cast<double>(M)));
+    Bc = std::max(1LL, std::min(Bc, M));
+    double* K1 = buf.get<double>(static_cast<size_t>(Bc) * M);
+    double* Kb[2] = {buf.get<double>(static_cast<size_t>(Bc) * M),
+                     buf.get<double>(static_cast<size_t>(Bc) * M)};
+    double* d = buf.get<double>(static_cast<size_t>(Bc) * M);
+    double* Dd = buf.get<double>(static_cast<size_t>(Bc) * M);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ad->device));
+    for (long long col0 = 0; col0 < M; col0 += Bc) {
+      const int nc = static_cast<int>(std::min(Bc, M - col0));
+      CK(cudaMemset(d, 0, sizeof(double) * static_cast<size_t>(nc) * M));
+      for (int i = 0; i < S; ++i) {
+        AdvArgs a = base;
+        a.col0 = col0;
+        a.ncols = nc;
+        a.stage = i;
+        a.K1 = K1;
+        a.Kp = i >= 2 ? Kb[(i - 1) & 1] : K1;
+        a.Kout = i == 0 ? K1 : Kb[i & 1];
+        a.d = d;
+        a.b = b[i];
+        a.list = lists[i];
+        a.nlist = nlist[i];
+        for (int lvl = 1; lvl <= R; ++lvl) {
+          const double* Am = &A[static_cast<size_t>(R - lvl) * S * S];
+          a.a1[lvl] = i >= 1 ? Am[static_cast<size_t>(i) * S] : 0.0;
+          a.ap[lvl] = i >= 2 ? Am[static_cast<size_t>(i) * S + i - 1] : 0.0;
+        }
+        const long long work = static_cast<long long>(nlist[i]) * npc * nc;
+        if (work == 0) continue;
+        const int grid = static_cast<int>(std::min<long long>((work + 255) / 256, 16LL * sms));
+        CK(launch_adv_stage(a, grid, nullptr));
+      }
+      const long long n = static_cast<long long>(nc) * M;
+      CK(launch_adv_final(d, M, col0, nc, gamma * dt, Dd,
+                          static_cast<int>(std::min<long long>((n + 255) / 256, 16LL * sms)),
+                          nullptr));
+      CK(cudaMemcpy(D + static_cast<size_t>(col0) * M, Dd, sizeof(double) * n,
+                    cudaMemcpyDeviceToHost));
+    }
   });
 }
 

@@ -45,6 +45,40 @@ def _f64(a):
 # meshes (mesh.hpp:22-33 plus the 3D extension), periodic rectilinear
 # ---------------------------------------------------------------------------
 @dataclass
+class Mesh1D:
+    """Periodic 1D mesh (mesh.hpp:13-20); only the advection update-matrix
+    engine (perrk_update_matrix) runs 1D."""
+    x_edges: Sequence[float]
+    periodic: bool = True
+
+    @property
+    def dim(self):
+        return 1
+
+    @property
+    def edges(self):
+        return [np.asarray(self.x_edges, float)]
+
+    def num_cells(self):
+        return len(self.x_edges) - 1
+
+    def shape(self):
+        return (self.num_cells(),)
+
+
+def build_uniform_mesh1d(x0, x1, n, periodic=True):
+    return Mesh1D(_uniform_edges(x0, x1, n), periodic)
+
+
+def build_two_level_advection_mesh():
+    """mesh.cpp:151-159: [-4, 4], h = 1/2 outside [-1, 1], 1/4 inside."""
+    e = [-4.0]
+    for a, b, n in ((-4.0, -1.0, 6), (-1.0, 1.0, 8), (1.0, 4.0, 6)):
+        e += _uniform_edges(a, b, n)[1:]
+    return Mesh1D(e, True)
+
+
+@dataclass
 class Mesh2DRect:
     x_edges: Sequence[float]
     y_edges: Sequence[float]
@@ -1033,3 +1067,92 @@ def write_snapshot_csv(semi, U, path):
         for n in range(U.shape[0]):
             cols = [x[n], y[n]] + ([z[n]] if semi.dim() == 3 else []) + list(U[n])
             f.write(",".join("%.17g" % v for v in cols) + "\n")
+
+
+# ---------------------------------------------------------------------------
+# linear advection: the update matrix of one step (analysis.hpp / analysis.cpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class AdvectionSpec:
+    """SemidiscretizationSpec with AdvectionPhysics(velocity) (physics.hpp:54-85)
+    on a periodic Mesh1D or Mesh2DRect."""
+    mesh: object
+    velocity: Sequence[float]
+    polydeg: int = 3
+    surface_flux: str = "upwind"
+    volume_mode: str = "flux_differencing"
+    volume_flux: str = "ec"
+    device: int = 0
+
+    def num_dofs(self):
+        return self.mesh.num_cells() * (self.polydeg + 1) ** self.mesh.dim
+
+
+@dataclass
+class UpdateMatrix:
+    gamma: float
+    dt: float
+    D: np.ndarray
+
+
+def _adv_desc(spec):
+    if spec.polydeg != 3:
+        raise Error(capi.PERRK_EUNSUP, "the device path is built for polydeg 3")
+    if not getattr(spec.mesh, "periodic", True):
+        raise Error(capi.PERRK_EUNSUP, "the update-matrix engine runs periodic meshes")
+    d = capi.AdvectionDesc()
+    d.dim = spec.mesh.dim
+    keep = [_f64(e) for e in spec.mesh.edges]
+    for a, e in enumerate(keep):
+        d.n[a] = len(e) - 1
+        d.edges[a] = _dp(e)
+    vel = list(spec.velocity)
+    if len(vel) != spec.mesh.dim:
+        raise Error(capi.PERRK_EINVAL, "physics/mesh dimension mismatch")
+    for a, v in enumerate(vel):
+        d.velocity[a] = float(v)
+    d.surface_flux = capi.FLUX[spec.surface_flux]
+    d.volume_mode = {"weak": 0, "flux_differencing": 1}[spec.volume_mode]
+    d.volume_flux = capi.FLUX[spec.volume_flux]
+    d.device = spec.device
+    return d, keep
+
+
+def assemble_update_matrix(family, pmap, spec, dt, gamma=1.0):
+    """analysis::assemble_update_matrix (analysis.cpp:11-32) on the device:
+    D[:, j] = perk_step(e_j) with relaxation off and gamma fixed, all columns
+    batched (perrk_update_matrix)."""
+    d, keep = _adv_desc(spec)
+    E = np.ascontiguousarray(family.E, dtype=np.int32)
+    A = _f64(family.A)
+    b, c = _f64(family.b), _f64(family.c)
+    eff = np.ascontiguousarray(pmap.effective_level, dtype=np.int32)
+    if eff.size != spec.mesh.num_cells():
+        raise Error(capi.PERRK_EINVAL, "partition map does not match mesh")
+    fd = capi.FamilyDesc(capi.FAMILY[family.kind], family.S, family.R, _ip(E), _dp(A), _dp(b),
+                         _dp(c))
+    M = C.c_int64()
+    check(lib().perrk_update_matrix(C.byref(d), C.byref(fd), _ip(eff), float(dt), float(gamma),
+                                    None, C.byref(M)))
+    out = np.zeros(M.value * M.value)
+    check(lib().perrk_update_matrix(C.byref(d), C.byref(fd), _ip(eff), float(dt), float(gamma),
+                                    _dp(out), C.byref(M)))
+    return UpdateMatrix(gamma, dt, out.reshape(M.value, M.value).T)  # column-major storage
+
+
+def monotonicity_metrics(D):
+    """analysis.cpp:34-40: (min entry, max entry, max |row sum - 1|)."""
+    D = np.asarray(D)
+    return float(D.min()), float(D.max()), float(np.abs(D.sum(axis=1) - 1.0).max())
+
+
+def spectral_radius(D):
+    """analysis.cpp:42-47 (eigenvalues on the host)."""
+    return float(np.abs(np.linalg.eigvals(np.asarray(D))).max())
+
+
+def save_matrix(D, path):
+    """analysis.cpp:49-60: rows of %.17g separated by single spaces."""
+    with open(path, "w") as fh:
+        for row in np.asarray(D):
+            fh.write(" ".join("%.17g" % v for v in row) + "\n")

@@ -146,3 +146,27 @@ def test_cpp_adapter_fails_loudly_without_device():
         pytest.skip("device present: covered by the gpu parity test")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 3, r.stdout + r.stderr
+
+
+def test_update_matrix_size_query_and_flux_errors_without_device():
+    """perrk_update_matrix (analysis.cpp:11-32): D = NULL queries M; HLLE/HLLC
+    are rejected for advection as in the reference (physics.cpp:73-78)."""
+    mesh = P.build_two_level_advection_mesh()
+    assert mesh.num_cells() == 20
+    assert np.allclose(np.diff(mesh.edges[0])[:6], 0.5) and np.allclose(np.diff(mesh.edges[0])[6:14], 0.25)
+    spec = P.AdvectionSpec(mesh, [1.0])
+    d, keep = P._adv_desc(spec)
+    M = C.c_int64()
+    assert capi.lib().perrk_update_matrix(C.byref(d), None, None, 0.1, 1.0, None, C.byref(M)) == 0
+    assert M.value == 80 == spec.num_dofs()
+    for bad in ("hlle", "hllc"):
+        d, keep = P._adv_desc(P.AdvectionSpec(mesh, [1.0], surface_flux=bad))
+        rc = capi.lib().perrk_update_matrix(C.byref(d), None, None, 0.1, 1.0, None, C.byref(M))
+        assert rc == capi.PERRK_EINVAL and b"not available" in capi.lib().perrk_last_error()
+    d, keep = P._adv_desc(P.AdvectionSpec(mesh, [1.0], volume_flux="rusanov"))
+    assert capi.lib().perrk_update_matrix(C.byref(d), None, None, 0.1, 1.0, None,
+                                          C.byref(M)) == capi.PERRK_EINVAL
+    with pytest.raises(P.Error):
+        P._adv_desc(P.AdvectionSpec(mesh, [1.0, 2.0]))
+    pm = P.make_partition_map(mesh, [2] * 6 + [1] * 8 + [2] * 6, 2)
+    assert list(pm.effective_level) == [2] * 5 + [1] * 10 + [2] * 5

@@ -49,6 +49,70 @@ def test_rhs_2d_random_state_all_surface_fluxes(surface):
     assert max_rel(semi.rhs(0.0, U), ref.rhs(0.0, U)) < 1e-12
 
 
+VOLUMES = [("weak", "ec"), ("flux_differencing", "central")]
+
+
+@pytest.mark.parametrize("mode,vflux", VOLUMES)
+@pytest.mark.parametrize("surface", SURFACES)
+def test_rhs_2d_volume_variants_vs_reference(mode, vflux, surface):
+    """Weak form (semidisc.cpp:429-445) and central flux differencing on the
+    device (the SIMPLE stage kernels)."""
+    mesh = mesh2d(9, 7, seed=13)
+    kw = dict(surface_flux=surface, volume_mode=mode, volume_flux=vflux)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, **kw))
+    U = smooth_state((semi.node_x(), semi.node_y()), 2, seed=17)
+    ref = O.Ref(mesh, **kw)
+    assert max_rel(semi.rhs(0.0, U), ref.rhs(0.0, U)) < 1e-12
+    mask = np.random.default_rng(6).integers(0, 2, semi.num_cells()).astype(np.int8)
+    assert max_rel(semi.rhs_masked(0.0, U, mask), ref.rhs_masked(0.0, U, mask)) < 1e-12
+
+
+@pytest.mark.parametrize("mode,vflux", VOLUMES)
+@pytest.mark.parametrize("surface", ["rusanov", "hlle", "ec"])
+def test_rhs_3d_volume_variants_vs_oracle(mode, vflux, surface):
+    mesh = mesh3d(4, 3, 5, seed=19)
+    kw = dict(surface_flux=surface, volume_mode=mode, volume_flux=vflux)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, **kw))
+    U = smooth_state((semi.node_x(), semi.node_y(), semi.node_z()), 3, seed=23)
+    orc = O.Orc(mesh, **kw)
+    assert max_rel(semi.rhs(0.0, U), orc.rhs(0.0, U)) < 1e-12
+
+
+@pytest.mark.parametrize("mode,vflux", VOLUMES)
+def test_multilevel_steps_volume_variants_vs_reference(mode, vflux):
+    """Unrelaxed multirate steps against the reference; relaxed steps (accurate
+    numerics) against the oracle for the gamma sequence."""
+    mesh = mesh2d(8, 8, seed=29)
+    fam = P.build_perk3_variant(7, [4, 7], [[0.3], [0.2, 0.25, 0.3, 0.35]])
+    rng = np.random.default_rng(8)
+    pm = P.make_partition_map(mesh, rng.integers(1, 3, mesh.num_cells()), 2)
+    kw = dict(surface_flux="hlle", volume_mode=mode, volume_flux=vflux)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, **kw))
+    ref, orc = O.Ref(mesh, **kw), O.Orc(mesh, **kw)
+    U0 = smooth_state((semi.node_x(), semi.node_y()), 2, seed=31, amp=0.2)
+    dt = 0.3 * ref.compute_dt(U0, False, 1.0)
+    Ug, Ur = U0.copy(), U0.copy()
+    for _ in range(5):
+        P.perk_step(Ug, 0.0, dt, fam, pm, semi, P.PerkStepOptions())
+        ref.perk_step(Ur, 0.0, dt, fam, pm.effective_level)
+    assert rel_err(Ug, Ur, 4) < 1e-12
+    rx = P.RelaxationConfig(numerics="accurate")
+    Ug, Uo = U0.copy(), U0.copy()
+    tg = to = 0.0
+    for _ in range(5):
+        tg, rg = P.perk_step(Ug, tg, dt, fam, pm, semi, P.PerkStepOptions(relaxation=rx))
+        to, ro = orc.perk_step(Uo, to, dt, fam, pm.effective_level, rx)
+        assert abs(rg.gamma - ro.gamma) < 1e-12 and rg.fell_back == bool(ro.fell_back)
+    assert rel_err(Ug, Uo, 4) < 1e-11
+
+
+def test_volume_variant_argument_errors():
+    mesh = mesh2d(4, 4)
+    with pytest.raises(P.Error):
+        P.Semidiscretization(P.SemidiscretizationSpec(mesh, volume_mode="flux_differencing",
+                                                      volume_flux="rusanov"))
+
+
 def test_rhs_masked_matches_reference_and_zero_fill():
     mesh = mesh2d(8, 8, seed=5)
     semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux="hlle"))

@@ -154,6 +154,36 @@ def test_orc_rhs_bitwise_equals_reference_2d(surface):
 
 
 @need_ref
+@pytest.mark.parametrize("mode,vflux", [("weak", "ec"), ("flux_differencing", "central")])
+@pytest.mark.parametrize("surface", ["rusanov", "hllc", "central"])
+def test_orc_volume_variants_bitwise_equal_reference_2d(mode, vflux, surface):
+    """Weak form (semidisc.cpp:429-445) and central flux differencing."""
+    mesh = mesh2d(6, 5, seed=12)
+    kw = dict(surface_flux=surface, volume_mode=mode, volume_flux=vflux)
+    orc, ref = O.Orc(mesh, **kw), O.Ref(mesh, **kw)
+    U = _orc_state(orc, seed=14)
+    assert np.array_equal(orc.rhs(0.0, U), ref.rhs(0.0, U))
+
+
+def test_orc_volume_variants_agree_on_smooth_data_3d():
+    """The three volume forms are consistent discretisations of the same
+    divergence: on a smooth state they agree to the discretisation error,
+    and on the free stream all vanish."""
+    mesh = mesh3d(3, 3, 3, seed=15)
+    outs = []
+    for mode, vflux in (("flux_differencing", "ec"), ("flux_differencing", "central"),
+                        ("weak", "ec")):
+        orc = O.Orc(mesh, surface_flux="rusanov", volume_mode=mode, volume_flux=vflux)
+        n = orc.ndofs // orc.V
+        Uf = np.tile([1.0, 0.5, -0.25, 0.125, 3.0], n)
+        assert np.abs(orc.rhs(0.0, Uf)).max() < 1e-12
+        outs.append(orc.rhs(0.0, _orc_state(orc, 16, amp=0.05)))
+    scale = np.abs(outs[0]).max()
+    for o in outs[1:]:
+        assert np.abs(o - outs[0]).max() < 0.2 * scale
+
+
+@need_ref
 def test_orc_reductions_equal_reference_2d():
     mesh = mesh2d(8, 5, seed=9)
     orc, ref = O.Orc(mesh), O.Ref(mesh)
@@ -373,3 +403,30 @@ def test_step_log_csv_matches_reference_writer(tmp_path):
     assert ref.L.ref_write_step_log(ref.h, len(log), O.dp(np.ascontiguousarray(rows)),
                                     str(theirs).encode()) == 0
     assert ours.read_bytes() == theirs.read_bytes()
+
+
+# --------------------------------------------------------------------------- update matrix
+@need_ref
+@pytest.mark.parametrize("surface", ["upwind", "central"])
+def test_reference_update_matrix_properties(surface):
+    """The reference's assemble_update_matrix loop (analysis.cpp:11-32 via
+    ref_shim.cpp) is the oracle for perrk_update_matrix.  Pins: linearity
+    (D u = perk_step(u)), constants preserved (row sums 1), and for the upwind
+    surface flux at a stable dt a spectral radius <= 1."""
+    mesh = P.build_two_level_advection_mesh()
+    ref = O.RefAdvection(mesh, [1.0], surface_flux=surface)
+    fam = P.build_perk3_variant(7, [4, 7], [[0.3], [0.2, 0.25, 0.3, 0.35]])
+    pm = P.make_partition_map(mesh, [2] * 6 + [1] * 8 + [2] * 6, 2)
+    dt = 0.05
+    D = ref.update_matrix(fam, pm.effective_level, dt, 1.0)
+    x = np.asarray(mesh.edges[0])
+    u = np.sin(np.linspace(0, 2 * np.pi, ref.ndofs, endpoint=False)) + 0.3
+    v = u.copy()
+    ref.perk_step(v, 0.0, dt, fam, pm.effective_level, None, gamma_override=1.0)
+    assert np.abs(D @ u - v).max() < 1e-13
+    assert np.abs(D.sum(axis=1) - 1.0).max() < 1e-13
+    mn, mx, dev = P.monotonicity_metrics(D)
+    assert dev < 1e-13 and mn < mx
+    if surface == "upwind":
+        assert P.spectral_radius(D) <= 1.0 + 1e-12
+    assert x.size == 21
