@@ -206,8 +206,8 @@ __device__ __forceinline__ void sflux(const Phys& ph, const Prim<DIM>& l, const 
   constexpr int V = DIM + 2;
   if constexpr (SURF == 5) {
     const double bl = l.rho * frcp(l.p), br = r.rho * frcp(r.p);
-    ec2<DIM>(ph, d, l.rho, l.v, l.p, log(l.rho), bl, log(bl), r.rho, r.v, r.p, log(r.rho), br,
-             log(br), f);
+    ec2<DIM>(ph, d, l.rho, l.v, l.p, flog(l.rho), bl, flog(bl), r.rho, r.v, r.p, flog(r.rho), br,
+             flog(br), f);
     return;
   }
   double fl[V], fr[V];
@@ -484,8 +484,9 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   const int cs = tid / NPC, l = tid % NPC;
   const int il[3] = {l % N1, (l / N1) % N1, l / (N1 * N1)};  // node position per axis
   dd acc_dh = dd_zero(), acc_h = dd_zero();
-  double dmax = 0.0;
-  bool dbad = false;
+  // max |d| as the bit pattern of |d| (non-negative doubles order like their
+  // bits; a NaN or inf lands at or above the infinity pattern)
+  unsigned long long dmax_bits = 0;
   const int ngroups = (a.n + CPB - 1) / CPB;
 
   // descriptor of one group (threads < CPB, one cell each) into buffer b
@@ -599,8 +600,8 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       own = prim_of<DIM>(ph, u);
       if (!prim_ok<DIM>(own)) report_bad(st, a.stage, a.ncells, m.gid ? m.gid[cell] : cell);
       be = own.rho * frcp(own.p);
-      lr = log(own.rho);
-      lb = log(be);
+      lr = flog(own.rho);
+      lb = flog(be);
       pr[S::RHO * T + tid] = own.rho;
 #pragma unroll
       for (int i = 0; i < DIM; ++i) pr[(S::V0 + i) * T + tid] = own.v[i];
@@ -825,8 +826,9 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
           const double dn = a.d_mode == 1 ? a.b * K[v] : fma(a.b, K[v], a.d[gi + v]);
           a.d[gi + v] = dn;
           if (a.want_dmax) {
-            dbad = dbad || !isfinite(dn);
-            dmax = fmax(dmax, fabs(dn));
+            const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(dn)) &
+                                         0x7fffffffffffffffULL;
+            dmax_bits = b > dmax_bits ? b : dmax_bits;
           }
         }
       }
@@ -836,9 +838,15 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
 
   // ---- grid epilogue --------------------------------------------------------
   if (a.want_dmax) {
-    dmax = warp_max(dmax);
-    if ((tid & 31) == 0) atomic_max_pos(&st->dmax_bits, dmax);
-    if (dbad) st->d_nonfinite = 1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_down_sync(0xffffffffu, dmax_bits, off);
+      dmax_bits = o > dmax_bits ? o : dmax_bits;
+    }
+    if ((tid & 31) == 0) {
+      if (dmax_bits >= 0x7ff0000000000000ULL) st->d_nonfinite = 1;
+      else atomicMax(&st->dmax_bits, dmax_bits);
+    }
   }
   dd v[2] = {acc_dh, acc_h}, tot[2];
   if (a.want_dh || a.want_h) block_reduce_dd<2>(v, s_red);
