@@ -48,7 +48,7 @@ struct StageGeo {
   static constexpr int NFP = 2 * DIM * FP;        // face points per cell
   static constexpr int T = 64;                    // threads per block
   static constexpr int CPB = T / NPC;             // cells per block (one node per thread)
-  static constexpr int NPR = DIM + 6;             // primitives per node (see slots)
+  static constexpr int NPR = DIM + 7;             // primitives per node (see slots)
   // shared memory (doubles)
   static constexpr int SM_PR = NPR * T;           // primitives, SoA [slot][cell*NPC+node]
   static constexpr int SM_NB = CPB * NFP * V;     // neighbour traces [cell][face][pt][var]
@@ -59,11 +59,12 @@ struct StageGeo {
   static constexpr int SM_PF = DIM * CPB * FP * 2 * V;  // distance-2 pair fluxes
 };
 
-// primitive slots: rho, v[DIM], p, E, log rho, beta, log beta
+// primitive slots: rho, v[DIM], p, E, log rho, beta, log beta, sound speed
+// (the last only for the Rusanov surface flux)
 template <int DIM>
 struct Slot {
   static constexpr int RHO = 0, V0 = 1, P = DIM + 1, E = DIM + 2, LRHO = DIM + 3,
-                       BETA = DIM + 4, LBETA = DIM + 5;
+                       BETA = DIM + 4, LBETA = DIM + 5, C = DIM + 6;
 };
 
 // a state in the primitive form the fluxes use
@@ -71,6 +72,22 @@ template <int DIM>
 struct Prim {
   double rho, v[DIM], p, E;
 };
+
+template <int DIM>
+__device__ __forceinline__ Prim<DIM> prim_of(const Phys& ph, const double* u, double& ir) {
+  Prim<DIM> q;
+  q.rho = u[0];
+  ir = frcp(u[0]);
+  double kin = 0.0;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    q.v[d] = u[1 + d] * ir;
+    kin = fma(u[1 + d], q.v[d], kin);
+  }
+  q.E = u[DIM + 1];
+  q.p = ph.gm1 * (q.E - 0.5 * kin);
+  return q;
+}
 
 template <int DIM>
 __device__ __forceinline__ Prim<DIM> prim_of(const Phys& ph, const double* u) {
@@ -272,6 +289,77 @@ __device__ __forceinline__ void sflux(const Phys& ph, const Prim<DIM>& l, const 
   }
 }
 
+// a[d] for a runtime direction d without a local-memory array
+template <int DIM, typename A>
+__device__ __forceinline__ double pick_rt(const A& a, int off, int d) {
+  if (DIM == 2) return d == 0 ? a[off] : a[off + 1];
+  return d == 0 ? a[off] : (d == 1 ? a[off + 1] : a[off + 2]);
+}
+
+// Rusanov (physics.cpp:52-59) or central (:46-50) surface flux at one face
+// point, runtime direction d, returned as the lifted contribution to the own
+// trace node (semidisc.cpp:489-556 strong form; weak form: the lift of f*
+// alone) plus the endpoint diagonal term -2J D_jj f(u_o) (:450-454).  With o
+// the own trace and n the neighbour's,
+//   f* - f(u_o) = 1/2 (f_n - f_o) + s 1/2 lam (u_n - u_o),
+// s = +1 when the own node is the right state (side 0) and -1 when it is the
+// left one (side 1), lam = max(|v_o,d| + c_o, |v_n,d| + c_n).  One code copy
+// for all faces (runtime d, side) keeps the kernel's instruction footprint
+// small.  Own primitives (and sound speed) come from shared memory; the
+// neighbour's conservative trace from registers.  Returns admissibility of
+// the neighbour's trace.
+template <int DIM, int SURF>
+__device__ __forceinline__ bool rus_lift(const Phys& ph, const double* pr, int oq,
+                                         const double (&un)[DIM + 2], int d, int side,
+                                         double cll, double sg, bool weak, double* out) {
+  using S = Slot<DIM>;
+  constexpr int V = DIM + 2, T = StageGeo<DIM>::T;
+  const double rn = un[0], En = un[V - 1];
+  const double irn = frcp(rn);
+  double vn[DIM], kin = 0.0;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    vn[i] = un[1 + i] * irn;
+    kin = fma(un[1 + i], vn[i], kin);
+  }
+  const double pn = ph.gm1 * (En - 0.5 * kin);
+  bool ok = rn > 0.0 && pn > 0.0 && isfinite(En);
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) ok = ok && isfinite(vn[i]);
+  const double ro = pr[S::RHO * T + oq], po = pr[S::P * T + oq], Eo = pr[S::E * T + oq];
+  double vo[DIM];
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) vo[i] = pr[(S::V0 + i) * T + oq];
+  const double vod = pick_rt<DIM>(vo, 0, d), vnd = pick_rt<DIM>(vn, 0, d);
+  const double mnd = pick_rt<DIM>(un, 1, d), mod = ro * vod;
+  double fo[V], g[V];
+  fo[0] = mod;
+  g[0] = 0.5 * (mnd - mod);
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    fo[1 + i] = fma(mod, vo[i], i == d ? po : 0.0);
+    g[1 + i] = 0.5 * (fma(mnd, vn[i], i == d ? pn : 0.0) - fo[1 + i]);
+  }
+  fo[V - 1] = (Eo + po) * vod;
+  g[V - 1] = 0.5 * ((En + pn) * vnd - fo[V - 1]);
+  if constexpr (SURF == 2) {
+    const double lam = fmax(fabs(vod) + pr[S::C * T + oq], fabs(vnd) + fsqrt(ph.gamma * pn * irn));
+    const double hl = side ? -0.5 * lam : 0.5 * lam;
+    g[0] = fma(hl, rn - ro, g[0]);
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) g[1 + i] = fma(hl, un[1 + i] - ro * vo[i], g[1 + i]);
+    g[V - 1] = fma(hl, En - Eo, g[V - 1]);
+  }
+  if (weak) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[v] = sg * (g[v] + fo[v]);
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[v] = fma(sg, g[v], -cll * fo[v]);
+  }
+  return ok;
+}
+
 template <int DIM>
 __device__ __forceinline__ int line_base(int d, int t1, int t2) {
   if (DIM == 2) return d == 0 ? N1 * t1 : t1;
@@ -345,7 +433,9 @@ __device__ __forceinline__ void dist2_pairs(const Phys& ph, const double* pr, do
   constexpr int NP = DIM * CPB * FP * 2;
 #pragma unroll
   for (int r = 0; r < (NP + T - 1) / T; ++r) {
-    const int p = tid + r * T;
+    // a partial last round goes to the upper warp: the surface phase's
+    // partial round (96 face points on 64 threads in 3D) runs on the lower one
+    const int p = (r ? tid ^ 32 : tid) + r * T;
     if (p >= NP) break;
     const int d = p / (CPB * FP * 2), rem = p % (CPB * FP * 2);
     const int c2 = rem / (FP * 2), li = (rem / 2) % FP, which = rem & 1;
@@ -597,8 +687,10 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
 #pragma unroll
         for (int v = 0; v < V; ++v) u[v] = fma(a1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
       }
-      own = prim_of<DIM>(ph, u);
+      double ir;
+      own = prim_of<DIM>(ph, u, ir);
       if (!prim_ok<DIM>(own)) report_bad(st, a.stage, a.ncells, m.gid ? m.gid[cell] : cell);
+      if constexpr (SURF == 2) pr[S::C * T + tid] = fsqrt(ph.gamma * own.p * ir);
       be = own.rho * frcp(own.p);
       lr = flog(own.rho);
       lb = flog(be);
@@ -679,6 +771,21 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       if (s_cell[c2] < 0) continue;
       const int own_q = c2 * NPC + line_base<DIM>(d, pt % N1, pt / N1) +
                         (side ? N1 - 1 : 0) * line_stride(d);
+      if constexpr (SURF == 0 || SURF == 2) {
+        const double J2 = s_J2[c2][d], lift = s_lift[c2][d];
+        const int j = side ? N1 - 1 : 0;
+        double o5[V];
+        const bool ok = rus_lift<DIM, SURF>(ph, pr, own_q, nbu[k], d, side, J2 * c_D[j * N1 + j],
+                                            side ? -lift : lift, SIMPLE && a.weak, o5);
+        if (!ok) {
+          const int nb = s_nbc[c2][f];  // global id of the neighbour, only on failure
+          report_bad(st, a.stage, a.ncells,
+                     nb < 0 ? m.ghost_gid[-1 - nb] : (m.gid ? m.gid[nb] : nb));
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) sf[q * V + v] = o5[v];
+        continue;
+      }
       Prim<DIM> o;
       o.rho = pr[S::RHO * T + own_q];
 #pragma unroll
