@@ -48,7 +48,7 @@ struct StageGeo {
   static constexpr int NFP = 2 * DIM * FP;        // face points per cell
   static constexpr int T = 64;                    // threads per block
   static constexpr int CPB = T / NPC;             // cells per block (one node per thread)
-  static constexpr int NPR = DIM + 7;             // primitives per node (see slots)
+  static constexpr int NPR = DIM + 5;             // primitives per node (see slots)
   // shared memory (doubles)
   static constexpr int SM_PR = NPR * T;           // primitives, SoA [slot][cell*NPC+node]
   static constexpr int SM_NB = CPB * NFP * V;     // neighbour traces [cell][face][pt][var]
@@ -59,12 +59,11 @@ struct StageGeo {
   static constexpr int SM_PF = DIM * CPB * FP * 2 * V;  // distance-2 pair fluxes
 };
 
-// primitive slots: rho, v[DIM], p, E, log rho, beta, log beta, sound speed
-// (the last only for the Rusanov surface flux)
+// primitive slots: rho, v[DIM], p, E, beta = rho / p, sound speed (the last
+// only for the Rusanov surface flux)
 template <int DIM>
 struct Slot {
-  static constexpr int RHO = 0, V0 = 1, P = DIM + 1, E = DIM + 2, LRHO = DIM + 3,
-                       BETA = DIM + 4, LBETA = DIM + 5, C = DIM + 6;
+  static constexpr int RHO = 0, V0 = 1, P = DIM + 1, E = DIM + 2, BETA = DIM + 3, C = DIM + 4;
 };
 
 // a state in the primitive form the fluxes use
@@ -130,14 +129,15 @@ __device__ __forceinline__ void pflux(const Prim<DIM>& q, int d, double* f) {
   f[DIM + 1] = (q.E + q.p) * vd;
 }
 
-// logmean (physics.cpp:30-38) with both logarithms precomputed.  Below the
-// reference's threshold u = ((a-b)/(a+b))^2 < 1e-4 the reference evaluates
+// logmean (physics.cpp:30-38).  Below the reference's threshold
+// u = ((a-b)/(a+b))^2 < 1e-4 the reference evaluates
 // 0.5 (a+b) / (1 + u/3 + u^2/5 + u^3/7); here the reciprocal of that
 // polynomial is taken as its series 1 - u/3 - 4u^2/45 - 44u^3/945 (the two
 // differ by O(u^4) < 1e-17 relative), so the branch needs no division and u
 // only to ~1e-12 relative (one Newton step on the reciprocal seed).  Above
-// it: (a - b) / (log a - log b).
-__device__ __forceinline__ double lmean(double a, double b, double la, double lb) {
+// it: (a - b) / (log a - log b), the logarithms evaluated in that branch only:
+// on smooth data (every pair of a TGV cell) no logarithm is taken at all.
+__device__ __forceinline__ double lmean(double a, double b) {
   const double s = a + b, dlt = a - b;
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
@@ -148,11 +148,11 @@ __device__ __forceinline__ double lmean(double a, double b, double la, double lb
     const double ip = fma(u, fma(u, fma(u, -44.0 / 945.0, -4.0 / 45.0), -1.0 / 3.0), 1.0);
     return 0.5 * s * ip;
   }
-  return dlt * frcp(la - lb);
+  return dlt * frcp(flog(a) - flog(b));
 }
 
 // 1 / logmean(a, b): 2 poly / (a + b) below the threshold
-__device__ __forceinline__ double inv_lmean(double a, double b, double la, double lb) {
+__device__ __forceinline__ double inv_lmean(double a, double b) {
   const double s = a + b, dlt = a - b;
   const double rs = frcp(s);
   const double f = dlt * rs;
@@ -161,17 +161,16 @@ __device__ __forceinline__ double inv_lmean(double a, double b, double la, doubl
     const double poly = fma(u, fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0), 1.0);
     return 2.0 * poly * rs;
   }
-  return (la - lb) * frcp(dlt);
+  return (flog(a) - flog(b)) * frcp(dlt);
 }
 
-// Ranocha EC flux (physics.cpp:157-179) from primitives + logs
+// Ranocha EC flux (physics.cpp:157-179) from primitives and beta = rho / p
 template <int DIM>
 __device__ __forceinline__ void ec2(const Phys& ph, int d, double rl, const double (&vl)[DIM],
-                                    double pl, double lrl, double bl, double lbl, double rr,
-                                    const double (&vr)[DIM], double pr, double lrr, double br,
-                                    double lbr, double* f) {
-  const double rho_log = lmean(rl, rr, lrl, lrr);
-  const double inv_b = inv_lmean(bl, br, lbl, lbr);
+                                    double pl, double bl, double rr, const double (&vr)[DIM],
+                                    double pr, double br, double* f) {
+  const double rho_log = lmean(rl, rr);
+  const double inv_b = inv_lmean(bl, br);
   double va[DIM], vlvr = 0.0;
 #pragma unroll
   for (int i = 0; i < DIM; ++i) {
@@ -223,8 +222,7 @@ __device__ __forceinline__ void sflux(const Phys& ph, const Prim<DIM>& l, const 
   constexpr int V = DIM + 2;
   if constexpr (SURF == 5) {
     const double bl = l.rho * frcp(l.p), br = r.rho * frcp(r.p);
-    ec2<DIM>(ph, d, l.rho, l.v, l.p, flog(l.rho), bl, flog(bl), r.rho, r.v, r.p, flog(r.rho), br,
-             flog(br), f);
+    ec2<DIM>(ph, d, l.rho, l.v, l.p, bl, r.rho, r.v, r.p, br, f);
     return;
   }
   double fl[V], fr[V];
@@ -377,7 +375,7 @@ __device__ __forceinline__ int pick_int3(const int (&a)[3], int i) {
 template <int DIM, int D>
 __device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, int tid,
                                              const int (&il)[3], double J2, const Prim<DIM>& own,
-                                             double lr, double be, double lb, double* K,
+                                             double be, double* K,
                                              double* zf = nullptr) {
   using G = StageGeo<DIM>;
   using S = Slot<DIM>;
@@ -396,9 +394,8 @@ __device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, i
     double vk[DIM];
 #pragma unroll
     for (int i = 0; i < DIM; ++i) vk[i] = pr[(S::V0 + i) * T + qk];
-    ec2<DIM>(ph, D, own.rho, own.v, own.p, lr, be, lb, pr[S::RHO * T + qk], vk,
-             pr[S::P * T + qk], pr[S::LRHO * T + qk], pr[S::BETA * T + qk],
-             pr[S::LBETA * T + qk], f);
+    ec2<DIM>(ph, D, own.rho, own.v, own.p, be, pr[S::RHO * T + qk], vk, pr[S::P * T + qk],
+             pr[S::BETA * T + qk], f);
   };
   // the distance-2 pair (j, j+2) is evaluated once per pair by dist2_pairs
   // and gathered after the block's next barrier (dist2_gather)
@@ -450,10 +447,8 @@ __device__ __forceinline__ void dist2_pairs(const Phys& ph, const double* pr, do
     double f[V];
     auto run = [&](auto dc) {
       constexpr int Dd = decltype(dc)::value;
-      ec2<DIM>(ph, Dd, pr[S::RHO * T + lo], vl, pr[S::P * T + lo], pr[S::LRHO * T + lo],
-               pr[S::BETA * T + lo], pr[S::LBETA * T + lo], pr[S::RHO * T + hi], vr,
-               pr[S::P * T + hi], pr[S::LRHO * T + hi], pr[S::BETA * T + hi],
-               pr[S::LBETA * T + hi], f);
+      ec2<DIM>(ph, Dd, pr[S::RHO * T + lo], vl, pr[S::P * T + lo], pr[S::BETA * T + lo],
+               pr[S::RHO * T + hi], vr, pr[S::P * T + hi], pr[S::BETA * T + hi], f);
     };
     if (d == 0)
       run(std::integral_constant<int, 0>{});
@@ -557,7 +552,6 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   // group descriptors, double-buffered: the next group's are written while
   // the current one computes
   __shared__ int s_cell_[2][CPB];
-  __shared__ int s_coord_[2][CPB][3];
   __shared__ double s_ca1_[2][CPB];
   __shared__ signed char s_cform_[2][CPB];
   __shared__ int s_lev_[2][CPB];
@@ -582,42 +576,35 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   // descriptor of one group (threads < CPB, one cell each) into buffer b
   auto describe = [&](int b, int t, int cell) {
       s_cell_[b][t] = cell;
-      const int cc = cell < 0 ? 0 : cell;               // local cell
-      const int g = m.gid ? m.gid[cc] : cc;             // global cell
-      int co[3] = {g % m.nc[0], (g / m.nc[0]) % m.nc[1], g / (m.nc[0] * m.nc[1])};
-      s_coord_[b][t][0] = co[0];
-      s_coord_[b][t][1] = co[1];
-      s_coord_[b][t][2] = co[2];
+      const int cc = cell < 0 ? 0 : cell;  // local cell
+      // static record (host.cpp build_cell_records): 2 x int4 + 4 x double2
+      const int4* ri = reinterpret_cast<const int4*>(m.rec + cc);
+      const double2* rd = reinterpret_cast<const double2*>(m.rec + cc) + 2;
+      const int4 n0 = __ldg(ri), n1 = __ldg(ri + 1);
+      const double2 j01 = __ldg(rd), j2l0 = __ldg(rd + 1), l12 = __ldg(rd + 2), ms = __ldg(rd + 3);
       const int lev = m.level[cc];
       s_ca1_[b][t] = dt * a.a1[lev];
       s_cform_[b][t] = a.formed[lev];
       s_lev_[b][t] = lev;
-      s_meas_[b][t] = DIM == 2 ? 0.25 * m.h[0][co[0]] * m.h[1][co[1]]
-                               : 0.125 * m.h[0][co[0]] * m.h[1][co[1]] * m.h[2][co[2]];
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        s_J2_[b][t][d] = 2.0 * m.jac[d][co[d]];
-        s_lift_[b][t][d] = m.lift[d][co[d]];
+      s_meas_[b][t] = ms.x;
+      s_J2_[b][t][0] = j01.x;
+      s_J2_[b][t][1] = j01.y;
+      s_lift_[b][t][0] = j2l0.y;
+      s_lift_[b][t][1] = l12.x;
+      if (DIM == 3) {
+        s_J2_[b][t][DIM - 1] = j2l0.x;
+        s_lift_[b][t][DIM - 1] = l12.y;
       }
+      const int nb[6] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y};
 #pragma unroll
-      for (int f = 0; f < 2 * DIM; ++f) {  // face neighbours (periodic / table / ghost), rows
-        int nbc;
-        if (m.nbr) {
-          nbc = m.nbr[static_cast<size_t>(cc) * 2 * DIM + f];
-        } else {
-          const int d = f >> 1, side = f & 1;
-          int c3[3] = {co[0], co[1], co[2]};
-          const int nd = m.nc[d];
-          c3[d] = side ? (c3[d] + 1 == nd ? 0 : c3[d] + 1) : (c3[d] == 0 ? nd - 1 : c3[d] - 1);
-          nbc = c3[0] + m.nc[0] * (c3[1] + m.nc[1] * c3[2]);
-        }
+      for (int f = 0; f < 2 * DIM; ++f) {  // face neighbours (local or ghost slot), rows
+        const int nbc = nb[f];
+        s_nbc_[b][t][f] = nbc;
         if (nbc < 0) {  // trace formed and sent by the neighbour's owner
-          s_nbc_[b][t][f] = nbc;
           s_na1_[b][t][f] = 0.0;
           s_nform_[b][t][f] = 1;
         } else {
           const int l2 = m.level[nbc];
-          s_nbc_[b][t][f] = nbc;
           s_na1_[b][t][f] = dt * a.a1[l2];
           s_nform_[b][t][f] = a.formed[l2];
         }
@@ -634,7 +621,6 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
   int buf = 0;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf ^= 1) {
     auto& s_cell = s_cell_[buf];
-    auto& s_coord = s_coord_[buf];
     auto& s_ca1 = s_ca1_[buf];
     auto& s_cform = s_cform_[buf];
     auto& s_lev = s_lev_[buf];
@@ -670,7 +656,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
     own.E = 2.5;
 #pragma unroll
     for (int i = 0; i < DIM; ++i) own.v[i] = 0.0;
-    double lr = 0.0, be = 1.0, lb = 0.0;
+    double be = 1.0;
     if (cell >= 0) {
       const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
       double u[V];
@@ -692,16 +678,12 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       if (!prim_ok<DIM>(own)) report_bad(st, a.stage, a.ncells, m.gid ? m.gid[cell] : cell);
       if constexpr (SURF == 2) pr[S::C * T + tid] = fsqrt(ph.gamma * own.p * ir);
       be = own.rho * frcp(own.p);
-      lr = flog(own.rho);
-      lb = flog(be);
       pr[S::RHO * T + tid] = own.rho;
 #pragma unroll
       for (int i = 0; i < DIM; ++i) pr[(S::V0 + i) * T + tid] = own.v[i];
       pr[S::P * T + tid] = own.p;
       pr[S::E * T + tid] = own.E;
-      pr[S::LRHO * T + tid] = lr;
       pr[S::BETA * T + tid] = be;
-      pr[S::LBETA * T + tid] = lb;
     }
     // ---- this thread's face points: the neighbour's trace, formed with the
     // neighbour's row (or received from the neighbouring slab), kept in
@@ -834,10 +816,10 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       simple_volume<DIM, 1>(pr, tid, il, s_J2[cs][1], own, a.weak, K);
       if constexpr (DIM == 3) simple_volume<DIM, DIM - 1>(pr, tid, il, s_J2[cs][DIM - 1], own, a.weak, K);
     } else {
-      volume_terms<DIM, 0>(ph, pr, tid, il, s_J2[cs][0], own, lr, be, lb, K);
-      volume_terms<DIM, 1>(ph, pr, tid, il, s_J2[cs][1], own, lr, be, lb, K);
+      volume_terms<DIM, 0>(ph, pr, tid, il, s_J2[cs][0], own, be, K);
+      volume_terms<DIM, 1>(ph, pr, tid, il, s_J2[cs][1], own, be, K);
       if constexpr (DIM == 3)
-        volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, lr, be, lb, K, zf);
+        volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, be, K, zf);
       dist2_pairs<DIM>(ph, pr, pf, tid);
     }
     if (dt_t >= 0) describe(buf ^ 1, dt_t, nx_cell);  // the next group, off the critical path
@@ -892,7 +874,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
       // ---- epilogue: entropy products, K and d stores (coalesced) -------------
       if (a.want_dh || a.want_h) {
         // log(p / rho^gamma) = -(log beta + (gamma - 1) log rho)
-        const double s_therm = -(lb + ph.gm1 * lr);
+        const double s_therm = -(flog(be) + ph.gm1 * flog(own.rho));
         // node_measure (semidisc.cpp:67) with the cell factor from the descriptor
         const double om = DIM == 2 ? s_meas[cs] * c_w[il[0]] * c_w[il[1]]
                                    : s_meas[cs] * c_w[il[0]] * c_w[il[1]] * c_w[il[2]];

@@ -335,6 +335,7 @@ struct perrk_ctx {
   std::vector<int> gid;    // local -> global cell
   std::vector<int> nbr_h;  // [local][2 dim]: local neighbour or -1 - ghost slot
   int *d_gid = nullptr, *d_nbr = nullptr, *d_send = nullptr;
+  dev::CellRec* d_rec = nullptr;  // static per-cell descriptors of the stage kernel
   long long* d_ghost_gid = nullptr;
   double *ghost = nullptr, *sendbuf = nullptr;  // [slot][FP][V], [entry][FP][V]
   std::vector<int> peers;                       // ascending
@@ -367,6 +368,7 @@ struct perrk_ctx {
     }
     m.dim = dim;
     m.level = dlevel;
+    m.rec = d_rec;
     if (slab) {
       m.gid = d_gid;
       m.nbr = d_nbr;
@@ -841,6 +843,39 @@ long long face_neighbour(int dim, const int* n, long long g, int f) {
   return co[0] + n[0] * (co[1] + static_cast<long long>(n[1]) * co[2]);
 }
 
+// Static per-cell descriptors of the stage kernel (dev::CellRec): face
+// neighbours (periodic, or the halo plan's local / ghost slots), global id
+// and the per-axis geometry factors of semidisc.cpp:50-70, 503, 513.
+void build_cell_records(perrk_ctx* c) {
+  const long long n = c->ncells;
+  const int nf = 2 * c->dim;
+  const double w0 = c->basis.w[0];
+  std::vector<dev::CellRec> r(static_cast<size_t>(n));
+  for (long long i = 0; i < n; ++i) {
+    const long long g = c->slab ? c->gid[i] : i;
+    const long long co[3] = {g % c->nc[0], (g / c->nc[0]) % c->nc[1],
+                             g / (static_cast<long long>(c->nc[0]) * c->nc[1])};
+    dev::CellRec& q = r[static_cast<size_t>(i)];
+    q = dev::CellRec{};
+    for (int f = 0; f < nf; ++f)
+      q.nb[f] = c->slab ? c->nbr_h[static_cast<size_t>(i) * nf + f]
+                        : static_cast<int>(face_neighbour(c->dim, c->nc, g, f));
+    q.gid = static_cast<int>(g);
+    double meas = 1.0;
+    for (int a = 0; a < c->dim; ++a) {
+      const double h = c->h[a][co[a]];
+      q.J2[a] = 2.0 * (2.0 / h);
+      q.lift[a] = 2.0 / (h * w0);  // semidisc.cpp:503,513
+      meas *= 0.5 * h;
+    }
+    q.meas = meas;
+  }
+  if (c->d_rec) cudaFree(c->d_rec);
+  c->d_rec = nullptr;
+  CK(cudaMalloc(&c->d_rec, sizeof(dev::CellRec) * r.size()));
+  CK(cudaMemcpy(c->d_rec, r.data(), sizeof(dev::CellRec) * r.size(), cudaMemcpyHostToDevice));
+}
+
 // Halo plan of one rank for an ownership map: the local cells (ascending
 // global id), per local cell and face the local neighbour or a ghost slot, and
 // per peer (ascending) the ghost slots it fills and the (local cell, face)
@@ -967,6 +1002,7 @@ void make_partition(perrk_ctx* c, int rank, int nranks, const int* owner) {
   if (!h.ghost_gid.empty())
     CK(cudaMemcpy(c->d_ghost_gid, h.ghost_gid.data(), sizeof(long long) * h.ghost_gid.size(),
                   cudaMemcpyHostToDevice));
+  build_cell_records(c);
   CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -1129,6 +1165,7 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     c->group = std::make_shared<Group>();
     c->group->members = {c};
     CK(upload_basis(c->basis.D.data(), c->basis.w.data()));
+    build_cell_records(c);
     CK(cudaStreamSynchronize(c->stream));
     *out = c;
   });
@@ -1153,6 +1190,7 @@ int perrk_destroy(perrk_ctx* c) {
   for (int* p : {c->d_gid, c->d_nbr, c->d_send})
     if (p) cudaFree(p);
   if (c->d_ghost_gid) cudaFree(c->d_ghost_gid);
+  if (c->d_rec) cudaFree(c->d_rec);
   if (c->counter) cudaFree(c->counter);
   if (c->dint) cudaFree(c->dint);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
