@@ -33,6 +33,7 @@ def build(force=False, verbose=False):
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
            "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"),
+           *os.environ.get("PERRK_NVCC_FLAGS", "").split(),
            *[os.path.join(CSRC, f) for f in SOURCES],
            "-o", LIB + ".tmp", "-lcudart", "-lnccl"]
     r = subprocess.run(cmd, capture_output=True, text=True)

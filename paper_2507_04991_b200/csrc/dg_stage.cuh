@@ -32,6 +32,11 @@
 
 #include <type_traits>
 
+// resident stage blocks per SM the register allocation targets (64 threads each)
+#ifndef PERRK_STAGE_MINB
+#define PERRK_STAGE_MINB 10
+#endif
+
 namespace perrk {
 namespace dev {
 
@@ -137,7 +142,8 @@ __device__ __forceinline__ void pflux(const Prim<DIM>& q, int d, double* f) {
 // only to ~1e-12 relative (one Newton step on the reciprocal seed).  Above
 // it: (a - b) / (log a - log b), the logarithms evaluated in that branch only:
 // on smooth data (every pair of a TGV cell) no logarithm is taken at all.
-__device__ __forceinline__ double lmean(double a, double b) {
+__device__ __forceinline__ double lmean_q(double a, double b) {
+  // returns logmean(a, b) / 4 (the factor folded into the series coefficients)
   const double s = a + b, dlt = a - b;
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
@@ -145,45 +151,49 @@ __device__ __forceinline__ double lmean(double a, double b) {
   const double f = dlt * r;
   const double u = f * f;
   if (u < 1e-4) {
-    const double ip = fma(u, fma(u, fma(u, -44.0 / 945.0, -4.0 / 45.0), -1.0 / 3.0), 1.0);
-    return 0.5 * s * ip;
+    const double ip =
+        fma(u, fma(u, fma(u, -11.0 / 1890.0, -1.0 / 90.0), -1.0 / 24.0), 0.125);
+    return s * ip;
   }
-  return dlt * frcp(flog(a) - flog(b));
+  return 0.25 * (dlt * frcp(flog(a) - flog(b)));
 }
 
-// 1 / logmean(a, b): 2 poly / (a + b) below the threshold
-__device__ __forceinline__ double inv_lmean(double a, double b) {
+// k / logmean(a, b): 2 k poly / (a + b) below the threshold (k2 = 2 k)
+__device__ __forceinline__ double inv_lmean_k(double a, double b, double k2) {
   const double s = a + b, dlt = a - b;
   const double rs = frcp(s);
   const double f = dlt * rs;
   const double u = f * f;
   if (u < 1e-4) {
     const double poly = fma(u, fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0), 1.0);
-    return 2.0 * poly * rs;
+    return poly * (k2 * rs);
   }
-  return (flog(a) - flog(b)) * frcp(dlt);
+  return 0.5 * k2 * ((flog(a) - flog(b)) * frcp(dlt));
 }
 
-// Ranocha EC flux (physics.cpp:157-179) from primitives and beta = rho / p
+// Ranocha EC flux (physics.cpp:157-179) from primitives and beta = rho / p:
+// with sigma = v_l + v_r, t = logmean(rho) sigma_d / 4,
+//   f_rho = 2 t,  f_m,i = t sigma_i + delta_id (p_l + p_r) / 2,
+//   f_E = f_rho (v_l.v_r / 2 + 1 / ((gamma - 1) logmean(beta))) + (p_l v_r,d + p_r v_l,d) / 2
 template <int DIM>
 __device__ __forceinline__ void ec2(const Phys& ph, int d, double rl, const double (&vl)[DIM],
                                     double pl, double bl, double rr, const double (&vr)[DIM],
                                     double pr, double br, double* f) {
-  const double rho_log = lmean(rl, rr);
-  const double inv_b = inv_lmean(bl, br);
-  double va[DIM], vlvr = 0.0;
+  const double lq = lmean_q(rl, rr);
+  const double ib = inv_lmean_k(bl, br, 2.0 * ph.inv_gm1);
+  double sg[DIM], vlvr = 0.0;
 #pragma unroll
   for (int i = 0; i < DIM; ++i) {
-    va[i] = 0.5 * (vl[i] + vr[i]);
+    sg[i] = vl[i] + vr[i];
     vlvr = fma(vl[i], vr[i], vlvr);
   }
-  const double fr = rho_log * pick<DIM>(va, d);
+  const double t = lq * pick<DIM>(sg, d);
+  const double fr = t + t;
   f[0] = fr;
   const double pavg = 0.5 * (pl + pr);
 #pragma unroll
-  for (int i = 0; i < DIM; ++i) f[1 + i] = fr * va[i] + (i == d ? pavg : 0.0);
-  f[DIM + 1] = fr * (0.5 * vlvr + ph.inv_gm1 * inv_b) +
-               0.5 * (pl * pick<DIM>(vr, d) + pr * pick<DIM>(vl, d));
+  for (int i = 0; i < DIM; ++i) f[1 + i] = i == d ? fma(t, sg[i], pavg) : t * sg[i];
+  f[DIM + 1] = fma(fr, fma(0.5, vlvr, ib), 0.5 * fma(pl, pick<DIM>(vr, d), pr * pick<DIM>(vl, d)));
 }
 
 // Roe-average wave speed estimates (physics.cpp:181-203)
@@ -535,7 +545,7 @@ __device__ __forceinline__ void simple_volume(const double* pr, int tid, const i
 }
 
 template <int DIM, int SURF, bool VISC, bool SIMPLE>
-__global__ void __launch_bounds__(StageGeo<DIM>::T, 8)
+__global__ void __launch_bounds__(StageGeo<DIM>::T, PERRK_STAGE_MINB)
     stage_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
                  unsigned* counter) {
   using G = StageGeo<DIM>;
