@@ -545,7 +545,7 @@ __device__ __forceinline__ void simple_volume(const double* pr, int tid, const i
 }
 
 template <int DIM, int SURF, bool VISC, bool SIMPLE>
-__global__ void __launch_bounds__(StageGeo<DIM>::T, PERRK_STAGE_MINB)
+__global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PERRK_STAGE_MINB)
     stage_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
                  unsigned* counter) {
   using G = StageGeo<DIM>;
@@ -584,26 +584,27 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, PERRK_STAGE_MINB)
   const int ngroups = (a.n + CPB - 1) / CPB;
 
   // descriptor of one group (threads < CPB, one cell each) into buffer b
+  // group descriptor of one cell into buffer b from its static record
+  // (host.cpp build_cell_records: neighbours, geometry, levels; 6 vector loads)
   auto describe = [&](int b, int t, int cell) {
       s_cell_[b][t] = cell;
-      const int cc = cell < 0 ? 0 : cell;  // local cell
-      // static record (host.cpp build_cell_records): 2 x int4 + 4 x double2
-      const int4* ri = reinterpret_cast<const int4*>(m.rec + cc);
-      const double2* rd = reinterpret_cast<const double2*>(m.rec + cc) + 2;
+      if (cell < 0) return;
+      const int4* ri = reinterpret_cast<const int4*>(m.rec + cell);
+      const double2* rd = reinterpret_cast<const double2*>(m.rec + cell);
       const int4 n0 = __ldg(ri), n1 = __ldg(ri + 1);
-      const double2 j01 = __ldg(rd), j2l0 = __ldg(rd + 1), l12 = __ldg(rd + 2), ms = __ldg(rd + 3);
-      const int lev = m.level[cc];
+      const double2 j01 = __ldg(rd + 2), j2l0 = __ldg(rd + 3), l12 = __ldg(rd + 4),
+                    ml = __ldg(rd + 5);
+      const unsigned long long lv = static_cast<unsigned long long>(__double_as_longlong(ml.y));
+      const int lev = static_cast<int>(lv & 0xff);
       s_ca1_[b][t] = dt * a.a1[lev];
       s_cform_[b][t] = a.formed[lev];
       s_lev_[b][t] = lev;
-      s_meas_[b][t] = ms.x;
-      s_J2_[b][t][0] = j01.x;
-      s_J2_[b][t][1] = j01.y;
-      s_lift_[b][t][0] = j2l0.y;
-      s_lift_[b][t][1] = l12.x;
-      if (DIM == 3) {
-        s_J2_[b][t][DIM - 1] = j2l0.x;
-        s_lift_[b][t][DIM - 1] = l12.y;
+      s_meas_[b][t] = ml.x;
+      const double J2[3] = {j01.x, j01.y, j2l0.x}, lift[3] = {j2l0.y, l12.x, l12.y};
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        s_J2_[b][t][d] = J2[d];
+        s_lift_[b][t][d] = lift[d];
       }
       const int nb[6] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y};
 #pragma unroll
@@ -614,7 +615,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, PERRK_STAGE_MINB)
           s_na1_[b][t][f] = 0.0;
           s_nform_[b][t][f] = 1;
         } else {
-          const int l2 = m.level[nbc];
+          const int l2 = static_cast<int>((lv >> (8 * (1 + f))) & 0xff);
           s_na1_[b][t][f] = dt * a.a1[l2];
           s_nform_[b][t][f] = a.formed[l2];
         }

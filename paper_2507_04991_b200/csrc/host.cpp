@@ -861,6 +861,11 @@ void build_cell_records(perrk_ctx* c) {
       q.nb[f] = c->slab ? c->nbr_h[static_cast<size_t>(i) * nf + f]
                         : static_cast<int>(face_neighbour(c->dim, c->nc, g, f));
     q.gid = static_cast<int>(g);
+    // levels (perrk_set_family; 1 before a family is set)
+    const bool lv = static_cast<long long>(c->eff.size()) == n;
+    q.lev[0] = static_cast<signed char>(lv ? c->eff[i] : 1);
+    for (int f = 0; f < nf; ++f)
+      q.lev[1 + f] = static_cast<signed char>(lv && q.nb[f] >= 0 ? c->eff[q.nb[f]] : 1);
     double meas = 1.0;
     for (int a = 0; a < c->dim; ++a) {
       const double h = c->h[a][co[a]];
@@ -1265,6 +1270,7 @@ int perrk_set_family(perrk_ctx* c, const perrk_family_desc* f, const int* eff) {
     std::vector<int8_t> lv(c->ncells);
     for (long long i = 0; i < c->ncells; ++i) lv[i] = static_cast<int8_t>(c->eff[i]);
     CK(cudaMemcpy(c->dlevel, lv.data(), c->ncells, cudaMemcpyHostToDevice));
+    build_cell_records(c);
     build_plan(c);
     c->has_family = true;
     c->plan_version += 1;
