@@ -142,33 +142,33 @@ __device__ __forceinline__ void pflux(const Prim<DIM>& q, int d, double* f) {
 // only to ~1e-12 relative (one Newton step on the reciprocal seed).  Above
 // it: (a - b) / (log a - log b), the logarithms evaluated in that branch only:
 // on smooth data (every pair of a TGV cell) no logarithm is taken at all.
-__device__ __forceinline__ double lmean_q(double a, double b) {
-  // returns logmean(a, b) / 4 (the factor folded into the series coefficients)
-  const double s = a + b, dlt = a - b;
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
-  r = fma(r, fma(-s, r, 1.0), r);
-  const double f = dlt * r;
-  const double u = f * f;
-  if (u < 1e-4) {
-    const double ip =
-        fma(u, fma(u, fma(u, -11.0 / 1890.0, -1.0 / 90.0), -1.0 / 24.0), 0.125);
-    return s * ip;
-  }
-  return 0.25 * (dlt * frcp(flog(a) - flog(b)));
-}
+// series coefficients and threshold in the constant bank: DFMA takes them as
+// c[][] operands (a literal double would be rebuilt in registers every use)
+__constant__ double c_lm[8] = {-11.0 / 1890.0, -1.0 / 90.0, -1.0 / 24.0, 0.125,
+                               1.0 / 7.0,      1.0 / 5.0,   1.0 / 3.0,   1e-4};
 
-// k / logmean(a, b): 2 k poly / (a + b) below the threshold (k2 = 2 k)
-__device__ __forceinline__ double inv_lmean_k(double a, double b, double k2) {
-  const double s = a + b, dlt = a - b;
-  const double rs = frcp(s);
-  const double f = dlt * rs;
-  const double u = f * f;
-  if (u < 1e-4) {
-    const double poly = fma(u, fma(u, fma(u, 1.0 / 7.0, 1.0 / 5.0), 1.0 / 3.0), 1.0);
-    return poly * (k2 * rs);
+// Both logarithmic means of one EC pair: lq = logmean(rl, rr) / 4 and
+// ib = k / logmean(bl, br) (k2 = 2 k).  The series (the factors folded into
+// its coefficients) is evaluated unconditionally; a warp vote sends the warp
+// to the logarithm branch only if one of its lanes has a pair above the
+// threshold, and there each lane keeps the reference's choice per value.
+__device__ __forceinline__ void lmeans(double rl, double rr, double bl, double br, double k2,
+                                       double& lq, double& ib) {
+  const double s1 = rl + rr, d1 = rl - rr;
+  double r1;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r1) : "d"(s1));
+  r1 = fma(r1, fma(-s1, r1, 1.0), r1);
+  const double f1 = d1 * r1, u1 = f1 * f1;
+  lq = s1 * fma(u1, fma(u1, fma(u1, c_lm[0], c_lm[1]), c_lm[2]), c_lm[3]);
+  const double s2 = bl + br, d2 = bl - br;
+  const double rs = frcp(s2);
+  const double f2 = d2 * rs, u2 = f2 * f2;
+  ib = fma(u2, fma(u2, fma(u2, c_lm[4], c_lm[5]), c_lm[6]), 1.0) * (k2 * rs);
+  const bool rough1 = !(u1 < c_lm[7]), rough2 = !(u2 < c_lm[7]);
+  if (__any_sync(__activemask(), rough1 || rough2)) {
+    if (rough1) lq = 0.25 * (d1 * frcp(flog(rl) - flog(rr)));
+    if (rough2) ib = 0.5 * k2 * ((flog(bl) - flog(br)) * frcp(d2));
   }
-  return 0.5 * k2 * ((flog(a) - flog(b)) * frcp(dlt));
 }
 
 // Ranocha EC flux (physics.cpp:157-179) from primitives and beta = rho / p:
@@ -179,8 +179,8 @@ template <int DIM>
 __device__ __forceinline__ void ec2(const Phys& ph, int d, double rl, const double (&vl)[DIM],
                                     double pl, double bl, double rr, const double (&vr)[DIM],
                                     double pr, double br, double* f) {
-  const double lq = lmean_q(rl, rr);
-  const double ib = inv_lmean_k(bl, br, 2.0 * ph.inv_gm1);
+  double lq, ib;
+  lmeans(rl, rr, bl, br, 2.0 * ph.inv_gm1, lq, ib);
   double sg[DIM], vlvr = 0.0;
 #pragma unroll
   for (int i = 0; i < DIM; ++i) {
