@@ -385,7 +385,7 @@ __device__ __forceinline__ int pick_int3(const int (&a)[3], int i) {
 template <int DIM, int D>
 __device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, int tid,
                                              const int (&il)[3], double J2, const Prim<DIM>& own,
-                                             double be, double* K,
+                                             double be, const double* cf, double* K,
                                              double* zf = nullptr) {
   using G = StageGeo<DIM>;
   using S = Slot<DIM>;
@@ -412,13 +412,13 @@ __device__ __forceinline__ void volume_terms(const Phys& ph, const double* pr, i
   const int kn = (j + 1) & (N1 - 1);
   double f1[V];
   ec_with(kn, f1);
-  const double cn = J2 * c_D[j * N1 + kn];
+  const double cn = J2 * cf[(3 * D) * T + tid];
 #pragma unroll
   for (int v = 0; v < V; ++v) K[v] = fma(-cn, f1[v], K[v]);
   if constexpr (D < 2) {
     const int kp = (j + N1 - 1) & (N1 - 1);
     const int src = (threadIdx.x & 31) + (kp - j) * stride;
-    const double cp = J2 * c_D[j * N1 + kp];
+    const double cp = J2 * cf[(3 * D + 1) * T + tid];
 #pragma unroll
     for (int v = 0; v < V; ++v) K[v] = fma(-cp, __shfl_sync(0xffffffffu, f1[v], src), K[v]);
   } else {
@@ -471,30 +471,61 @@ __device__ __forceinline__ void dist2_pairs(const Phys& ph, const double* pr, do
   }
 }
 
+// per-thread constants of the volume and gather phases, set once per launch
+// (kernel prologue) so the group loop reads them with fixed-offset shared
+// loads instead of re-deriving node indices: [3 d + 0/1/2][T] the SBP
+// coefficients D_{j,j+1}, D_{j,j-1}, D_{j,j^2} of the node's d-line, and
+// integer offsets (in doubles) of the node's distance-2 pair flux per d, of
+// its z-partner's published pair flux, and of its face slots per d (-1: the
+// node is not on a d-face).
 template <int DIM>
-__device__ __forceinline__ void dist2_gather(const double* pf, int cs, const int (&il)[3],
-                                             const double* J2, double* K) {
+struct ThreadTab {
+  static constexpr int NCF = 3 * DIM;
+  static constexpr int I_D2 = 0, I_ZF = DIM, I_FACE = DIM + 1, NI = 2 * DIM + 1;
+};
+
+template <int DIM>
+__device__ __forceinline__ void thread_tab_init(double* cf, int* ti, int tid, int cs,
+                                                const int (&il)[3]) {
   using G = StageGeo<DIM>;
-  constexpr int V = G::V, FP = G::FP, CPB = G::CPB;
+  using TT = ThreadTab<DIM>;
+  constexpr int V = G::V, FP = G::FP, CPB = G::CPB, T = G::T, NFP = G::NFP;
 #pragma unroll
   for (int d = 0; d < DIM; ++d) {
-    const int j = il[d], k2 = j ^ 2;
+    const int j = il[d];
+    cf[(3 * d + 0) * T + tid] = c_D[j * N1 + ((j + 1) & (N1 - 1))];
+    cf[(3 * d + 1) * T + tid] = c_D[j * N1 + ((j + N1 - 1) & (N1 - 1))];
+    cf[(3 * d + 2) * T + tid] = c_D[j * N1 + (j ^ 2)];
     const int li = d == 0 ? il[1] + N1 * il[2] : (d == 1 ? il[0] + N1 * il[2] : il[0] + N1 * il[1]);
-    const int p = ((d * CPB + cs) * FP + li) * 2 + (j & 1);
-    const double c2 = J2[d] * c_D[j * N1 + k2];
+    ti[(TT::I_D2 + d) * T + tid] = (((d * CPB + cs) * FP + li) * 2 + (j & 1)) * V;
+    ti[(TT::I_FACE + d) * T + tid] =
+        (j == 0 || j == N1 - 1) ? ((cs * NFP + (2 * d + (j ? 1 : 0)) * FP) + li) * V : -1;
+  }
+  const int jz = il[2], kz = (jz + N1 - 1) & (N1 - 1);
+  ti[TT::I_ZF * T + tid] = (tid + (kz - jz) * N1 * N1) * V;
+}
+
+template <int DIM>
+__device__ __forceinline__ void dist2_gather(const double* pf, const double* cf, const int* ti,
+                                             int tid, const double* J2, double* K) {
+  using G = StageGeo<DIM>;
+  constexpr int V = G::V, T = G::T;
 #pragma unroll
-    for (int v = 0; v < V; ++v) K[v] = fma(-c2, pf[p * V + v], K[v]);
+  for (int d = 0; d < DIM; ++d) {
+    const double c2 = J2[d] * cf[(3 * d + 2) * T + tid];
+    const double* f = pf + ti[(ThreadTab<DIM>::I_D2 + d) * T + tid];
+#pragma unroll
+    for (int v = 0; v < V; ++v) K[v] = fma(-c2, f[v], K[v]);
   }
 }
 
 // the z-partner's published pair flux f(j-1, j) (after a block barrier)
 template <int DIM>
-__device__ __forceinline__ void zf_gather(const double* zf, int tid, const int (&il)[3],
-                                          double J2, double* K) {
-  constexpr int V = DIM + 2, stride = N1 * N1;
-  const int j = il[2], kp = (j + N1 - 1) & (N1 - 1);
-  const double cp = J2 * c_D[j * N1 + kp];
-  const double* f = zf + (tid + (kp - j) * stride) * V;
+__device__ __forceinline__ void zf_gather(const double* zf, const double* cf, const int* ti,
+                                          int tid, double J2, double* K) {
+  constexpr int V = DIM + 2, T = StageGeo<DIM>::T;
+  const double cp = J2 * cf[(3 * 2 + 1) * T + tid];
+  const double* f = zf + ti[ThreadTab<DIM>::I_ZF * T + tid];
 #pragma unroll
   for (int v = 0; v < V; ++v) K[v] = fma(-cp, f[v], K[v]);
 }
@@ -572,11 +603,15 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
   __shared__ signed char s_nform_[2][CPB][2 * DIM];
   __shared__ double s_red[2 * 2 * (T / 32)];
 
+  __shared__ double s_cf[ThreadTab<DIM>::NCF * T];
+  __shared__ int s_ti[ThreadTab<DIM>::NI * T];
+
   if (st->aborted || st->finished) return;  // uniform across the grid
   const int tid = threadIdx.x;
   const double dt = st->dt;
   const int cs = tid / NPC, l = tid % NPC;
   const int il[3] = {l % N1, (l / N1) % N1, l / (N1 * N1)};  // node position per axis
+  thread_tab_init<DIM>(s_cf, s_ti, tid, cs, il);
   dd acc_dh = dd_zero(), acc_h = dd_zero();
   // max |d| as the bit pattern of |d| (non-negative doubles order like their
   // bits; a NaN or inf lands at or above the infinity pattern)
@@ -827,27 +862,26 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
       simple_volume<DIM, 1>(pr, tid, il, s_J2[cs][1], own, a.weak, K);
       if constexpr (DIM == 3) simple_volume<DIM, DIM - 1>(pr, tid, il, s_J2[cs][DIM - 1], own, a.weak, K);
     } else {
-      volume_terms<DIM, 0>(ph, pr, tid, il, s_J2[cs][0], own, be, K);
-      volume_terms<DIM, 1>(ph, pr, tid, il, s_J2[cs][1], own, be, K);
+      volume_terms<DIM, 0>(ph, pr, tid, il, s_J2[cs][0], own, be, s_cf, K);
+      volume_terms<DIM, 1>(ph, pr, tid, il, s_J2[cs][1], own, be, s_cf, K);
       if constexpr (DIM == 3)
-        volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, be, K, zf);
+        volume_terms<DIM, DIM - 1>(ph, pr, tid, il, s_J2[cs][DIM - 1], own, be, s_cf, K, zf);
       dist2_pairs<DIM>(ph, pr, pf, tid);
     }
     if (dt_t >= 0) describe(buf ^ 1, dt_t, nx_cell);  // the next group, off the critical path
     __syncthreads();  // surface terms of every face point visible
 
     if constexpr (!SIMPLE) {
-      if constexpr (DIM == 3) zf_gather<DIM>(zf, tid, il, s_J2[cs][DIM - 1], K);
-      dist2_gather<DIM>(pf, cs, il, s_J2[cs], K);
+      if constexpr (DIM == 3) zf_gather<DIM>(zf, s_cf, s_ti, tid, s_J2[cs][DIM - 1], K);
+      dist2_gather<DIM>(pf, s_cf, s_ti, tid, s_J2[cs], K);
     }
     if (cell >= 0) {
       // gather the node's face contributions (one per direction it ends)
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
-        const int j = il[d];
-        if (j == 0 || j == N1 - 1) {
-          const int pt = d == 0 ? il[1] + N1 * il[2] : (d == 1 ? il[0] + N1 * il[2] : il[0] + N1 * il[1]);
-          const double* c = sf + ((cs * 2 * DIM + 2 * d + (j ? 1 : 0)) * FP + pt) * V;
+        const int off = s_ti[(ThreadTab<DIM>::I_FACE + d) * T + tid];
+        if (off >= 0) {
+          const double* c = sf + off;
 #pragma unroll
           for (int v = 0; v < V; ++v) K[v] += c[v];
         }
