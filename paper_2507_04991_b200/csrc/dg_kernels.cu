@@ -68,6 +68,7 @@ __device__ __forceinline__ void report_bad(StepState* st, int stage, long long n
 }  // namespace perrk
 
 #include "dg_stage.cuh"
+#include "dg_stage3w.cuh"
 #include "dg_visc.cuh"
 #include "dg_advection.cuh"
 
@@ -874,7 +875,50 @@ static int stage_occ_d(int surf) {
   return 1;
 }
 
+// 3D EC volume with the Rusanov or central surface flux runs the warp-per-cell
+// kernel (dg_stage3w.cuh); every other variant the block-per-cell one
+static bool use_w3(int dim, int surf, int vol, bool visc) {
+#ifdef PERRK_NO_W3
+  (void)dim; (void)surf; (void)vol; (void)visc;
+  return false;
+#else
+  return dim == 3 && vol == VOL_EC && !visc && (surf == 0 || surf == 2);
+#endif
+}
+
+template <int SURF>
+static void configure_w3() {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(stage3w_kernel<SURF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(double) * W3::SM_TOTAL));
+    configured = true;
+  }
+}
+
+template <int SURF>
+static int w3_occ() {
+  configure_w3<SURF>();
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, stage3w_kernel<SURF>, W3::T,
+                                                sizeof(double) * W3::SM_TOTAL);
+  return n;
+}
+
+template <int SURF>
+static cudaError_t launch_w3(const StageArgs& a, const MeshDev& m, const Phys& ph, StepState* st,
+                             double* partials, unsigned* counter, int grid, cudaStream_t s) {
+  configure_w3<SURF>();
+  const int blocks = (a.n + W3::WPB - 1) / W3::WPB;
+  const int g = blocks < grid ? blocks : grid;
+  if (g <= 0) return cudaSuccess;
+  stage3w_kernel<SURF><<<g, W3::T, sizeof(double) * W3::SM_TOTAL, s>>>(a, m, ph, st, partials,
+                                                                       counter);
+  return cudaGetLastError();
+}
+
 int stage_blocks_per_sm(int dim, int surf, int vol) {
+  if (use_w3(dim, surf, vol, false)) return surf == 2 ? w3_occ<2>() : w3_occ<0>();
   const bool simple = vol != VOL_EC;
   if (dim == 2) return simple ? stage_occ_d<2, true>(surf) : stage_occ_d<2, false>(surf);
   return simple ? stage_occ_d<3, true>(surf) : stage_occ_d<3, false>(surf);
@@ -891,6 +935,9 @@ cudaError_t launch_stage(int dim, int surf, int vol, const StageArgs& a0, const 
     if (dim != 2 || vol != VOL_EC) return cudaErrorInvalidValue;
     return launch_stage_d<2, true, false>(surf, a, m, ph, st, partials, counter, grid, s);
   }
+  if (use_w3(dim, surf, vol, false))
+    return surf == 2 ? launch_w3<2>(a, m, ph, st, partials, counter, grid, s)
+                     : launch_w3<0>(a, m, ph, st, partials, counter, grid, s);
   if (vol == VOL_EC)
     return dim == 2 ? launch_stage_d<2, false, false>(surf, a, m, ph, st, partials, counter, grid, s)
                     : launch_stage_d<3, false, false>(surf, a, m, ph, st, partials, counter, grid, s);

@@ -1,0 +1,433 @@
+// Stage kernel, 3D Euler with the EC volume flux and the Rusanov / central
+// surface flux: one warp per cell, two LGL nodes per lane, no block barriers.
+//
+// Same work per active cell as stage_kernel (dg_stage.cuh; reference
+// semidisc.cpp:409-557 via rhs_masked :126-138, stepper.cpp:52-92 around it):
+// stage-state formation, flux-differencing volume term with the Ranocha EC
+// flux, surface flux + strong-form lift + endpoint diagonal term, b-stage
+// epilogue and the next stage's formed state.
+//
+// Mapping.  A 4x4x4 cell (node n = ix + 4 iy + 16 iz) is one warp: lane l
+// owns nodes A = l (iz = l >> 4 in {0, 1}) and B = l + 32 (iz + 2).  Then
+//   * x- and y-lines lie in groups of four lanes, once for the A layer and
+//     once for the B layer: each node evaluates its pair (j, j+1 mod 4) and
+//     receives (j-1, j) by shuffle; the distance-2 pairs of the two layers
+//     are split between the lanes (j < 2: the A pair, j >= 2: the B pair) and
+//     exchanged with a lane^2 (x) / lane^8 (y) shuffle;
+//   * z-lines pair lane l with lane l^16: the distance-2 pair (A, B) is inside
+//     the lane, and each node's (j, j+1 mod 4) pair goes to the partner lane
+//     by a lane^16 shuffle.
+// So every lane evaluates exactly 9 EC fluxes (4.5 per node, each pair once)
+// and 3 face points (96 per cell, one direction per round, compile time).
+// Warps never wait for one another: the cell's primitives and surface terms
+// live in the warp's own shared-memory slice, ordered by __syncwarp.  The
+// neighbours' face traces are staged into that slice with cp.async while the
+// volume terms are computed.
+#pragma once
+
+namespace perrk {
+namespace dev {
+
+struct W3 {
+  static constexpr int V = 5, NPC = 64, FP = 16, WPB = 4, T = 32 * WPB;
+  static constexpr int NPR = 8;  // rho, vx, vy, vz, p, E, beta, c
+  static constexpr int RHO = 0, VX = 1, P = 4, E = 5, BETA = 6, C = 7;
+  // per warp: primitives [NPR][64], face slots [3 rounds][32 lanes][2 arrays][V]
+  static constexpr int SM_PR = NPR * NPC;
+  static constexpr int SM_FS = 3 * 32 * 2 * V;
+  static constexpr int SM_WARP = SM_PR + SM_FS;
+  static constexpr int SM_TOTAL = WPB * SM_WARP;  // doubles per block
+};
+
+// rus_lift (dg_stage.cuh) reads the own trace's primitives with the
+// block-per-cell kernel's slot layout; the warp slice uses the same one
+static_assert(W3::RHO == Slot<3>::RHO && W3::VX == Slot<3>::V0 && W3::P == Slot<3>::P &&
+                  W3::E == Slot<3>::E && W3::BETA == Slot<3>::BETA && W3::C == Slot<3>::C &&
+                  W3::NPC == StageGeo<3>::T,
+              "warp slice layout must match Slot<3> / StageGeo<3>::T");
+
+#ifndef PERRK_W3_MINB
+#define PERRK_W3_MINB 4
+#endif
+
+// node on face (d, side) at face point pt (t1 + 4 t2, the line_base order)
+__device__ __forceinline__ int w3_face_node(int d, int side, int pt) {
+  const int t1 = pt & 3, t2 = pt >> 2;
+  return d == 0 ? 3 * side + 4 * t1 + 16 * t2
+                : (d == 1 ? t1 + 12 * side + 16 * t2 : t1 + 4 * t2 + 48 * side);
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+// EC flux between smem nodes p and q in direction D (compile time)
+template <int D>
+__device__ __forceinline__ void w3_ec(const Phys& ph, const double* pr, int p, int q, double* f) {
+  using S = W3;
+  constexpr int N = S::NPC;
+  const double vl[3] = {pr[S::VX * N + p], pr[(S::VX + 1) * N + p], pr[(S::VX + 2) * N + p]};
+  const double vr[3] = {pr[S::VX * N + q], pr[(S::VX + 1) * N + q], pr[(S::VX + 2) * N + q]};
+  ec2<3>(ph, D, pr[S::RHO * N + p], vl, pr[S::P * N + p], pr[S::BETA * N + p], pr[S::RHO * N + q],
+         vr, pr[S::P * N + q], pr[S::BETA * N + q], f);
+}
+
+// x / y lines (D = 0, 1): the lane's two layers.  Each node evaluates
+// f(j, j+1 mod 4) and receives f(j-1, j); the distance-2 pairs: lanes with
+// j < 2 evaluate the A layer's (j, j+2), lanes with j >= 2 the B layer's
+// (j-2, j), exchanged with the lane 2 stride(D) positions away.
+template <int D>
+__device__ __forceinline__ void w3_inplane(const Phys& ph, const double* pr, int lane, int j,
+                                           double J2, double* KA, double* KB) {
+  constexpr int V = W3::V;
+  constexpr int st = D == 0 ? 1 : 4;  // lane / node stride along the line
+  const int kn = (j + 1) & 3, kp = (j + 3) & 3;
+  const double cn = J2 * c_D[j * N1 + kn], cp = J2 * c_D[j * N1 + kp], c2 = J2 * c_D[j * N1 + (j ^ 2)];
+  const int pn = lane + (kn - j) * st;  // partner lane for (j, j+1)
+  const int src = lane + (kp - j) * st;
+  double f[V];
+  // A layer
+  w3_ec<D>(ph, pr, lane, pn, f);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    KA[v] = fma(-cn, f[v], KA[v]);
+    KA[v] = fma(-cp, __shfl_sync(0xffffffffu, f[v], src), KA[v]);
+  }
+  // B layer
+  w3_ec<D>(ph, pr, lane + 32, pn + 32, f);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    KB[v] = fma(-cn, f[v], KB[v]);
+    KB[v] = fma(-cp, __shfl_sync(0xffffffffu, f[v], src), KB[v]);
+  }
+  // distance 2: j < 2 -> (A_j, A_j+2); j >= 2 -> (B_j, B_j-2)
+  const bool lo = j < 2;
+  const int own = lo ? lane : lane + 32;
+  w3_ec<D>(ph, pr, own, own ^ (2 * st), f);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double r = __shfl_xor_sync(0xffffffffu, f[v], 2 * st);
+    KA[v] = fma(-c2, lo ? f[v] : r, KA[v]);
+    KB[v] = fma(-c2, lo ? r : f[v], KB[v]);
+  }
+}
+
+// z lines: lane l holds z = zA and zA + 2, lane l^16 the other two.
+template <bool DUMMY = true>
+__device__ __forceinline__ void w3_z(const Phys& ph, const double* pr, int lane, int zA,
+                                     double J2, double* KA, double* KB) {
+  constexpr int V = W3::V;
+  const int zB = zA + 2;
+  double f[V];
+  // distance 2 inside the lane: (A, B)
+  w3_ec<2>(ph, pr, lane, lane + 32, f);
+  const double cab = J2 * c_D[zA * N1 + zB], cba = J2 * c_D[zB * N1 + zA];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    KA[v] = fma(-cab, f[v], KA[v]);
+    KB[v] = fma(-cba, f[v], KB[v]);
+  }
+  // (j, j+1 mod 4) of both nodes; partner lane l^16 holds the j+1 nodes:
+  // zA = 0: A(0)-A'(1), B(2)-B'(3);  zA = 1: A(1)-B'(2), B(3)-A'(0)
+  const int pl = lane ^ 16;
+  const int pA = zA ? pl + 32 : pl, pB = zA ? pl : pl + 32;
+  const double cnA = J2 * c_D[zA * N1 + ((zA + 1) & 3)], cnB = J2 * c_D[zB * N1 + ((zB + 1) & 3)];
+  const double cpA = J2 * c_D[zA * N1 + ((zA + 3) & 3)], cpB = J2 * c_D[zB * N1 + ((zB + 3) & 3)];
+  double g[V];
+  w3_ec<2>(ph, pr, lane, pA, f);       // A's (j, j+1): to the partner's node pA
+  w3_ec<2>(ph, pr, lane + 32, pB, g);  // B's (j, j+1): to the partner's node pB
+  // received: the partner's pair ending at my node.  Partner zA' = 1 - zA:
+  // zA = 0 -> its A pair (1,2) ends at my B, its B pair (3,0) at my A;
+  // zA = 1 -> its A pair (0,1) ends at my A, its B pair (2,3) at my B.
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double rA = __shfl_xor_sync(0xffffffffu, f[v], 16);
+    const double rB = __shfl_xor_sync(0xffffffffu, g[v], 16);
+    KA[v] = fma(-cnA, f[v], KA[v]);
+    KB[v] = fma(-cnB, g[v], KB[v]);
+    KA[v] = fma(-cpA, zA ? rA : rB, KA[v]);
+    KB[v] = fma(-cpB, zA ? rB : rA, KB[v]);
+  }
+}
+
+template <int SURF>
+__global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
+    stage3w_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
+                   unsigned* counter) {
+  using S = W3;
+  constexpr int V = S::V, N = S::NPC, FP = S::FP;
+  extern __shared__ double smem[];
+  __shared__ double s_red[2 * 2 * S::WPB];
+  if (st->aborted || st->finished) return;  // uniform across the grid
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* pr = smem + wib * S::SM_WARP;  // [NPR][64]
+  double* fs = pr + S::SM_PR;            // [3][32][2][V]: staged traces, then surface terms
+  const double dt = st->dt;
+  const int ix = lane & 3, iy = (lane >> 2) & 3, zA = lane >> 4, zB = zA + 2;
+  const int side = zA, pt = lane & 15;
+  dd acc_dh = dd_zero(), acc_h = dd_zero();
+  unsigned long long dmax_bits = 0;
+  const int nw = gridDim.x * S::WPB;
+  int slot = blockIdx.x * S::WPB + wib;
+  int cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
+
+  while (cell >= 0) {
+    // next cell: list entry now, its state arrays to L2 (bulk prefetch)
+    const int nslot = slot + nw;
+    const int ncell = nslot < a.n ? (a.list ? a.list[nslot] : nslot) : -1;
+    if (lane == 0 && ncell >= 0) {
+      constexpr unsigned kBytes = N * V * sizeof(double);
+      const size_t off = static_cast<size_t>(ncell) * N * V;
+      if (a.form) l2_prefetch(a.Us + off, kBytes);
+      l2_prefetch(a.U + off, kBytes);
+      if (a.write_next && a.form) l2_prefetch(a.K1 + off, kBytes);
+      if (a.d_mode == 2) l2_prefetch(a.d + off, kBytes);
+    }
+    // ---- descriptor (host.cpp build_cell_records) ---------------------------
+    const CellRec* rp = m.rec + cell;
+    const unsigned long long lv =
+        static_cast<unsigned long long>(__ldg(reinterpret_cast<const long long*>(rp->lev)));
+    const int lev = static_cast<int>(lv & 0xff);
+    const double J2x = __ldg(&rp->J2[0]), J2y = __ldg(&rp->J2[1]), J2z = __ldg(&rp->J2[2]);
+    // ---- own nodes A, B: formed stage state (stepper.cpp:60-72) -------------
+    const size_t gA = (static_cast<size_t>(cell) * N + lane) * V, gB = gA + 32 * V;
+    double uA[V], uB[V];
+    if (!a.form) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        uA[v] = __ldg(a.U + gA + v);
+        uB[v] = __ldg(a.U + gB + v);
+      }
+    } else if (a.formed[lev]) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        uA[v] = __ldg(a.Us + gA + v);
+        uB[v] = __ldg(a.Us + gB + v);
+      }
+    } else {
+      const double a1 = dt * a.a1[lev];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        uA[v] = fma(a1, __ldg(a.K1 + gA + v), __ldg(a.U + gA + v));
+        uB[v] = fma(a1, __ldg(a.K1 + gB + v), __ldg(a.U + gB + v));
+      }
+    }
+    // ---- neighbour face traces -> the warp's face slots (cp.async), one
+    // direction per round: round d, face 2 d + side, point pt -------------------
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int nbc = __ldg(&rp->nb[2 * d + side]);
+      double* dst = fs + (d * 32 + lane) * 2 * V;
+      if (nbc < 0) {
+        const double* g = m.ghost + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
+#pragma unroll
+        for (int v = 0; v < V; ++v) cp_async8(dst + v, g + v);
+      } else {
+        const size_t gi = (static_cast<size_t>(nbc) * N + w3_face_node(d, 1 - side, pt)) * V;
+        const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
+        if (!a.form) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) cp_async8(dst + v, a.U + gi + v);
+        } else if (a.formed[l2]) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) cp_async8(dst + v, a.Us + gi + v);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            cp_async8(dst + v, a.U + gi + v);
+            cp_async8(dst + V + v, a.K1 + gi + v);
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    // ---- primitives of A and B -> the warp's slice -------------------------
+    bool okAB = true;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int n = lane + 32 * h;
+      double ir;
+      const Prim<3> q = prim_of<3>(ph, h ? uB : uA, ir);
+      okAB = okAB && prim_ok<3>(q);
+      pr[S::RHO * N + n] = q.rho;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) pr[(S::VX + i) * N + n] = q.v[i];
+      pr[S::P * N + n] = q.p;
+      pr[S::E * N + n] = q.E;
+      pr[S::BETA * N + n] = q.rho * frcp(q.p);
+      if constexpr (SURF == 2) pr[S::C * N + n] = fsqrt(ph.gamma * q.p * ir);
+    }
+    if (!okAB) report_bad(st, a.stage, a.ncells, m.gid ? m.gid[cell] : cell);
+    __syncwarp();
+
+    // ---- flux-differencing volume terms (semidisc.cpp:455-464) --------------
+    double KA[V], KB[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) KA[v] = KB[v] = 0.0;
+    w3_inplane<0>(ph, pr, lane, ix, J2x, KA, KB);
+    w3_inplane<1>(ph, pr, lane, iy, J2y, KA, KB);
+    w3_z(ph, pr, lane, zA, J2z, KA, KB);
+
+    // ---- surface flux + lift + endpoint diagonal at the lane's three face
+    // points (semidisc.cpp:489-556, :450-454) ---------------------------------
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double* slotp = fs + (d * 32 + lane) * 2 * V;
+      const int nbc = __ldg(&rp->nb[2 * d + side]);
+      double un[V];
+      if (nbc >= 0 && a.form) {
+        const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
+        if (a.formed[l2]) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) un[v] = slotp[v];
+        } else {
+          const double b1 = dt * a.a1[l2];
+#pragma unroll
+          for (int v = 0; v < V; ++v) un[v] = fma(b1, slotp[V + v], slotp[v]);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) un[v] = slotp[v];
+      }
+      const double J2 = d == 0 ? J2x : (d == 1 ? J2y : J2z);
+      const double lift = __ldg(&rp->lift[d]);
+      const int j = side ? N1 - 1 : 0;
+      double o5[V];
+      const bool ok = rus_lift<3, SURF>(ph, pr, w3_face_node(d, side, pt), un, d, side,
+                                        J2 * c_D[j * N1 + j], side ? -lift : lift, false, o5);
+      if (!ok)
+        report_bad(st, a.stage, a.ncells,
+                   nbc < 0 ? m.ghost_gid[-1 - nbc] : (m.gid ? m.gid[nbc] : nbc));
+#pragma unroll
+      for (int v = 0; v < V; ++v) slotp[v] = o5[v];
+    }
+    __syncwarp();
+    // gather: node A / B on face (d, side) takes the term of face point
+    // (d, side, pt(node, d)) = slot d * 32 + 16 side + pt
+    {
+      const int jA[3] = {ix, iy, zA}, jB[3] = {ix, iy, zB};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int ptA = d == 0 ? iy + 4 * zA : (d == 1 ? ix + 4 * zA : ix + 4 * iy);
+        const int ptB = d == 0 ? iy + 4 * zB : (d == 1 ? ix + 4 * zB : ix + 4 * iy);
+        if (jA[d] == 0 || jA[d] == N1 - 1) {
+          const double* c = fs + (d * 32 + 16 * (jA[d] ? 1 : 0) + ptA) * 2 * V;
+#pragma unroll
+          for (int v = 0; v < V; ++v) KA[v] += c[v];
+        }
+        if (jB[d] == 0 || jB[d] == N1 - 1) {
+          const double* c = fs + (d * 32 + 16 * (jB[d] ? 1 : 0) + ptB) * 2 * V;
+#pragma unroll
+          for (int v = 0; v < V; ++v) KB[v] += c[v];
+        }
+      }
+    }
+
+    // ---- epilogue (stepper.cpp:52-55, 60-72, 89-92) ---------------------------
+    if (a.want_dh || a.want_h) {
+      const double meas = __ldg(&rp->meas);
+      const double wxy = c_w[ix] * c_w[iy];
+      // own primitives from the slice (not kept in registers across the volume phase)
+      auto node = [&](int n, const double* K, int iz) {
+        Prim<3> q;
+        q.rho = pr[S::RHO * N + n];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) q.v[i] = pr[(S::VX + i) * N + n];
+        const double be = pr[S::BETA * N + n];
+        const double s_therm = -(flog(be) + ph.gm1 * flog(q.rho));
+        const double om = meas * wxy * c_w[iz];
+        if (a.want_dh) {
+          double v2 = 0.0, dot = 0.0;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            v2 = fma(q.v[i], q.v[i], v2);
+            dot = fma(ph.gm1 * be * q.v[i], K[1 + i], dot);
+          }
+          dot = fma(ph.gamma - s_therm - 0.5 * ph.gm1 * be * v2, K[0], dot);
+          dot = fma(-ph.gm1 * be, K[V - 1], dot);
+          acc_dh = dd_add_prod(acc_dh, om, dot);
+        }
+        if (a.want_h) acc_h = dd_add_prod(acc_h, om, -q.rho * s_therm);
+      };
+      node(lane, KA, zA);
+      node(lane + 32, KB, zB);
+    }
+    if (a.write_k) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        a.Kout[gA + v] = KA[v];
+        a.Kout[gB + v] = KB[v];
+      }
+    }
+    if (a.write_next) {
+      const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
+      if (!a.form) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          a.Usn[gA + v] = fma(an, KA[v], __ldg(a.U + gA + v));
+          a.Usn[gB + v] = fma(an, KB[v], __ldg(a.U + gB + v));
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          a.Usn[gA + v] = __ldg(a.U + gA + v) + fma(an, __ldg(a.K1 + gA + v), pn * KA[v]);
+          a.Usn[gB + v] = __ldg(a.U + gB + v) + fma(an, __ldg(a.K1 + gB + v), pn * KB[v]);
+        }
+      }
+    }
+    if (a.d_mode) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const double dA = a.d_mode == 1 ? a.b * KA[v] : fma(a.b, KA[v], a.d[gA + v]);
+        const double dB = a.d_mode == 1 ? a.b * KB[v] : fma(a.b, KB[v], a.d[gB + v]);
+        a.d[gA + v] = dA;
+        a.d[gB + v] = dB;
+        if (a.want_dmax) {
+          const unsigned long long bA2 =
+              static_cast<unsigned long long>(__double_as_longlong(dA)) & 0x7fffffffffffffffULL;
+          const unsigned long long bB2 =
+              static_cast<unsigned long long>(__double_as_longlong(dB)) & 0x7fffffffffffffffULL;
+          dmax_bits = bA2 > dmax_bits ? bA2 : dmax_bits;
+          dmax_bits = bB2 > dmax_bits ? bB2 : dmax_bits;
+        }
+      }
+    }
+    __syncwarp();  // the slice is rewritten by the next cell
+    slot = nslot;
+    cell = ncell;
+  }
+
+  // ---- grid epilogue (as stage_kernel) --------------------------------------
+  if (a.want_dmax) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_down_sync(0xffffffffu, dmax_bits, off);
+      dmax_bits = o > dmax_bits ? o : dmax_bits;
+    }
+    if (lane == 0) {
+      if (dmax_bits >= 0x7ff0000000000000ULL) st->d_nonfinite = 1;
+      else atomicMax(&st->dmax_bits, dmax_bits);
+    }
+  }
+  dd v[2] = {acc_dh, acc_h}, tot[2];
+  if (a.want_dh || a.want_h) block_reduce_dd<2>(v, s_red);
+  if (grid_reduce_dd<2>(v, partials, counter, s_red, tot) && threadIdx.x == 0) {
+    if (a.want_dh) {
+      const dd inc = dd_mul_d(tot[0], dt * a.b);
+      const dd cur = {st->dh_hi, st->dh_lo};
+      const dd nw2 = dd_add(cur, inc);
+      st->dh_hi = nw2.hi;
+      st->dh_lo = nw2.lo;
+    }
+    if (a.want_h) {
+      st->h_hi = tot[1].hi;
+      st->h_lo = tot[1].lo;
+    }
+    if (st->bad_code != kNoBad) st->aborted = 1;
+  }
+}
+
+}  // namespace dev
+}  // namespace perrk
