@@ -32,10 +32,12 @@ struct W3 {
   static constexpr int V = 5, NPC = 64, FP = 16, WPB = 4, T = 32 * WPB;
   static constexpr int NPR = 8;  // rho, vx, vy, vz, p, E, beta, c
   static constexpr int RHO = 0, VX = 1, P = 4, E = 5, BETA = 6, C = 7;
-  // per warp: primitives [NPR][64], face slots [3 rounds][32 lanes][2 arrays][V]
+  // per warp: primitives [NPR][64], face slots [3 rounds][32 lanes][V], the
+  // cell's U and K1 for the epilogue's formation [2][64 V]
   static constexpr int SM_PR = NPR * NPC;
-  static constexpr int SM_FS = 3 * 32 * 2 * V;
-  static constexpr int SM_WARP = SM_PR + SM_FS;
+  static constexpr int SM_FS = 3 * 32 * V;
+  static constexpr int SM_EP = PERRK_W3_EPI_STAGE ? 2 * NPC * V : 0;
+  static constexpr int SM_WARP = SM_PR + SM_FS + SM_EP;
   static constexpr int SM_TOTAL = WPB * SM_WARP;  // doubles per block
 };
 
@@ -45,6 +47,10 @@ static_assert(W3::RHO == Slot<3>::RHO && W3::VX == Slot<3>::V0 && W3::P == Slot<
                   W3::E == Slot<3>::E && W3::BETA == Slot<3>::BETA && W3::C == Slot<3>::C &&
                   W3::NPC == StageGeo<3>::T,
               "warp slice layout must match Slot<3> / StageGeo<3>::T");
+
+#ifndef PERRK_W3_EPI_STAGE
+#define PERRK_W3_EPI_STAGE 0  // 1: stage the epilogue's U, K1 blocks in shared memory
+#endif
 
 #ifndef PERRK_W3_MINB
 #define PERRK_W3_MINB 4
@@ -60,6 +66,27 @@ __device__ __forceinline__ int w3_face_node(int d, int side, int pt) {
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int NPENDING>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(NPENDING) : "memory");
+}
+
+// one cell's contiguous block of a state array (64 V doubles) into the warp's slice
+__device__ __forceinline__ void w3_stage_cell(double* dst, const double* src, int lane) {
+#pragma unroll
+  for (int k = 0; k < W3::NPC * W3::V / 2 / 32; ++k)
+    cp_async16(dst + 2 * (lane + 32 * k), src + 2 * (lane + 32 * k));
 }
 
 // EC flux between smem nodes p and q in direction D (compile time)
@@ -159,10 +186,20 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   constexpr int V = S::V, N = S::NPC, FP = S::FP;
   extern __shared__ double smem[];
   __shared__ double s_red[2 * 2 * S::WPB];
+  __shared__ CellRec s_rec[S::WPB][2];  // descriptors, prefetched one cell ahead
   if (st->aborted || st->finished) return;  // uniform across the grid
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* pr = smem + wib * S::SM_WARP;  // [NPR][64]
-  double* fs = pr + S::SM_PR;            // [3][32][2][V]: staged traces, then surface terms
+  double* fs = pr + S::SM_PR;            // [3][32][V]: staged traces, then surface terms
+  double* eU = fs + S::SM_FS;            // the cell's U [64 V] and K1 [64 V] (epilogue)
+  double* eK = eU + N * V;
+  // descriptor of one cell into the warp's buffer b (lanes 0-5, 16 B each)
+  auto fetch_rec = [&](int b, int c) {
+    if (c >= 0 && lane < static_cast<int>(sizeof(CellRec) / 16))
+      cp_async16(reinterpret_cast<char*>(&s_rec[wib][b]) + 16 * lane,
+                 reinterpret_cast<const char*>(m.rec + c) + 16 * lane);
+    cp_async_commit();
+  };
   const double dt = st->dt;
   const int ix = lane & 3, iy = (lane >> 2) & 3, zA = lane >> 4, zB = zA + 2;
   const int side = zA, pt = lane & 15;
@@ -171,6 +208,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   const int nw = gridDim.x * S::WPB;
   int slot = blockIdx.x * S::WPB + wib;
   int cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
+  int rb = 0;
+  fetch_rec(0, cell);
 
   while (cell >= 0) {
     // next cell: list entry now, its state arrays to L2 (bulk prefetch)
@@ -184,12 +223,14 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       if (a.write_next && a.form) l2_prefetch(a.K1 + off, kBytes);
       if (a.d_mode == 2) l2_prefetch(a.d + off, kBytes);
     }
-    // ---- descriptor (host.cpp build_cell_records) ---------------------------
-    const CellRec* rp = m.rec + cell;
+    // ---- descriptor (host.cpp build_cell_records), fetched a cell ago -------
+    cp_async_wait<0>();
+    __syncwarp();
+    const CellRec* rp = &s_rec[wib][rb];
     const unsigned long long lv =
-        static_cast<unsigned long long>(__ldg(reinterpret_cast<const long long*>(rp->lev)));
+        static_cast<unsigned long long>(*reinterpret_cast<const long long*>(rp->lev));
     const int lev = static_cast<int>(lv & 0xff);
-    const double J2x = __ldg(&rp->J2[0]), J2y = __ldg(&rp->J2[1]), J2z = __ldg(&rp->J2[2]);
+    const double J2x = rp->J2[0], J2y = rp->J2[1], J2z = rp->J2[2];
     // ---- own nodes A, B: formed stage state (stepper.cpp:60-72) -------------
     const size_t gA = (static_cast<size_t>(cell) * N + lane) * V, gB = gA + 32 * V;
     double uA[V], uB[V];
@@ -217,8 +258,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     // direction per round: round d, face 2 d + side, point pt -------------------
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const int nbc = __ldg(&rp->nb[2 * d + side]);
-      double* dst = fs + (d * 32 + lane) * 2 * V;
+      const int nbc = rp->nb[2 * d + side];
+      double* dst = fs + (d * 32 + lane) * V;
       if (nbc < 0) {
         const double* g = m.ghost + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
 #pragma unroll
@@ -232,16 +273,17 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         } else if (a.formed[l2]) {
 #pragma unroll
           for (int v = 0; v < V; ++v) cp_async8(dst + v, a.Us + gi + v);
-        } else {
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            cp_async8(dst + v, a.U + gi + v);
-            cp_async8(dst + V + v, a.K1 + gi + v);
-          }
-        }
+        }  // else: formed from U and K1 in the surface phase (first active stage only)
       }
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    // the epilogue's U and K1 of this cell (contiguous blocks)
+    const size_t cbase = static_cast<size_t>(cell) * N * V;
+    if (PERRK_W3_EPI_STAGE && a.write_next) {
+      w3_stage_cell(eU, a.U + cbase, lane);
+      if (a.form) w3_stage_cell(eK, a.K1 + cbase, lane);
+    }
+    cp_async_commit();
+    fetch_rec(rb ^ 1, ncell);  // the next cell's descriptor
     // ---- primitives of A and B -> the warp's slice -------------------------
     bool okAB = true;
 #pragma unroll
@@ -271,11 +313,12 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 
     // ---- surface flux + lift + endpoint diagonal at the lane's three face
     // points (semidisc.cpp:489-556, :450-454) ---------------------------------
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    cp_async_wait<1>();  // traces and epilogue blocks (the next descriptor may fly on)
+    __syncwarp();
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      double* slotp = fs + (d * 32 + lane) * 2 * V;
-      const int nbc = __ldg(&rp->nb[2 * d + side]);
+      double* slotp = fs + (d * 32 + lane) * V;
+      const int nbc = rp->nb[2 * d + side];
       double un[V];
       if (nbc >= 0 && a.form) {
         const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
@@ -283,16 +326,17 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
           for (int v = 0; v < V; ++v) un[v] = slotp[v];
         } else {
+          const size_t gi = (static_cast<size_t>(nbc) * N + w3_face_node(d, 1 - side, pt)) * V;
           const double b1 = dt * a.a1[l2];
 #pragma unroll
-          for (int v = 0; v < V; ++v) un[v] = fma(b1, slotp[V + v], slotp[v]);
+          for (int v = 0; v < V; ++v) un[v] = fma(b1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
         }
       } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) un[v] = slotp[v];
       }
       const double J2 = d == 0 ? J2x : (d == 1 ? J2y : J2z);
-      const double lift = __ldg(&rp->lift[d]);
+      const double lift = rp->lift[d];
       const int j = side ? N1 - 1 : 0;
       double o5[V];
       const bool ok = rus_lift<3, SURF>(ph, pr, w3_face_node(d, side, pt), un, d, side,
@@ -313,12 +357,12 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         const int ptA = d == 0 ? iy + 4 * zA : (d == 1 ? ix + 4 * zA : ix + 4 * iy);
         const int ptB = d == 0 ? iy + 4 * zB : (d == 1 ? ix + 4 * zB : ix + 4 * iy);
         if (jA[d] == 0 || jA[d] == N1 - 1) {
-          const double* c = fs + (d * 32 + 16 * (jA[d] ? 1 : 0) + ptA) * 2 * V;
+          const double* c = fs + (d * 32 + 16 * (jA[d] ? 1 : 0) + ptA) * V;
 #pragma unroll
           for (int v = 0; v < V; ++v) KA[v] += c[v];
         }
         if (jB[d] == 0 || jB[d] == N1 - 1) {
-          const double* c = fs + (d * 32 + 16 * (jB[d] ? 1 : 0) + ptB) * 2 * V;
+          const double* c = fs + (d * 32 + 16 * (jB[d] ? 1 : 0) + ptB) * V;
 #pragma unroll
           for (int v = 0; v < V; ++v) KB[v] += c[v];
         }
@@ -327,7 +371,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 
     // ---- epilogue (stepper.cpp:52-55, 60-72, 89-92) ---------------------------
     if (a.want_dh || a.want_h) {
-      const double meas = __ldg(&rp->meas);
+      const double meas = rp->meas;
       const double wxy = c_w[ix] * c_w[iy];
       // own primitives from the slice (not kept in registers across the volume phase)
       auto node = [&](int n, const double* K, int iz) {
@@ -363,17 +407,20 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     }
     if (a.write_next) {
       const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
+      const int oA = lane * V, oB = oA + 32 * V;
+      const double* eUp = PERRK_W3_EPI_STAGE ? eU : a.U + cbase;
+      const double* eKp = PERRK_W3_EPI_STAGE ? eK : a.K1 + cbase;
       if (!a.form) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          a.Usn[gA + v] = fma(an, KA[v], __ldg(a.U + gA + v));
-          a.Usn[gB + v] = fma(an, KB[v], __ldg(a.U + gB + v));
+          a.Usn[gA + v] = fma(an, KA[v], eUp[oA + v]);
+          a.Usn[gB + v] = fma(an, KB[v], eUp[oB + v]);
         }
       } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          a.Usn[gA + v] = __ldg(a.U + gA + v) + fma(an, __ldg(a.K1 + gA + v), pn * KA[v]);
-          a.Usn[gB + v] = __ldg(a.U + gB + v) + fma(an, __ldg(a.K1 + gB + v), pn * KB[v]);
+          a.Usn[gA + v] = eUp[oA + v] + fma(an, eKp[oA + v], pn * KA[v]);
+          a.Usn[gB + v] = eUp[oB + v] + fma(an, eKp[oB + v], pn * KB[v]);
         }
       }
     }
@@ -397,6 +444,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     __syncwarp();  // the slice is rewritten by the next cell
     slot = nslot;
     cell = ncell;
+    rb ^= 1;
   }
 
   // ---- grid epilogue (as stage_kernel) --------------------------------------
