@@ -28,6 +28,10 @@
 namespace perrk {
 namespace dev {
 
+#ifndef PERRK_W3_EPI_STAGE
+#define PERRK_W3_EPI_STAGE 0  // 1: stage the epilogue's U, K1 blocks in shared memory
+#endif
+
 struct W3 {
   static constexpr int V = 5, NPC = 64, FP = 16, WPB = 4, T = 32 * WPB;
   static constexpr int NPR = 8;  // rho, vx, vy, vz, p, E, beta, c
@@ -47,10 +51,6 @@ static_assert(W3::RHO == Slot<3>::RHO && W3::VX == Slot<3>::V0 && W3::P == Slot<
                   W3::E == Slot<3>::E && W3::BETA == Slot<3>::BETA && W3::C == Slot<3>::C &&
                   W3::NPC == StageGeo<3>::T,
               "warp slice layout must match Slot<3> / StageGeo<3>::T");
-
-#ifndef PERRK_W3_EPI_STAGE
-#define PERRK_W3_EPI_STAGE 0  // 1: stage the epilogue's U, K1 blocks in shared memory
-#endif
 
 #ifndef PERRK_W3_MINB
 #define PERRK_W3_MINB 4
