@@ -405,39 +405,47 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         a.Kout[gB + v] = KB[v];
       }
     }
-    if (a.write_next) {
+    // U_{i+1} and d, node by node, each batch with all its loads issued
+    // before its first store (the compiler cannot tell that Usn / d do not
+    // alias U / K1, and would otherwise serialise load -> store pairs)
+    {
+      const double* Up = PERRK_W3_EPI_STAGE ? eU : a.U + cbase;
+      const double* Kp = PERRK_W3_EPI_STAGE ? eK : a.K1 + cbase;
       const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
-      const int oA = lane * V, oB = oA + 32 * V;
-      const double* eUp = PERRK_W3_EPI_STAGE ? eU : a.U + cbase;
-      const double* eKp = PERRK_W3_EPI_STAGE ? eK : a.K1 + cbase;
-      if (!a.form) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          a.Usn[gA + v] = fma(an, KA[v], eUp[oA + v]);
-          a.Usn[gB + v] = fma(an, KB[v], eUp[oB + v]);
+      for (int h = 0; h < 2; ++h) {
+        const double* K = h ? KB : KA;
+        const int o = (lane + 32 * h) * V;
+        const size_t g = h ? gB : gA;
+        double x[V], y[V];
+        if (a.write_next) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) x[v] = Up[o + v];
+          if (a.form) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) y[v] = Kp[o + v];
+#pragma unroll
+            for (int v = 0; v < V; ++v) a.Usn[g + v] = x[v] + fma(an, y[v], pn * K[v]);
+          } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) a.Usn[g + v] = fma(an, K[v], x[v]);
+          }
         }
-      } else {
+        if (a.d_mode) {
+          if (a.d_mode == 2) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          a.Usn[gA + v] = eUp[oA + v] + fma(an, eKp[oA + v], pn * KA[v]);
-          a.Usn[gB + v] = eUp[oB + v] + fma(an, eKp[oB + v], pn * KB[v]);
-        }
-      }
-    }
-    if (a.d_mode) {
+            for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], a.d[g + v]);
+          } else {
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const double dA = a.d_mode == 1 ? a.b * KA[v] : fma(a.b, KA[v], a.d[gA + v]);
-        const double dB = a.d_mode == 1 ? a.b * KB[v] : fma(a.b, KB[v], a.d[gB + v]);
-        a.d[gA + v] = dA;
-        a.d[gB + v] = dB;
-        if (a.want_dmax) {
-          const unsigned long long bA2 =
-              static_cast<unsigned long long>(__double_as_longlong(dA)) & 0x7fffffffffffffffULL;
-          const unsigned long long bB2 =
-              static_cast<unsigned long long>(__double_as_longlong(dB)) & 0x7fffffffffffffffULL;
-          dmax_bits = bA2 > dmax_bits ? bA2 : dmax_bits;
-          dmax_bits = bB2 > dmax_bits ? bB2 : dmax_bits;
+            for (int v = 0; v < V; ++v) x[v] = a.b * K[v];
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            a.d[g + v] = x[v];
+            const unsigned long long bits =
+                static_cast<unsigned long long>(__double_as_longlong(x[v])) & 0x7fffffffffffffffULL;
+            if (a.want_dmax) dmax_bits = bits > dmax_bits ? bits : dmax_bits;
+          }
         }
       }
     }
