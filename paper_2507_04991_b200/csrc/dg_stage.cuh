@@ -943,21 +943,30 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
       if (a.write_next) {
         // U_{i+1} = U + dt (a_{i+1,1} K1 + a_{i+1,i} K_i) with the cell's row
         // (stepper.cpp:60-72, one stage ahead); at stage 0, K1 = K_0 = K
+        // (all loads of a batch before its stores: the compiler cannot tell
+        // that Usn / d do not alias U / K1 and would serialise the pairs)
         const int lev = s_lev[cs];
         const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
+        double x[V], y[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) x[v] = __ldg(a.U + gi + v);
         if (!a.form) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) a.Usn[gi + v] = fma(an, K[v], __ldg(a.U + gi + v));
+          for (int v = 0; v < V; ++v) a.Usn[gi + v] = fma(an, K[v], x[v]);
         } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v)
-            a.Usn[gi + v] = __ldg(a.U + gi + v) + fma(an, __ldg(a.K1 + gi + v), pn * K[v]);
+          for (int v = 0; v < V; ++v) y[v] = __ldg(a.K1 + gi + v);
+#pragma unroll
+          for (int v = 0; v < V; ++v) a.Usn[gi + v] = x[v] + fma(an, y[v], pn * K[v]);
         }
       }
       if (a.d_mode) {
+        double dn5[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) dn5[v] = a.d_mode == 1 ? a.b * K[v] : fma(a.b, K[v], a.d[gi + v]);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          const double dn = a.d_mode == 1 ? a.b * K[v] : fma(a.b, K[v], a.d[gi + v]);
+          const double dn = dn5[v];
           a.d[gi + v] = dn;
           if (a.want_dmax) {
             const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(dn)) &
