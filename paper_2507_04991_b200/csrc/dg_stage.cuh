@@ -147,6 +147,16 @@ __device__ __forceinline__ void pflux(const Prim<DIM>& q, int d, double* f) {
 __constant__ double c_lm[8] = {-11.0 / 1890.0, -1.0 / 90.0, -1.0 / 24.0, 0.125,
                                1.0 / 7.0,      1.0 / 5.0,   1.0 / 3.0,   1e-4};
 
+// logarithm branch of lmeans (physics.cpp:37), out of line: the hot code
+// stays compact (one copy instead of one per inlined flux) and it runs only
+// for warps with a pair above the series threshold
+__device__ __noinline__ double2 lmeans_log(double rl, double rr, double bl, double br, double k2,
+                                           bool rough1, bool rough2, double lq, double ib) {
+  if (rough1) lq = 0.25 * ((rl - rr) * frcp(flog(rl) - flog(rr)));
+  if (rough2) ib = 0.5 * k2 * ((flog(bl) - flog(br)) * frcp(bl - br));
+  return make_double2(lq, ib);
+}
+
 // Both logarithmic means of one EC pair: lq = logmean(rl, rr) / 4 and
 // ib = k / logmean(bl, br) (k2 = 2 k).  The series (the factors folded into
 // its coefficients) is evaluated unconditionally; a warp vote sends the warp
@@ -166,8 +176,9 @@ __device__ __forceinline__ void lmeans(double rl, double rr, double bl, double b
   ib = fma(u2, fma(u2, fma(u2, c_lm[4], c_lm[5]), c_lm[6]), 1.0) * (k2 * rs);
   const bool rough1 = !(u1 < c_lm[7]), rough2 = !(u2 < c_lm[7]);
   if (__any_sync(__activemask(), rough1 || rough2)) {
-    if (rough1) lq = 0.25 * (d1 * frcp(flog(rl) - flog(rr)));
-    if (rough2) ib = 0.5 * k2 * ((flog(bl) - flog(br)) * frcp(d2));
+    const double2 r = lmeans_log(rl, rr, bl, br, k2, rough1, rough2, lq, ib);
+    lq = r.x;
+    ib = r.y;
   }
 }
 
