@@ -162,6 +162,10 @@ __device__ __noinline__ double2 lmeans_log(double rl, double rr, double bl, doub
 // its coefficients) is evaluated unconditionally; a warp vote sends the warp
 // to the logarithm branch only if one of its lanes has a pair above the
 // threshold, and there each lane keeps the reference's choice per value.
+// SMOOTH: the caller guarantees every pair is below the threshold (w3 kernel's
+// per-cell range test), so the series is taken without the vote and branch
+// and consecutive fluxes schedule as one straight-line block.
+template <bool SMOOTH = false>
 __device__ __forceinline__ void lmeans(double rl, double rr, double bl, double br, double k2,
                                        double& lq, double& ib) {
   const double s1 = rl + rr, d1 = rl - rr;
@@ -174,6 +178,7 @@ __device__ __forceinline__ void lmeans(double rl, double rr, double bl, double b
   const double rs = frcp(s2);
   const double f2 = d2 * rs, u2 = f2 * f2;
   ib = fma(u2, fma(u2, fma(u2, c_lm[4], c_lm[5]), c_lm[6]), 1.0) * (k2 * rs);
+  if (SMOOTH) return;
   const bool rough1 = !(u1 < c_lm[7]), rough2 = !(u2 < c_lm[7]);
   if (__any_sync(__activemask(), rough1 || rough2)) {
     const double2 r = lmeans_log(rl, rr, bl, br, k2, rough1, rough2, lq, ib);
@@ -186,12 +191,12 @@ __device__ __forceinline__ void lmeans(double rl, double rr, double bl, double b
 // with sigma = v_l + v_r, t = logmean(rho) sigma_d / 4,
 //   f_rho = 2 t,  f_m,i = t sigma_i + delta_id (p_l + p_r) / 2,
 //   f_E = f_rho (v_l.v_r / 2 + 1 / ((gamma - 1) logmean(beta))) + (p_l v_r,d + p_r v_l,d) / 2
-template <int DIM>
+template <int DIM, bool SMOOTH = false>
 __device__ __forceinline__ void ec2(const Phys& ph, int d, double rl, const double (&vl)[DIM],
                                     double pl, double bl, double rr, const double (&vr)[DIM],
                                     double pr, double br, double* f) {
   double lq, ib;
-  lmeans(rl, rr, bl, br, 2.0 * ph.inv_gm1, lq, ib);
+  lmeans<SMOOTH>(rl, rr, bl, br, 2.0 * ph.inv_gm1, lq, ib);
   double sg[DIM], vlvr = 0.0;
 #pragma unroll
   for (int i = 0; i < DIM; ++i) {
