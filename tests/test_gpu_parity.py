@@ -439,3 +439,52 @@ def test_snapshot_csv_matches_reference_writer(tmp_path):
     P.write_snapshot_csv(semi, U0, str(ours))
     assert ref.L.ref_write_snapshot(ref.h, O.dp(U0), str(theirs).encode()) == 0
     assert ours.read_bytes() == theirs.read_bytes()
+
+
+def _mixed_state_3d(semi, seed=5):
+    """A 3D state with smooth cells (rho, beta within 0.5 % per cell: the
+    warp-per-cell kernel's series-only path) and rough ones (a strong
+    Gaussian bump: the per-pair logarithm branch), with the cell split checked."""
+    x, y, z = semi.node_x(), semi.node_y(), semi.node_z()
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-0.5, 0.5, 3)
+    bump = np.exp(-((x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2) / 0.08)
+    rho = 1.0 + 0.002 * np.sin(math.pi * x) + 0.8 * bump
+    v = [0.1 * np.cos(math.pi * y), 0.1 * np.sin(math.pi * z), 0.05 + 0.3 * bump]
+    p = 1.0 + 0.002 * np.cos(math.pi * z) + 0.5 * bump
+    U = np.stack([rho] + [rho * vv for vv in v] + [p / 0.4 + 0.5 * rho * sum(vv * vv for vv in v)])
+    r = rho.reshape(-1, 64)
+    ratio = r.max(axis=1) / r.min(axis=1)
+    assert (ratio < 1.01).sum() > 0 and (ratio > 1.05).sum() > 0
+    return np.ascontiguousarray(U.T).reshape(-1)
+
+
+@pytest.mark.parametrize("surface", ["rusanov", "central"])
+def test_w3_kernel_mixed_smooth_rough_cells_vs_oracle(surface):
+    """The 3D warp-per-cell stage kernel (dg_stage3w.cuh) on cells that take
+    its series-only path and cells that take the logarithm branch, full and
+    masked (active-list) RHS against the oracle."""
+    mesh = mesh3d(6, 5, 4, seed=71)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux=surface))
+    orc = O.Orc(mesh, surface_flux=surface)
+    U = _mixed_state_3d(semi)
+    assert max_rel(semi.rhs(0.0, U), orc.rhs(0.0, U)) < 1e-12
+    mask = np.random.default_rng(8).integers(0, 2, semi.num_cells()).astype(np.int8)
+    assert max_rel(semi.rhs_masked(0.0, U, mask), orc.rhs_masked(0.0, U, mask)) < 1e-12
+
+
+def test_w3_kernel_multilevel_relaxed_mixed_vs_oracle():
+    mesh = mesh3d(5, 4, 4, seed=73)
+    fam = P.build_perk4(14, [5, 8, 14], [[], [0.5] * 3, [0.7] * 9])
+    pm = _multilevel(mesh, 3, 9)
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh))
+    orc = O.Orc(mesh)
+    U0 = _mixed_state_3d(semi, seed=6)
+    dt = 0.3 * orc.compute_dt(U0, False, 1.0)
+    rx = P.RelaxationConfig(numerics="accurate")
+    Ug, Uo = U0.copy(), U0.copy()
+    for _ in range(2):
+        _, rg = P.perk_step(Ug, 0.0, dt, fam, pm, semi, P.PerkStepOptions(relaxation=rx))
+        _, ro = orc.perk_step(Uo, 0.0, dt, fam, pm.effective_level, rx)
+        assert abs(rg.gamma - ro.gamma) < 1e-12
+    assert rel_err(Ug, Uo, 5) < 1e-11
