@@ -60,6 +60,16 @@ __device__ __forceinline__ double node_measure(const MeshDev& m, int ci, int cj,
   return 0.125 * m.h[0][ci] * m.h[1][cj] * m.h[2][ck] * c_w[ix] * c_w[iy] * c_w[iz];
 }
 
+// the same measure from the cell's static record (host.cpp build_cell_records:
+// meas = (h_x/2)(h_y/2)(h_z/2), bitwise 0.125 h_x h_y h_z), no index division
+template <int DIM>
+__device__ __forceinline__ double node_measure_rec(const MeshDev& m, int cell, int l) {
+  const int ix = l % N1, iy = (l / N1) % N1, iz = l / (N1 * N1);
+  const double meas = __ldg(&m.rec[cell].meas);
+  if (DIM == 2) return meas * c_w[ix] * c_w[iy];
+  return meas * c_w[ix] * c_w[iy] * c_w[iz];
+}
+
 __device__ __forceinline__ void report_bad(StepState* st, int stage, long long ncells, long long cell) {
   atomicMin(&st->bad_code, static_cast<long long>(stage) * ncells + cell);
 }
@@ -314,9 +324,7 @@ __global__ void __launch_bounds__(256)
   for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < nnodes;
        n += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
-    int ci, cj, ck;
-    cell_coords(m, cell, ci, cj, ck);
-    const double om = node_measure<DIM>(m, ci, cj, ck, l);
+    const double om = node_measure_rec<DIM>(m, cell, l);
     double u[V], dv[V], T[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -378,9 +386,6 @@ __global__ void __launch_bounds__(256)
     }
     if (want_nu || want_record) {
       const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
-      int ci, cj, ck;
-      cell_coords(m, cell, ci, cj, ck);
-      const int cc[3] = {ci, cj, ck};
       // one pressure / sound speed per node (mesh.cpp:97-129 takes
       // |v_dir| + c per direction; 1/h_dir = jac_dir / 2 exactly)
       const double ir = frcp(u[0]);
@@ -389,15 +394,15 @@ __global__ void __launch_bounds__(256)
       for (int dir = 0; dir < DIM; ++dir) m2 = fma(u[1 + dir], u[1 + dir], m2);
       const double p = ph.gm1 * (u[DIM + 1] - 0.5 * m2 * ir);
       if (want_nu) {
-        const double c = sqrt(ph.gamma * p * ir);
+        const double c = fsqrt(ph.gamma * p * ir);
 #pragma unroll
         for (int dir = 0; dir < DIM; ++dir)
-          numax = fmax(numax, (fabs(u[1 + dir]) * ir + c) * (0.5 * m.jac[dir][cc[dir]]));
+          numax = fmax(numax, (fabs(u[1 + dir]) * ir + c) * (0.25 * __ldg(&m.rec[cell].J2[dir])));
       }
       if (want_record) {
-        const double om = node_measure<DIM>(m, ci, cj, ck, l);
+        const double om = node_measure_rec<DIM>(m, cell, l);
         // s = -rho log(p / rho^gamma) (physics.cpp:130-132) as -rho (log p - gamma log rho)
-        acc[0] = dd_add_prod(acc[0], om, -u[0] * (log(p) - ph.gamma * log(u[0])));
+        acc[0] = dd_add_prod(acc[0], om, -u[0] * (flog(p) - ph.gamma * flog(u[0])));
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[1 + v] = dd_add_prod(acc[1 + v], om, u[v]);
       }
