@@ -32,8 +32,12 @@ namespace dev {
 #define PERRK_W3_EPI_STAGE 0  // 1: stage the epilogue's U, K1 blocks in shared memory
 #endif
 
+#ifndef PERRK_W3_WPB
+#define PERRK_W3_WPB 8  // warps (cells in flight) per block
+#endif
+
 struct W3 {
-  static constexpr int V = 5, NPC = 64, FP = 16, WPB = 4, T = 32 * WPB;
+  static constexpr int V = 5, NPC = 64, FP = 16, WPB = PERRK_W3_WPB, T = 32 * WPB;
   static constexpr int NPR = 8;  // rho, vx, vy, vz, p, E, beta, c
   static constexpr int RHO = 0, VX = 1, P = 4, E = 5, BETA = 6, C = 7;
   // per warp: primitives [NPR][64], face slots [3 rounds][32 lanes][V], the
@@ -53,7 +57,7 @@ static_assert(W3::RHO == Slot<3>::RHO && W3::VX == Slot<3>::V0 && W3::P == Slot<
               "warp slice layout must match Slot<3> / StageGeo<3>::T");
 
 #ifndef PERRK_W3_MINB
-#define PERRK_W3_MINB 4
+#define PERRK_W3_MINB (16 / PERRK_W3_WPB)
 #endif
 
 // node on face (d, side) at face point pt (t1 + 4 t2, the line_base order)
