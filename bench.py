@@ -350,8 +350,11 @@ def perrk_arm(args):
         fp64_achieved = flops / (stage_ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "traffic": traffic,
-                    "kernel": f"stage_kernel<{cfg.dim},{cfg.surface_flux}> (volume + surface + "
-                              "lift + stage formation)",
+                    "kernel": (f"stage3w_kernel<{cfg.surface_flux}> (warp per cell: volume + "
+                               "surface + lift + stage formation)"
+                               if cfg.dim == 3 and cfg.surface_flux in ("rusanov", "central")
+                               else f"stage_kernel<{cfg.dim},{cfg.surface_flux}> (volume + "
+                                    "surface + lift + stage formation)"),
                     "peak_kind": f"{hbm_kind} hbm_gbs (MEASURED_PEAKS.json)",
                     "stage_kernel_share": stage_ms / ms,
                     "launches": stage_launches, "ms_per_launch": stage_ms / stage_launches,
