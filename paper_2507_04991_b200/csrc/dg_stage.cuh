@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
       constexpr unsigned kBytes = NPC * V * sizeof(double);
       const size_t off = static_cast<size_t>(nx_cell) * NPC * V;
       if (a.form) l2_prefetch(a.Us + off, kBytes);
-      l2_prefetch(a.U + off, kBytes);                       // stage 0 state / epilogue
+      if (!a.form || a.write_next) l2_prefetch(a.U + off, kBytes);  // stage 0 state / epilogue
       if (a.write_next && a.form) l2_prefetch(a.K1 + off, kBytes);  // epilogue formation
       if (a.d_mode == 2) l2_prefetch(a.d + off, kBytes);              // d read-modify-write
     }

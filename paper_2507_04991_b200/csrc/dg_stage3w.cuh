@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       constexpr unsigned kBytes = N * V * sizeof(double);
       const size_t off = static_cast<size_t>(ncell) * N * V;
       if (a.form) l2_prefetch(a.Us + off, kBytes);
-      l2_prefetch(a.U + off, kBytes);
+      if (!a.form || a.write_next) l2_prefetch(a.U + off, kBytes);  // stage 0 state / epilogue
       if (a.write_next && a.form) l2_prefetch(a.K1 + off, kBytes);
       if (a.d_mode == 2) l2_prefetch(a.d + off, kBytes);
     }
