@@ -975,13 +975,29 @@ cudaError_t launch_begin_step(StepState* st, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// grid of a grid-stride node kernel: the resident capacity (one wave, so no
+// block waits for a second wave), at most the caller's grid; a function of the
+// device only, so the fixed-order reductions stay reproducible
+template <typename K>
+static int resident_grid(K kernel, int threads, int cap) {
+  int dev = 0, sms = 148, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0);
+  const int g = sms * (occ > 0 ? occ : 1);
+  return g < cap ? g : cap;
+}
+
 cudaError_t launch_relax_pass(int dim, const double* U, const double* d, const MeshDev& m,
                               const Phys& ph, StepState* st, double* partials, unsigned* counter,
                               long long nnodes, int grid, cudaStream_t s) {
-  if (dim == 2)
-    relax_pass_kernel<2><<<grid, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
-  else
-    relax_pass_kernel<3><<<grid, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
+  if (dim == 2) {
+    static const int g = resident_grid(relax_pass_kernel<2>, 256, grid);
+    relax_pass_kernel<2><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
+  } else {
+    static const int g = resident_grid(relax_pass_kernel<3>, 256, grid);
+    relax_pass_kernel<3><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
+  }
   return cudaGetLastError();
 }
 
@@ -989,12 +1005,15 @@ cudaError_t launch_update(int dim, double* U, const double* d, const MeshDev& m,
                           StepState* st, double* partials, unsigned* counter, long long nnodes,
                           int want_nu, int want_record, double* records, int grid,
                           cudaStream_t s) {
-  if (dim == 2)
-    update_kernel<2><<<grid, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes, want_nu,
-                                          want_record, records);
-  else
-    update_kernel<3><<<grid, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes, want_nu,
-                                          want_record, records);
+  if (dim == 2) {
+    static const int g = resident_grid(update_kernel<2>, 256, grid);
+    update_kernel<2><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes, want_nu,
+                                       want_record, records);
+  } else {
+    static const int g = resident_grid(update_kernel<3>, 256, grid);
+    update_kernel<3><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes, want_nu,
+                                       want_record, records);
+  }
   return cudaGetLastError();
 }
 
