@@ -333,11 +333,11 @@ __device__ __forceinline__ double pick_rt(const A& a, int off, int d) {
 // neighbour's conservative trace from registers.  Returns admissibility of
 // the neighbour's trace.
 template <int DIM, int SURF>
-__device__ __forceinline__ bool rus_lift(const Phys& ph, const double* pr, int oq,
-                                         const double (&un)[DIM + 2], int d, int side,
-                                         double cll, double sg, bool weak, double* out) {
-  using S = Slot<DIM>;
-  constexpr int V = DIM + 2, T = StageGeo<DIM>::T;
+__device__ __forceinline__ bool rus_lift_v(const Phys& ph, double ro, const double (&vo)[DIM],
+                                           double po, double Eo, double co,
+                                           const double (&un)[DIM + 2], int d, int side,
+                                           double cll, double sg, bool weak, double* out) {
+  constexpr int V = DIM + 2;
   const double rn = un[0], En = un[V - 1];
   const double irn = frcp(rn);
   double vn[DIM], kin = 0.0;
@@ -350,10 +350,6 @@ __device__ __forceinline__ bool rus_lift(const Phys& ph, const double* pr, int o
   bool ok = rn > 0.0 && pn > 0.0 && isfinite(En);
 #pragma unroll
   for (int i = 0; i < DIM; ++i) ok = ok && isfinite(vn[i]);
-  const double ro = pr[S::RHO * T + oq], po = pr[S::P * T + oq], Eo = pr[S::E * T + oq];
-  double vo[DIM];
-#pragma unroll
-  for (int i = 0; i < DIM; ++i) vo[i] = pr[(S::V0 + i) * T + oq];
   const double vod = pick_rt<DIM>(vo, 0, d), vnd = pick_rt<DIM>(vn, 0, d);
   const double mnd = pick_rt<DIM>(un, 1, d), mod = ro * vod;
   double fo[V], g[V];
@@ -367,7 +363,7 @@ __device__ __forceinline__ bool rus_lift(const Phys& ph, const double* pr, int o
   fo[V - 1] = (Eo + po) * vod;
   g[V - 1] = 0.5 * ((En + pn) * vnd - fo[V - 1]);
   if constexpr (SURF == 2) {
-    const double lam = fmax(fabs(vod) + pr[S::C * T + oq], fabs(vnd) + fsqrt(ph.gamma * pn * irn));
+    const double lam = fmax(fabs(vod) + co, fabs(vnd) + fsqrt(ph.gamma * pn * irn));
     const double hl = side ? -0.5 * lam : 0.5 * lam;
     g[0] = fma(hl, rn - ro, g[0]);
 #pragma unroll
@@ -382,6 +378,22 @@ __device__ __forceinline__ bool rus_lift(const Phys& ph, const double* pr, int o
     for (int v = 0; v < V; ++v) out[v] = fma(sg, g[v], -cll * fo[v]);
   }
   return ok;
+}
+
+// rus_lift_v with the own trace's primitives from the block-per-cell
+// kernel's shared-memory slots
+template <int DIM, int SURF>
+__device__ __forceinline__ bool rus_lift(const Phys& ph, const double* pr, int oq,
+                                         const double (&un)[DIM + 2], int d, int side,
+                                         double cll, double sg, bool weak, double* out) {
+  using S = Slot<DIM>;
+  constexpr int T = StageGeo<DIM>::T;
+  double vo[DIM];
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) vo[i] = pr[(S::V0 + i) * T + oq];
+  return rus_lift_v<DIM, SURF>(ph, pr[S::RHO * T + oq], vo, pr[S::P * T + oq], pr[S::E * T + oq],
+                               SURF == 2 ? pr[S::C * T + oq] : 0.0, un, d, side, cll, sg, weak,
+                               out);
 }
 
 template <int DIM>

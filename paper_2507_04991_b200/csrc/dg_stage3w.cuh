@@ -38,9 +38,12 @@ namespace dev {
 
 struct W3 {
   static constexpr int V = 5, NPC = 64, FP = 16, WPB = PERRK_W3_WPB, T = 32 * WPB;
-  static constexpr int NPR = 8;  // rho, vx, vy, vz, p, E, beta, c
-  static constexpr int RHO = 0, VX = 1, P = 4, E = 5, BETA = 6, C = 7;
-  // per warp: primitives [NPR][64], face slots [3 rounds][32 lanes][V], the
+  // node-major primitives, 10 doubles (80 bytes) per node: (rho, beta),
+  // (vx, vy), (vz, p), (E, c) as 16-byte pairs, so a flux partner is three
+  // 16-byte shared loads; the 80-byte stride keeps eight consecutive nodes on
+  // distinct bank groups
+  static constexpr int NPR = 10;
+  // per warp: primitives [64][NPR], face slots [3 rounds][32 lanes][V], the
   // cell's U and K1 for the epilogue's formation [2][64 V]
   static constexpr int SM_PR = NPR * NPC;
   static constexpr int SM_FS = 3 * 32 * V;
@@ -49,12 +52,23 @@ struct W3 {
   static constexpr int SM_TOTAL = WPB * SM_WARP;  // doubles per block
 };
 
-// rus_lift (dg_stage.cuh) reads the own trace's primitives with the
-// block-per-cell kernel's slot layout; the warp slice uses the same one
-static_assert(W3::RHO == Slot<3>::RHO && W3::VX == Slot<3>::V0 && W3::P == Slot<3>::P &&
-                  W3::E == Slot<3>::E && W3::BETA == Slot<3>::BETA && W3::C == Slot<3>::C &&
-                  W3::NPC == StageGeo<3>::T,
-              "warp slice layout must match Slot<3> / StageGeo<3>::T");
+// the flux inputs of one node from the warp slice (three 16-byte loads)
+struct W3Prim {
+  double rho, beta, v[3], p;
+};
+
+__device__ __forceinline__ W3Prim w3_load(const double* pr, int n) {
+  const double2* q = reinterpret_cast<const double2*>(pr + n * W3::NPR);
+  const double2 a = q[0], b = q[1], c = q[2];
+  W3Prim r;
+  r.rho = a.x;
+  r.beta = a.y;
+  r.v[0] = b.x;
+  r.v[1] = b.y;
+  r.v[2] = c.x;
+  r.p = c.y;
+  return r;
+}
 
 #ifndef PERRK_W3_MINB
 #define PERRK_W3_MINB (16 / PERRK_W3_WPB)
@@ -96,12 +110,8 @@ __device__ __forceinline__ void w3_stage_cell(double* dst, const double* src, in
 // EC flux between smem nodes p and q in direction D (compile time)
 template <int D, bool SM>
 __device__ __forceinline__ void w3_ec(const Phys& ph, const double* pr, int p, int q, double* f) {
-  using S = W3;
-  constexpr int N = S::NPC;
-  const double vl[3] = {pr[S::VX * N + p], pr[(S::VX + 1) * N + p], pr[(S::VX + 2) * N + p]};
-  const double vr[3] = {pr[S::VX * N + q], pr[(S::VX + 1) * N + q], pr[(S::VX + 2) * N + q]};
-  ec2<3, SM>(ph, D, pr[S::RHO * N + p], vl, pr[S::P * N + p], pr[S::BETA * N + p], pr[S::RHO * N + q],
-         vr, pr[S::P * N + q], pr[S::BETA * N + q], f);
+  const W3Prim L = w3_load(pr, p), R = w3_load(pr, q);
+  ec2<3, SM>(ph, D, L.rho, L.v, L.p, L.beta, R.rho, R.v, R.p, R.beta, f);
 }
 
 // x / y lines (D = 0, 1): the lane's two layers.  Each node evaluates
@@ -299,20 +309,18 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       double ir;
       const Prim<3> q = prim_of<3>(ph, h ? uB : uA, ir);
       okAB = okAB && prim_ok<3>(q);
-      pr[S::RHO * N + n] = q.rho;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) pr[(S::VX + i) * N + n] = q.v[i];
-      pr[S::P * N + n] = q.p;
-      pr[S::E * N + n] = q.E;
       const double be = q.rho * frcp(q.p);
-      pr[S::BETA * N + n] = be;
+      double2* dst = reinterpret_cast<double2*>(pr + n * S::NPR);
+      dst[0] = make_double2(q.rho, be);
+      dst[1] = make_double2(q.v[0], q.v[1]);
+      dst[2] = make_double2(q.v[2], q.p);
+      dst[3] = make_double2(q.E, SURF == 2 ? fsqrt(ph.gamma * q.p * ir) : 0.0);
       const unsigned hr = static_cast<unsigned>(__double2hiint(q.rho));
       const unsigned hb = static_cast<unsigned>(__double2hiint(be));
       hr_lo = min(hr_lo, hr);
       hr_hi = max(hr_hi, hr);
       hb_lo = min(hb_lo, hb);
       hb_hi = max(hb_hi, hb);
-      if constexpr (SURF == 2) pr[S::C * N + n] = fsqrt(ph.gamma * q.p * ir);
     }
     if (!okAB) report_bad(st, a.stage, a.ncells, m.gid ? m.gid[cell] : cell);
     // smooth cell: max / min < 1.0198 for both, so every pair of the cell has
@@ -375,8 +383,11 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const double lift = rp->lift[d];
       const int j = side ? N1 - 1 : 0;
       double o5[V];
-      const bool ok = rus_lift<3, SURF>(ph, pr, w3_face_node(d, side, pt), un, d, side,
-                                        J2 * c_D[j * N1 + j], side ? -lift : lift, false, o5);
+      const double2* on = reinterpret_cast<const double2*>(pr + w3_face_node(d, side, pt) * S::NPR);
+      const double2 o0 = on[0], o1 = on[1], o2 = on[2], o3 = on[3];
+      const double vo[3] = {o1.x, o1.y, o2.x};
+      const bool ok = rus_lift_v<3, SURF>(ph, o0.x, vo, o2.y, o3.x, o3.y, un, d, side,
+                                          J2 * c_D[j * N1 + j], side ? -lift : lift, false, o5);
       if (!ok)
         report_bad(st, a.stage, a.ncells,
                    nbc < 0 ? m.ghost_gid[-1 - nbc] : (m.gid ? m.gid[nbc] : nbc));
@@ -411,11 +422,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const double wxy = c_w[ix] * c_w[iy];
       // own primitives from the slice (not kept in registers across the volume phase)
       auto node = [&](int n, const double* K, int iz) {
-        Prim<3> q;
-        q.rho = pr[S::RHO * N + n];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) q.v[i] = pr[(S::VX + i) * N + n];
-        const double be = pr[S::BETA * N + n];
+        const W3Prim q = w3_load(pr, n);
+        const double be = q.beta;
         const double s_therm = -(flog(be) + ph.gm1 * flog(q.rho));
         const double om = meas * wxy * c_w[iz];
         if (a.want_dh) {
