@@ -46,11 +46,30 @@ struct W3 {
   // per warp: primitives [64][NPR], face slots [3 rounds][32 lanes][V], the
   // cell's U and K1 for the epilogue's formation [2][64 V]
   static constexpr int SM_PR = NPR * NPC;
-  static constexpr int SM_FS = 3 * 32 * V;
+  static constexpr int FS = 6;  // face slot stride (doubles): 48 bytes, 16-byte loads
+  static constexpr int SM_FS = 3 * 32 * FS;
   static constexpr int SM_EP = PERRK_W3_EPI_STAGE ? 2 * NPC * V : 0;
   static constexpr int SM_WARP = SM_PR + SM_FS + SM_EP;
   static constexpr int SM_TOTAL = WPB * SM_WARP;  // doubles per block
 };
+
+// a face slot (5 doubles in 48 bytes) with 16-byte shared loads / stores
+__device__ __forceinline__ void w3_slot_load(const double* p, double (&u)[5]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = q[0], b = q[1];
+  u[0] = a.x;
+  u[1] = a.y;
+  u[2] = b.x;
+  u[3] = b.y;
+  u[4] = p[4];
+}
+
+__device__ __forceinline__ void w3_slot_store(double* p, const double (&u)[5]) {
+  double2* q = reinterpret_cast<double2*>(p);
+  q[0] = make_double2(u[0], u[1]);
+  q[1] = make_double2(u[2], u[3]);
+  p[4] = u[4];
+}
 
 // the flux inputs of one node from the warp slice (three 16-byte loads)
 struct W3Prim {
@@ -273,7 +292,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const int nbc = rp->nb[2 * d + side];
-      double* dst = fs + (d * 32 + lane) * V;
+      double* dst = fs + (d * 32 + lane) * S::FS;
       if (nbc < 0) {
         const double* g = m.ghost + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
 #pragma unroll
@@ -361,14 +380,13 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     __syncwarp();
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      double* slotp = fs + (d * 32 + lane) * V;
+      double* slotp = fs + (d * 32 + lane) * S::FS;
       const int nbc = rp->nb[2 * d + side];
       double un[V];
       if (nbc >= 0 && a.form) {
         const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
         if (a.formed[l2]) {
-#pragma unroll
-          for (int v = 0; v < V; ++v) un[v] = slotp[v];
+          w3_slot_load(slotp, un);
         } else {
           const size_t gi = (static_cast<size_t>(nbc) * N + w3_face_node(d, 1 - side, pt)) * V;
           const double b1 = dt * a.a1[l2];
@@ -376,8 +394,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
           for (int v = 0; v < V; ++v) un[v] = fma(b1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
         }
       } else {
-#pragma unroll
-        for (int v = 0; v < V; ++v) un[v] = slotp[v];
+        w3_slot_load(slotp, un);
       }
       const double J2 = d == 0 ? J2x : (d == 1 ? J2y : J2z);
       const double lift = rp->lift[d];
@@ -391,8 +408,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       if (!ok)
         report_bad(st, a.stage, a.ncells,
                    nbc < 0 ? m.ghost_gid[-1 - nbc] : (m.gid ? m.gid[nbc] : nbc));
-#pragma unroll
-      for (int v = 0; v < V; ++v) slotp[v] = o5[v];
+      w3_slot_store(slotp, o5);
     }
     __syncwarp();
     // gather: node A / B on face (d, side) takes the term of face point
@@ -404,12 +420,14 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         const int ptA = d == 0 ? iy + 4 * zA : (d == 1 ? ix + 4 * zA : ix + 4 * iy);
         const int ptB = d == 0 ? iy + 4 * zB : (d == 1 ? ix + 4 * zB : ix + 4 * iy);
         if (jA[d] == 0 || jA[d] == N1 - 1) {
-          const double* c = fs + (d * 32 + 16 * (jA[d] ? 1 : 0) + ptA) * V;
+          double c[V];
+          w3_slot_load(fs + (d * 32 + 16 * (jA[d] ? 1 : 0) + ptA) * S::FS, c);
 #pragma unroll
           for (int v = 0; v < V; ++v) KA[v] += c[v];
         }
         if (jB[d] == 0 || jB[d] == N1 - 1) {
-          const double* c = fs + (d * 32 + 16 * (jB[d] ? 1 : 0) + ptB) * V;
+          double c[V];
+          w3_slot_load(fs + (d * 32 + 16 * (jB[d] ? 1 : 0) + ptB) * S::FS, c);
 #pragma unroll
           for (int v = 0; v < V; ++v) KB[v] += c[v];
         }
