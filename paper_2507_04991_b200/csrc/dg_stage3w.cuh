@@ -38,37 +38,45 @@ namespace dev {
 
 struct W3 {
   static constexpr int V = 5, NPC = 64, FP = 16, WPB = PERRK_W3_WPB, T = 32 * WPB;
-  // node-major primitives, 10 doubles (80 bytes) per node: (rho, beta),
-  // (vx, vy), (vz, p), (E, c) as 16-byte pairs, so a flux partner is three
-  // 16-byte shared loads; the 80-byte stride keeps eight consecutive nodes on
-  // distinct bank groups
-  static constexpr int NPR = 10;
-  // per warp: primitives [64][NPR], face slots [3 rounds][32 lanes][V], the
-  // cell's U and K1 for the epilogue's formation [2][64 V]
+  // Shared-memory layouts chosen so that every warp access of the kernel is
+  // free of bank conflicts (profiles/r01_x1_*: the L1/shared data pipe, not
+  // the FP64 pipe, binds this kernel).
+  //  * primitives: four arrays of 16-byte pairs, (rho, beta), (vx, vy),
+  //    (vz, p), (E, c), 64 nodes each, node n at entry w3_sw(n): the low three
+  //    bits of n XORed with h((n >> 3) & 3), h = {0, 1, 6, 7}.  Each of the
+  //    kernel's access patterns (own node, x/y/z partners and distance-2
+  //    pairs, the face nodes of the three surface rounds) then puts the eight
+  //    lanes of every quarter-warp on eight distinct 16-byte bank groups.
+  //  * face slots: 5 doubles (40 bytes) per slot, slot s at w3_fs(s) =
+  //    s + 4 (s >> 4), read and written with 8-byte accesses: lane-indexed
+  //    staging / surface and the node-indexed gather are all conflict free.
+  static constexpr int NPR = 8;
   static constexpr int SM_PR = NPR * NPC;
-  static constexpr int FS = 6;  // face slot stride (doubles): 48 bytes, 16-byte loads
-  static constexpr int SM_FS = 3 * 32 * FS;
+  static constexpr int FS = 5;
+  static constexpr int SM_FS = (96 + 4 * 5) * FS;
   static constexpr int SM_EP = PERRK_W3_EPI_STAGE ? 2 * NPC * V : 0;
   static constexpr int SM_WARP = SM_PR + SM_FS + SM_EP;
   static constexpr int SM_TOTAL = WPB * SM_WARP;  // doubles per block
 };
 
-// a face slot (5 doubles in 48 bytes) with 16-byte shared loads / stores
+// swizzled entry of node n in the primitive arrays
+__device__ __forceinline__ int w3_sw(int n) {
+  const int k = (n >> 3) & 3;
+  return n ^ ((k & 1) | ((k >> 1) * 6));
+}
+
+// first double of face slot s
+__device__ __forceinline__ int w3_fs(int s) { return (s + 4 * (s >> 4)) * W3::FS; }
+
+// a face slot (5 doubles) with 8-byte shared loads / stores
 __device__ __forceinline__ void w3_slot_load(const double* p, double (&u)[5]) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-  const double2 a = q[0], b = q[1];
-  u[0] = a.x;
-  u[1] = a.y;
-  u[2] = b.x;
-  u[3] = b.y;
-  u[4] = p[4];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) u[v] = p[v];
 }
 
 __device__ __forceinline__ void w3_slot_store(double* p, const double (&u)[5]) {
-  double2* q = reinterpret_cast<double2*>(p);
-  q[0] = make_double2(u[0], u[1]);
-  q[1] = make_double2(u[2], u[3]);
-  p[4] = u[4];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) p[v] = u[v];
 }
 
 // the flux inputs of one node from the warp slice (three 16-byte loads)
@@ -77,8 +85,8 @@ struct W3Prim {
 };
 
 __device__ __forceinline__ W3Prim w3_load(const double* pr, int n) {
-  const double2* q = reinterpret_cast<const double2*>(pr + n * W3::NPR);
-  const double2 a = q[0], b = q[1], c = q[2];
+  const double2* q = reinterpret_cast<const double2*>(pr) + w3_sw(n);
+  const double2 a = q[0], b = q[W3::NPC], c = q[2 * W3::NPC];
   W3Prim r;
   r.rho = a.x;
   r.beta = a.y;
@@ -222,8 +230,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   __shared__ CellRec s_rec[S::WPB][2];  // descriptors, prefetched one cell ahead
   if (st->aborted || st->finished) return;  // uniform across the grid
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* pr = smem + wib * S::SM_WARP;  // [NPR][64]
-  double* fs = pr + S::SM_PR;            // [3][32][V]: staged traces, then surface terms
+  double* pr = smem + wib * S::SM_WARP;  // [4][64] double2, swizzled (w3_sw)
+  double* fs = pr + S::SM_PR;            // face slots (w3_fs): staged traces, then surface terms
   double* eU = fs + S::SM_FS;            // the cell's U [64 V] and K1 [64 V] (epilogue)
   double* eK = eU + N * V;
   // descriptor of one cell into the warp's buffer b (lanes 0-5, 16 B each)
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const int nbc = rp->nb[2 * d + side];
-      double* dst = fs + (d * 32 + lane) * S::FS;
+      double* dst = fs + w3_fs(d * 32 + lane);
       if (nbc < 0) {
         const double* g = m.ghost + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
 #pragma unroll
@@ -329,11 +337,11 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const Prim<3> q = prim_of<3>(ph, h ? uB : uA, ir);
       okAB = okAB && prim_ok<3>(q);
       const double be = q.rho * frcp(q.p);
-      double2* dst = reinterpret_cast<double2*>(pr + n * S::NPR);
+      double2* dst = reinterpret_cast<double2*>(pr) + w3_sw(n);
       dst[0] = make_double2(q.rho, be);
-      dst[1] = make_double2(q.v[0], q.v[1]);
-      dst[2] = make_double2(q.v[2], q.p);
-      dst[3] = make_double2(q.E, SURF == 2 ? fsqrt(ph.gamma * q.p * ir) : 0.0);
+      dst[N] = make_double2(q.v[0], q.v[1]);
+      dst[2 * N] = make_double2(q.v[2], q.p);
+      dst[3 * N] = make_double2(q.E, SURF == 2 ? fsqrt(ph.gamma * q.p * ir) : 0.0);
       const unsigned hr = static_cast<unsigned>(__double2hiint(q.rho));
       const unsigned hb = static_cast<unsigned>(__double2hiint(be));
       hr_lo = min(hr_lo, hr);
@@ -380,7 +388,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     __syncwarp();
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      double* slotp = fs + (d * 32 + lane) * S::FS;
+      double* slotp = fs + w3_fs(d * 32 + lane);
       const int nbc = rp->nb[2 * d + side];
       double un[V];
       if (nbc >= 0 && a.form) {
@@ -400,8 +408,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const double lift = rp->lift[d];
       const int j = side ? N1 - 1 : 0;
       double o5[V];
-      const double2* on = reinterpret_cast<const double2*>(pr + w3_face_node(d, side, pt) * S::NPR);
-      const double2 o0 = on[0], o1 = on[1], o2 = on[2], o3 = on[3];
+      const double2* on = reinterpret_cast<const double2*>(pr) + w3_sw(w3_face_node(d, side, pt));
+      const double2 o0 = on[0], o1 = on[N], o2 = on[2 * N], o3 = on[3 * N];
       const double vo[3] = {o1.x, o1.y, o2.x};
       const bool ok = rus_lift_v<3, SURF>(ph, o0.x, vo, o2.y, o3.x, o3.y, un, d, side,
                                           J2 * c_D[j * N1 + j], side ? -lift : lift, false, o5);
@@ -421,13 +429,13 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         const int ptB = d == 0 ? iy + 4 * zB : (d == 1 ? ix + 4 * zB : ix + 4 * iy);
         if (jA[d] == 0 || jA[d] == N1 - 1) {
           double c[V];
-          w3_slot_load(fs + (d * 32 + 16 * (jA[d] ? 1 : 0) + ptA) * S::FS, c);
+          w3_slot_load(fs + w3_fs(d * 32 + 16 * (jA[d] ? 1 : 0) + ptA), c);
 #pragma unroll
           for (int v = 0; v < V; ++v) KA[v] += c[v];
         }
         if (jB[d] == 0 || jB[d] == N1 - 1) {
           double c[V];
-          w3_slot_load(fs + (d * 32 + 16 * (jB[d] ? 1 : 0) + ptB) * S::FS, c);
+          w3_slot_load(fs + w3_fs(d * 32 + 16 * (jB[d] ? 1 : 0) + ptB), c);
 #pragma unroll
           for (int v = 0; v < V; ++v) KB[v] += c[v];
         }
