@@ -28,8 +28,8 @@
 namespace perrk {
 namespace dev {
 
-#ifndef PERRK_W3_EPI_STAGE
-#define PERRK_W3_EPI_STAGE 0  // 1: stage the epilogue's U, K1 blocks in shared memory
+#ifndef PERRK_W3_COAL
+#define PERRK_W3_COAL 1  // epilogue U / K1 / U_{i+1} blocks through the slice (coalesced)
 #endif
 
 #ifndef PERRK_W3_WPB
@@ -54,8 +54,9 @@ struct W3 {
   static constexpr int SM_PR = NPR * NPC;
   static constexpr int FS = 5;
   static constexpr int SM_FS = (96 + 4 * 5) * FS;
-  static constexpr int SM_EP = PERRK_W3_EPI_STAGE ? 2 * NPC * V : 0;
-  static constexpr int SM_WARP = SM_PR + SM_FS + SM_EP;
+  static constexpr int SM_WARP = SM_PR + SM_FS;
+  static_assert(SM_WARP >= 2 * NPC * V, "the epilogue stages U and K1 in the slice");
+  static_assert(SM_WARP % 2 == 0, "16-byte aligned slices");
   static constexpr int SM_TOTAL = WPB * SM_WARP;  // doubles per block
 };
 
@@ -125,6 +126,29 @@ __device__ __forceinline__ void cp_async_commit() {
 template <int NPENDING>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(NPENDING) : "memory");
+}
+
+// bulk (TMA-path) store of a shared-memory block to global memory: the
+// writing lanes fence their generic-proxy stores first; one lane issues
+__device__ __forceinline__ void bulk_store_fence() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_store(double* gdst, const double* ssrc, unsigned bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// the source of every committed bulk store has been read (smem reusable)
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // one cell's contiguous block of a state array (64 V doubles) into the warp's slice
@@ -232,8 +256,6 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* pr = smem + wib * S::SM_WARP;  // [4][64] double2, swizzled (w3_sw)
   double* fs = pr + S::SM_PR;            // face slots (w3_fs): staged traces, then surface terms
-  double* eU = fs + S::SM_FS;            // the cell's U [64 V] and K1 [64 V] (epilogue)
-  double* eK = eU + N * V;
   // descriptor of one cell into the warp's buffer b (lanes 0-5, 16 B each)
   auto fetch_rec = [&](int b, int c) {
     if (c >= 0 && lane < static_cast<int>(sizeof(CellRec) / 16))
@@ -266,6 +288,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     }
     // ---- descriptor (host.cpp build_cell_records), fetched a cell ago -------
     cp_async_wait<0>();
+    if (PERRK_W3_COAL && lane == 0) bulk_wait_read();  // the previous U_{i+1} left the slice
     __syncwarp();
     const CellRec* rp = &s_rec[wib][rb];
     const unsigned long long lv =
@@ -317,12 +340,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         }  // else: formed from U and K1 in the surface phase (first active stage only)
       }
     }
-    // the epilogue's U and K1 of this cell (contiguous blocks)
     const size_t cbase = static_cast<size_t>(cell) * N * V;
-    if (PERRK_W3_EPI_STAGE && a.write_next) {
-      w3_stage_cell(eU, a.U + cbase, lane);
-      if (a.form) w3_stage_cell(eK, a.K1 + cbase, lane);
-    }
     cp_async_commit();
     fetch_rec(rb ^ 1, ncell);  // the next cell's descriptor
     // ---- primitives of A and B -> the warp's slice -------------------------
@@ -475,20 +493,56 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         a.Kout[gB + v] = KB[v];
       }
     }
-    // U_{i+1} and d, node by node, each batch with all its loads issued
-    // before its first store (the compiler cannot tell that Usn / d do not
-    // alias U / K1, and would otherwise serialise load -> store pairs)
+    const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
+#if PERRK_W3_COAL
+    // U_{i+1} = U + dt (a_{i+1,1} K1 + a_{i+1,i} K_i): the cell's U and K1
+    // blocks (2560 contiguous bytes each) come in with coalesced 16-byte
+    // cp.async into the slice (the primitives and face slots are dead by
+    // now), are read node-wise with 8-byte loads (40-byte stride, conflict
+    // free), and U_{i+1} is written back in place and leaves as one bulk copy
+    // (cp.async.bulk, the TMA path: no per-lane store wavefronts).
+    if (a.write_next) {
+      double* eb = pr;
+      __syncwarp();  // every lane is done with the primitives and face slots
+      w3_stage_cell(eb, a.U + cbase, lane);
+      if (a.form) w3_stage_cell(eb + N * V, a.K1 + cbase, lane);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double* K = h ? KB : KA;
+        double* e = eb + (lane + 32 * h) * V;
+        double x[V];
+        if (a.form) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) x[v] = e[v] + fma(an, e[N * V + v], pn * K[v]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) x[v] = fma(an, K[v], e[v]);
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) e[v] = x[v];
+      }
+      bulk_store_fence();
+      __syncwarp();
+      if (lane == 0) bulk_store(a.Usn + cbase, eb, N * V * sizeof(double));
+    }
+#endif
+    // d (and, without the coalesced path, U_{i+1}) node by node, each batch
+    // with all its loads issued before its first store (the compiler cannot
+    // tell that Usn / d do not alias U / K1, and would otherwise serialise
+    // load -> store pairs)
     {
-      const double* Up = PERRK_W3_EPI_STAGE ? eU : a.U + cbase;
-      const double* Kp = PERRK_W3_EPI_STAGE ? eK : a.K1 + cbase;
-      const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double* K = h ? KB : KA;
         const int o = (lane + 32 * h) * V;
         const size_t g = h ? gB : gA;
         double x[V], y[V];
-        if (a.write_next) {
+        if (!PERRK_W3_COAL && a.write_next) {
+          const double* Up = a.U + cbase;
+          const double* Kp = a.K1 + cbase;
 #pragma unroll
           for (int v = 0; v < V; ++v) x[v] = Up[o + v];
           if (a.form) {
@@ -525,6 +579,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     rb ^= 1;
   }
 
+  if (PERRK_W3_COAL && lane == 0) bulk_wait_all();
   // ---- grid epilogue (as stage_kernel) --------------------------------------
   if (a.want_dmax) {
 #pragma unroll
