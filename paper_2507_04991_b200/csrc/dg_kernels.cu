@@ -295,12 +295,19 @@ __device__ void relax_update(StepState* st, dd A, dd B) {
   st->iters = it;
 }
 
+// One relaxation pass.  Each warp walks blocks of 32 consecutive nodes: the
+// block's U and d (32 V doubles each, contiguous) arrive by coalesced 16-byte
+// cp.async into a double-buffered per-warp staging area one block ahead, and
+// each lane reads its node with 8-byte loads (40- / 32-byte stride: conflict
+// free).  The previous layout (a thread's own node straight from global
+// memory, stride V doubles) cost 5x the L1 wavefronts per byte.
 template <int DIM>
 __global__ void __launch_bounds__(256)
     relax_pass_kernel(const double* __restrict__ U, const double* __restrict__ d, MeshDev m,
                       Phys ph, StepState* st, double* partials, unsigned* counter, long long nnodes) {
-  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC, BLK = 32 * V;  // doubles per block and array
   __shared__ double s_red[2 * 2 * 8];
+  __shared__ __align__(16) double s_stage[8][2][2][BLK];  // [warp][buffer][U, d][block]
   if (st->aborted || st->finished || st->relax_done) return;
   const double dmax = __longlong_as_double(static_cast<long long>(st->dmax_bits));
   if (st->d_nonfinite || dmax == 0.0) {
@@ -320,30 +327,71 @@ __global__ void __launch_bounds__(256)
   const double gamma = st->gamma;
   const double gdt = gamma * st->dt;
   const int numerics = st->numerics;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long nblk = (nnodes + 31) / 32;
+  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  // stage block k (all of it that exists) into buffer b
+  auto stage = [&](long long k, int b) {
+    if (k < nblk) {
+      const long long n0 = k * 32;
+      const int nd = static_cast<int>(min(32LL, nnodes - n0)) * V;  // doubles in the block
+      const double* gu = U + n0 * V;
+      const double* gd = d + n0 * V;
+      double* su = s_stage[wib][b][0];
+      double* sd = s_stage[wib][b][1];
+      if (nd == BLK && ((n0 * V) & 1) == 0) {
+#pragma unroll
+        for (int q = lane; q < BLK / 2; q += 32) {
+          cp_async16(su + 2 * q, gu + 2 * q);
+          cp_async16(sd + 2 * q, gd + 2 * q);
+        }
+      } else {
+        for (int q = lane; q < nd; q += 32) {
+          cp_async8(su + q, gu + q);
+          cp_async8(sd + q, gd + q);
+        }
+      }
+    }
+    cp_async_commit();
+  };
   dd A = dd_zero(), B = dd_zero();
-  for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < nnodes;
-       n += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
-    const double om = node_measure_rec<DIM>(m, cell, l);
-    double u[V], dv[V], T[V];
+  long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
+  int b = 0;
+  stage(k, 0);
+  for (; k < nblk; k += stride, b ^= 1) {
+    stage(k + stride, b ^ 1);
+    cp_async_wait<1>();
+    __syncwarp();
+    const long long n = k * 32 + lane;
+    if (n < nnodes) {
+      const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
+      const double om = node_measure_rec<DIM>(m, cell, l);
+      const double* su = s_stage[wib][b][0] + lane * V;
+      const double* sd = s_stage[wib][b][1] + lane * V;
+      double u[V], dv[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      u[v] = __ldg(U + n * V + v);
-      dv[v] = __ldg(d + n * V + v);
-      T[v] = u[v] + gdt * dv[v];
-    }
-    if (numerics == 1) {
-      double du[V], a, b;
+      for (int v = 0; v < V; ++v) {
+        u[v] = su[v];
+        dv[v] = sd[v];
+      }
+      if (numerics == 1) {
+        double du[V], ra, rb;
 #pragma unroll
-      for (int v = 0; v < V; ++v) du[v] = gdt * dv[v];
-      relax_terms<DIM>(ph, u, du, dv, a, b);
-      A = dd_add_prod(A, om, a);
-      B = dd_add_prod(B, om, b);
-    } else {  // the reference's residual / derivative on the rounded trial state
-      A = dd_add_prod(A, om, entropy<DIM>(ph, T));
-      B = dd_add_prod(B, om, entropy_dot<DIM>(ph, T, dv));
+        for (int v = 0; v < V; ++v) du[v] = gdt * dv[v];
+        relax_terms<DIM>(ph, u, du, dv, ra, rb);
+        A = dd_add_prod(A, om, ra);
+        B = dd_add_prod(B, om, rb);
+      } else {  // the reference's residual / derivative on the rounded trial state
+        double T[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) T[v] = u[v] + gdt * dv[v];
+        A = dd_add_prod(A, om, entropy<DIM>(ph, T));
+        B = dd_add_prod(B, om, entropy_dot<DIM>(ph, T, dv));
+      }
     }
+    __syncwarp();  // buffer b is restaged two blocks on
   }
+  cp_async_wait<0>();
   dd v[2] = {A, B}, tot[2];
   block_reduce_dd<2>(v, s_red);
   if (grid_reduce_dd<2>(v, partials, counter, s_red, tot) && threadIdx.x == 0) {
