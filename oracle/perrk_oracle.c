@@ -1074,8 +1074,9 @@ static int solve_relaxation(relax_ctx* r, const orc_relax* cfg, double gamma_see
 
   if (cfg->method == 0 && r->numerics == 1) {
     /* H1.4: always take >= 1 Newton step from the seed; stop on a relative
-     * step below 1e-13 or on noise-floor stagnation; fall back only on
-     * non-finite values or gamma <= 0. */
+     * step below 1e-13 (from the second step on, the iterate is then kept:
+     * the correction is noise) or on noise-floor stagnation; fall back only
+     * on non-finite values or gamma <= 0. */
     double gamma = cfg->seed_from_previous ? gamma_seed : 1.0;
     double prev = 0.0;
     for (int it = 1; it <= cfg->max_iter; ++it) {
@@ -1088,6 +1089,12 @@ static int solve_relaxation(relax_ctx* r, const orc_relax* cfg, double gamma_see
         return 0;
       }
       const double step = res / dr;
+      /* after the first step, a correction below 1e-13 gamma is under the
+       * residual's noise floor: the current iterate is kept as the root */
+      if (it >= 2 && fabs(step) <= 1e-13 * gamma && gamma > 0.0) {
+        out->gamma = gamma;
+        return 0;
+      }
       gamma -= step;
       if (!isfinite(gamma) || !(gamma > 0.0)) {
         *out = fallback(it, res);

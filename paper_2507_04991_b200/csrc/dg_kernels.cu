@@ -127,6 +127,8 @@ __global__ void begin_step_kernel(StepState* st) {
   st->pass = 0;
   st->fell_back = 0;
   st->relax_done = st->relax_enabled ? 0 : 1;
+  st->spec_done = 0;
+  st->numax_spec_bits = 0ull;
 }
 
 // ---------------------------------------------------------------------------
@@ -162,6 +164,14 @@ __device__ void relax_newton_update(StepState* st, dd A, dd B) {
     st->residual = r;
     if (dr == 0.0 || !isfinite(dr) || !isfinite(r)) return relax_fallback(st, it, r);
     const double step = r / dr;
+    // after the first step (always take >= 1), a
+    // correction below 1e-13 gamma is under the residual's noise floor: the
+    // current iterate is the root and is kept, not moved by the noise (which
+    // also lets relax_spec_kernel's update at this gamma stand)
+    if (it >= 2 && fabs(step) <= 1e-13 * gamma && gamma > 0.0) {
+      st->relax_done = 1;
+      return;
+    }
     const double g2 = gamma - step;
     if (!isfinite(g2) || !(g2 > 0.0)) return relax_fallback(st, it, r);
     st->gamma = g2;
@@ -295,6 +305,35 @@ __device__ void relax_update(StepState* st, dd A, dd B) {
   st->iters = it;
 }
 
+// One warp's 32-node block k of two state arrays (U and d, 32 V contiguous
+// doubles each) into shared memory by coalesced cp.async (16-byte pieces when
+// the block is whole), one commit group per call (empty past the end).
+template <int V>
+__device__ __forceinline__ void stage_pair(const double* A, const double* B, long long nnodes,
+                                           long long nblk, long long k, double* sa, double* sb,
+                                           int lane) {
+  if (k < nblk) {
+    constexpr int BLK = 32 * V;
+    const long long n0 = k * 32;
+    const int nd = static_cast<int>(min(32LL, nnodes - n0)) * V;
+    const double* ga = A + n0 * V;
+    const double* gb = B + n0 * V;
+    if (nd == BLK) {
+#pragma unroll
+      for (int q = lane; q < BLK / 2; q += 32) {
+        cp_async16(sa + 2 * q, ga + 2 * q);
+        cp_async16(sb + 2 * q, gb + 2 * q);
+      }
+    } else {
+      for (int q = lane; q < nd; q += 32) {
+        cp_async8(sa + q, ga + q);
+        cp_async8(sb + q, gb + q);
+      }
+    }
+  }
+  cp_async_commit();
+}
+
 // One relaxation pass.  Each warp walks blocks of 32 consecutive nodes: the
 // block's U and d (32 V doubles each, contiguous) arrive by coalesced 16-byte
 // cp.async into a double-buffered per-warp staging area one block ahead, and
@@ -330,31 +369,10 @@ __global__ void __launch_bounds__(256)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const long long nblk = (nnodes + 31) / 32;
   const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-  // stage block k (all of it that exists) into buffer b
   auto stage = [&](long long k, int b) {
-    if (k < nblk) {
-      const long long n0 = k * 32;
-      const int nd = static_cast<int>(min(32LL, nnodes - n0)) * V;  // doubles in the block
-      const double* gu = U + n0 * V;
-      const double* gd = d + n0 * V;
-      double* su = s_stage[wib][b][0];
-      double* sd = s_stage[wib][b][1];
-      if (nd == BLK && ((n0 * V) & 1) == 0) {
-#pragma unroll
-        for (int q = lane; q < BLK / 2; q += 32) {
-          cp_async16(su + 2 * q, gu + 2 * q);
-          cp_async16(sd + 2 * q, gd + 2 * q);
-        }
-      } else {
-        for (int q = lane; q < nd; q += 32) {
-          cp_async8(su + q, gu + q);
-          cp_async8(sd + q, gd + q);
-        }
-      }
-    }
-    cp_async_commit();
+    stage_pair<V>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
   };
-  dd A = dd_zero(), B = dd_zero();
+  ksum A = ks_zero(), B = ks_zero();
   long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
   int b = 0;
   stage(k, 0);
@@ -376,23 +394,25 @@ __global__ void __launch_bounds__(256)
       }
       if (numerics == 1) {
         double du[V], ra, rb;
+        // rounded products (never contracted into later sums): the same bits
+        // in relax_spec_kernel
 #pragma unroll
-        for (int v = 0; v < V; ++v) du[v] = gdt * dv[v];
-        relax_terms<DIM>(ph, u, du, dv, ra, rb);
-        A = dd_add_prod(A, om, ra);
-        B = dd_add_prod(B, om, rb);
+        for (int v = 0; v < V; ++v) du[v] = __dmul_rn(gdt, dv[v]);
+        relax_terms<DIM>(ph, u, du, dv, trial_state<DIM>(ph, u, du), ra, rb);
+        ks_add_prod(A, om, ra);
+        ks_add_prod(B, om, rb);
       } else {  // the reference's residual / derivative on the rounded trial state
         double T[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) T[v] = u[v] + gdt * dv[v];
-        A = dd_add_prod(A, om, entropy<DIM>(ph, T));
-        B = dd_add_prod(B, om, entropy_dot<DIM>(ph, T, dv));
+        ks_add_prod(A, om, entropy<DIM>(ph, T));
+        ks_add_prod(B, om, entropy_dot<DIM>(ph, T, dv));
       }
     }
     __syncwarp();  // buffer b is restaged two blocks on
   }
   cp_async_wait<0>();
-  dd v[2] = {A, B}, tot[2];
+  dd v[2] = {ks_dd(A), ks_dd(B)}, tot[2];
   block_reduce_dd<2>(v, s_red);
   if (grid_reduce_dd<2>(v, partials, counter, s_red, tot) && threadIdx.x == 0) {
     if (st->slab) {  // gathered over ranks, then combine_kernel(COMBINE_RELAX)
@@ -410,59 +430,122 @@ __global__ void __launch_bounds__(256)
 // final update, CFL speed, step record
 // ---------------------------------------------------------------------------
 
+// the update's per-node terms of the new state u: the next step's CFL speed
+// (mesh.cpp:97-129 takes |v_dir| + c per direction; 1/h_dir = jac_dir / 2
+// exactly, one pressure / sound speed per node) and the StepRecord H and
+// invariants (stepper.cpp:179-180)
+template <int DIM>
+__device__ __forceinline__ void update_node_terms(const MeshDev& m, const Phys& ph, const double* u,
+                                                  long long n, int want_nu, int want_record,
+                                                  double s_new, double& numax, ksum* acc) {
+  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
+  if (want_nu) {
+    const double ir = frcp(u[0]);
+    double m2 = 0.0;
+#pragma unroll
+    for (int dir = 0; dir < DIM; ++dir) m2 = fma(u[1 + dir], u[1 + dir], m2);
+    const double p = ph.gm1 * (u[DIM + 1] - 0.5 * m2 * ir);
+    const double c = fsqrt(ph.gamma * p * ir);
+#pragma unroll
+    for (int dir = 0; dir < DIM; ++dir)
+      numax = fmax(numax, (fabs(u[1 + dir]) * ir + c) * (0.25 * __ldg(&m.rec[cell].J2[dir])));
+  }
+  if (want_record) {
+    const double om = node_measure_rec<DIM>(m, cell, l);
+    ks_add_prod(acc[0], om, s_new);
+#pragma unroll
+    for (int v = 0; v < V; ++v) ks_add_prod(acc[1 + v], om, u[v]);
+  }
+}
+
+// StepRecord entropy of the new state u + du, s = -rho log(p / rho^gamma)
+// (physics.cpp:130-132), from the trial state's logarithms
+__device__ __forceinline__ double trial_entropy(const Phys& ph, const Trial& t) {
+  return -t.rho_t * (t.lp_t - ph.gamma * t.lr_t);
+}
+
+// the update's last-block step: clock advance (stepper.cpp:107-113), the
+// StepRecord row, the next gamma seed
+__device__ void finish_step(StepState* st, double gamma, const dd* tot, int V, int want_record,
+                            double* records) {
+  const double dt = st->dt;
+  if (st->relax_enabled && !st->idt)
+    st->t += gamma * dt;
+  else
+    st->t += dt;
+  if (want_record && records) {
+    double* row = records + static_cast<size_t>(st->steps_taken) * 11;
+    row[0] = st->t;
+    row[1] = dt;
+    row[2] = gamma;
+    row[3] = st->iters;
+    row[4] = st->fell_back;
+    row[5] = tot[0].hi + tot[0].lo;
+    for (int v = 0; v < V; ++v) row[6 + v] = tot[1 + v].hi + tot[1 + v].lo;
+  }
+  st->gamma_seed = st->fell_back ? 1.0 : gamma;
+  st->steps_taken += 1;
+}
+
+// U_out = U_in + gamma dt d (in place when U_out == U_in; out of place after
+// a relax_spec_kernel, which has already done it when its speculation held).
+// Same node walk as the relaxation passes (warp blocks of 32 nodes staged by
+// coalesced cp.async, launched on relax_pass_kernel's grid), so the StepRecord
+// sums come out bitwise the same as relax_spec_kernel's.
 template <int DIM>
 __global__ void __launch_bounds__(256)
-    update_kernel(double* __restrict__ U, const double* __restrict__ d, MeshDev m, Phys ph,
-                  StepState* st, double* partials, unsigned* counter, long long nnodes,
+    update_kernel(double* Uout, const double* Uin, const double* __restrict__ d, MeshDev m,
+                  Phys ph, StepState* st, double* partials, unsigned* counter, long long nnodes,
                   int want_nu, int want_record, double* records) {
-  constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
+  constexpr int V = DIM + 2, BLK = 32 * V;
   __shared__ double s_red[2 * 6 * 8];
-  if (st->aborted || st->finished) return;
+  __shared__ __align__(16) double s_stage[8][2][2][BLK];  // [warp][buffer][U, d][block]
+  if (st->aborted || st->finished || st->spec_done) return;
   const double gamma = st->relax_enabled ? st->gamma : st->gamma_override;
   const double scale = gamma * st->dt;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long nblk = (nnodes + 31) / 32;
+  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   double numax = 0.0;
-  dd acc[6];
+  ksum acc[6];
 #pragma unroll
-  for (int r = 0; r < 6; ++r) acc[r] = dd_zero();
-  for (long long n = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; n < nnodes;
-       n += static_cast<long long>(gridDim.x) * blockDim.x) {
-    double u[V];
+  for (int r = 0; r < 6; ++r) acc[r] = ks_zero();
+  long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
+  int b = 0;
+  stage_pair<V>(Uin, d, nnodes, nblk, k, s_stage[wib][0][0], s_stage[wib][0][1], lane);
+  for (; k < nblk; k += stride, b ^= 1) {
+    stage_pair<V>(Uin, d, nnodes, nblk, k + stride, s_stage[wib][b ^ 1][0],
+                  s_stage[wib][b ^ 1][1], lane);
+    cp_async_wait<1>();
+    __syncwarp();
+    const long long n = k * 32 + lane;
+    if (n < nnodes) {
+      const double* su = s_stage[wib][b][0] + lane * V;
+      const double* sd = s_stage[wib][b][1] + lane * V;
+      double u[V], du[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      u[v] = U[n * V + v] + scale * __ldg(d + n * V + v);
-      U[n * V + v] = u[v];
-    }
-    if (want_nu || want_record) {
-      const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
-      // one pressure / sound speed per node (mesh.cpp:97-129 takes
-      // |v_dir| + c per direction; 1/h_dir = jac_dir / 2 exactly)
-      const double ir = frcp(u[0]);
-      double m2 = 0.0;
-#pragma unroll
-      for (int dir = 0; dir < DIM; ++dir) m2 = fma(u[1 + dir], u[1 + dir], m2);
-      const double p = ph.gm1 * (u[DIM + 1] - 0.5 * m2 * ir);
-      if (want_nu) {
-        const double c = fsqrt(ph.gamma * p * ir);
-#pragma unroll
-        for (int dir = 0; dir < DIM; ++dir)
-          numax = fmax(numax, (fabs(u[1 + dir]) * ir + c) * (0.25 * __ldg(&m.rec[cell].J2[dir])));
+      for (int v = 0; v < V; ++v) {
+        u[v] = fma(scale, sd[v], su[v]);
+        du[v] = __dmul_rn(scale, sd[v]);
+        Uout[n * V + v] = u[v];
       }
-      if (want_record) {
-        const double om = node_measure_rec<DIM>(m, cell, l);
-        // s = -rho log(p / rho^gamma) (physics.cpp:130-132) as -rho (log p - gamma log rho)
-        acc[0] = dd_add_prod(acc[0], om, -u[0] * (flog(p) - ph.gamma * flog(u[0])));
-#pragma unroll
-        for (int v = 0; v < V; ++v) acc[1 + v] = dd_add_prod(acc[1 + v], om, u[v]);
-      }
+      const double s_new = want_record ? trial_entropy(ph, trial_state<DIM>(ph, su, du)) : 0.0;
+      if (want_nu || want_record)
+        update_node_terms<DIM>(m, ph, u, n, want_nu, want_record, s_new, numax, acc);
     }
+    __syncwarp();
   }
+  cp_async_wait<0>();
   if (want_nu) {
     numax = warp_max(numax);
-    if ((threadIdx.x & 31) == 0) atomic_max_pos(&st->numax_bits, numax);
+    if (lane == 0) atomic_max_pos(&st->numax_bits, numax);
   }
-  dd tot[6];
-  if (want_record) block_reduce_dd<6>(acc, s_red);
-  if (grid_reduce_dd<6>(acc, partials, counter, s_red, tot) && threadIdx.x == 0) {
+  dd tot[6], accd[6];
+#pragma unroll
+  for (int r = 0; r < 6; ++r) accd[r] = ks_dd(acc[r]);
+  if (want_record) block_reduce_dd<6>(accd, s_red);
+  if (grid_reduce_dd<6>(accd, partials, counter, s_red, tot) && threadIdx.x == 0) {
     if (st->slab) {  // gathered over ranks, then combine_kernel(COMBINE_UPDATE)
       for (int r = 0; r < 6; ++r) {
         st->red_local[R_REC0 + 2 * r] = tot[r].hi;
@@ -470,23 +553,94 @@ __global__ void __launch_bounds__(256)
       }
       return;
     }
-    const double dt = st->dt;
-    if (st->relax_enabled && !st->idt)
-      st->t += gamma * dt;
-    else
-      st->t += dt;
-    if (want_record && records) {
-      double* row = records + static_cast<size_t>(st->steps_taken) * 11;
-      row[0] = st->t;
-      row[1] = dt;
-      row[2] = gamma;
-      row[3] = st->iters;
-      row[4] = st->fell_back;
-      row[5] = tot[0].hi + tot[0].lo;
-      for (int v = 0; v < V; ++v) row[6 + v] = tot[1 + v].hi + tot[1 + v].lo;
+    finish_step(st, gamma, tot, V, want_record, records);
+  }
+}
+
+// Newton pass 2 of the accurate relaxation fused with a speculative final
+// update.  Pass 1 has produced gamma_1; Newton from the previous step's gamma
+// converges in that one step (the next correction is ~1e-22, below half an
+// ulp of gamma), so this pass evaluates r(gamma_1), r'(gamma_1) (exactly as
+// relax_pass_kernel) and, from the same U and d, the state U + gamma_1 dt d
+// into U_out with the update's CFL speed and StepRecord terms (exactly as
+// update_kernel).  Its last block runs the Newton logic; if that finishes at
+// gamma_1 itself, the speculation is the update and the step is completed
+// here (spec_done: update_kernel returns at once).  Otherwise the remaining
+// passes and update_kernel proceed from the untouched U_in.  One full read of
+// U and d per step is saved (SURVEY.md 7.3 H1 numerics only).
+template <int DIM>
+__global__ void __launch_bounds__(256)
+    relax_spec_kernel(const double* __restrict__ U, const double* __restrict__ d,
+                      double* __restrict__ Uout, MeshDev m, Phys ph, StepState* st,
+                      double* partials, unsigned* counter, long long nnodes, int want_nu,
+                      int want_record, double* records) {
+  constexpr int V = DIM + 2, BLK = 32 * V;
+  __shared__ double s_red[2 * 8 * 8];
+  __shared__ __align__(16) double s_stage[8][2][2][BLK];  // [warp][buffer][U, d][block]
+  if (st->aborted || st->finished || st->relax_done) return;
+  const double dmax = __longlong_as_double(static_cast<long long>(st->dmax_bits));
+  if (st->d_nonfinite || dmax == 0.0) return;  // handled by pass 1
+  const double gamma = st->gamma;
+  const double gdt = gamma * st->dt;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long nblk = (nnodes + 31) / 32;
+  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  auto stage = [&](long long k, int b) {
+    stage_pair<V>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
+  };
+  ksum acc[8];  // A, B, then the update's six record sums
+#pragma unroll
+  for (int r = 0; r < 8; ++r) acc[r] = ks_zero();
+  double numax = 0.0;
+  long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
+  int b = 0;
+  stage(k, 0);
+  for (; k < nblk; k += stride, b ^= 1) {
+    stage(k + stride, b ^ 1);
+    cp_async_wait<1>();
+    __syncwarp();
+    const long long n = k * 32 + lane;
+    if (n < nnodes) {
+      const double* su = s_stage[wib][b][0] + lane * V;
+      const double* sd = s_stage[wib][b][1] + lane * V;
+      double u[V], dv[V], du[V], T[V], ra, rb;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        u[v] = su[v];
+        dv[v] = sd[v];
+        du[v] = __dmul_rn(gdt, dv[v]);
+        T[v] = fma(gdt, dv[v], u[v]);  // update_kernel's U + (gamma dt) d
+      }
+      const double om = node_measure_rec<DIM>(m, static_cast<int>(n / Geo<DIM>::NPC),
+                                              static_cast<int>(n % Geo<DIM>::NPC));
+      const Trial tr = trial_state<DIM>(ph, u, du);
+      relax_terms<DIM>(ph, u, du, dv, tr, ra, rb);
+      ks_add_prod(acc[0], om, ra);
+      ks_add_prod(acc[1], om, rb);
+#pragma unroll
+      for (int v = 0; v < V; ++v) Uout[n * V + v] = T[v];
+      if (want_nu || want_record)
+        update_node_terms<DIM>(m, ph, T, n, want_nu, want_record, trial_entropy(ph, tr), numax,
+                               acc + 2);
     }
-    st->gamma_seed = st->fell_back ? 1.0 : gamma;
-    st->steps_taken += 1;
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  if (want_nu) {
+    numax = warp_max(numax);
+    if (lane == 0) atomic_max_pos(&st->numax_spec_bits, numax);
+  }
+  dd tot[8], accd[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) accd[r] = ks_dd(acc[r]);
+  block_reduce_dd<8>(accd, s_red);
+  if (grid_reduce_dd<8>(accd, partials, counter, s_red, tot) && threadIdx.x == 0) {
+    relax_update(st, tot[0], tot[1]);
+    if (st->relax_done && !st->fell_back && st->gamma == gamma) {
+      st->spec_done = 1;
+      if (want_nu) st->numax_bits = st->numax_spec_bits;
+      finish_step(st, gamma, tot + 2, V, want_record, records);
+    }
   }
 }
 
@@ -1049,18 +1203,37 @@ cudaError_t launch_relax_pass(int dim, const double* U, const double* d, const M
   return cudaGetLastError();
 }
 
-cudaError_t launch_update(int dim, double* U, const double* d, const MeshDev& m, const Phys& ph,
-                          StepState* st, double* partials, unsigned* counter, long long nnodes,
-                          int want_nu, int want_record, double* records, int grid,
-                          cudaStream_t s) {
+cudaError_t launch_update(int dim, double* Uout, const double* Uin, const double* d,
+                          const MeshDev& m, const Phys& ph, StepState* st, double* partials,
+                          unsigned* counter, long long nnodes, int want_nu, int want_record,
+                          double* records, int grid, cudaStream_t s) {
+  // relax_pass_kernel's grid: the node walk (and record sums) of relax_spec_kernel
   if (dim == 2) {
-    static const int g = resident_grid(update_kernel<2>, 256, grid);
-    update_kernel<2><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes, want_nu,
-                                       want_record, records);
+    static const int g = resident_grid(relax_pass_kernel<2>, 256, grid);
+    update_kernel<2><<<g, 256, 0, s>>>(Uout, Uin, d, m, ph, st, partials, counter, nnodes,
+                                       want_nu, want_record, records);
   } else {
-    static const int g = resident_grid(update_kernel<3>, 256, grid);
-    update_kernel<3><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes, want_nu,
-                                       want_record, records);
+    static const int g = resident_grid(relax_pass_kernel<3>, 256, grid);
+    update_kernel<3><<<g, 256, 0, s>>>(Uout, Uin, d, m, ph, st, partials, counter, nnodes,
+                                       want_nu, want_record, records);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relax_spec(int dim, const double* U, const double* d, double* Uout,
+                              const MeshDev& m, const Phys& ph, StepState* st, double* partials,
+                              unsigned* counter, long long nnodes, int want_nu, int want_record,
+                              double* records, int grid, cudaStream_t s) {
+  // the grid of relax_pass_kernel: the same nodes per warp, so the same
+  // summation order of r and r' (bitwise the unfused pass)
+  if (dim == 2) {
+    static const int g = resident_grid(relax_pass_kernel<2>, 256, grid);
+    relax_spec_kernel<2><<<g, 256, 0, s>>>(U, d, Uout, m, ph, st, partials, counter, nnodes,
+                                           want_nu, want_record, records);
+  } else {
+    static const int g = resident_grid(relax_pass_kernel<3>, 256, grid);
+    relax_spec_kernel<3><<<g, 256, 0, s>>>(U, d, Uout, m, ph, st, partials, counter, nnodes,
+                                           want_nu, want_record, records);
   }
   return cudaGetLastError();
 }

@@ -83,10 +83,14 @@ cudaError_t launch_begin_step(dev::StepState* st, cudaStream_t s);
 cudaError_t launch_relax_pass(int dim, const double* U, const double* d, const dev::MeshDev& m,
                               const dev::Phys& ph, dev::StepState* st, double* partials,
                               unsigned* counter, long long nnodes, int grid, cudaStream_t s);
-cudaError_t launch_update(int dim, double* U, const double* d, const dev::MeshDev& m,
-                          const dev::Phys& ph, dev::StepState* st, double* partials,
-                          unsigned* counter, long long nnodes, int want_nu, int want_record,
-                          double* records, int grid, cudaStream_t s);
+cudaError_t launch_update(int dim, double* Uout, const double* Uin, const double* d,
+                          const dev::MeshDev& m, const dev::Phys& ph, dev::StepState* st,
+                          double* partials, unsigned* counter, long long nnodes, int want_nu,
+                          int want_record, double* records, int grid, cudaStream_t s);
+cudaError_t launch_relax_spec(int dim, const double* U, const double* d, double* Uout,
+                              const dev::MeshDev& m, const dev::Phys& ph, dev::StepState* st,
+                              double* partials, unsigned* counter, long long nnodes, int want_nu,
+                              int want_record, double* records, int grid, cudaStream_t s);
 cudaError_t launch_numax(int dim, const double* U, const dev::MeshDev& m, const dev::Phys& ph,
                          dev::StepState* st, long long nnodes, int grid, cudaStream_t s);
 cudaError_t launch_nu_cell(int dim, const double* U, const dev::MeshDev& m, const dev::Phys& ph,

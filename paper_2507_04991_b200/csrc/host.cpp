@@ -3,6 +3,7 @@
 // over device-resident state, plus the host-side inputs of the hot path
 // (GLL basis, P-ERK family builders, level assignment, partition map).  The
 // exported entry points are the C-ABI declared in include/perrk_b200.h.
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -303,6 +304,9 @@ struct perrk_ctx {
   double mu = 0.0, prandtl = 1.0;
   // device buffers
   double *U = nullptr, *K1 = nullptr, *d = nullptr;
+  // second state buffer of perrk_advance's fused relaxation (relax_spec_kernel):
+  // each step reads U and writes the new state to Ualt, then the two swap
+  double* Ualt = nullptr;
   double *Ka = nullptr, *Kb = nullptr;  // formed stage states U_i, ping-pong by stage parity
   double *tU = nullptr, *tK = nullptr;  // scratch for host-buffer queries
   double* G = nullptr;                   // BR1 viscous fluxes [2][ndofs] (NSF only)
@@ -346,6 +350,7 @@ struct perrk_ctx {
   // CUDA graph of one run() step (perrk_advance): launch latency matters for
   // the small configurations (C1 is 4096 nodes, ~20 kernels per step)
   bool use_graphs = true;
+  bool use_fused = true;  // perrk_advance: relax_spec_kernel (PERRK_NO_FUSED_RELAX=1 disables)
   cudaGraphExec_t graph_exec = nullptr;
   std::string graph_key;
   int64_t graph_launches = 0;  // kernels per graph launch
@@ -561,6 +566,10 @@ struct StepMode {
   bool want_record = false;
   double* records = nullptr;  // non-null: each member writes its own c->records
   double* records_of(perrk_ctx* c) const { return records ? c->records : nullptr; }
+  // single context, accurate-numerics Newton: Newton pass 2 fused with a
+  // speculative out-of-place update (relax_spec_kernel); the step's new state
+  // lands in c->Ualt and enqueue_step swaps c->U / c->Ualt
+  bool fused = false;
 };
 
 // Enqueue the stage launch of stage i of one context; part 0: all the
@@ -667,18 +676,26 @@ void enqueue_step(Group& g, const StepMode& mode, bool want_h) {
     const int passes = relax_passes(mode.cfg);
     for (int p = 0; p < passes; ++p) {
       for (perrk_ctx* c : g.members) {
-        CK(launch_relax_pass(c->dim, c->U, c->d, c->mesh(), c->ph, c->st, c->partials,
-                             c->counter, c->nnodes, c->grid_flat, c->stream));
+        if (mode.fused && p == 1)
+          CK(launch_relax_spec(c->dim, c->U, c->d, c->Ualt, c->mesh(), c->ph, c->st, c->partials,
+                               c->counter, c->nnodes, mode.want_nu ? 1 : 0,
+                               mode.want_record ? 1 : 0, mode.records_of(c), c->grid_flat,
+                               c->stream));
+        else
+          CK(launch_relax_pass(c->dim, c->U, c->d, c->mesh(), c->ph, c->st, c->partials,
+                               c->counter, c->nnodes, c->grid_flat, c->stream));
         c->launches += 1;
       }
       if (slab) reduce_point(g, RED_RELAX, false);
     }
   }
   for (perrk_ctx* c : g.members) {
-    CK(launch_update(c->dim, c->U, c->d, c->mesh(), c->ph, c->st, c->partials, c->counter,
-                     c->nnodes, mode.want_nu ? 1 : 0, mode.want_record ? 1 : 0,
-                     slab ? nullptr : mode.records_of(c), c->grid_flat, c->stream));
+    CK(launch_update(c->dim, mode.fused ? c->Ualt : c->U, c->U, c->d, c->mesh(), c->ph, c->st,
+                     c->partials, c->counter, c->nnodes, mode.want_nu ? 1 : 0,
+                     mode.want_record ? 1 : 0, slab ? nullptr : mode.records_of(c), c->grid_flat,
+                     c->stream));
     c->launches += 1;
+    if (mode.fused) std::swap(c->U, c->Ualt);
   }
   if (slab) reduce_point(g, RED_UPDATE, true, mode.want_record ? mode.records : nullptr);
 }
@@ -726,7 +743,7 @@ void alloc_cell_buffers(perrk_ctx* c) {
 
 void free_cell_buffers(perrk_ctx* c) {
   for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK, &c->dnu, &c->G,
-                     &c->ghost, &c->sendbuf, &c->red_all}) {
+                     &c->ghost, &c->sendbuf, &c->red_all, &c->Ualt}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -1099,6 +1116,7 @@ int perrk_create(const perrk_semi_desc* dsc, perrk_ctx** out) {
     REQUIRE(sf >= 0 && sf <= 5, "unknown surface flux");
     REQUIRE(dsc->gamma > 1.0, "gamma must exceed 1");
     c = new perrk_ctx;
+    if (const char* e = std::getenv("PERRK_NO_FUSED_RELAX")) c->use_fused = e[0] != '1';
     c->device = dsc->device;
     c->dim = dsc->dim;
     c->V = dsc->dim + 2;
@@ -1574,6 +1592,11 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
       if (g.ex) reduce_point(g, RED_NUMAX, true);
     }
     const bool want_h = needs_h(mode.relax, cfg->relax, s.h_ref);
+    mode.fused = mode.relax && cfg->relax.numerics == 1 && cfg->relax.method == 0 &&
+                 cfg->relax.max_iter >= 2 && !g.ex && g.members.size() == 1 && c->use_fused;
+    if (mode.fused && !c->Ualt) CK(cudaMalloc(&c->Ualt, sizeof(double) * c->ndofs_()));
+    double* const U_first = c->U;  // the state buffer of step 0; steps alternate with Ualt
+    double* const U_second = c->Ualt;
     bool graphs = c->use_graphs && nsteps > 1;
     for (perrk_ctx* m : g.members) graphs = graphs && !m->profiling;
     if (graphs) {
@@ -1583,6 +1606,7 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
       std::string key;
       for (perrk_ctx* m : g.members) key += std::to_string(m->plan_version) + ":" +
                                            std::to_string(reinterpret_cast<uintptr_t>(m->records)) + ";";
+      key += std::to_string(reinterpret_cast<uintptr_t>(c->U)) + (mode.fused ? "F" : "-");
       key += std::to_string(mode.relax) + std::to_string(mode.cfg.numerics) + ":" +
              std::to_string(mode.cfg.max_iter) + std::to_string(mode.want_nu) +
              std::to_string(mode.want_record) + std::to_string(want_h);
@@ -1595,6 +1619,7 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
         enqueue_step(g, mode, want_h);
+        if (mode.fused) enqueue_step(g, mode, want_h);  // two steps: the buffers are back in place
         CK(cudaStreamEndCapture(c->stream, &graph));
         CK(cudaGraphInstantiate(&c->graph_exec, graph, 0));
         cudaGraphDestroy(graph);
@@ -1602,14 +1627,21 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
         c->graph_launches = c->launches - l0;
         c->launches = l0;
       }
-      for (int k = 0; k < nsteps; ++k) {
+      const int per = mode.fused ? 2 : 1;
+      for (int k = 0; k + per <= nsteps; k += per) {
         CK(cudaGraphLaunch(c->graph_exec, c->stream));
         c->launches += c->graph_launches;
       }
+      if (nsteps % per) enqueue_step(g, mode, want_h);
     } else {
       for (int k = 0; k < nsteps; ++k) enqueue_step(g, mode, want_h);
     }
     const StepState r = get_state(c);
+    if (mode.fused) {  // the state of the last step taken (a stopped step writes nothing)
+      const bool odd = (r.steps_taken & 1) != 0;
+      c->U = odd ? U_second : U_first;
+      c->Ualt = odd ? U_first : U_second;
+    }
     if (r.error == 1) throw Fail(PERRK_ENUMERIC, "non-finite update direction");
     if (r.error == 2) throw Fail(PERRK_EINVAL, "vanishing characteristic speed");
     *t = r.t;

@@ -1,0 +1,60 @@
+"""GPU: perrk_advance's fused relaxation (relax_spec_kernel: Newton pass 2
+fused with a speculative out-of-place final update, host.cpp enqueue_step)
+against the unfused chain of relax_pass_kernel + update_kernel.
+
+The speculation is accepted only when Newton finishes at the gamma the pass
+evaluated, so the two chains must agree bitwise: state, step records, time.
+C1's first steps start from gamma_seed = 1 far from the root (pass 2 does not
+converge there: the speculation is rejected and the ordinary passes and
+update take over); later steps accept it.  Odd and even step counts and a
+chunked run() exercise the buffer alternation (c->U / c->Ualt)."""
+import numpy as np
+import pytest
+
+from paper_2507_04991_b200 import perrk as P
+from paper_2507_04991_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _advance(cfg, U0, coords_of, chunks, fused, monkeypatch):
+    monkeypatch.setenv("PERRK_NO_FUSED_RELAX", "0" if fused else "1")
+    semi = P.Semidiscretization(cfg.spec())
+    U = U0(semi)
+    semi.upload(U)
+    rc = P.IntegratorConfig(tf=1e9, time=P.TimeControl(fixed=False, ramp=P.CflRamp(cfg.cfl, cfg.cfl)),
+                            relaxation=P.RelaxationConfig(numerics="accurate"))
+    t, recs = 0.0, []
+    for n in chunks:
+        t, taken, aborted, r = P.advance(semi, cfg.family, cfg.partition_map(), rc, t, n)
+        assert taken == n and not aborted
+        recs += r
+    return semi.download(), recs, t
+
+
+def _compare(cfg, U0, chunks, monkeypatch):
+    Uf, rf, tf = _advance(cfg, U0, None, chunks, True, monkeypatch)
+    Uu, ru, tu = _advance(cfg, U0, None, chunks, False, monkeypatch)
+    assert np.array_equal(Uf, Uu)
+    assert tf == tu
+    for a, b in zip(rf, ru):
+        assert (a.t, a.dt, a.gamma, a.newton_iters, a.entropy, a.fell_back) == \
+               (b.t, b.dt, b.gamma, b.newton_iters, b.entropy, b.fell_back)
+        assert list(a.invariants) == list(b.invariants)
+    return rf
+
+
+@pytest.mark.parametrize("chunks", [[7], [8], [3, 4, 5]])
+def test_fused_relaxation_bitwise_c1(chunks, monkeypatch):
+    cfg = W.make_config("c1")
+    U0 = lambda semi: W.initial_state_for(cfg, (semi.node_x(), semi.node_y(), None))
+    recs = _compare(cfg, U0, chunks, monkeypatch)
+    # the first step needs more than two Newton passes (speculation rejected)
+    assert recs[0].newton_iters > 2
+
+
+@pytest.mark.parametrize("chunks", [[5], [2, 3]])
+def test_fused_relaxation_bitwise_tgv_sample(chunks, monkeypatch):
+    cfg = W.sample_config(W.make_config("c5"))
+    U0 = lambda semi: W.initial_state_for(cfg, (semi.node_x(), semi.node_y(), semi.node_z()))
+    _compare(cfg, U0, chunks, monkeypatch)
