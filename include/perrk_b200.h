@@ -163,7 +163,9 @@ int perrk_set_family(perrk_ctx* ctx, const perrk_family_desc* fam, const int* ef
 /* ---- resident state (the product path keeps U in HBM between steps) --- */
 int perrk_upload_state(perrk_ctx* ctx, const double* U, size_t n);
 int perrk_download_state(perrk_ctx* ctx, double* U, size_t n);
-/* device pointer of the resident state (for zero-copy interop) */
+/* device pointer of the resident state (for zero-copy interop); valid until
+ * the next perrk_advance, which alternates the state between two buffers when
+ * it fuses the relaxation with the update (relax_spec_kernel) */
 int perrk_state_device_ptr(perrk_ctx* ctx, double** dptr);
 int perrk_sync(perrk_ctx* ctx);
 
