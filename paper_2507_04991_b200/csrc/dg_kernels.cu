@@ -15,6 +15,7 @@
 //                  step's CFL speed (mesh.cpp:97-129), the StepRecord H and
 //                  invariants (stepper.cpp:179-180) and the clock advance.
 //   begin_step     compute_dt (stepper.cpp:116-127) and per-step resets.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cstdio>
@@ -1190,14 +1191,26 @@ static int resident_grid(K kernel, int threads, int cap) {
   return g < cap ? g : cap;
 }
 
+// One grid for relax_pass_kernel, relax_spec_kernel and update_kernel: the
+// three walk the nodes in the same warp-block order, so their sums agree bit
+// for bit (the fused and unfused relaxation chains give the same step).  It
+// is relax_pass_kernel's resident grid; relax_spec_kernel (128 registers)
+// holds two of its three blocks per SM at once.  Measured: sizing all three to
+// relax_spec_kernel's residency costs the passes more than the spec kernel's
+// tail (-4%), and capping relax_spec_kernel at 80 registers spills (neutral).
+template <int DIM>
+static int relax_grid(int cap) {
+  return resident_grid(relax_pass_kernel<DIM>, 256, cap);
+}
+
 cudaError_t launch_relax_pass(int dim, const double* U, const double* d, const MeshDev& m,
                               const Phys& ph, StepState* st, double* partials, unsigned* counter,
                               long long nnodes, int grid, cudaStream_t s) {
   if (dim == 2) {
-    static const int g = resident_grid(relax_pass_kernel<2>, 256, grid);
+    static const int g = relax_grid<2>(grid);
     relax_pass_kernel<2><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
   } else {
-    static const int g = resident_grid(relax_pass_kernel<3>, 256, grid);
+    static const int g = relax_grid<3>(grid);
     relax_pass_kernel<3><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
   }
   return cudaGetLastError();
@@ -1209,11 +1222,11 @@ cudaError_t launch_update(int dim, double* Uout, const double* Uin, const double
                           double* records, int grid, cudaStream_t s) {
   // relax_pass_kernel's grid: the node walk (and record sums) of relax_spec_kernel
   if (dim == 2) {
-    static const int g = resident_grid(relax_pass_kernel<2>, 256, grid);
+    static const int g = relax_grid<2>(grid);
     update_kernel<2><<<g, 256, 0, s>>>(Uout, Uin, d, m, ph, st, partials, counter, nnodes,
                                        want_nu, want_record, records);
   } else {
-    static const int g = resident_grid(relax_pass_kernel<3>, 256, grid);
+    static const int g = relax_grid<3>(grid);
     update_kernel<3><<<g, 256, 0, s>>>(Uout, Uin, d, m, ph, st, partials, counter, nnodes,
                                        want_nu, want_record, records);
   }
@@ -1227,11 +1240,11 @@ cudaError_t launch_relax_spec(int dim, const double* U, const double* d, double*
   // the grid of relax_pass_kernel: the same nodes per warp, so the same
   // summation order of r and r' (bitwise the unfused pass)
   if (dim == 2) {
-    static const int g = resident_grid(relax_pass_kernel<2>, 256, grid);
+    static const int g = relax_grid<2>(grid);
     relax_spec_kernel<2><<<g, 256, 0, s>>>(U, d, Uout, m, ph, st, partials, counter, nnodes,
                                            want_nu, want_record, records);
   } else {
-    static const int g = resident_grid(relax_pass_kernel<3>, 256, grid);
+    static const int g = relax_grid<3>(grid);
     relax_spec_kernel<3><<<g, 256, 0, s>>>(U, d, Uout, m, ph, st, partials, counter, nnodes,
                                            want_nu, want_record, records);
   }

@@ -28,6 +28,14 @@
 namespace perrk {
 namespace dev {
 
+#ifndef PERRK_W3_DESC_CA
+#define PERRK_W3_DESC_CA 0  // 1: descriptor prefetch through L1 (cp.async.ca)
+#endif
+
+#ifndef PERRK_W3_NOSEL
+#define PERRK_W3_NOSEL 0  // 1: distance-2 exchange without selects
+#endif
+
 #ifndef PERRK_W3_COAL
 #define PERRK_W3_COAL 1  // epilogue U / K1 / U_{i+1} blocks through the slice (coalesced)
 #endif
@@ -119,6 +127,11 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
 
+__device__ __forceinline__ void cp_async16_ca(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -197,12 +210,23 @@ __device__ __forceinline__ void w3_inplane(const Phys& ph, const double* pr, int
   const bool lo = j < 2;
   const int own = lo ? lane : lane + 32;
   w3_ec<D, SM>(ph, pr, own, own ^ (2 * st), f);
+#if PERRK_W3_NOSEL
+  // no selects: the pair's two terms weighted by c2 or 0 (DFMA instead of FSEL pairs)
+  const double cA = lo ? c2 : 0.0, cB = lo ? 0.0 : c2;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double r = __shfl_xor_sync(0xffffffffu, f[v], 2 * st);
+    KA[v] = fma(-cA, f[v], fma(-cB, r, KA[v]));
+    KB[v] = fma(-cB, f[v], fma(-cA, r, KB[v]));
+  }
+#else
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const double r = __shfl_xor_sync(0xffffffffu, f[v], 2 * st);
     KA[v] = fma(-c2, lo ? f[v] : r, KA[v]);
     KB[v] = fma(-c2, lo ? r : f[v], KB[v]);
   }
+#endif
 }
 
 // z lines: lane l holds z = zA and zA + 2, lane l^16 the other two.
@@ -259,8 +283,13 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   // descriptor of one cell into the warp's buffer b (lanes 0-5, 16 B each)
   auto fetch_rec = [&](int b, int c) {
     if (c >= 0 && lane < static_cast<int>(sizeof(CellRec) / 16))
+#if PERRK_W3_DESC_CA
+      cp_async16_ca(reinterpret_cast<char*>(&s_rec[wib][b]) + 16 * lane,
+                    reinterpret_cast<const char*>(m.rec + c) + 16 * lane);
+#else
       cp_async16(reinterpret_cast<char*>(&s_rec[wib][b]) + 16 * lane,
                  reinterpret_cast<const char*>(m.rec + c) + 16 * lane);
+#endif
     cp_async_commit();
   };
   const double dt = st->dt;
