@@ -57,4 +57,8 @@ def test_fused_relaxation_bitwise_c1(chunks, monkeypatch):
 def test_fused_relaxation_bitwise_tgv_sample(chunks, monkeypatch):
     cfg = W.sample_config(W.make_config("c5"))
     U0 = lambda semi: W.initial_state_for(cfg, (semi.node_x(), semi.node_y(), semi.node_z()))
-    _compare(cfg, U0, chunks, monkeypatch)
+    recs = _compare(cfg, U0, chunks, monkeypatch)
+    # steps 1-2 start far from the root (speculation rejected), later steps
+    # finish at pass 2 (accepted: the update came from relax_spec_kernel)
+    iters = [r.newton_iters for r in recs]
+    assert iters[0] > 2 and 2 in iters
