@@ -62,3 +62,35 @@ def test_fused_relaxation_bitwise_tgv_sample(chunks, monkeypatch):
     # finish at pass 2 (accepted: the update came from relax_spec_kernel)
     iters = [r.newton_iters for r in recs]
     assert iters[0] > 2 and 2 in iters
+
+
+def test_anchored_relaxation_fused_vs_oracle(monkeypatch):
+    """Anchored relaxation (h_ref = H(U_0), stepper.cpp:154-156) through
+    perrk_advance: fused and unfused chains bitwise equal, and 40 C1 steps
+    against the oracle restatement (state 1e-11 rel L2 per variable, gamma and
+    H within 1e-12)."""
+    import oracle as O
+    from helpers import rel_err
+    cfg = W.make_config("c1")
+    out = {}
+    for fused in (True, False):
+        monkeypatch.setenv("PERRK_NO_FUSED_RELAX", "0" if fused else "1")
+        semi = P.Semidiscretization(cfg.spec())
+        U0 = W.initial_state_for(cfg, (semi.node_x(), semi.node_y(), None))
+        semi.upload(U0)
+        rc = P.IntegratorConfig(tf=1e9, time=P.TimeControl(fixed=False, ramp=P.CflRamp(0.9, 0.9)),
+                                relaxation=P.RelaxationConfig(numerics="accurate"), anchor="initial")
+        t, taken, aborted, recs = P.advance(semi, cfg.family, cfg.partition_map(), rc, 0.0, 40)
+        assert taken == 40 and not aborted
+        out[fused] = (semi.download(), recs)
+    (Uf, rf), (Uu, ru) = out[True], out[False]
+    assert np.array_equal(Uf, Uu)
+    assert [r.gamma for r in rf] == [r.gamma for r in ru]
+    orc = O.Orc(cfg.mesh)
+    Uo = U0.copy()
+    _, taken, log, _ = orc.run_steps(Uo, 0.0, 40, cfg.family, cfg.partition_map().effective_level,
+                                     P.RelaxationConfig(numerics="accurate"), False, 0.9, anchor=True)
+    assert taken == 40
+    assert rel_err(Uf, Uo, 4) < 1e-11
+    assert np.abs(np.array([r.gamma for r in rf]) - log[:, 2]).max() < 1e-12
+    assert np.abs(np.array([r.entropy for r in rf]) - log[:, 4]).max() < 1e-12
