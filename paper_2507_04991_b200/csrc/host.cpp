@@ -351,9 +351,14 @@ struct perrk_ctx {
   // the small configurations (C1 is 4096 nodes, ~20 kernels per step)
   bool use_graphs = true;
   bool use_fused = true;  // perrk_advance: relax_spec_kernel (PERRK_NO_FUSED_RELAX=1 disables)
-  cudaGraphExec_t graph_exec = nullptr;
-  std::string graph_key;
-  int64_t graph_launches = 0;  // kernels per graph launch
+  // captured steps by key (plan, records, mode, and the current state buffer:
+  // the fused path alternates two, so two graphs stay cached)
+  struct StepGraph {
+    std::string key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;  // kernels per graph launch
+  };
+  std::vector<StepGraph> graphs;
   uint64_t plan_version = 0;
   // instrumentation: launch counter and per-stage-launch event pairs
   bool own_stream = true;
@@ -1217,7 +1222,7 @@ int perrk_destroy(perrk_ctx* c) {
   if (c->counter) cudaFree(c->counter);
   if (c->dint) cudaFree(c->dint);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  for (auto& gr : c->graphs) cudaGraphExecDestroy(gr.exec);
   if (c->group) {  // leave the group (the exchange dies with its last member)
     auto& mem = c->group->members;
     for (size_t i = 0; i < mem.size(); ++i)
@@ -1610,27 +1615,33 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
       key += std::to_string(mode.relax) + std::to_string(mode.cfg.numerics) + ":" +
              std::to_string(mode.cfg.max_iter) + std::to_string(mode.want_nu) +
              std::to_string(mode.want_record) + std::to_string(want_h);
-      if (!c->graph_exec || c->graph_key != key) {
-        if (c->graph_exec) {
-          cudaGraphExecDestroy(c->graph_exec);
-          c->graph_exec = nullptr;
+      perrk_ctx::StepGraph* gr = nullptr;
+      for (auto& x : c->graphs)
+        if (x.key == key) gr = &x;
+      if (!gr) {
+        if (c->graphs.size() >= 4) {  // drop the oldest
+          cudaGraphExecDestroy(c->graphs.front().exec);
+          c->graphs.erase(c->graphs.begin());
         }
         const int64_t l0 = c->launches;
         cudaGraph_t graph;
+        perrk_ctx::StepGraph ng;
+        ng.key = key;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
         enqueue_step(g, mode, want_h);
         if (mode.fused) enqueue_step(g, mode, want_h);  // two steps: the buffers are back in place
         CK(cudaStreamEndCapture(c->stream, &graph));
-        CK(cudaGraphInstantiate(&c->graph_exec, graph, 0));
+        CK(cudaGraphInstantiate(&ng.exec, graph, 0));
         cudaGraphDestroy(graph);
-        c->graph_key = key;
-        c->graph_launches = c->launches - l0;
+        ng.launches = c->launches - l0;
         c->launches = l0;
+        c->graphs.push_back(ng);
+        gr = &c->graphs.back();
       }
       const int per = mode.fused ? 2 : 1;
       for (int k = 0; k + per <= nsteps; k += per) {
-        CK(cudaGraphLaunch(c->graph_exec, c->stream));
-        c->launches += c->graph_launches;
+        CK(cudaGraphLaunch(gr->exec, c->stream));
+        c->launches += gr->launches;
       }
       if (nsteps % per) enqueue_step(g, mode, want_h);
     } else {
