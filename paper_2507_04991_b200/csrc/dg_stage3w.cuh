@@ -63,7 +63,7 @@ struct W3 {
   static constexpr int FS = 5;
   static constexpr int SM_FS = (96 + 4 * 5) * FS;
   static constexpr int SM_WARP = SM_PR + SM_FS;
-  static_assert(SM_WARP >= 2 * NPC * V, "the epilogue stages U and K1 in the slice");
+  static_assert(SM_WARP >= 3 * NPC * V, "the epilogue stages U, K1 and d in the slice");
   static_assert(SM_WARP % 2 == 0, "16-byte aligned slices");
   static constexpr int SM_TOTAL = WPB * SM_WARP;  // doubles per block
 };
@@ -515,6 +515,68 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       node(lane, KA, zA);
       node(lane + 32, KB, zB);
     }
+    const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
+#if PERRK_W3_COAL
+    // Epilogue through the slice (dead after the gather and the dH terms):
+    // the cell's blocks of U, K1 and d (2560 contiguous bytes each) come in by
+    // coalesced 16-byte cp.async, are read node-wise with conflict-free 8-byte
+    // loads, and the results, U_{i+1} = U + dt (a_{i+1,1} K1 + a_{i+1,i} K_i)
+    // in place of U, K1 = K_0 (stage 0) and d in place, leave as bulk copies
+    // (cp.async.bulk, the TMA path: no per-lane store wavefronts).  A direct
+    // 40-byte-stride LDG.64 / STG.64 touches 10 lines per instruction.
+    //   slice: U [0, 64V) | K1 or K_0 [64V, 128V) | d [128V, 192V)
+    {
+      double* eu = pr;
+      double* ek = pr + N * V;
+      double* ed = pr + 2 * N * V;
+      __syncwarp();  // every lane is done with the primitives and face slots
+      if (a.write_next) w3_stage_cell(eu, a.U + cbase, lane);
+      if (a.write_next && a.form) w3_stage_cell(ek, a.K1 + cbase, lane);
+      if (a.d_mode == 2) w3_stage_cell(ed, a.d + cbase, lane);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double* K = h ? KB : KA;
+        const int o = (lane + 32 * h) * V;
+        if (a.write_k) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) ek[o + v] = K[v];
+        }
+        if (a.write_next) {
+          double x[V];
+          if (a.form) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) x[v] = eu[o + v] + fma(an, ek[o + v], pn * K[v]);
+          } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) x[v] = fma(an, K[v], eu[o + v]);
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) eu[o + v] = x[v];
+        }
+        if (a.d_mode) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const double x = a.d_mode == 2 ? fma(a.b, K[v], ed[o + v]) : a.b * K[v];
+            ed[o + v] = x;
+            const unsigned long long bits =
+                static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7fffffffffffffffULL;
+            if (a.want_dmax) dmax_bits = bits > dmax_bits ? bits : dmax_bits;
+          }
+        }
+      }
+      bulk_store_fence();
+      __syncwarp();
+      if (lane == 0) {
+        constexpr unsigned kBytes = N * V * sizeof(double);
+        if (a.write_next) bulk_store(a.Usn + cbase, eu, kBytes);
+        if (a.write_k) bulk_store(a.Kout + cbase, ek, kBytes);
+        if (a.d_mode) bulk_store(a.d + cbase, ed, kBytes);
+      }
+    }
+#else
     if (a.write_k) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -522,86 +584,48 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         a.Kout[gB + v] = KB[v];
       }
     }
-    const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
-#if PERRK_W3_COAL
-    // U_{i+1} = U + dt (a_{i+1,1} K1 + a_{i+1,i} K_i): the cell's U and K1
-    // blocks (2560 contiguous bytes each) come in with coalesced 16-byte
-    // cp.async into the slice (the primitives and face slots are dead by
-    // now), are read node-wise with 8-byte loads (40-byte stride, conflict
-    // free), and U_{i+1} is written back in place and leaves as one bulk copy
-    // (cp.async.bulk, the TMA path: no per-lane store wavefronts).
-    if (a.write_next) {
-      double* eb = pr;
-      __syncwarp();  // every lane is done with the primitives and face slots
-      w3_stage_cell(eb, a.U + cbase, lane);
-      if (a.form) w3_stage_cell(eb + N * V, a.K1 + cbase, lane);
-      cp_async_commit();
-      cp_async_wait<0>();
-      __syncwarp();
+    // U_{i+1} and d node by node, each batch with all its loads issued before
+    // its first store (the compiler cannot tell that Usn / d do not alias
+    // U / K1, and would otherwise serialise load -> store pairs)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const double* K = h ? KB : KA;
-        double* e = eb + (lane + 32 * h) * V;
-        double x[V];
+    for (int h = 0; h < 2; ++h) {
+      const double* K = h ? KB : KA;
+      const int o = (lane + 32 * h) * V;
+      const size_t g = h ? gB : gA;
+      double x[V], y[V];
+      if (a.write_next) {
+        const double* Up = a.U + cbase;
+        const double* Kp = a.K1 + cbase;
+#pragma unroll
+        for (int v = 0; v < V; ++v) x[v] = Up[o + v];
         if (a.form) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = e[v] + fma(an, e[N * V + v], pn * K[v]);
+          for (int v = 0; v < V; ++v) y[v] = Kp[o + v];
+#pragma unroll
+          for (int v = 0; v < V; ++v) a.Usn[g + v] = x[v] + fma(an, y[v], pn * K[v]);
         } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = fma(an, K[v], e[v]);
+          for (int v = 0; v < V; ++v) a.Usn[g + v] = fma(an, K[v], x[v]);
+        }
+      }
+      if (a.d_mode) {
+        if (a.d_mode == 2) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], a.d[g + v]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) x[v] = a.b * K[v];
         }
 #pragma unroll
-        for (int v = 0; v < V; ++v) e[v] = x[v];
+        for (int v = 0; v < V; ++v) {
+          a.d[g + v] = x[v];
+          const unsigned long long bits =
+              static_cast<unsigned long long>(__double_as_longlong(x[v])) & 0x7fffffffffffffffULL;
+          if (a.want_dmax) dmax_bits = bits > dmax_bits ? bits : dmax_bits;
+        }
       }
-      bulk_store_fence();
-      __syncwarp();
-      if (lane == 0) bulk_store(a.Usn + cbase, eb, N * V * sizeof(double));
     }
 #endif
-    // d (and, without the coalesced path, U_{i+1}) node by node, each batch
-    // with all its loads issued before its first store (the compiler cannot
-    // tell that Usn / d do not alias U / K1, and would otherwise serialise
-    // load -> store pairs)
-    {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const double* K = h ? KB : KA;
-        const int o = (lane + 32 * h) * V;
-        const size_t g = h ? gB : gA;
-        double x[V], y[V];
-        if (!PERRK_W3_COAL && a.write_next) {
-          const double* Up = a.U + cbase;
-          const double* Kp = a.K1 + cbase;
-#pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = Up[o + v];
-          if (a.form) {
-#pragma unroll
-            for (int v = 0; v < V; ++v) y[v] = Kp[o + v];
-#pragma unroll
-            for (int v = 0; v < V; ++v) a.Usn[g + v] = x[v] + fma(an, y[v], pn * K[v]);
-          } else {
-#pragma unroll
-            for (int v = 0; v < V; ++v) a.Usn[g + v] = fma(an, K[v], x[v]);
-          }
-        }
-        if (a.d_mode) {
-          if (a.d_mode == 2) {
-#pragma unroll
-            for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], a.d[g + v]);
-          } else {
-#pragma unroll
-            for (int v = 0; v < V; ++v) x[v] = a.b * K[v];
-          }
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            a.d[g + v] = x[v];
-            const unsigned long long bits =
-                static_cast<unsigned long long>(__double_as_longlong(x[v])) & 0x7fffffffffffffffULL;
-            if (a.want_dmax) dmax_bits = bits > dmax_bits ? bits : dmax_bits;
-          }
-        }
-      }
-    }
     __syncwarp();  // the slice is rewritten by the next cell
     slot = nslot;
     cell = ncell;
