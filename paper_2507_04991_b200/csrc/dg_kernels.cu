@@ -435,10 +435,18 @@ __global__ void __launch_bounds__(256)
 // (mesh.cpp:97-129 takes |v_dir| + c per direction; 1/h_dir = jac_dir / 2
 // exactly, one pressure / sound speed per node) and the StepRecord H and
 // invariants (stepper.cpp:179-180)
-template <int DIM>
+// per-thread accumulators kept in shared memory, thread-interleaved (no bank
+// conflicts), to hold relax_spec_kernel's registers for three blocks per SM
+struct KsShared {
+  ksum* base;  // &arr[0][threadIdx.x] of a [rows][blockDim] array
+  int stride;  // blockDim.x
+  __device__ __forceinline__ ksum& operator[](int r) const { return base[r * stride]; }
+};
+
+template <int DIM, class Acc>
 __device__ __forceinline__ void update_node_terms(const MeshDev& m, const Phys& ph, const double* u,
                                                   long long n, int want_nu, int want_record,
-                                                  double s_new, double& numax, ksum* acc) {
+                                                  double s_new, double& numax, Acc acc) {
   constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
   const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
   if (want_nu) {
@@ -570,14 +578,17 @@ __global__ void __launch_bounds__(256)
 // passes and update_kernel proceed from the untouched U_in.  One full read of
 // U and d per step is saved (SURVEY.md 7.3 H1 numerics only).
 template <int DIM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     relax_spec_kernel(const double* __restrict__ U, const double* __restrict__ d,
                       double* __restrict__ Uout, MeshDev m, Phys ph, StepState* st,
                       double* partials, unsigned* counter, long long nnodes, int want_nu,
                       int want_record, double* records) {
   constexpr int V = DIM + 2, BLK = 32 * V;
   __shared__ double s_red[2 * 8 * 8];
-  __shared__ __align__(16) double s_stage[8][2][2][BLK];  // [warp][buffer][U, d][block]
+  // dynamic shared memory (66.5 KB: over the 48 KB static limit):
+  // [warp][buffer][U, d][block] staging, then the six per-thread record sums
+  extern __shared__ __align__(16) double spec_smem[];
+  auto s_stage = reinterpret_cast<double(*)[2][2][BLK]>(spec_smem);
   if (st->aborted || st->finished || st->relax_done) return;
   const double dmax = __longlong_as_double(static_cast<long long>(st->dmax_bits));
   if (st->d_nonfinite || dmax == 0.0) return;  // handled by pass 1
@@ -589,9 +600,12 @@ __global__ void __launch_bounds__(256)
   auto stage = [&](long long k, int b) {
     stage_pair<V>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
   };
-  ksum acc[8];  // A, B, then the update's six record sums
+  ksum acc[2];  // A, B in registers; the update's six record sums in shared memory
+  acc[0] = acc[1] = ks_zero();
+  ksum* s_acc = reinterpret_cast<ksum*>(spec_smem + 8 * 2 * 2 * BLK);  // [6][blockDim]
+  const KsShared racc{s_acc + threadIdx.x, static_cast<int>(blockDim.x)};
 #pragma unroll
-  for (int r = 0; r < 8; ++r) acc[r] = ks_zero();
+  for (int r = 0; r < 6; ++r) racc[r] = ks_zero();
   double numax = 0.0;
   long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
   int b = 0;
@@ -622,7 +636,7 @@ __global__ void __launch_bounds__(256)
       for (int v = 0; v < V; ++v) Uout[n * V + v] = T[v];
       if (want_nu || want_record)
         update_node_terms<DIM>(m, ph, T, n, want_nu, want_record, trial_entropy(ph, tr), numax,
-                               acc + 2);
+                               racc);
     }
     __syncwarp();
   }
@@ -633,7 +647,7 @@ __global__ void __launch_bounds__(256)
   }
   dd tot[8], accd[8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) accd[r] = ks_dd(acc[r]);
+  for (int r = 0; r < 8; ++r) accd[r] = ks_dd(r < 2 ? acc[r] : racc[r - 2]);
   block_reduce_dd<8>(accd, s_red);
   if (grid_reduce_dd<8>(accd, partials, counter, s_red, tot) && threadIdx.x == 0) {
     relax_update(st, tot[0], tot[1]);
@@ -1233,6 +1247,21 @@ cudaError_t launch_update(int dim, double* Uout, const double* Uin, const double
   return cudaGetLastError();
 }
 
+template <int DIM>
+static size_t spec_smem_bytes() {
+  return sizeof(double) * 8 * 2 * 2 * 32 * (DIM + 2) + sizeof(ksum) * 6 * 256;
+}
+
+template <int DIM>
+static void configure_spec() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(relax_spec_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(spec_smem_bytes<DIM>()));
+    done = true;
+  }
+}
+
 cudaError_t launch_relax_spec(int dim, const double* U, const double* d, double* Uout,
                               const MeshDev& m, const Phys& ph, StepState* st, double* partials,
                               unsigned* counter, long long nnodes, int want_nu, int want_record,
@@ -1240,13 +1269,17 @@ cudaError_t launch_relax_spec(int dim, const double* U, const double* d, double*
   // the grid of relax_pass_kernel: the same nodes per warp, so the same
   // summation order of r and r' (bitwise the unfused pass)
   if (dim == 2) {
+    configure_spec<2>();
     static const int g = relax_grid<2>(grid);
-    relax_spec_kernel<2><<<g, 256, 0, s>>>(U, d, Uout, m, ph, st, partials, counter, nnodes,
-                                           want_nu, want_record, records);
+    relax_spec_kernel<2><<<g, 256, spec_smem_bytes<2>(), s>>>(U, d, Uout, m, ph, st, partials,
+                                                              counter, nnodes, want_nu,
+                                                              want_record, records);
   } else {
+    configure_spec<3>();
     static const int g = relax_grid<3>(grid);
-    relax_spec_kernel<3><<<g, 256, 0, s>>>(U, d, Uout, m, ph, st, partials, counter, nnodes,
-                                           want_nu, want_record, records);
+    relax_spec_kernel<3><<<g, 256, spec_smem_bytes<3>(), s>>>(U, d, Uout, m, ph, st, partials,
+                                                              counter, nnodes, want_nu,
+                                                              want_record, records);
   }
   return cudaGetLastError();
 }
