@@ -203,6 +203,18 @@ int perrk_perk_step_resident(perrk_ctx* ctx, double* t, double dt, const perrk_s
 int perrk_advance(perrk_ctx* ctx, const perrk_run_cfg* cfg, double* t, int nsteps,
                   perrk_step_record* log, int* steps_taken, int* aborted);
 
+/* probe_jacobian (specopt.cpp:18-35; declared specopt.hpp:25-26, default
+ * epsilon 1e-6): dense central-difference Jacobian of the full RHS at `base`,
+ * column j stepped by epsilon*(1+|base_j|), guarded to M <= 5000.  J is the
+ * M x M matrix in column-major order (Eigen's MatrixXd storage):
+ * J[j*M + i] = (rhs_i(u + h_j e_j) - rhs_i(u - h_j e_j)) / (2 h_j).  The
+ * columns are probed in colours: one local DOF of a distance-2 independent
+ * set of cells per RHS pair, so 2 * n_colours * nodes*V RHS evaluations
+ * replace the reference's 2M, and each entry equals the single-column probe
+ * bit for bit.  n_colours (may be NULL) receives the number of cell colours. */
+int perrk_probe_jacobian(perrk_ctx* ctx, const double* base, double t, double epsilon, double* J,
+                         int* n_colours);
+
 /* error_norms (stepper.cpp:195-265): L1 (domain-normalised) and Linf of the
  * DG solution interpolated to the degree-2k GLL points against an exact
  * solution; exact = 0: the 2D isentropic vortex (isentropic_vortex_state,

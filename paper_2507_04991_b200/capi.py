@@ -86,6 +86,7 @@ _PROTOS = {
     "perrk_state_device_ptr": (C.c_int, [_P, C.POINTER(_D)]),
     "perrk_sync": (C.c_int, [_P]),
     "perrk_rhs_masked": (C.c_int, [_P, C.c_double, _D, _D, C.c_char_p]),
+    "perrk_probe_jacobian": (C.c_int, [_P, _D, C.c_double, C.c_double, _D, _I]),
     "perrk_br1_gradients": (C.c_int, [_P, C.c_double, _D, _D]),
     "perrk_total_entropy": (C.c_int, [_P, _D, _D]),
     "perrk_entropy_inner_product": (C.c_int, [_P, _D, _D, _D]),

@@ -1322,4 +1322,44 @@ cudaError_t launch_admissible(int dim, const double* U, const Phys& ph, int* fir
   return cudaGetLastError();
 }
 
+// ---- dense Jacobian probe (specopt.cpp:18-35) --------------------------------
+// One colour of the probe perturbs local DOF l of every cell in `cells`; the
+// colouring (host) keeps their dependency stencils disjoint, so each RHS row
+// sees at most one perturbed input and equals the single-column probe bit for
+// bit.  h, the u +/- h values and (fp - fm) / (2h) follow specopt.cpp:25-32.
+__global__ void probe_set_kernel(double* up, double* um, const double* base, const double* h,
+                                 const int* cells, int n, long long stride, int l, int on) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const long long j = static_cast<long long>(cells[q]) * stride + l;
+  up[j] = on ? base[j] + h[j] : base[j];
+  um[j] = on ? base[j] - h[j] : base[j];
+}
+
+__global__ void probe_scatter_kernel(double* J, const double* fp, const double* fm,
+                                     const double* h, const int* owner, long long M,
+                                     long long stride, int l) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < M;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int p = owner[i / stride];
+    if (p < 0) continue;
+    const long long j = static_cast<long long>(p) * stride + l;
+    J[j * M + i] = (fp[i] - fm[i]) / (2.0 * h[j]);
+  }
+}
+
+cudaError_t launch_probe_set(double* up, double* um, const double* base, const double* h,
+                             const int* cells, int n, long long stride, int l, int on,
+                             cudaStream_t s) {
+  if (n > 0) probe_set_kernel<<<(n + 127) / 128, 128, 0, s>>>(up, um, base, h, cells, n, stride, l, on);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe_scatter(double* J, const double* fp, const double* fm, const double* h,
+                                 const int* owner, long long M, long long stride, int l, int grid,
+                                 cudaStream_t s) {
+  probe_scatter_kernel<<<grid, 256, 0, s>>>(J, fp, fm, h, owner, M, stride, l);
+  return cudaGetLastError();
+}
+
 }  // namespace perrk

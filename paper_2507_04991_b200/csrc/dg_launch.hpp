@@ -112,6 +112,12 @@ cudaError_t launch_pack_traces(int dim, const StageArgs& a, const dev::MeshDev& 
 cudaError_t launch_stash(dev::StepState* st, int mode, cudaStream_t s);
 cudaError_t launch_combine(dev::StepState* st, const double* all, int nranks, int mode, int V,
                            double* records, cudaStream_t s);
+cudaError_t launch_probe_set(double* up, double* um, const double* base, const double* h,
+                             const int* cells, int n, long long stride, int l, int on,
+                             cudaStream_t s);
+cudaError_t launch_probe_scatter(double* J, const double* fp, const double* fm, const double* h,
+                                 const int* owner, long long M, long long stride, int l, int grid,
+                                 cudaStream_t s);
 cudaError_t launch_admissible(int dim, const double* U, const dev::Phys& ph, int* first_bad,
                               long long nnodes, int grid, cudaStream_t s);
 

@@ -1388,6 +1388,147 @@ int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const
   });
 }
 
+namespace {
+// Full (unmasked) RHS of device state dU into dK, as perrk_rhs_masked(mask = NULL).
+void rhs_full_device(perrk_ctx* c, const double* dU, double* dK, int* gl_all) {
+  CK(cudaMemsetAsync(dK, 0, sizeof(double) * c->ndofs, c->stream));
+  c->evals += static_cast<uint64_t>(c->ncells) * c->npc * c->V;
+  StepState s = fresh_state();
+  put_state(c, s);
+  StageArgs a{};
+  a.U = dU;
+  a.K1 = dU;
+  a.Kout = dK;
+  a.list = nullptr;
+  a.n = static_cast<int>(c->ncells);
+  a.write_k = 1;
+  a.ncells = c->ncells_global;
+  a.ndofs = c->ndofs;
+  if (c->physics == 1) {
+    StageArgs ga = a;
+    ga.list = gl_all;
+    CK(launch_grad(ga, c->mesh(), c->ph, c->st, c->G, c->ndofs, 0, c->grid_stage, c->stream));
+    a.G = c->G;
+  }
+  CK(launch_stage(c->dim, c->surface, c->vol(), a, c->mesh(), c->ph, c->st, c->partials, c->counter,
+                  c->grid_stage, c->stream));
+  const StepState r = get_state(c);
+  if (r.bad_code != std::numeric_limits<long long>::max())
+    throw Fail(PERRK_ENUMERIC, "inadmissible state passed to numerical flux");
+}
+
+// Cells whose RHS rows read cell p: its face neighbours out to `rad` steps.
+std::vector<int> probe_stencil(const perrk_ctx* c, int p, int rad) {
+  std::vector<int> out{p};
+  size_t lo = 0;
+  for (int r = 0; r < rad; ++r) {
+    const size_t hi = out.size();
+    for (size_t q = lo; q < hi; ++q)
+      for (int f = 0; f < 2 * c->dim; ++f) {
+        const int g = static_cast<int>(face_neighbour(c->dim, c->nc, out[q], f));
+        if (std::find(out.begin(), out.end(), g) == out.end()) out.push_back(g);
+      }
+    lo = hi;
+  }
+  return out;
+}
+}  // namespace
+
+int perrk_probe_jacobian(perrk_ctx* c, const double* base, double t, double epsilon, double* J,
+                         int* n_colours) {
+  (void)t;  // autonomous RHS (semidisc.cpp:411)
+  return guarded([&] {
+    REQUIRE(c && base && J, "null argument");
+    no_slab(c, "probe_jacobian");
+    const long long M = c->ndofs;
+    REQUIRE(M <= 5000, "dense Jacobian probing guarded to M <= 5000");
+    REQUIRE(std::isfinite(epsilon) && epsilon > 0.0, "epsilon must be positive");
+    set_device(c);
+    const int nc = static_cast<int>(c->ncells);
+    const long long stride = static_cast<long long>(c->npc) * c->V;
+    // Distance-2 greedy colouring of the cells over the RHS dependency graph
+    // (BR1 widens each stencil to two face steps, semidisc.cpp:254-263).
+    const int rad = c->physics == 1 ? 2 : 1;
+    std::vector<std::vector<int>> sten(nc);
+    for (int p = 0; p < nc; ++p) sten[p] = probe_stencil(c, p, rad);
+    std::vector<std::vector<int>> readers(nc);  // cells whose stencil holds q
+    for (int p = 0; p < nc; ++p)
+      for (int q : sten[p]) readers[q].push_back(p);
+    std::vector<int> colour(nc, -1);
+    int ncol = 0;
+    for (int p = 0; p < nc; ++p) {
+      std::vector<char> used(ncol + 1, 0);
+      for (int q : sten[p])
+        for (int o : readers[q])
+          if (colour[o] >= 0) used[colour[o]] = 1;
+      int k = 0;
+      while (used[k]) ++k;
+      colour[p] = k;
+      ncol = std::max(ncol, k + 1);
+    }
+    std::vector<double> h(M);
+    for (long long j = 0; j < M; ++j) h[j] = epsilon * (1.0 + std::fabs(base[j]));
+    const size_t vb = sizeof(double) * M;
+    std::vector<void*> bufs;
+    auto dalloc = [&](size_t n) {
+      void* q = nullptr;
+      CK(cudaMalloc(&q, n));
+      bufs.push_back(q);
+      return q;
+    };
+    try {
+      double* dJ = static_cast<double*>(dalloc(vb * M));
+      double* dbase = static_cast<double*>(dalloc(vb));
+      double* dh = static_cast<double*>(dalloc(vb));
+      double* up = static_cast<double*>(dalloc(vb));
+      double* um = static_cast<double*>(dalloc(vb));
+      double* fp = static_cast<double*>(dalloc(vb));
+      double* fm = static_cast<double*>(dalloc(vb));
+      int* dcells = static_cast<int*>(dalloc(sizeof(int) * nc));
+      int* downer = static_cast<int*>(dalloc(sizeof(int) * nc));
+      int* dall = static_cast<int*>(dalloc(sizeof(int) * nc));
+      std::vector<int> all(nc);
+      for (int p = 0; p < nc; ++p) all[p] = p;
+      CK(cudaMemcpyAsync(dall, all.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(dbase, base, vb, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(dh, h.data(), vb, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(up, dbase, vb, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(um, dbase, vb, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemsetAsync(dJ, 0, vb * M, c->stream));
+      const int sgrid = static_cast<int>(std::min<long long>((M + 255) / 256, c->grid_flat));
+      for (int k = 0; k < ncol; ++k) {
+        std::vector<int> cells, owner(nc, -1);
+        for (int p = 0; p < nc; ++p)
+          if (colour[p] == k) {
+            cells.push_back(p);
+            for (int q : sten[p]) owner[q] = p;
+          }
+        CK(cudaMemcpyAsync(dcells, cells.data(), sizeof(int) * cells.size(),
+                           cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(downer, owner.data(), sizeof(int) * nc, cudaMemcpyHostToDevice,
+                           c->stream));
+        const int n = static_cast<int>(cells.size());
+        for (int l = 0; l < stride; ++l) {
+          CK(launch_probe_set(up, um, dbase, dh, dcells, n, stride, l, 1, c->stream));
+          rhs_full_device(c, up, fp, dall);
+          rhs_full_device(c, um, fm, dall);
+          CK(launch_probe_set(up, um, dbase, dh, dcells, n, stride, l, 0, c->stream));
+          CK(launch_probe_scatter(dJ, fp, fm, dh, downer, M, stride, l, sgrid, c->stream));
+        }
+        CK(cudaStreamSynchronize(c->stream));  // owner / cells host vectors die here
+      }
+      CK(cudaMemcpyAsync(J, dJ, vb * M, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+      cudaStreamSynchronize(c->stream);
+      for (void* q : bufs) cudaFree(q);
+      throw;
+    }
+    for (void* q : bufs) cudaFree(q);
+    if (n_colours) *n_colours = ncol;
+  });
+}
+
 int perrk_br1_gradients(perrk_ctx* c, double t, const double* U, double* grads) {
   (void)t;
   return guarded([&] {

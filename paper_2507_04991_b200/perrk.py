@@ -263,6 +263,21 @@ class Semidiscretization:
         check(lib().perrk_rhs_masked(self._h, float(t), _dp(U), _dp(out), mb))
         return out
 
+    def probe_jacobian(self, base, t=0.0, epsilon=1e-6, return_colours=False):
+        """probe_jacobian (specopt.cpp:18-35): dense central-difference
+        Jacobian of the RHS, M x M with J[i, j] = d rhs_i / d u_j, guarded to
+        M <= 5000.  Probed on the device in cell colours (include/perrk_b200.h)."""
+        U = self._state(base)
+        M = U.size
+        if M > 5000:
+            raise Error(capi.PERRK_EINVAL, "dense Jacobian probing guarded to M <= 5000")
+        Jc = np.empty(M * M)
+        ncol = C.c_int(0)
+        check(lib().perrk_probe_jacobian(self._h, _dp(U), float(t), float(epsilon), _dp(Jc),
+                                         C.byref(ncol)))
+        J = Jc.reshape(M, M).T  # column-major storage
+        return (J, ncol.value) if return_colours else J
+
     def br1_gradients(self, t, U):
         """BR1 auxiliary gradients (semidisc.hpp:75), NSF physics: [dim][dofs]."""
         U = self._state(U)
@@ -943,16 +958,20 @@ def _color_period(n, radius):
     return n
 
 
-def probe_jacobian(semi, U, t=0.0, epsilon=1e-7, colored=True):
+def probe_jacobian(semi, U, t=0.0, epsilon=1e-7, colored=True, device=True):
     """Dense Jacobian of the device RHS by central differences, column j with
     h_j = epsilon (1 + |U_j|) as specopt.cpp:18-35.  With `colored`, the
     columns of cells that are far enough apart are probed in one RHS pair
     (compressed Jacobian): a cell's RHS depends on its face neighbours (BR1:
     on their neighbours too), so cells whose footprints do not overlap share
     an evaluation; 2 x colours x (nodes per cell x V) RHS calls instead of
-    2 M."""
+    2 M.  With `device` (and M <= 5000) the whole probe runs inside the
+    library (perrk_probe_jacobian): perturbation, RHS pairs and the column
+    scatter stay on the GPU, one M x M copy back."""
     U = semi._state(U)
     M, npc, V = U.size, semi.nodes_per_cell(), semi.num_vars()
+    if colored and device and M <= 5000:
+        return semi.probe_jacobian(U, t, epsilon)
     if M > 5000 and not colored:
         raise Error(capi.PERRK_EINVAL, "dense Jacobian probing guarded to M <= 5000")
     shape = semi.spec.mesh.shape()

@@ -56,3 +56,50 @@ def test_probed_spectrum_supports_the_c1_family_at_its_cfl():
                                                                       P.CflRamp(0.9, 0.9))), 0.0)
     margin = P.stability_margin(cfg.family, eigs, dt)
     assert margin[0] < 1.0 + 1e-2
+
+
+def _single_column(semi, U, j, eps):
+    """specopt.cpp:25-32 for one column, through the device RHS."""
+    h = eps * (1.0 + abs(U[j]))
+    up, um = U.copy(), U.copy()
+    up[j] = U[j] + h
+    um[j] = U[j] - h
+    return (semi.rhs(0.0, up) - semi.rhs(0.0, um)) / (2.0 * h)
+
+
+def _nsf(mesh):
+    return P.Semidiscretization(P.SemidiscretizationSpec(mesh, physics="nsf", mu=2e-2,
+                                                         prandtl=0.72, surface_flux="hlle"))
+
+
+@pytest.mark.parametrize("case", ["2d", "3d", "nsf"])
+def test_device_probe_equals_single_column_probes_bitwise(case):
+    """perrk_probe_jacobian (include/perrk_b200.h): each coloured column equals
+    the reference's one-column-at-a-time probe on the same RHS bit for bit,
+    and the colour count is independent of the column count."""
+    if case == "3d":
+        from helpers import mesh3d
+        semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh3d(3, 2, 2, seed=9)))
+        U = smooth_state((semi.node_x(), semi.node_y(), semi.node_z()), 3, seed=6, amp=0.2)
+    else:
+        mesh = mesh2d(7, 6, seed=8)
+        semi = _nsf(mesh) if case == "nsf" else \
+            P.Semidiscretization(P.SemidiscretizationSpec(mesh, surface_flux="hlle"))
+        U = smooth_state((semi.node_x(), semi.node_y()), 2, seed=6, amp=0.2)
+    eps = 1e-6
+    J, ncol = semi.probe_jacobian(U, 0.0, eps, return_colours=True)
+    assert J.shape == (U.size, U.size)
+    assert ncol < semi.num_cells() or case == "3d"
+    cols = np.random.default_rng(3).choice(U.size, 12, replace=False)
+    for j in cols:
+        assert np.array_equal(J[:, j], _single_column(semi, U, j, eps)), j
+    # same matrix as the host-driven coloured probe
+    assert np.array_equal(J, P.probe_jacobian(semi, U, 0.0, eps, device=False))
+
+
+def test_device_probe_guard():
+    mesh = mesh2d(10, 9, seed=2)  # 90 cells x 64 DOFs > 5000
+    semi = P.Semidiscretization(P.SemidiscretizationSpec(mesh))
+    U = smooth_state((semi.node_x(), semi.node_y()), 2, seed=1)
+    with pytest.raises(P.Error):
+        semi.probe_jacobian(U)
