@@ -1390,7 +1390,7 @@ int perrk_rhs_masked(perrk_ctx* c, double t, const double* U, double* out, const
 
 namespace {
 // Full (unmasked) RHS of device state dU into dK, as perrk_rhs_masked(mask = NULL).
-void rhs_full_device(perrk_ctx* c, const double* dU, double* dK, int* gl_all) {
+static void rhs_full_device(perrk_ctx* c, const double* dU, double* dK, int* gl_all) {
   CK(cudaMemsetAsync(dK, 0, sizeof(double) * c->ndofs, c->stream));
   c->evals += static_cast<uint64_t>(c->ncells) * c->npc * c->V;
   StepState s = fresh_state();
@@ -1418,7 +1418,7 @@ void rhs_full_device(perrk_ctx* c, const double* dU, double* dK, int* gl_all) {
 }
 
 // Cells whose RHS rows read cell p: its face neighbours out to `rad` steps.
-std::vector<int> probe_stencil(const perrk_ctx* c, int p, int rad) {
+static std::vector<int> probe_stencil(const perrk_ctx* c, int p, int rad) {
   std::vector<int> out{p};
   size_t lo = 0;
   for (int r = 0; r < rad; ++r) {
