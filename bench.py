@@ -146,67 +146,80 @@ def traffic_fixture(config):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline / reference arm: the oracle port on a bounded sample
+# CPU baseline / reference arm: the oracle port (never the product library)
 # ---------------------------------------------------------------------------
-def cpu_sample(config, threads):
+def cpu_runs():
+    """oracle/cpu_runs.py: the workloads of configs/spec.py on the CPU
+    checkers, built without importing paper_2507_04991_b200."""
     if ORACLE_DIR not in sys.path:  # checker library; only bench's cpu/reference legs use it
         sys.path.insert(0, ORACLE_DIR)
-    import oracle as O
-    from paper_2507_04991_b200 import workloads as W
-    cfg = W.make_config(config)
-    sample = W.sample_config(cfg)
-    orc = O.Orc(sample.mesh, surface_flux=sample.surface_flux, threads=threads)
-    x, y, z, _ = orc.node_coords()
-    U0 = W.initial_state_for(sample, (x, y, z))
-    pm = sample.partition_map()
-    per_step = W.dof_stage_updates_per_step(sample.family, pm, sample.nodes_per_cell())
-    return sample, orc, U0, pm, per_step
+    import cpu_runs as CR
+    return CR
 
 
-def run_cpu(config, threads, seconds=None, steps=None, warmup=0):
-    sample, orc, U0, pm, per_step = cpu_sample(config, threads)
-    U = U0.copy()
+def run_cpu(spec, threads, seconds=None, steps=None, warmup=0):
+    """Time the oracle port's run() loop (stepper.cpp:144-188) on `spec`:
+    `warmup` untimed steps, then `steps` timed ones (or as many as fit in
+    `seconds`).  Returns (DOF-stage/s, steps, seconds, description)."""
+    CR = cpu_runs()
+    run = CR.CpuConfig(spec, threads=threads)
+    U = run.initial_state()
+    per_step = run.dof_stage_updates_per_step()
     t = 0.0
     if warmup:
-        t, _, _, _ = orc.run_steps(U, t, warmup, sample.family, pm.effective_level,
-                                   sample.relaxation, False, sample.cfl, records=False)
+        t, _, _, _ = run.run(U, warmup, t, records=False)
     if steps is None:  # calibrate to the time budget
-        t, n1, _, s1 = orc.run_steps(U, t, 1, sample.family, pm.effective_level,
-                                     sample.relaxation, False, sample.cfl, records=False)
-        steps = max(1, int(seconds / max(s1, 1e-6)) - 1)
+        t, n1, _, s1 = run.run(U, 1, t, records=False)
+        steps = max(0, int(seconds / max(s1, 1e-6)) - 1)
         tot_steps, tot_s = n1, s1
     else:
         tot_steps, tot_s = 0, 0.0
-    t, n, _, secs = orc.run_steps(U, t, steps, sample.family, pm.effective_level,
-                                  sample.relaxation, False, sample.cfl, records=False)
-    tot_steps += n
-    tot_s += secs
+    if steps:
+        t, n, _, secs = run.run(U, steps, t, records=False)
+        tot_steps += n
+        tot_s += secs
     desc = (f"oracle port (perrk_oracle.c, -O3 -ffp-contract=off, {threads} threads) on "
-            f"{sample.description}: {tot_steps} steps, {per_step} DOF-stage/step")
+            f"{spec.description} ({spec.mesh.num_cells()} cells): {tot_steps} timed steps, "
+            f"{per_step} DOF-stage/step")
     return per_step * tot_steps / tot_s, tot_steps, tot_s, desc
 
 
 def reference_arm(args):
+    """`--impl reference`: the reference CPU implementation of the path on the
+    host cores, on the SAME workload and config as the B200 arm (the full
+    mesh; C5 is 3D, which the reference lacks, so the oracle port stands in
+    for it).  Rank 0 alone works under torchrun."""
     rank, _, world = dist_env()
     if rank != 0:
         return
+    CR = cpu_runs()
+    spec = CR.S.make_spec(args.config)
     threads = os.cpu_count() or 1
-    value, steps, secs, desc = run_cpu(args.config, threads, steps=args.steps,
-                                       warmup=args.warmup)
-    from paper_2507_04991_b200 import workloads as W
-    cfg = W.make_config(args.config)
+    value, steps, secs, desc = run_cpu(spec, threads, steps=args.steps, warmup=args.warmup)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / max(steps, 1), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.description, "sample": desc},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": CR.S.bench_config(spec),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(config, seconds):
+    """The GPU line's cpu_baseline: the oracle port on a bounded sample of the
+    workload (configs/spec.py sample_spec), all host threads, and one thread."""
+    CR = cpu_runs()
+    spec = CR.S.sample_spec(CR.S.make_spec(config))
+    threads = os.cpu_count() or 1
+    v, n, s, desc = run_cpu(spec, threads, seconds=seconds)
+    v1, n1, s1, desc1 = run_cpu(spec, 1, seconds=seconds / 2)
+    return {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc,
+            "threads_1": {"value": v1, "cores": 1, "sample": desc1}}
 
 
 # ---------------------------------------------------------------------------
@@ -368,9 +381,7 @@ def perrk_arm(args):
     # ---- CPU baseline (rank 0, N = 1) ----------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        v, n, s, desc = run_cpu(args.config, threads, seconds=args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+        cpu = cpu_baseline(args.config, args.cpu_seconds)
 
     if rank == 0:
         line = {
@@ -378,14 +389,11 @@ def perrk_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.description, "nodes": int(run.total_nodes()),
-                       "dof_stage_per_step": int(total_per_step), "cfl": cfg.cfl,
-                       "family": f"{fam.kind} S={fam.S} E={fam.E}",
-                       "relaxation": "newton, accurate numerics (SURVEY 7.3 H1)",
-                       "l2": "inputs larger than L2 (state 5 x 640 MiB)",
-                       "parallelism": (f"{run.partition}-partition x{world} (NCCL halo)"
-                                       if world > 1 else "single"),
-                       "halo_traces": run.halo_traces() if world > 1 else 0},
+            "config": W.S.bench_config(cfg.spec_),
+            "partition": {"parallelism": (f"{run.partition}-partition x{world} (NCCL halo)"
+                                          if world > 1 else "single"),
+                          "halo_traces": run.halo_traces() if world > 1 else 0,
+                          "dof_stage_per_step_all_ranks": int(total_per_step)},
             "gpu_launches": int(launches), "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu, "clocks": clk,
             "run": {"gamma_min": min(gammas), "gamma_max": max(gammas), "fell_back": fell_back,
@@ -397,12 +405,38 @@ def perrk_arm(args):
         dist.destroy_process_group()
 
 
+def launch_ranks(args):
+    """`--gpus N` without a launcher: re-exec this command under
+    torch.distributed.run with N ranks (one per GPU).  Fewer than N visible
+    GPUs is an error, never a silent single-rank run."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, "
+                         f"found {have}\n")
+        sys.exit(2)
+    import socket
+    with socket.socket() as sk:  # a free rendezvous port on the loopback address
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         reference_arm(args)
-    else:
-        perrk_arm(args)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        launch_ranks(args)
+    _, _, world = dist_env()
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
+    perrk_arm(args)
 
 
 if __name__ == "__main__":

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define PERRK_B200_ABI_VERSION 1
+#define PERRK_B200_ABI_VERSION 2
 
 /* status codes */
 #define PERRK_OK 0
@@ -131,6 +131,14 @@ typedef struct {
   int idt;
   int records;               /* fill the per-step log */
   double cfl0, t_ramp, t0;   /* CflRamp and IntegratorConfig::t0 */
+  /* continuing one run() over several perrk_advance calls (stepper.cpp:
+   * 144-188 keeps gamma_seed and h0 across the whole loop): carry == 0 starts
+   * a run (seed 1, anchor H of the resident state); carry == 1 continues one
+   * with the previous call's next seed (fell_back ? 1 : gamma of its last
+   * step, stepper.cpp:170) and the run's anchor H(U_0) (stepper.cpp:151) */
+  int carry;
+  double gamma_seed;
+  double h_anchor;
 } perrk_run_cfg;
 
 /* One row of the step log; replaces StepRecord (stepper.hpp:43-52). */
@@ -140,6 +148,7 @@ typedef struct {
   int fell_back;
   double entropy;
   double invariants[5];
+  double delta_h;            /* PerkStepResult::delta_h of the step (stepper.hpp:62-68) */
 } perrk_step_record;
 
 /* ---- errors / version -------------------------------------------------- */

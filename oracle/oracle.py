@@ -157,6 +157,7 @@ def orc_lib():
             "orc_rhs_masked": (C.c_int, [C.c_void_p, C.c_double, _D, _D, C.c_char_p]),
             "orc_br1_gradients": (C.c_int, [C.c_void_p, C.c_double, _D, _D]),
             "orc_total_entropy": (C.c_double, [C.c_void_p, _D]),
+            "orc_total_entropy_acc": (C.c_double, [C.c_void_p, _D]),
             "orc_entropy_inner_product": (C.c_double, [C.c_void_p, _D, _D]),
             "orc_integral_per_variable": (None, [C.c_void_p, _D, _D]),
             "orc_admissible": (C.c_int, [C.c_void_p, _D, _I]),
@@ -223,12 +224,14 @@ class _Base:
 
     def run_steps(self, U, t, nsteps, fam, eff, relax=None, fixed=False, dt_or_cfl=0.5,
                   anchor=False, records=True):
-        """run() loop for exactly nsteps steps; returns (t, taken, log[nsteps, 6+V], seconds)."""
+        """run() loop for exactly nsteps steps; returns (t, taken, log, seconds), log rows
+        [t, dt, gamma, iters, H, fell_back, invariants[V]] (+ [delta_h, H_acc] for Orc)."""
         f = self._fam(fam)
         eff = np.ascontiguousarray(eff, dtype=np.int32)
         rx = self._relax(relax)
         tt = C.c_double(t)
-        log = np.zeros((max(nsteps, 1), 6 + self.V))
+        cols = 6 + self.V + (2 if self.kind == "orc" else 0)  # orc adds delta_h, H_acc
+        log = np.zeros((max(nsteps, 1), cols))
         secs = C.c_double()
         fn = self.L.ref_run_steps if self.kind == "ref" else self.L.orc_run_steps
         taken = fn(self.h, dp(U), C.byref(tt), nsteps, C.byref(f), ip(eff),
@@ -453,6 +456,10 @@ class Orc(_Base):
 
     def total_entropy(self, U):
         return self.L.orc_total_entropy(self.h, dp(np.ascontiguousarray(U)))
+
+    def total_entropy_acc(self, U):
+        """total_entropy as a compensated sum (accurate numerics)."""
+        return self.L.orc_total_entropy_acc(self.h, dp(np.ascontiguousarray(U)))
 
     def entropy_inner_product(self, U, K):
         return self.L.orc_entropy_inner_product(self.h, dp(np.ascontiguousarray(U)),

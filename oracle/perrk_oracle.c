@@ -948,6 +948,10 @@ static ksum_t entropy_acc(const orc_semi* s, const double* U) {
   return acc;
 }
 
+double orc_total_entropy_acc(const orc_semi* s, const double* U) {
+  return kval(entropy_acc(s, U));
+}
+
 /* mesh.cpp:97-129 (3D: third direction) */
 void orc_characteristic_speed(const orc_semi* s, const double* U, double* nu) {
   const int V = s->P.V;
@@ -1075,8 +1079,9 @@ static int solve_relaxation(relax_ctx* r, const orc_relax* cfg, double gamma_see
   if (cfg->method == 0 && r->numerics == 1) {
     /* H1.4: always take >= 1 Newton step from the seed; stop on a relative
      * step below 1e-13 (from the second step on, the iterate is then kept:
-     * the correction is noise) or on noise-floor stagnation; fall back only
-     * on non-finite values or gamma <= 0. */
+     * the correction is noise) or on noise-floor stagnation; fall back on
+     * non-finite values, gamma <= 0, or a last correction above 1e-10 gamma
+     * at max_iter (not converged). */
     double gamma = cfg->seed_from_previous ? gamma_seed : 1.0;
     double prev = 0.0;
     for (int it = 1; it <= cfg->max_iter; ++it) {
@@ -1103,6 +1108,12 @@ static int solve_relaxation(relax_ctx* r, const orc_relax* cfg, double gamma_see
       out->gamma = gamma;
       if (fabs(step) <= 1e-13 * gamma) return 0;
       if (it >= 2 && fabs(step) < 1e-10 * gamma && fabs(step) > 0.5 * fabs(prev)) return 0;
+      /* out of iterations: converged only if the last correction is inside
+       * the noise band, else the reference's fallback (relax.cpp:104) */
+      if (it == cfg->max_iter && fabs(step) > 1e-10 * gamma) {
+        *out = fallback(it, res);
+        return 0;
+      }
       prev = step;
     }
     return 0; /* accepted after max_iter */
@@ -1355,7 +1366,10 @@ done:
 }
 
 /* run() loop body, stepper.cpp:144-188, for exactly nsteps steps; log rows
- * [t, dt, gamma, iters, H, fell_back, inv_0 .. inv_{V-1}] */
+ * [t, dt, gamma, iters, H, fell_back, inv_0 .. inv_{V-1}, delta_h, H_acc]:
+ * delta_h is PerkStepResult::delta_h (stepper.hpp:62-68), H_acc the total
+ * entropy as a compensated sum (H is the reference's naive serial sum,
+ * semidisc.cpp:561-566) */
 int orc_run_steps(orc_semi* s, double* U, double* t, int nsteps, const orc_family* fam,
                   const int* eff, const orc_relax* relax, int fixed, double dt_or_cfl, int anchor,
                   int records, double* log, double* seconds) {
@@ -1374,7 +1388,7 @@ int orc_run_steps(orc_semi* s, double* U, double* t, int nsteps, const orc_famil
     if (r.aborted) break;
     gamma_seed = r.fell_back ? 1.0 : r.gamma;
     if (records) {
-      double* row = log + (size_t)step * (6 + V);
+      double* row = log + (size_t)step * (8 + V);
       row[0] = *t;
       row[1] = dt;
       row[2] = r.gamma;
@@ -1382,6 +1396,8 @@ int orc_run_steps(orc_semi* s, double* U, double* t, int nsteps, const orc_famil
       row[4] = orc_total_entropy(s, U);
       row[5] = r.fell_back;
       orc_integral_per_variable(s, U, row + 6);
+      row[6 + V] = r.delta_h;
+      row[7 + V] = kval(entropy_acc(s, U));
     }
     ++taken;
   }

@@ -96,6 +96,8 @@ int orc_rhs_masked(orc_semi* s, double t, const double* U, double* out, const ch
 int orc_br1_gradients(orc_semi* s, double t, const double* U, double* grads);
 
 double orc_total_entropy(const orc_semi* s, const double* U);
+/* the same as a compensated (Kahan-Babuska) sum, for the accurate numerics */
+double orc_total_entropy_acc(const orc_semi* s, const double* U);
 double orc_entropy_inner_product(const orc_semi* s, const double* U, const double* K);
 void orc_integral_per_variable(const orc_semi* s, const double* U, double* out);
 int orc_admissible(const orc_semi* s, const double* U, int* first_bad_cell);

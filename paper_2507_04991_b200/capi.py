@@ -60,13 +60,14 @@ class RunCfg(C.Structure):
     _fields_ = [("fixed_dt", C.c_int), ("dt_or_cfl", C.c_double), ("tf", C.c_double),
                 ("relax_enabled", C.c_int), ("relax", RelaxCfg), ("anchor_initial", C.c_int),
                 ("idt", C.c_int), ("records", C.c_int), ("cfl0", C.c_double),
-                ("t_ramp", C.c_double), ("t0", C.c_double)]
+                ("t_ramp", C.c_double), ("t0", C.c_double), ("carry", C.c_int),
+                ("gamma_seed", C.c_double), ("h_anchor", C.c_double)]
 
 
 class StepRecord(C.Structure):
     _fields_ = [("t", C.c_double), ("dt", C.c_double), ("gamma", C.c_double),
                 ("newton_iters", C.c_int), ("fell_back", C.c_int), ("entropy", C.c_double),
-                ("invariants", C.c_double * 5)]
+                ("invariants", C.c_double * 5), ("delta_h", C.c_double)]
 
 
 _P = C.c_void_p

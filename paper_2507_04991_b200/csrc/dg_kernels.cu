@@ -177,9 +177,18 @@ __device__ void relax_newton_update(StepState* st, dd A, dd B) {
     if (!isfinite(g2) || !(g2 > 0.0)) return relax_fallback(st, it, r);
     st->gamma = g2;
     if (fabs(step) <= 1e-13 * g2 ||
-        (it >= 2 && fabs(step) < 1e-10 * g2 && fabs(step) > 0.5 * fabs(st->prev_step)) ||
-        it >= st->max_iter) {
+        (it >= 2 && fabs(step) < 1e-10 * g2 && fabs(step) > 0.5 * fabs(st->prev_step))) {
       st->relax_done = 1;
+      return;
+    }
+    if (it >= st->max_iter) {
+      // out of iterations: a last correction inside the noise band (1e-10
+      // gamma) is converged; anything larger has not, and falls back to
+      // gamma = 1 as the reference does (relax.cpp:104)
+      if (fabs(step) <= 1e-10 * g2)
+        st->relax_done = 1;
+      else
+        relax_fallback(st, it, r);
       return;
     }
     st->prev_step = step;
@@ -484,7 +493,7 @@ __device__ void finish_step(StepState* st, double gamma, const dd* tot, int V, i
   else
     st->t += dt;
   if (want_record && records) {
-    double* row = records + static_cast<size_t>(st->steps_taken) * 11;
+    double* row = records + static_cast<size_t>(st->steps_taken) * REC_COLS;
     row[0] = st->t;
     row[1] = dt;
     row[2] = gamma;
@@ -492,6 +501,7 @@ __device__ void finish_step(StepState* st, double gamma, const dd* tot, int V, i
     row[4] = st->fell_back;
     row[5] = tot[0].hi + tot[0].lo;
     for (int v = 0; v < V; ++v) row[6 + v] = tot[1 + v].hi + tot[1 + v].lo;
+    row[11] = st->dh_hi + st->dh_lo;
   }
   st->gamma_seed = st->fell_back ? 1.0 : gamma;
   st->steps_taken += 1;
@@ -775,14 +785,24 @@ static size_t stage_smem() {
           (VISC ? StageGeo<DIM>::SM_VISC : 0));
 }
 
+// function attributes are per device: the launch helpers configure each
+// kernel once per device ordinal
+constexpr int MAX_DEVICES = 64;
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < MAX_DEVICES ? dev : 0;
+}
+
 template <int DIM, int SURF, bool VISC, bool SIMPLE>
 static void configure_stage() {
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[MAX_DEVICES] = {};
+  const int dev = current_device();
+  if (!configured[dev]) {
     cudaFuncSetAttribute(stage_kernel<DIM, SURF, VISC, SIMPLE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(stage_smem<DIM, VISC>()));
-    configured = true;
+    configured[dev] = true;
   }
 }
 
@@ -908,7 +928,8 @@ __global__ void combine_kernel(StepState* st, const double* all, int nranks, int
 // host-side sequencing right after combine_kernel
 __global__ void record_kernel(StepState* st, const double* all, int nranks, int V, double* records) {
   if (st->aborted || st->finished || !records) return;
-  double* row = records + static_cast<size_t>(st->steps_taken - 1) * 11;
+  double* row = records + static_cast<size_t>(st->steps_taken - 1) * REC_COLS;
+  row[11] = st->dh_hi + st->dh_lo;
   row[0] = st->t;
   row[1] = st->dt;
   row[2] = st->relax_enabled ? st->gamma : st->gamma_override;
@@ -1110,11 +1131,12 @@ static bool use_w3(int dim, int surf, int vol, bool visc) {
 
 template <int SURF>
 static void configure_w3() {
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[MAX_DEVICES] = {};
+  const int dev = current_device();
+  if (!configured[dev]) {
     cudaFuncSetAttribute(stage3w_kernel<SURF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(double) * W3::SM_TOTAL));
-    configured = true;
+    configured[dev] = true;
   }
 }
 
@@ -1212,19 +1234,25 @@ static int resident_grid(K kernel, int threads, int cap) {
 // holds two of its three blocks per SM at once.  Measured: sizing all three to
 // relax_spec_kernel's residency costs the passes more than the spec kernel's
 // tail (-4%), and capping relax_spec_kernel at 80 registers spills (neutral).
+// Cached per device ordinal (contexts on different devices get their own
+// residency), capped by the caller's grid on every call.
+
 template <int DIM>
 static int relax_grid(int cap) {
-  return resident_grid(relax_pass_kernel<DIM>, 256, cap);
+  static int resident[MAX_DEVICES] = {};
+  const int dev = current_device();
+  if (!resident[dev]) resident[dev] = resident_grid(relax_pass_kernel<DIM>, 256, 1 << 30);
+  return resident[dev] < cap ? resident[dev] : cap;
 }
 
 cudaError_t launch_relax_pass(int dim, const double* U, const double* d, const MeshDev& m,
                               const Phys& ph, StepState* st, double* partials, unsigned* counter,
                               long long nnodes, int grid, cudaStream_t s) {
   if (dim == 2) {
-    static const int g = relax_grid<2>(grid);
+    const int g = relax_grid<2>(grid);
     relax_pass_kernel<2><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
   } else {
-    static const int g = relax_grid<3>(grid);
+    const int g = relax_grid<3>(grid);
     relax_pass_kernel<3><<<g, 256, 0, s>>>(U, d, m, ph, st, partials, counter, nnodes);
   }
   return cudaGetLastError();
@@ -1236,11 +1264,11 @@ cudaError_t launch_update(int dim, double* Uout, const double* Uin, const double
                           double* records, int grid, cudaStream_t s) {
   // relax_pass_kernel's grid: the node walk (and record sums) of relax_spec_kernel
   if (dim == 2) {
-    static const int g = relax_grid<2>(grid);
+    const int g = relax_grid<2>(grid);
     update_kernel<2><<<g, 256, 0, s>>>(Uout, Uin, d, m, ph, st, partials, counter, nnodes,
                                        want_nu, want_record, records);
   } else {
-    static const int g = relax_grid<3>(grid);
+    const int g = relax_grid<3>(grid);
     update_kernel<3><<<g, 256, 0, s>>>(Uout, Uin, d, m, ph, st, partials, counter, nnodes,
                                        want_nu, want_record, records);
   }
@@ -1253,12 +1281,13 @@ static size_t spec_smem_bytes() {
 }
 
 template <int DIM>
-static void configure_spec() {
-  static bool done = false;
-  if (!done) {
+static void configure_spec() {  // a function attribute is per device
+  static bool done[MAX_DEVICES] = {};
+  const int dev = current_device();
+  if (!done[dev]) {
     cudaFuncSetAttribute(relax_spec_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(spec_smem_bytes<DIM>()));
-    done = true;
+    done[dev] = true;
   }
 }
 
@@ -1270,13 +1299,13 @@ cudaError_t launch_relax_spec(int dim, const double* U, const double* d, double*
   // summation order of r and r' (bitwise the unfused pass)
   if (dim == 2) {
     configure_spec<2>();
-    static const int g = relax_grid<2>(grid);
+    const int g = relax_grid<2>(grid);
     relax_spec_kernel<2><<<g, 256, spec_smem_bytes<2>(), s>>>(U, d, Uout, m, ph, st, partials,
                                                               counter, nnodes, want_nu,
                                                               want_record, records);
   } else {
     configure_spec<3>();
-    static const int g = relax_grid<3>(grid);
+    const int g = relax_grid<3>(grid);
     relax_spec_kernel<3><<<g, 256, spec_smem_bytes<3>(), s>>>(U, d, Uout, m, ph, st, partials,
                                                               counter, nnodes, want_nu,
                                                               want_record, records);

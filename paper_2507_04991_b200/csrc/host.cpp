@@ -1705,10 +1705,13 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
     s.t_ramp = cfg->cfl0 == cfg->dt_or_cfl ? 0.0 : cfg->t_ramp;
     s.t0 = cfg->t0;
     s.idt = cfg->idt;
-    s.gamma_seed = 1.0;
+    // run() keeps the gamma seed and the anchor across its whole loop
+    // (stepper.cpp:151,153,170): a continued run carries them in
+    s.gamma_seed = cfg->carry ? cfg->gamma_seed : 1.0;
+    if (cfg->carry) REQUIRE(cfg->gamma_seed > 0.0, "carried gamma seed must be positive");
     configure_relax(s, cfg->relax_enabled != 0, cfg->relax);
     if (cfg->relax_enabled && cfg->anchor_initial)
-      s.h_ref = quad(c, c->U, nullptr, 0, nullptr);  // H(U_0)
+      s.h_ref = cfg->carry ? cfg->h_anchor : quad(c, c->U, nullptr, 0, nullptr);  // H(U_0)
     Group& g = *c->group;
     REQUIRE(!(g.ex && cfg->relax_enabled && cfg->anchor_initial),
             "anchored relaxation is not supported with the slab decomposition");
@@ -1720,7 +1723,7 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
     for (perrk_ctx* m : g.members)
       if (rec && m->records_cap < nsteps) {
         if (m->records) cudaFree(m->records);
-        CK(cudaMalloc(&m->records, sizeof(double) * 11 * nsteps));
+        CK(cudaMalloc(&m->records, sizeof(double) * dev::REC_COLS * nsteps));
         m->records_cap = nsteps;
       }
     StepMode mode;
@@ -1753,8 +1756,11 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
       for (perrk_ctx* m : g.members) key += std::to_string(m->plan_version) + ":" +
                                            std::to_string(reinterpret_cast<uintptr_t>(m->records)) + ";";
       key += std::to_string(reinterpret_cast<uintptr_t>(c->U)) + (mode.fused ? "F" : "-");
+      // everything enqueue_step branches on: the relaxation method decides the
+      // number of captured passes (relax_passes), so it is part of the key
       key += std::to_string(mode.relax) + std::to_string(mode.cfg.numerics) + ":" +
-             std::to_string(mode.cfg.max_iter) + std::to_string(mode.want_nu) +
+             std::to_string(mode.cfg.method) + ":" + std::to_string(relax_passes(mode.cfg)) +
+             ":" + std::to_string(mode.cfg.max_iter) + std::to_string(mode.want_nu) +
              std::to_string(mode.want_record) + std::to_string(want_h);
       perrk_ctx::StepGraph* gr = nullptr;
       for (auto& x : c->graphs)
@@ -1802,10 +1808,10 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
     for (perrk_ctx* m : g.members)
       m->evals += evals_per_step(m) * static_cast<uint64_t>(r.steps_taken + (r.aborted ? 1 : 0));
     if (rec && r.steps_taken > 0) {
-      std::vector<double> raw(static_cast<size_t>(11) * r.steps_taken);
+      std::vector<double> raw(static_cast<size_t>(dev::REC_COLS) * r.steps_taken);
       CK(cudaMemcpy(raw.data(), c->records, sizeof(double) * raw.size(), cudaMemcpyDeviceToHost));
       for (int k = 0; k < r.steps_taken; ++k) {
-        const double* row = &raw[static_cast<size_t>(k) * 11];
+        const double* row = &raw[static_cast<size_t>(k) * dev::REC_COLS];
         perrk_step_record& o = log[k];
         o.t = row[0];
         o.dt = row[1];
@@ -1814,6 +1820,7 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
         o.fell_back = static_cast<int>(row[4]);
         o.entropy = row[5];
         for (int v = 0; v < 5; ++v) o.invariants[v] = v < c->V ? row[6 + v] : 0.0;
+        o.delta_h = row[11];
       }
     }
   });

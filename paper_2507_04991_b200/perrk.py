@@ -865,6 +865,7 @@ class StepRecord:
     entropy: float
     invariants: np.ndarray
     fell_back: bool
+    delta_h: float = 0.0  # PerkStepResult::delta_h of the step (stepper.hpp:62-68)
 
 
 @dataclass
@@ -877,7 +878,7 @@ class RunResult:
     initial_entropy: float
 
 
-def _run_cfg(config: IntegratorConfig, records=True):
+def _run_cfg(config: IntegratorConfig, records=True, carry=None):
     r = config.time.ramp
     rc = capi.RunCfg()
     rc.cfl0 = r.cfl0
@@ -892,20 +893,30 @@ def _run_cfg(config: IntegratorConfig, records=True):
     rc.anchor_initial = int(config.anchor == "initial")
     rc.idt = int(config.idt)
     rc.records = int(records)
+    if carry is not None:  # continue a run: (next gamma seed, anchor H(U_0))
+        rc.carry = 1
+        rc.gamma_seed, rc.h_anchor = carry
     return rc
 
 
-def advance(semi, family, pmap, config: IntegratorConfig, t, nsteps, records=True):
+def advance(semi, family, pmap, config: IntegratorConfig, t, nsteps, records=True, carry=None):
     """Up to nsteps steps of run()'s loop on the resident state, on the
-    device (one host sync at the end).  Returns (t, steps, aborted, records)."""
+    device (one host sync at the end).  Returns (t, steps, aborted, records).
+    `carry` = (gamma_seed, h_anchor) continues a run started by an earlier
+    call (perrk_run_cfg.carry)."""
     semi._use_family(family, pmap)
-    rc = _run_cfg(config, records)
+    rc = _run_cfg(config, records, carry)
     log = (capi.StepRecord * max(nsteps, 1))()
     tt = C.c_double(t)
     taken, ab = C.c_int(), C.c_int()
     check(lib().perrk_advance(semi._h, C.byref(rc), C.byref(tt), int(nsteps),
                               log if records else None, C.byref(taken), C.byref(ab)))
     return tt.value, taken.value, bool(ab.value), list(log)[: taken.value] if records else []
+
+
+def _record(step, r, V):
+    return StepRecord(step, r.t, r.dt, r.gamma, r.newton_iters, r.entropy,
+                      np.array(r.invariants[:V]), bool(r.fell_back), r.delta_h)
 
 
 def run(config: IntegratorConfig, family, pmap, semi, U0, chunk=64):
@@ -918,14 +929,17 @@ def run(config: IntegratorConfig, family, pmap, semi, U0, chunk=64):
     log: List[StepRecord] = []
     aborted = False
     t_eps = 1e-12 * max(1.0, abs(config.tf))
+    carry = None  # the chunks are ONE run: gamma seed and anchor carry over
     while t < config.tf - t_eps and not aborted:
         if len(log) >= config.max_steps:
             raise Error(capi.PERRK_EINVAL, "step limit exceeded")
         n = min(chunk, config.max_steps - len(log))
-        t, taken, aborted, recs = advance(semi, family, pmap, config, t, n, True)
+        t, taken, aborted, recs = advance(semi, family, pmap, config, t, n, True, carry)
         for r in recs:
-            log.append(StepRecord(len(log) + 1, r.t, r.dt, r.gamma, r.newton_iters, r.entropy,
-                                  np.array(r.invariants[: semi.num_vars()]), bool(r.fell_back)))
+            log.append(_record(len(log) + 1, r, semi.num_vars()))
+        if log:
+            last = log[-1]
+            carry = (1.0 if last.fell_back else last.gamma, h0)
         if taken == 0 and not aborted:
             break
     return RunResult(semi.download(), log, t, aborted, semi.rhs_cell_evaluations(), h0)
@@ -938,9 +952,7 @@ def run_steps(config: IntegratorConfig, family, pmap, semi, U0, nsteps, out=None
     U0 = semi._state(U0)
     semi.upload(U0)
     t, taken, aborted, recs = advance(semi, family, pmap, config, config.t0, nsteps, True)
-    log = [StepRecord(k + 1, r.t, r.dt, r.gamma, r.newton_iters, r.entropy,
-                      np.array(r.invariants[: semi.num_vars()]), bool(r.fell_back))
-           for k, r in enumerate(recs)]
+    log = [_record(k + 1, r, semi.num_vars()) for k, r in enumerate(recs)]
     U = semi.download(out)
     return RunResult(U, log, t, aborted, semi.rhs_cell_evaluations(), float("nan"))
 
@@ -958,7 +970,7 @@ def _color_period(n, radius):
     return n
 
 
-def probe_jacobian(semi, U, t=0.0, epsilon=1e-7, colored=True, device=True):
+def probe_jacobian(semi, U, t=0.0, epsilon=1e-6, colored=True, device=True):
     """Dense Jacobian of the device RHS by central differences, column j with
     h_j = epsilon (1 + |U_j|) as specopt.cpp:18-35.  With `colored`, the
     columns of cells that are far enough apart are probed in one RHS pair

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(capi.EXPORTED)
-    assert L.perrk_abi_version() == 1
+    assert L.perrk_abi_version() == 2
 
 
 def test_library_is_cuda_code():

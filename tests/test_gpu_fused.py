@@ -94,3 +94,55 @@ def test_anchored_relaxation_fused_vs_oracle(monkeypatch):
     assert rel_err(Uf, Uo, 4) < 1e-11
     assert np.abs(np.array([r.gamma for r in rf]) - log[:, 2]).max() < 1e-12
     assert np.abs(np.array([r.entropy for r in rf]) - log[:, 4]).max() < 1e-12
+
+
+@pytest.mark.parametrize("numerics,anchor", [("accurate", "initial"), ("reference", "step"),
+                                             ("reference", "initial"), ("accurate", "step")])
+def test_chunked_run_is_one_run(numerics, anchor):
+    """run() in chunks (perrk.run -> several perrk_advance calls) is ONE run:
+    the gamma seed and the anchor H(U_0) carry across the chunks
+    (stepper.cpp:151,153,170), so run(chunk=7) equals one advance call of the
+    same steps bit for bit (state, gamma, Newton iterations, H)."""
+    cfg = W.make_config("c1")
+    relax = P.RelaxationConfig(numerics=numerics)
+    steps = 30
+    semi = P.Semidiscretization(cfg.spec())
+    U0 = W.initial_state_for(cfg, (semi.node_x(), semi.node_y(), None))
+    semi.upload(U0)
+    rc = P.IntegratorConfig(tf=1e9, time=P.TimeControl(fixed=False, ramp=P.CflRamp(0.9, 0.9)),
+                            relaxation=relax, anchor=anchor)
+    _, taken, _, one = P.advance(semi, cfg.family, cfg.partition_map(), rc, 0.0, steps)
+    assert taken == steps
+    U_one = semi.download()
+    # run() stops at tf: put tf just past the one-call run's final time
+    rc2 = P.IntegratorConfig(tf=one[-1].t, time=rc.time, relaxation=relax, anchor=anchor)
+    res = P.run(rc2, cfg.family, cfg.partition_map(), semi, U0, chunk=7)
+    assert len(res.log) == steps
+    assert np.array_equal(res.U, U_one)
+    assert [r.gamma for r in res.log] == [r.gamma for r in one]
+    assert [r.newton_iters for r in res.log] == [r.newton_iters for r in one]
+    assert [r.entropy for r in res.log] == [r.entropy for r in one]
+    assert [r.delta_h for r in res.log] == [r.delta_h for r in one]
+
+
+def test_relaxation_methods_alternate_on_one_context():
+    """The captured step graph is keyed by the relaxation method (bisection
+    and secant capture more passes than Newton): Newton, bisection, secant,
+    Newton again on ONE context, nsteps > 1 each, equal to fresh contexts."""
+    cfg = W.make_config("c1")
+    rc_of = lambda m: P.IntegratorConfig(
+        tf=1e9, time=P.TimeControl(fixed=False, ramp=P.CflRamp(0.9, 0.9)),
+        relaxation=P.RelaxationConfig(method=m, numerics="reference"))
+    shared = P.Semidiscretization(cfg.spec())
+    U0 = W.initial_state_for(cfg, (shared.node_x(), shared.node_y(), None))
+    for m in ["newton", "bisection", "secant", "newton"]:
+        shared.upload(U0)
+        _, n1, _, r1 = P.advance(shared, cfg.family, cfg.partition_map(), rc_of(m), 0.0, 4)
+        fresh = P.Semidiscretization(cfg.spec())
+        fresh.upload(U0)
+        _, n2, _, r2 = P.advance(fresh, cfg.family, cfg.partition_map(), rc_of(m), 0.0, 4)
+        assert n1 == n2 == 4
+        assert np.array_equal(shared.download(), fresh.download()), m
+        assert [r.gamma for r in r1] == [r.gamma for r in r2], m
+        assert [(r.newton_iters, r.fell_back) for r in r1] == \
+               [(r.newton_iters, r.fell_back) for r in r2], m

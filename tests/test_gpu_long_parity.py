@@ -1,0 +1,38 @@
+"""GPU: north_star parity gate at each config's STATED step count.
+
+C1 100, C2 500, C3 200, C4 200 and C5 100 steps on the B200 path against the
+oracle's committed long-run fixtures (tests/golden/long_<cfg>.npz, made by
+tests/golden/make_long_parity.py; the reference's run loop stepper.cpp:144-188
+with the relaxation relax.cpp:51-104), plus C1 against the unmodified
+reference with its own relaxation numerics (c1ref).
+
+Tolerances (written here, as the gate states them):
+  state    1e-11 relative L2 per conserved variable (literal per variable),
+           on the fixture's 32768-node sample and, where the full oracle state
+           is present (baseline/_ref/parity), over every node
+  gamma    1e-12 absolute, every step
+  delta_h  1e-12 absolute, every step (PerkStepResult::delta_h)
+  H_n-H_0  1e-12 absolute, every step (compensated sums on both sides)
+The metric dicts are printed (pytest -s) so the numbers are kept with the
+run; tests/long_parity.py is the same comparison as a script.
+"""
+import json
+
+import pytest
+
+import long_parity as LP
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = ["c1", "c1ref", "c2", "c3", "c4", "c5"]
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_long_parity_stated_steps(name):
+    if not LP.have_fixture(name):
+        pytest.skip(f"no long-run fixture for {name}")
+    m = LP.compare(name)
+    print(json.dumps(m))
+    assert m["fell_back_gpu"] == m["fell_back_oracle"], m
+    failing = [k for k, ok in m["gate"].items() if not ok]
+    assert not failing, (failing, m)

