@@ -233,6 +233,11 @@ FAMILIES = [
     ("c3_p4_5_9_16", "p4", 16, [5, 9, 16], 2),
     ("c4_p3_4_8", "p3", 8, [4, 8], 2),
     ("c5_p4_5_8_14", "p4", 14, [5, 8, 14], 3),
+    # SPEC.md acceptance criteria 1/2/10 (weak blast wave, three-level mesh):
+    # E2 = {3,5,9}, E3 = {4,7,13}, E4 = {6,10,18}
+    ("blast_p2_3_5_9", "p2", 9, [3, 5, 9], 1),
+    ("blast_p3_4_7_13", "p3", 13, [4, 7, 13], 1),
+    ("blast_p4_6_10_18", "p4", 18, [6, 10, 18], 1),
 ]
 
 if __name__ == "__main__":

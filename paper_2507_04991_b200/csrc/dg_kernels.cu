@@ -452,23 +452,33 @@ struct KsShared {
   __device__ __forceinline__ ksum& operator[](int r) const { return base[r * stride]; }
 };
 
+// max_dir lambda_dir / h_dir of one node (mesh.cpp:97-129 divided by k+1):
+// the ONE expression of the CFL speed, used by the update kernels (the next
+// step's speed) and numax_kernel (the first step's), so a run split over
+// several perrk_advance calls takes the same dt as one call
+template <int DIM>
+__device__ __forceinline__ double node_speed_over_h(const MeshDev& m, const Phys& ph,
+                                                    const double* u, int cell) {
+  const double ir = frcp(u[0]);
+  double m2 = 0.0;
+#pragma unroll
+  for (int dir = 0; dir < DIM; ++dir) m2 = fma(u[1 + dir], u[1 + dir], m2);
+  const double p = ph.gm1 * (u[DIM + 1] - 0.5 * m2 * ir);
+  const double c = fsqrt(ph.gamma * p * ir);
+  double best = 0.0;
+#pragma unroll
+  for (int dir = 0; dir < DIM; ++dir)
+    best = fmax(best, (fabs(u[1 + dir]) * ir + c) * (0.25 * __ldg(&m.rec[cell].J2[dir])));
+  return best;
+}
+
 template <int DIM, class Acc>
 __device__ __forceinline__ void update_node_terms(const MeshDev& m, const Phys& ph, const double* u,
                                                   long long n, int want_nu, int want_record,
                                                   double s_new, double& numax, Acc acc) {
   constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC;
   const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
-  if (want_nu) {
-    const double ir = frcp(u[0]);
-    double m2 = 0.0;
-#pragma unroll
-    for (int dir = 0; dir < DIM; ++dir) m2 = fma(u[1 + dir], u[1 + dir], m2);
-    const double p = ph.gm1 * (u[DIM + 1] - 0.5 * m2 * ir);
-    const double c = fsqrt(ph.gamma * p * ir);
-#pragma unroll
-    for (int dir = 0; dir < DIM; ++dir)
-      numax = fmax(numax, (fabs(u[1 + dir]) * ir + c) * (0.25 * __ldg(&m.rec[cell].J2[dir])));
-  }
+  if (want_nu) numax = fmax(numax, node_speed_over_h<DIM>(m, ph, u, cell));
   if (want_record) {
     const double om = node_measure_rec<DIM>(m, cell, l);
     ks_add_prod(acc[0], om, s_new);
@@ -682,13 +692,7 @@ __global__ void __launch_bounds__(256)
     double u[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) u[v] = __ldg(U + n * V + v);
-    int ci, cj, ck;
-    cell_coords(m, static_cast<int>(n / NPC), ci, cj, ck);
-    const int cc[3] = {ci, cj, ck};
-    const double p = pressure<DIM>(ph, u);
-#pragma unroll
-    for (int dir = 0; dir < DIM; ++dir)
-      best = fmax(best, max_wave_speed<DIM>(ph, u, p, dir) / m.h[dir][cc[dir]]);
+    best = fmax(best, node_speed_over_h<DIM>(m, ph, u, static_cast<int>(n / NPC)));
   }
   best = warp_max(best);
   if ((threadIdx.x & 31) == 0) atomic_max_pos(&st->numax_bits, best);

@@ -243,25 +243,59 @@ def test_partition_union_orc_3d():
     assert np.array_equal(r1 + r2, full)
 
 
+def _embed_2d(U2, axes, n_other):
+    """2D state [J][I][iy][ix][4] -> 3D [K][J3][I3][iz][iy][ix][5] on the
+    axis pair `axes` (2D x -> axes[0], 2D y -> axes[1]), constant along the
+    third axis (n_other cells), zero velocity along it."""
+    J, I = U2.shape[:2]
+    a, b = axes
+    other = 3 - a - b
+    # 3D [cell z][cell y][cell x][iz][iy][ix]; place (cell, node) axes of the pair
+    cells = [None, None, None]  # per 3D axis: ("J"|"I"|"other")
+    cells[a], cells[b], cells[other] = "I", "J", "O"
+    sizes = {"I": I, "J": J, "O": n_other}
+    shape = (sizes[cells[2]], sizes[cells[1]], sizes[cells[0]], 4, 4, 4)
+    U3 = np.zeros(shape + (5,))
+    # index grids of the 3D array
+    kz, ky, kx, iz, iy, ix = np.indices(shape)
+    cidx = {0: kx, 1: ky, 2: kz}
+    nidx = {0: ix, 1: iy, 2: iz}
+    src = U2[cidx[b], cidx[a], nidx[b], nidx[a]]  # [..., 4]
+    U3[..., 0] = src[..., 0]
+    U3[..., 1 + a] = src[..., 1]
+    U3[..., 1 + b] = src[..., 2]
+    U3[..., 4] = src[..., 3]
+    return U3, (cidx, nidx)
+
+
 @need_ref
-def test_3d_reduces_to_reference_2d_on_z_constant_data():
-    """Oracle extension pin: z-independent 3D data with w = 0 gives the 2D
-    reference RHS in (rho, mx, my, E) and a zero z-momentum RHS."""
+@pytest.mark.parametrize("axes", [(0, 1), (0, 2), (1, 2), (2, 0)])
+def test_3d_reduces_to_reference_2d_on_each_axis_pair(axes):
+    """Oracle extension pin (semidisc.cpp:446-556 extended to 3D): 2D data on
+    the axis pair `axes`, constant along the third axis with zero velocity
+    there, gives the 2D reference RHS on that pair and a zero RHS for the
+    third momentum.  The (x,z), (y,z) and (z,x) pairs carry real z-line and
+    z-face terms (the (x,y) pair alone would leave them identically zero)."""
     m2 = mesh2d(5, 4, seed=21)
-    m3 = P.Mesh3DRect(m2.x_edges, m2.y_edges, [0.0, 0.7, 1.5, 2.0])
-    ref, orc3 = O.Ref(m2), O.Orc(m3)
+    ref = O.Ref(m2)
+    edges = [None, None, None]
+    a, b = axes
+    edges[a], edges[b] = list(m2.x_edges), list(m2.y_edges)
+    other = 3 - a - b
+    edges[other] = [0.0, 0.7, 1.5, 2.0]
+    orc3 = O.Orc(P.Mesh3DRect(*edges))
     x2, y2, _, _ = ref.node_coords()
-    U2 = smooth_state((x2, y2), 2, seed=8).reshape(-1, 16, 4)
-    nz = 3
-    U3 = np.zeros((nz, m2.num_cells(), 4, 4, 4, 5))  # [kz][cell2][iz][iy][ix][v]
-    u2 = U2.reshape(-1, 4, 4, 4)                      # [cell2][iy][ix][v]
-    for v, v3 in ((0, 0), (1, 1), (2, 2), (3, 4)):
-        U3[..., v3] = u2[None, :, None, :, :, v]
+    U2 = smooth_state((x2, y2), 2, seed=8)
+    J, I = m2.ny(), m2.nx()
+    U2g = U2.reshape(J, I, 4, 4, 4)
+    U3, (cidx, nidx) = _embed_2d(U2g, axes, 3)
     r3 = orc3.rhs(0.0, U3.reshape(-1)).reshape(U3.shape)
-    r2 = ref.rhs(0.0, U2.reshape(-1)).reshape(-1, 4, 4, 4)
-    for v, v3 in ((0, 0), (1, 1), (2, 2), (3, 4)):
-        assert np.abs(r3[..., v3] - r2[None, :, None, :, :, v]).max() < 1e-12 * np.abs(r2).max()
-    assert np.abs(r3[..., 3]).max() < 1e-12 * np.abs(r2).max()
+    r2 = ref.rhs(0.0, U2).reshape(J, I, 4, 4, 4)
+    r2e = r2[cidx[b], cidx[a], nidx[b], nidx[a]]
+    scale = np.abs(r2).max()
+    for v, v3 in ((0, 0), (1, 1 + a), (2, 1 + b), (3, 4)):
+        assert np.abs(r3[..., v3] - r2e[..., v]).max() < 1e-12 * scale, (axes, v)
+    assert np.abs(r3[..., 1 + other]).max() < 1e-12 * scale
 
 
 # --------------------------------------------------------------------------- relaxation
