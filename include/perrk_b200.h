@@ -212,6 +212,22 @@ int perrk_perk_step_resident(perrk_ctx* ctx, double* t, double dt, const perrk_s
 int perrk_advance(perrk_ctx* ctx, const perrk_run_cfg* cfg, double* t, int nsteps,
                   perrk_step_record* log, int* steps_taken, int* aborted);
 
+/* Matrix-free spectrum estimation: the dense probe of
+ * specopt.cpp:18-35 needs an M x M Jacobian (guarded to M <= 5000); this
+ * runs m steps of Arnoldi (classical Gram-Schmidt applied twice) on the
+ * central-difference Jacobian-vector product of the full RHS at `base`
+ * (host, NULL: the resident state),
+ *   J v = (rhs(u + h v) - rhs(u - h v)) / (2 h),  h = epsilon (1 + max|u|),
+ * |v|_2 = 1, entirely on the device; the Krylov basis needs (m + 1) M
+ * doubles of device memory.  cell_mask (NULL: every cell) restricts the
+ * operator to the flagged cells (v and J v zero elsewhere): a level's own
+ * block of the Jacobian.  H receives the (m + 1) x m upper Hessenberg
+ * matrix, column-major; the eigenvalues of its leading m_done x m_done block
+ * are the Ritz values (m_done < m: an invariant subspace was found, and those
+ * Ritz values are eigenvalues of the probed operator). */
+int perrk_krylov_hessenberg(perrk_ctx* ctx, const double* base, double t, double epsilon, int m,
+                            const char* cell_mask, double* H, int* m_done);
+
 /* probe_jacobian (specopt.cpp:18-35; declared specopt.hpp:25-26, default
  * epsilon 1e-6): dense central-difference Jacobian of the full RHS at `base`,
  * column j stepped by epsilon*(1+|base_j|), guarded to M <= 5000.  J is the

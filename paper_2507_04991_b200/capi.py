@@ -101,6 +101,8 @@ _PROTOS = {
                                            C.POINTER(StepResult)]),
     "perrk_advance": (C.c_int, [_P, C.POINTER(RunCfg), _D, C.c_int, C.POINTER(StepRecord),
                                 _I, _I]),
+    "perrk_krylov_hessenberg": (C.c_int, [_P, _D, C.c_double, C.c_double, C.c_int, C.c_char_p,
+                                          _D, _I]),
     "perrk_error_norms": (C.c_int, [_P, _D, C.c_int, _D, C.c_double, _D, _D]),
     "perrk_rhs_cell_evaluations": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "perrk_reset_counter": (C.c_int, [_P]),

@@ -82,6 +82,7 @@ __device__ __forceinline__ void report_bad(StepState* st, int stage, long long n
 #include "dg_stage3w.cuh"
 #include "dg_visc.cuh"
 #include "dg_advection.cuh"
+#include "dg_krylov.cuh"
 
 namespace perrk {
 namespace dev {
@@ -1392,6 +1393,46 @@ cudaError_t launch_probe_scatter(double* J, const double* fp, const double* fm, 
                                  const int* owner, long long M, long long stride, int l, int grid,
                                  cudaStream_t s) {
   probe_scatter_kernel<<<grid, 256, 0, s>>>(J, fp, fm, h, owner, M, stride, l);
+  return cudaGetLastError();
+}
+
+// ---- matrix-free spectrum estimation (dg_krylov.cuh) -------------------------
+cudaError_t launch_krylov_perturb(double* up, double* um, const double* u, const double* v,
+                                  double h, long long n, int grid, cudaStream_t s) {
+  krylov_perturb_kernel<<<grid, 256, 0, s>>>(up, um, u, v, h, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_krylov_fd(double* w, const double* fp, const double* fm, double inv2h,
+                             const unsigned char* cmask, long long stride, long long n, int grid,
+                             cudaStream_t s) {
+  krylov_fd_kernel<<<grid, 256, 0, s>>>(w, fp, fm, inv2h, cmask, stride, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_krylov_seed(double* v, const unsigned char* cmask, long long stride,
+                               long long n, unsigned long long seed, int grid, cudaStream_t s) {
+  krylov_seed_kernel<<<grid, 256, 0, s>>>(v, cmask, stride, n, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_krylov_dots(const double* Vb, long long ld, int k, const double* w,
+                               double* partials, int nblocks, double* out, long long n,
+                               cudaStream_t s) {
+  krylov_dots_kernel<<<dim3(nblocks, k), 256, 0, s>>>(Vb, ld, w, partials, n);
+  krylov_dots_finish_kernel<<<(k + 127) / 128, 128, 0, s>>>(partials, nblocks, k, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_krylov_project(double* w, const double* Vb, long long ld, const double* c,
+                                  int k, long long n, int grid, cudaStream_t s) {
+  krylov_project_kernel<<<grid, 256, 0, s>>>(w, Vb, ld, c, k, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_krylov_scale(double* dst, const double* src, double sc, long long n, int grid,
+                                cudaStream_t s) {
+  krylov_scale_kernel<<<grid, 256, 0, s>>>(dst, src, sc, n);
   return cudaGetLastError();
 }
 

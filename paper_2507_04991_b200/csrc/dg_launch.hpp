@@ -118,6 +118,21 @@ cudaError_t launch_probe_set(double* up, double* um, const double* base, const d
 cudaError_t launch_probe_scatter(double* J, const double* fp, const double* fm, const double* h,
                                  const int* owner, long long M, long long stride, int l, int grid,
                                  cudaStream_t s);
+// matrix-free spectrum estimation (dg_krylov.cuh)
+cudaError_t launch_krylov_perturb(double* up, double* um, const double* u, const double* v,
+                                  double h, long long n, int grid, cudaStream_t s);
+cudaError_t launch_krylov_fd(double* w, const double* fp, const double* fm, double inv2h,
+                             const unsigned char* cmask, long long stride, long long n, int grid,
+                             cudaStream_t s);
+cudaError_t launch_krylov_seed(double* v, const unsigned char* cmask, long long stride,
+                               long long n, unsigned long long seed, int grid, cudaStream_t s);
+cudaError_t launch_krylov_dots(const double* Vb, long long ld, int k, const double* w,
+                               double* partials, int nblocks, double* out, long long n,
+                               cudaStream_t s);
+cudaError_t launch_krylov_project(double* w, const double* Vb, long long ld, const double* c,
+                                  int k, long long n, int grid, cudaStream_t s);
+cudaError_t launch_krylov_scale(double* dst, const double* src, double sc, long long n, int grid,
+                                cudaStream_t s);
 cudaError_t launch_admissible(int dim, const double* U, const dev::Phys& ph, int* first_bad,
                               long long nnodes, int grid, cudaStream_t s);
 

@@ -1434,6 +1434,109 @@ static std::vector<int> probe_stencil(const perrk_ctx* c, int p, int rad) {
 }
 }  // namespace
 
+int perrk_krylov_hessenberg(perrk_ctx* c, const double* base, double t, double epsilon, int m,
+                            const char* cell_mask, double* H, int* m_done) {
+  (void)t;  // autonomous RHS (semidisc.cpp:411)
+  return guarded([&] {
+    REQUIRE(c && H && m_done, "null argument");
+    no_slab(c, "krylov_hessenberg");
+    REQUIRE(m >= 1, "m must be at least 1");
+    REQUIRE(std::isfinite(epsilon) && epsilon > 0.0, "epsilon must be positive");
+    const long long M = c->ndofs;
+    REQUIRE(m <= M, "m exceeds the number of DOFs");
+    set_device(c);
+    const int nc = static_cast<int>(c->ncells);
+    const long long stride = static_cast<long long>(c->npc) * c->V;
+    const int grid = c->grid_flat;
+    std::vector<void*> bufs;
+    auto dalloc = [&](size_t n) {
+      void* q = nullptr;
+      CK(cudaMalloc(&q, n));
+      bufs.push_back(q);
+      return q;
+    };
+    *m_done = 0;
+    try {
+      const size_t vb = sizeof(double) * M;
+      double* Vb = static_cast<double*>(dalloc(vb * (m + 1)));  // Krylov basis
+      double* dbase = static_cast<double*>(dalloc(vb));
+      double* up = static_cast<double*>(dalloc(vb));
+      double* um = static_cast<double*>(dalloc(vb));
+      double* fp = static_cast<double*>(dalloc(vb));
+      double* fm = static_cast<double*>(dalloc(vb));
+      double* w = static_cast<double*>(dalloc(vb));
+      const int nblk = c->grid_flat / 4;  // two blocks per SM
+      double* partials = static_cast<double*>(dalloc(sizeof(double) * 2 * nblk * (m + 1)));
+      double* coef = static_cast<double*>(dalloc(sizeof(double) * 2 * (m + 1)));
+      unsigned char* dmask = nullptr;
+      int* dall = static_cast<int*>(dalloc(sizeof(int) * nc));
+      std::vector<int> all(nc);
+      for (int p = 0; p < nc; ++p) all[p] = p;
+      CK(cudaMemcpyAsync(dall, all.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, c->stream));
+      if (cell_mask) {
+        dmask = static_cast<unsigned char*>(dalloc(nc));
+        CK(cudaMemcpyAsync(dmask, cell_mask, nc, cudaMemcpyHostToDevice, c->stream));
+      }
+      // the base state and its max norm (the step scale of specopt.cpp:25-26)
+      std::vector<double> hb;
+      const double* bsrc = base;
+      if (!base) {
+        hb.resize(M);
+        download(c, hb.data(), c->U);
+        bsrc = hb.data();
+      }
+      double umax = 0.0;
+      for (long long i = 0; i < M; ++i) umax = std::max(umax, std::fabs(bsrc[i]));
+      CK(cudaMemcpyAsync(dbase, bsrc, vb, cudaMemcpyHostToDevice, c->stream));
+      const double h = epsilon * (1.0 + umax);
+      std::vector<double> Hh(static_cast<size_t>(m + 1) * m, 0.0), c1(m + 1), c2(m + 1);
+      auto norm2 = [&](const double* x) {
+        CK(launch_krylov_dots(x, 0, 1, x, partials, nblk, coef, M, c->stream));
+        double r = 0.0;
+        CK(cudaMemcpyAsync(&r, coef, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return std::sqrt(r);
+      };
+      CK(launch_krylov_seed(Vb, dmask, stride, M, 0x5eedULL, grid, c->stream));
+      const double n0 = norm2(Vb);
+      REQUIRE(n0 > 0.0, "empty cell mask");
+      CK(launch_krylov_scale(Vb, Vb, 1.0 / n0, M, grid, c->stream));
+      int done = 0;
+      for (int k = 0; k < m; ++k) {
+        double* vk = Vb + static_cast<long long>(k) * M;
+        CK(launch_krylov_perturb(up, um, dbase, vk, h, M, grid, c->stream));
+        rhs_full_device(c, up, fp, dall);
+        rhs_full_device(c, um, fm, dall);
+        CK(launch_krylov_fd(w, fp, fm, 0.5 / h, dmask, stride, M, grid, c->stream));
+        // classical Gram-Schmidt, applied twice (CGS2): orthogonal to working precision
+        for (int pass = 0; pass < 2; ++pass) {
+          CK(launch_krylov_dots(Vb, M, k + 1, w, partials, nblk, coef, M, c->stream));
+          CK(launch_krylov_project(w, Vb, M, coef, k + 1, M, grid, c->stream));
+          CK(cudaMemcpyAsync((pass ? c2 : c1).data(), coef, sizeof(double) * (k + 1),
+                             cudaMemcpyDeviceToHost, c->stream));
+        }
+        const double beta = norm2(w);  // synchronizes: c1, c2 are on the host
+        for (int j = 0; j <= k; ++j) Hh[j + static_cast<size_t>(m + 1) * k] = c1[j] + c2[j];
+        Hh[k + 1 + static_cast<size_t>(m + 1) * k] = beta;
+        done = k + 1;
+        double col = 0.0;
+        for (int j = 0; j <= k; ++j) col = std::max(col, std::fabs(c1[j] + c2[j]));
+        if (!(beta > 1e-13 * col)) break;  // invariant subspace: the Ritz values are exact
+        CK(launch_krylov_scale(Vb + static_cast<long long>(k + 1) * M, w, 1.0 / beta, M, grid,
+                               c->stream));
+      }
+      CK(cudaStreamSynchronize(c->stream));
+      std::copy(Hh.begin(), Hh.end(), H);
+      *m_done = done;
+    } catch (...) {
+      cudaStreamSynchronize(c->stream);
+      for (void* q : bufs) cudaFree(q);
+      throw;
+    }
+    for (void* q : bufs) cudaFree(q);
+  });
+}
+
 int perrk_probe_jacobian(perrk_ctx* c, const double* base, double t, double epsilon, double* J,
                          int* n_colours) {
   (void)t;  // autonomous RHS (semidisc.cpp:411)

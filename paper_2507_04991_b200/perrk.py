@@ -278,6 +278,27 @@ class Semidiscretization:
         J = Jc.reshape(M, M).T  # column-major storage
         return (J, ncol.value) if return_colours else J
 
+    def krylov_hessenberg(self, base=None, m=60, t=0.0, epsilon=1e-6, cell_mask=None):
+        """Matrix-free spectrum estimation (SURVEY.md 8f item 1;
+        perrk_krylov_hessenberg): m Arnoldi steps on the central-difference
+        Jacobian-vector product of the RHS at `base` (None: the resident
+        state), on the device.  cell_mask (per cell, nonzero = on) restricts
+        the operator to those cells.  Returns the (m_done + 1) x m_done
+        Hessenberg matrix."""
+        Up = None if base is None else _dp(self._state(base))
+        H = np.zeros((m + 1) * m)
+        done = C.c_int(0)
+        mb = None
+        if cell_mask is not None:
+            mk = np.ascontiguousarray(cell_mask, dtype=np.int8)
+            if mk.size != self.num_cells():
+                raise Error(capi.PERRK_EINVAL, "cell mask size must equal the cell count")
+            mb = mk.tobytes()
+        check(lib().perrk_krylov_hessenberg(self._h, Up, float(t), float(epsilon), int(m), mb,
+                                            _dp(H), C.byref(done)))
+        k = done.value
+        return H.reshape(m, m + 1).T[: k + 1, :k]
+
     def br1_gradients(self, t, U):
         """BR1 auxiliary gradients (semidisc.hpp:75), NSF physics: [dim][dofs]."""
         U = self._state(U)
@@ -945,14 +966,28 @@ def run(config: IntegratorConfig, family, pmap, semi, U0, chunk=64):
     return RunResult(semi.download(), log, t, aborted, semi.rhs_cell_evaluations(), h0)
 
 
-def run_steps(config: IntegratorConfig, family, pmap, semi, U0, nsteps, out=None):
+def run_steps(config: IntegratorConfig, family, pmap, semi, U0, nsteps, out=None, chunk=None):
     """run() (stepper.cpp:129-193) for exactly nsteps steps (the reference's
     run has no step-count mode): U0 (host) -> device once, the
-    steps resident with the step log, the final state -> `out` (host)."""
+    steps resident, the final state -> `out` (host).  The step log comes back
+    to the host every `chunk` steps (None: once at the end; 1: every step's
+    StepRecord is on the host before the next step is issued, as run()'s
+    on_step callback sees it, stepper.cpp:182); gamma seed and anchor carry
+    across the chunks."""
     U0 = semi._state(U0)
+    h0 = semi.total_entropy(U0) if (chunk and config.relaxation is not None
+                                    and config.anchor == "initial") else float("nan")
     semi.upload(U0)
-    t, taken, aborted, recs = advance(semi, family, pmap, config, config.t0, nsteps, True)
-    log = [_record(k + 1, r, semi.num_vars()) for k, r in enumerate(recs)]
+    chunk = chunk or max(nsteps, 1)
+    t, log, aborted, carry = config.t0, [], False, None
+    while len(log) < nsteps and not aborted:
+        n = min(chunk, nsteps - len(log))
+        t, taken, aborted, recs = advance(semi, family, pmap, config, t, n, True, carry)
+        for r in recs:
+            log.append(_record(len(log) + 1, r, semi.num_vars()))
+        if not recs:
+            break
+        carry = (1.0 if log[-1].fell_back else log[-1].gamma, h0)
     U = semi.download(out)
     return RunResult(U, log, t, aborted, semi.rhs_cell_evaluations(), float("nan"))
 
@@ -1046,9 +1081,20 @@ def clean_spectrum(eigs, relative_tol=1e-10):
     return re + 1j * im
 
 
-def probe_spectrum(semi, U, t=0.0, colored=True):
+def probe_spectrum(semi, U, t=0.0, colored=True, epsilon=1e-6):
     """probe_spectrum (specopt.cpp:56-60) on the device RHS."""
-    return clean_spectrum(np.linalg.eigvals(probe_jacobian(semi, U, t, colored=colored)))
+    return clean_spectrum(np.linalg.eigvals(probe_jacobian(semi, U, t, epsilon=epsilon,
+                                                           colored=colored)))
+
+
+def krylov_spectrum(semi, U=None, m=60, t=0.0, epsilon=1e-6, cell_mask=None):
+    """Ritz values of m matrix-free Arnoldi steps (Semidiscretization.
+    krylov_hessenberg): the spectral envelope of the RHS Jacobian (largest
+    |lambda|, the extreme real and imaginary parts) on meshes of any size,
+    where probe_spectrum's dense M x M probe is guarded to M <= 5000."""
+    H = semi.krylov_hessenberg(U, m, t, epsilon, cell_mask)
+    k = H.shape[1]
+    return clean_spectrum(np.linalg.eigvals(H[:k, :k]))
 
 
 def stability_margin(family, eigs, dt):
