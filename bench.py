@@ -318,13 +318,13 @@ def perrk_arm(args):
         U_host[:] = semi.download()
         U_out = torch.empty(U0.size, dtype=torch.float64, pin_memory=True).numpy()
         rc_run = P.IntegratorConfig(t0=t, tf=1e30, time=rc.time, relaxation=cfg.relaxation)
-        P.run_steps(rc_run, fam, pm, semi, U_host, 2, out=U_out, chunk=1)  # untimed first call
+        P.run_steps(rc_run, fam, pm, semi, U_host, 2, out=U_out)  # untimed first call
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
         e0.record(stream)
-        res = P.run_steps(rc_run, fam, pm, semi, U_host, args.steps, out=U_out, chunk=1)
+        res = P.run_steps(rc_run, fam, pm, semi, U_host, args.steps, out=U_out)
         e1.record(stream)
         torch.cuda.synchronize()
         rms = e0.elapsed_time(e1)
@@ -352,16 +352,14 @@ def perrk_arm(args):
             m = torch.tensor([rms, ems], device="cuda")
             dist.all_reduce(m, op=dist.ReduceOp.MAX)
             rms, ems = (float(x) for x in m.tolist())
-        import ctypes
-        rec_bytes = ctypes.sizeof(P.capi.StepRecord)  # one StepRecord row, read every step
+        rec_bytes = 12 * 8  # one device StepRecord row (REC_COLS doubles), copied every step
         e2e = {"value": total_per_step * args.steps / (rms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(U_host.nbytes // args.steps),
                "d2h_bytes_per_step": int(U_out.nbytes // args.steps + rec_bytes),
                "ms_per_step": rms / args.steps, "wall_ms_per_step": 1e3 * rwall / args.steps,
-               "path": f"run() for {args.steps} steps: perrk_upload_state (pinned U0), then "
-                       "per step perrk_advance(1 step) with its StepRecord read back to the host "
-                       "before the next step is issued (on_step, stepper.cpp:182), "
-                       "perrk_download_state (pinned U) at the end",
+               "path": f"run() for {args.steps} steps: perrk_upload_state (pinned U0), "
+                       "perrk_advance with every step's StepRecord row copied device-to-host "
+                       "(pinned) as that step completes, perrk_download_state (pinned U)",
                "host_state_every_step": {
                    "value": total_per_step * args.steps / (ems * 1e-3), "unit": UNIT,
                    "h2d_bytes_per_step": int(Uh.nbytes), "d2h_bytes_per_step": int(Uh.nbytes),

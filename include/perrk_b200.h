@@ -174,7 +174,11 @@ int perrk_upload_state(perrk_ctx* ctx, const double* U, size_t n);
 int perrk_download_state(perrk_ctx* ctx, double* U, size_t n);
 /* device pointer of the resident state (for zero-copy interop); valid until
  * the next perrk_advance, which alternates the state between two buffers when
- * it fuses the relaxation with the update (relax_spec_kernel) */
+ * it fuses the relaxation with the update (relax_spec_kernel).  The resident
+ * state is in the DEVICE layout, cell-blocked SoA: entry (cell c, node l,
+ * variable v) at (c V + v) nodes_per_cell + l.  Host buffers of every other
+ * entry point use the reference's canonical layout ((c nodes_per_cell + l) V
+ * + v, common.hpp:11-13); upload / download transpose between the two. */
 int perrk_state_device_ptr(perrk_ctx* ctx, double** dptr);
 int perrk_sync(perrk_ctx* ctx);
 

@@ -316,29 +316,25 @@ __device__ void relax_update(StepState* st, dd A, dd B) {
   st->iters = it;
 }
 
-// One warp's 32-node block k of two state arrays (U and d, 32 V contiguous
-// doubles each) into shared memory by coalesced cp.async (16-byte pieces when
-// the block is whole), one commit group per call (empty past the end).
-template <int V>
+// One warp's 32-node block k of two state arrays (U and d) into shared
+// memory by coalesced 16-byte cp.async, one commit group per call (empty past
+// the end).  In the device layout (sidx) a block's variable v is 32 (3D) or
+// two runs of 16 (2D) contiguous doubles; the staging area is [v][32], read
+// by lane with conflict-free 8-byte loads (s[v * 32 + lane]).
+template <int DIM>
 __device__ __forceinline__ void stage_pair(const double* A, const double* B, long long nnodes,
                                            long long nblk, long long k, double* sa, double* sb,
                                            int lane) {
+  constexpr int V = DIM + 2;
   if (k < nblk) {
-    constexpr int BLK = 32 * V;
     const long long n0 = k * 32;
-    const int nd = static_cast<int>(min(32LL, nnodes - n0)) * V;
-    const double* ga = A + n0 * V;
-    const double* gb = B + n0 * V;
-    if (nd == BLK) {
 #pragma unroll
-      for (int q = lane; q < BLK / 2; q += 32) {
-        cp_async16(sa + 2 * q, ga + 2 * q);
-        cp_async16(sb + 2 * q, gb + 2 * q);
-      }
-    } else {
-      for (int q = lane; q < nd; q += 32) {
-        cp_async8(sa + q, ga + q);
-        cp_async8(sb + q, gb + q);
+    for (int q = lane; q < V * 16; q += 32) {
+      const int v = q >> 4, p = q & 15;
+      const long long n = n0 + 2 * p;  // nodes n, n + 1: same cell (NPC is even)
+      if (n < nnodes) {
+        cp_async16(sa + v * 32 + 2 * p, A + sidx_n<DIM>(n, v));
+        cp_async16(sb + v * 32 + 2 * p, B + sidx_n<DIM>(n, v));
       }
     }
   }
@@ -381,7 +377,7 @@ __global__ void __launch_bounds__(256)
   const long long nblk = (nnodes + 31) / 32;
   const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   auto stage = [&](long long k, int b) {
-    stage_pair<V>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
+    stage_pair<DIM>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
   };
   ksum A = ks_zero(), B = ks_zero();
   long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
@@ -395,13 +391,13 @@ __global__ void __launch_bounds__(256)
     if (n < nnodes) {
       const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
       const double om = node_measure_rec<DIM>(m, cell, l);
-      const double* su = s_stage[wib][b][0] + lane * V;
-      const double* sd = s_stage[wib][b][1] + lane * V;
+      const double* su = s_stage[wib][b][0] + lane;
+      const double* sd = s_stage[wib][b][1] + lane;
       double u[V], dv[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        u[v] = su[v];
-        dv[v] = sd[v];
+        u[v] = su[32 * v];
+        dv[v] = sd[32 * v];
       }
       if (numerics == 1) {
         double du[V], ra, rb;
@@ -543,24 +539,24 @@ __global__ void __launch_bounds__(256)
   for (int r = 0; r < 6; ++r) acc[r] = ks_zero();
   long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
   int b = 0;
-  stage_pair<V>(Uin, d, nnodes, nblk, k, s_stage[wib][0][0], s_stage[wib][0][1], lane);
+  stage_pair<DIM>(Uin, d, nnodes, nblk, k, s_stage[wib][0][0], s_stage[wib][0][1], lane);
   for (; k < nblk; k += stride, b ^= 1) {
-    stage_pair<V>(Uin, d, nnodes, nblk, k + stride, s_stage[wib][b ^ 1][0],
-                  s_stage[wib][b ^ 1][1], lane);
+    stage_pair<DIM>(Uin, d, nnodes, nblk, k + stride, s_stage[wib][b ^ 1][0],
+                    s_stage[wib][b ^ 1][1], lane);
     cp_async_wait<1>();
     __syncwarp();
     const long long n = k * 32 + lane;
     if (n < nnodes) {
-      const double* su = s_stage[wib][b][0] + lane * V;
-      const double* sd = s_stage[wib][b][1] + lane * V;
-      double u[V], du[V];
+      double u0[V], u[V], du[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        u[v] = fma(scale, sd[v], su[v]);
-        du[v] = __dmul_rn(scale, sd[v]);
-        Uout[n * V + v] = u[v];
+        u0[v] = s_stage[wib][b][0][32 * v + lane];
+        const double dv = s_stage[wib][b][1][32 * v + lane];
+        u[v] = fma(scale, dv, u0[v]);
+        du[v] = __dmul_rn(scale, dv);
+        Uout[sidx_n<DIM>(n, v)] = u[v];
       }
-      const double s_new = want_record ? trial_entropy(ph, trial_state<DIM>(ph, su, du)) : 0.0;
+      const double s_new = want_record ? trial_entropy(ph, trial_state<DIM>(ph, u0, du)) : 0.0;
       if (want_nu || want_record)
         update_node_terms<DIM>(m, ph, u, n, want_nu, want_record, s_new, numax, acc);
     }
@@ -619,7 +615,7 @@ __global__ void __launch_bounds__(256, 3)
   const long long nblk = (nnodes + 31) / 32;
   const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   auto stage = [&](long long k, int b) {
-    stage_pair<V>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
+    stage_pair<DIM>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
   };
   ksum acc[2];  // A, B in registers; the update's six record sums in shared memory
   acc[0] = acc[1] = ks_zero();
@@ -637,13 +633,11 @@ __global__ void __launch_bounds__(256, 3)
     __syncwarp();
     const long long n = k * 32 + lane;
     if (n < nnodes) {
-      const double* su = s_stage[wib][b][0] + lane * V;
-      const double* sd = s_stage[wib][b][1] + lane * V;
       double u[V], dv[V], du[V], T[V], ra, rb;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        u[v] = su[v];
-        dv[v] = sd[v];
+        u[v] = s_stage[wib][b][0][32 * v + lane];
+        dv[v] = s_stage[wib][b][1][32 * v + lane];
         du[v] = __dmul_rn(gdt, dv[v]);
         T[v] = fma(gdt, dv[v], u[v]);  // update_kernel's U + (gamma dt) d
       }
@@ -654,7 +648,7 @@ __global__ void __launch_bounds__(256, 3)
       ks_add_prod(acc[0], om, ra);
       ks_add_prod(acc[1], om, rb);
 #pragma unroll
-      for (int v = 0; v < V; ++v) Uout[n * V + v] = T[v];
+      for (int v = 0; v < V; ++v) Uout[sidx_n<DIM>(n, v)] = T[v];
       if (want_nu || want_record)
         update_node_terms<DIM>(m, ph, T, n, want_nu, want_record, trial_entropy(ph, tr), numax,
                                racc);
@@ -692,7 +686,7 @@ __global__ void __launch_bounds__(256)
        n += static_cast<long long>(gridDim.x) * blockDim.x) {
     double u[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) u[v] = __ldg(U + n * V + v);
+    for (int v = 0; v < V; ++v) u[v] = __ldg(U + sidx_n<DIM>(n, v));
     best = fmax(best, node_speed_over_h<DIM>(m, ph, u, static_cast<int>(n / NPC)));
   }
   best = warp_max(best);
@@ -710,7 +704,7 @@ __global__ void nu_cell_kernel(const double* __restrict__ U, MeshDev m, Phys ph,
     for (int l = 0; l < NPC; ++l) {
       double u[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) u[v] = U[(c * NPC + l) * V + v];
+      for (int v = 0; v < V; ++v) u[v] = U[sidx<DIM>(c, l, v)];
       const double p = pressure<DIM>(ph, u);
 #pragma unroll
       for (int dir = 0; dir < DIM; ++dir) r[dir] = fmax(r[dir], max_wave_speed<DIM>(ph, u, p, dir));
@@ -747,13 +741,13 @@ __global__ void __launch_bounds__(256)
     const double om = node_measure<DIM>(m, ci, cj, ck, l);
     double u[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) u[v] = __ldg(U + n * V + v);
+    for (int v = 0; v < V; ++v) u[v] = __ldg(U + sidx_n<DIM>(n, v));
     if (mode == 0) {
       acc[0] = dd_add_prod(acc[0], om, entropy<DIM>(ph, u));
     } else if (mode == 1) {
       double k[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) k[v] = __ldg(K + n * V + v);
+      for (int v = 0; v < V; ++v) k[v] = __ldg(K + sidx_n<DIM>(n, v));
       acc[0] = dd_add_prod(acc[0], om, entropy_dot<DIM>(ph, u, k));
     } else {
 #pragma unroll
@@ -774,7 +768,7 @@ __global__ void admissible_kernel(const double* __restrict__ U, Phys ph, int* fi
        n += static_cast<long long>(gridDim.x) * blockDim.x) {
     double u[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) u[v] = U[n * V + v];
+    for (int v = 0; v < V; ++v) u[v] = U[sidx_n<DIM>(n, v)];
     if (!admissible<DIM>(ph, u)) atomicMin(first_bad, static_cast<int>(n / NPC));
   }
 }
@@ -1009,7 +1003,7 @@ __global__ void __launch_bounds__(256)
       for (int l = 0; l < N1; ++l)
 #pragma unroll
         for (int v = 0; v < V; ++v)
-          row[v] += L[qx * N1 + l] * __ldg(U + (static_cast<size_t>(cell) * NPC + l + N1 * iy) * V + v);
+          row[v] += L[qx * N1 + l] * __ldg(U + sidx<2>(cell, l + N1 * iy, v));
 #pragma unroll
       for (int v = 0; v < V; ++v) val[v] += L[qy * N1 + iy] * row[v];
     }
@@ -1370,15 +1364,26 @@ __global__ void probe_set_kernel(double* up, double* um, const double* base, con
   um[j] = on ? base[j] - h[j] : base[j];
 }
 
+// canonical index of device-layout entry i (sidx): a cell's local offset
+// v NPC + node is node V + v in the reference's layout
+__device__ __forceinline__ long long canonical_of(long long i, long long stride, int npc) {
+  const long long c = i / stride;
+  const int o = static_cast<int>(i - c * stride);
+  const int V = static_cast<int>(stride / npc);
+  return c * stride + static_cast<long long>(o % npc) * V + o / npc;
+}
+
 __global__ void probe_scatter_kernel(double* J, const double* fp, const double* fm,
                                      const double* h, const int* owner, long long M,
-                                     long long stride, int l) {
+                                     long long stride, int l, int npc) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < M;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int p = owner[i / stride];
     if (p < 0) continue;
-    const long long j = static_cast<long long>(p) * stride + l;
-    J[j * M + i] = (fp[i] - fm[i]) / (2.0 * h[j]);
+    const long long j = static_cast<long long>(p) * stride + l;  // device layout
+    // J in the reference's (canonical) column-major order
+    J[canonical_of(j, stride, npc) * M + canonical_of(i, stride, npc)] =
+        (fp[i] - fm[i]) / (2.0 * h[j]);
   }
 }
 
@@ -1390,9 +1395,31 @@ cudaError_t launch_probe_set(double* up, double* um, const double* base, const d
 }
 
 cudaError_t launch_probe_scatter(double* J, const double* fp, const double* fm, const double* h,
-                                 const int* owner, long long M, long long stride, int l, int grid,
-                                 cudaStream_t s) {
-  probe_scatter_kernel<<<grid, 256, 0, s>>>(J, fp, fm, h, owner, M, stride, l);
+                                 const int* owner, long long M, long long stride, int l, int npc,
+                                 int grid, cudaStream_t s) {
+  probe_scatter_kernel<<<grid, 256, 0, s>>>(J, fp, fm, h, owner, M, stride, l, npc);
+  return cudaGetLastError();
+}
+
+// ---- canonical <-> device layout (sidx), at upload / download ----------------
+// Writes are coalesced; each thread's read stays inside its cell's block
+// (2.5 KB in 3D), which L1 holds.
+__global__ void layout_kernel(double* dst, const double* src, long long ncells, int npc, int V,
+                              int to_device) {
+  const long long stride = static_cast<long long>(npc) * V, n = ncells * stride;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long c = i / stride;
+    const int o = static_cast<int>(i - c * stride);
+    // to_device: i is (v, node) with o = v npc + node; else (node, v), o = node V + v
+    const int other = to_device ? (o % npc) * V + o / npc : (o % V) * npc + o / V;
+    dst[i] = src[c * stride + other];
+  }
+}
+
+cudaError_t launch_layout(double* dst, const double* src, long long ncells, int npc, int V,
+                          int to_device, int grid, cudaStream_t s) {
+  layout_kernel<<<grid, 256, 0, s>>>(dst, src, ncells, npc, V, to_device);
   return cudaGetLastError();
 }
 

@@ -116,8 +116,11 @@ cudaError_t launch_probe_set(double* up, double* um, const double* base, const d
                              const int* cells, int n, long long stride, int l, int on,
                              cudaStream_t s);
 cudaError_t launch_probe_scatter(double* J, const double* fp, const double* fm, const double* h,
-                                 const int* owner, long long M, long long stride, int l, int grid,
-                                 cudaStream_t s);
+                                 const int* owner, long long M, long long stride, int l, int npc,
+                                 int grid, cudaStream_t s);
+// canonical (reference) <-> device (sidx) layout of ncells cell blocks
+cudaError_t launch_layout(double* dst, const double* src, long long ncells, int npc, int V,
+                          int to_device, int grid, cudaStream_t s);
 // matrix-free spectrum estimation (dg_krylov.cuh)
 cudaError_t launch_krylov_perturb(double* up, double* um, const double* u, const double* v,
                                   double h, long long n, int grid, cudaStream_t s);

@@ -732,20 +732,22 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
     for (int i = 0; i < DIM; ++i) own.v[i] = 0.0;
     double be = 1.0;
     if (cell >= 0) {
-      const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
+      // device layout (sidx): variable v at gi + v NPC
+      const size_t gi = static_cast<size_t>(cell) * NPC * V + l;
       double u[V];
       // U_i: from the previous stage's epilogue, or formed here from the first
       // column (cells that were inactive at i-1, whose a_{i,i-1} = 0)
       if (!a.form) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
+        for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v * NPC);
       } else if (s_cform[cs]) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) u[v] = __ldg(a.Us + gi + v);
+        for (int v = 0; v < V; ++v) u[v] = __ldg(a.Us + gi + v * NPC);
       } else {
         const double a1 = s_ca1[cs];
 #pragma unroll
-        for (int v = 0; v < V; ++v) u[v] = fma(a1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
+        for (int v = 0; v < V; ++v)
+          u[v] = fma(a1, __ldg(a.K1 + gi + v * NPC), __ldg(a.U + gi + v * NPC));
       }
       double ir;
       own = prim_of<DIM>(ph, u, ir);
@@ -780,27 +782,28 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
       // the neighbour's node on the shared face: far end of the same line
       const int node =
           line_base<DIM>(d, pt % N1, pt / N1) + (side ? 0 : N1 - 1) * line_stride(d);
-      const size_t gi = (static_cast<size_t>(nbc) * NPC + node) * V;
+      const size_t gi = static_cast<size_t>(nbc) * NPC * V + node;
       if (!a.form) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) nbu[k][v] = __ldg(a.U + gi + v);
+        for (int v = 0; v < V; ++v) nbu[k][v] = __ldg(a.U + gi + v * NPC);
       } else if (s_nform[c2][f]) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) nbu[k][v] = __ldg(a.Us + gi + v);
+        for (int v = 0; v < V; ++v) nbu[k][v] = __ldg(a.Us + gi + v * NPC);
       } else {
         const double b1 = s_na1[c2][f];
 #pragma unroll
-        for (int v = 0; v < V; ++v) nbu[k][v] = fma(b1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
+        for (int v = 0; v < V; ++v)
+          nbu[k][v] = fma(b1, __ldg(a.K1 + gi + v * NPC), __ldg(a.U + gi + v * NPC));
       }
     }
     if constexpr (VISC) {  // BR1 viscous fluxes from grad_kernel (2D)
       const size_t nd = static_cast<size_t>(a.ndofs);
       if (cell >= 0) {
-        const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
+        const size_t gi = static_cast<size_t>(cell) * NPC * V + l;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          vg[tid * V + v] = a.G[gi + v];
-          vg[(T + tid) * V + v] = a.G[nd + gi + v];
+          vg[tid * V + v] = a.G[gi + v * NPC];
+          vg[(T + tid) * V + v] = a.G[nd + gi + v * NPC];
         }
       }
       for (int q = tid; q < CPB * NFP; q += T) {
@@ -809,9 +812,9 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
         const int d = f >> 1, side = f & 1;
         const int node =
             line_base<DIM>(d, pt % N1, pt / N1) + (side ? 0 : N1 - 1) * line_stride(d);
-        const size_t gi = (static_cast<size_t>(s_nbc[c2][f]) * NPC + node) * V + d * nd;
+        const size_t gi = static_cast<size_t>(s_nbc[c2][f]) * NPC * V + node + d * nd;
 #pragma unroll
-        for (int v = 0; v < V; ++v) vn[q * V + v] = a.G[gi + v];
+        for (int v = 0; v < V; ++v) vn[q * V + v] = a.G[gi + v * NPC];
       }
     }
     __syncthreads();
@@ -964,10 +967,10 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
         }
         if (a.want_h) acc_h = dd_add_prod(acc_h, om, -own.rho * s_therm);
       }
-      const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
+      const size_t gi = static_cast<size_t>(cell) * NPC * V + l;  // variable v at gi + v NPC
       if (a.write_k)
 #pragma unroll
-        for (int v = 0; v < V; ++v) a.Kout[gi + v] = K[v];
+        for (int v = 0; v < V; ++v) a.Kout[gi + v * NPC] = K[v];
       if (a.write_next) {
         // U_{i+1} = U + dt (a_{i+1,1} K1 + a_{i+1,i} K_i) with the cell's row
         // (stepper.cpp:60-72, one stage ahead); at stage 0, K1 = K_0 = K
@@ -977,25 +980,26 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
         const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
         double x[V], y[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) x[v] = __ldg(a.U + gi + v);
+        for (int v = 0; v < V; ++v) x[v] = __ldg(a.U + gi + v * NPC);
         if (!a.form) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) a.Usn[gi + v] = fma(an, K[v], x[v]);
+          for (int v = 0; v < V; ++v) a.Usn[gi + v * NPC] = fma(an, K[v], x[v]);
         } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v) y[v] = __ldg(a.K1 + gi + v);
+          for (int v = 0; v < V; ++v) y[v] = __ldg(a.K1 + gi + v * NPC);
 #pragma unroll
-          for (int v = 0; v < V; ++v) a.Usn[gi + v] = x[v] + fma(an, y[v], pn * K[v]);
+          for (int v = 0; v < V; ++v) a.Usn[gi + v * NPC] = x[v] + fma(an, y[v], pn * K[v]);
         }
       }
       if (a.d_mode) {
         double dn5[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) dn5[v] = a.d_mode == 1 ? a.b * K[v] : fma(a.b, K[v], a.d[gi + v]);
+        for (int v = 0; v < V; ++v)
+          dn5[v] = a.d_mode == 1 ? a.b * K[v] : fma(a.b, K[v], a.d[gi + v * NPC]);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const double dn = dn5[v];
-          a.d[gi + v] = dn;
+          a.d[gi + v * NPC] = dn;
           if (a.want_dmax) {
             const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(dn)) &
                                          0x7fffffffffffffffULL;
@@ -1055,19 +1059,20 @@ __global__ void __launch_bounds__(256)
     const int cell = send[2 * e], f = send[2 * e + 1];
     const int d = f >> 1, side = f & 1;
     const int node = line_base<DIM>(d, pt % N1, pt / N1) + (side ? N1 - 1 : 0) * line_stride(d);
-    const size_t gi = (static_cast<size_t>(cell) * NPC + node) * V;
+    const size_t gi = static_cast<size_t>(cell) * NPC * V + node;  // device layout (sidx)
     double u[V];
     const int lev = m.level[cell];
     if (!a.form) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v);
+      for (int v = 0; v < V; ++v) u[v] = __ldg(a.U + gi + v * NPC);
     } else if (a.formed[lev]) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) u[v] = __ldg(a.Us + gi + v);
+      for (int v = 0; v < V; ++v) u[v] = __ldg(a.Us + gi + v * NPC);
     } else {
       const double b1 = dt * a.a1[lev];
 #pragma unroll
-      for (int v = 0; v < V; ++v) u[v] = fma(b1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
+      for (int v = 0; v < V; ++v)
+        u[v] = fma(b1, __ldg(a.K1 + gi + v * NPC), __ldg(a.U + gi + v * NPC));
     }
     double* o = out + (static_cast<size_t>(e) * FP + pt) * V;
 #pragma unroll

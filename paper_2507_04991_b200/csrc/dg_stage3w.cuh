@@ -325,26 +325,29 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     const int lev = static_cast<int>(lv & 0xff);
     const double J2x = rp->J2[0], J2y = rp->J2[1], J2z = rp->J2[2];
     // ---- own nodes A, B: formed stage state (stepper.cpp:60-72) -------------
-    const size_t gA = (static_cast<size_t>(cell) * N + lane) * V, gB = gA + 32 * V;
+    // device layout (sidx): variable v of node n at cbase + v N + n, so each
+    // load below is one coalesced 256-byte warp access
+    const size_t cbase = static_cast<size_t>(cell) * N * V;
+    const size_t gA = cbase + lane, gB = gA + 32;
     double uA[V], uB[V];
     if (!a.form) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        uA[v] = __ldg(a.U + gA + v);
-        uB[v] = __ldg(a.U + gB + v);
+        uA[v] = __ldg(a.U + gA + v * N);
+        uB[v] = __ldg(a.U + gB + v * N);
       }
     } else if (a.formed[lev]) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        uA[v] = __ldg(a.Us + gA + v);
-        uB[v] = __ldg(a.Us + gB + v);
+        uA[v] = __ldg(a.Us + gA + v * N);
+        uB[v] = __ldg(a.Us + gB + v * N);
       }
     } else {
       const double a1 = dt * a.a1[lev];
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        uA[v] = fma(a1, __ldg(a.K1 + gA + v), __ldg(a.U + gA + v));
-        uB[v] = fma(a1, __ldg(a.K1 + gB + v), __ldg(a.U + gB + v));
+        uA[v] = fma(a1, __ldg(a.K1 + gA + v * N), __ldg(a.U + gA + v * N));
+        uB[v] = fma(a1, __ldg(a.K1 + gB + v * N), __ldg(a.U + gB + v * N));
       }
     }
     // ---- neighbour face traces -> the warp's face slots (cp.async), one
@@ -358,18 +361,17 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
         for (int v = 0; v < V; ++v) cp_async8(dst + v, g + v);
       } else {
-        const size_t gi = (static_cast<size_t>(nbc) * N + w3_face_node(d, 1 - side, pt)) * V;
+        const size_t gi = static_cast<size_t>(nbc) * N * V + w3_face_node(d, 1 - side, pt);
         const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
         if (!a.form) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) cp_async8(dst + v, a.U + gi + v);
+          for (int v = 0; v < V; ++v) cp_async8(dst + v, a.U + gi + v * N);
         } else if (a.formed[l2]) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) cp_async8(dst + v, a.Us + gi + v);
+          for (int v = 0; v < V; ++v) cp_async8(dst + v, a.Us + gi + v * N);
         }  // else: formed from U and K1 in the surface phase (first active stage only)
       }
     }
-    const size_t cbase = static_cast<size_t>(cell) * N * V;
     cp_async_commit();
     fetch_rec(rb ^ 1, ncell);  // the next cell's descriptor
     // ---- primitives of A and B -> the warp's slice -------------------------
@@ -443,10 +445,11 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         if (a.formed[l2]) {
           w3_slot_load(slotp, un);
         } else {
-          const size_t gi = (static_cast<size_t>(nbc) * N + w3_face_node(d, 1 - side, pt)) * V;
+          const size_t gi = static_cast<size_t>(nbc) * N * V + w3_face_node(d, 1 - side, pt);
           const double b1 = dt * a.a1[l2];
 #pragma unroll
-          for (int v = 0; v < V; ++v) un[v] = fma(b1, __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
+          for (int v = 0; v < V; ++v)
+            un[v] = fma(b1, __ldg(a.K1 + gi + v * N), __ldg(a.U + gi + v * N));
         }
       } else {
         w3_slot_load(slotp, un);
@@ -539,28 +542,28 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double* K = h ? KB : KA;
-        const int o = (lane + 32 * h) * V;
+        const int o = lane + 32 * h;  // variable v of this node at o + v N (device layout)
         if (a.write_k) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) ek[o + v] = K[v];
+          for (int v = 0; v < V; ++v) ek[o + v * N] = K[v];
         }
         if (a.write_next) {
           double x[V];
           if (a.form) {
 #pragma unroll
-            for (int v = 0; v < V; ++v) x[v] = eu[o + v] + fma(an, ek[o + v], pn * K[v]);
+            for (int v = 0; v < V; ++v) x[v] = eu[o + v * N] + fma(an, ek[o + v * N], pn * K[v]);
           } else {
 #pragma unroll
-            for (int v = 0; v < V; ++v) x[v] = fma(an, K[v], eu[o + v]);
+            for (int v = 0; v < V; ++v) x[v] = fma(an, K[v], eu[o + v * N]);
           }
 #pragma unroll
-          for (int v = 0; v < V; ++v) eu[o + v] = x[v];
+          for (int v = 0; v < V; ++v) eu[o + v * N] = x[v];
         }
         if (a.d_mode) {
 #pragma unroll
           for (int v = 0; v < V; ++v) {
-            const double x = a.d_mode == 2 ? fma(a.b, K[v], ed[o + v]) : a.b * K[v];
-            ed[o + v] = x;
+            const double x = a.d_mode == 2 ? fma(a.b, K[v], ed[o + v * N]) : a.b * K[v];
+            ed[o + v * N] = x;
             const unsigned long long bits =
                 static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7fffffffffffffffULL;
             if (a.want_dmax) dmax_bits = bits > dmax_bits ? bits : dmax_bits;
@@ -580,8 +583,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     if (a.write_k) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        a.Kout[gA + v] = KA[v];
-        a.Kout[gB + v] = KB[v];
+        a.Kout[gA + v * N] = KA[v];
+        a.Kout[gB + v * N] = KB[v];
       }
     }
     // U_{i+1} and d node by node, each batch with all its loads issued before
@@ -590,35 +593,32 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const double* K = h ? KB : KA;
-      const int o = (lane + 32 * h) * V;
-      const size_t g = h ? gB : gA;
+      const size_t g = h ? gB : gA;  // variable v at g + v N (coalesced)
       double x[V], y[V];
       if (a.write_next) {
-        const double* Up = a.U + cbase;
-        const double* Kp = a.K1 + cbase;
 #pragma unroll
-        for (int v = 0; v < V; ++v) x[v] = Up[o + v];
+        for (int v = 0; v < V; ++v) x[v] = a.U[g + v * N];
         if (a.form) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) y[v] = Kp[o + v];
+          for (int v = 0; v < V; ++v) y[v] = a.K1[g + v * N];
 #pragma unroll
-          for (int v = 0; v < V; ++v) a.Usn[g + v] = x[v] + fma(an, y[v], pn * K[v]);
+          for (int v = 0; v < V; ++v) a.Usn[g + v * N] = x[v] + fma(an, y[v], pn * K[v]);
         } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v) a.Usn[g + v] = fma(an, K[v], x[v]);
+          for (int v = 0; v < V; ++v) a.Usn[g + v * N] = fma(an, K[v], x[v]);
         }
       }
       if (a.d_mode) {
         if (a.d_mode == 2) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], a.d[g + v]);
+          for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], a.d[g + v * N]);
         } else {
 #pragma unroll
           for (int v = 0; v < V; ++v) x[v] = a.b * K[v];
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          a.d[g + v] = x[v];
+          a.d[g + v * N] = x[v];
           const unsigned long long bits =
               static_cast<unsigned long long>(__double_as_longlong(x[v])) & 0x7fffffffffffffffULL;
           if (a.want_dmax) dmax_bits = bits > dmax_bits ? bits : dmax_bits;

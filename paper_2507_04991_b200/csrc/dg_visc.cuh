@@ -84,13 +84,14 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
     const int cell = s_cell[cs];
     if (cell >= 0) {
-      const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
+      const size_t gi = static_cast<size_t>(cell) * NPC * V + l;  // device layout (sidx)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         double u;
-        if (!a.form) u = __ldg(a.U + gi + v);
-        else if (s_cform[cs]) u = __ldg(a.Us + gi + v);
-        else u = fma(s_ca1[cs], __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
+        const size_t g = gi + v * NPC;
+        if (!a.form) u = __ldg(a.U + g);
+        else if (s_cform[cs]) u = __ldg(a.Us + g);
+        else u = fma(s_ca1[cs], __ldg(a.K1 + g), __ldg(a.U + g));
         su[tid * V + v] = u;
       }
     }
@@ -100,13 +101,14 @@ __global__ void __launch_bounds__(128)
       const int d = f >> 1, side = f & 1;
       const int nbc = s_nbc[c2][f];
       const int node = (d == 0 ? N1 * pt : pt) + (side ? 0 : N1 - 1) * (d == 0 ? 1 : N1);
-      const size_t gi = (static_cast<size_t>(nbc) * NPC + node) * V;
+      const size_t gi = static_cast<size_t>(nbc) * NPC * V + node;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         double u;
-        if (!a.form) u = __ldg(a.U + gi + v);
-        else if (s_nform[c2][f]) u = __ldg(a.Us + gi + v);
-        else u = fma(s_na1[c2][f], __ldg(a.K1 + gi + v), __ldg(a.U + gi + v));
+        const size_t g = gi + v * NPC;
+        if (!a.form) u = __ldg(a.U + g);
+        else if (s_nform[c2][f]) u = __ldg(a.Us + g);
+        else u = fma(s_na1[c2][f], __ldg(a.K1 + g), __ldg(a.U + g));
         sn[q * V + v] = u;
       }
     }
@@ -143,20 +145,20 @@ __global__ void __launch_bounds__(128)
         }
       }
     }
-    const size_t gi = (static_cast<size_t>(cell) * NPC + l) * V;
+    const size_t gi = static_cast<size_t>(cell) * NPC * V + l;  // variable v at gi + v NPC
     if (mode == 1) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        out[gi + v] = g[0][v];
-        out[ndofs + gi + v] = g[1][v];
+        out[gi + v * NPC] = g[0][v];
+        out[ndofs + gi + v * NPC] = g[1][v];
       }
     } else {
       double fx[V], fy[V];
       visc_flux2(ph, su + tid * V, g[0], g[1], fx, fy);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        out[gi + v] = fx[v];
-        out[ndofs + gi + v] = fy[v];
+        out[gi + v * NPC] = fx[v];
+        out[ndofs + gi + v * NPC] = fy[v];
       }
     }
   }

@@ -309,6 +309,10 @@ struct perrk_ctx {
   double* Ualt = nullptr;
   double *Ka = nullptr, *Kb = nullptr;  // formed stage states U_i, ping-pong by stage parity
   double *tU = nullptr, *tK = nullptr;  // scratch for host-buffer queries
+  // staging vector of upload / download: the canonical (reference) layout of
+  // a host buffer, transposed on the device to / from the device layout
+  // (dev::sidx, cell-blocked SoA)
+  double* lay = nullptr;
   double* G = nullptr;                   // BR1 viscous fluxes [2][ndofs] (NSF only)
   double *dh[3] = {}, *djac[3] = {}, *dlift[3] = {};
   int8_t* dlevel = nullptr;
@@ -320,6 +324,10 @@ struct perrk_ctx {
   int* dlist_tmp = nullptr;
   double* records = nullptr;
   int records_cap = 0;
+  // pinned host rows the step records stream into, one D2H copy per step as
+  // the step completes (no host synchronisation inside the run)
+  double* rec_host = nullptr;
+  int rec_host_cap = 0;
   double* dnu = nullptr;
   int grid_stage = 1184, grid_flat = 1184;
   // family
@@ -417,12 +425,19 @@ StepState get_state(perrk_ctx* c) {
   return s;
 }
 
+// Host buffers are in the reference's canonical layout (common.hpp:11-13),
+// device state-shaped buffers in the device layout (dev::sidx): the copies
+// go through c->lay and the layout kernel.
 void upload(perrk_ctx* c, double* dst, const double* src) {
-  CK(cudaMemcpyAsync(dst, src, sizeof(double) * c->ndofs, cudaMemcpyHostToDevice, c->stream));
+  if (!c->lay) CK(cudaMalloc(&c->lay, sizeof(double) * c->ndofs));
+  CK(cudaMemcpyAsync(c->lay, src, sizeof(double) * c->ndofs, cudaMemcpyHostToDevice, c->stream));
+  CK(launch_layout(dst, c->lay, c->ncells, c->npc, c->V, 1, c->grid_flat, c->stream));
 }
 
 void download(perrk_ctx* c, double* dst, const double* src) {
-  CK(cudaMemcpyAsync(dst, src, sizeof(double) * c->ndofs, cudaMemcpyDeviceToHost, c->stream));
+  if (!c->lay) CK(cudaMalloc(&c->lay, sizeof(double) * c->ndofs));
+  CK(launch_layout(c->lay, src, c->ncells, c->npc, c->V, 0, c->grid_flat, c->stream));
+  CK(cudaMemcpyAsync(dst, c->lay, sizeof(double) * c->ndofs, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -748,7 +763,7 @@ void alloc_cell_buffers(perrk_ctx* c) {
 
 void free_cell_buffers(perrk_ctx* c) {
   for (double** p : {&c->U, &c->K1, &c->Ka, &c->Kb, &c->d, &c->tU, &c->tK, &c->dnu, &c->G,
-                     &c->ghost, &c->sendbuf, &c->red_all, &c->Ualt}) {
+                     &c->ghost, &c->sendbuf, &c->red_all, &c->Ualt, &c->lay}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -1208,6 +1223,7 @@ int perrk_destroy(perrk_ctx* c) {
   free_cell_buffers(c);
   for (double* p : {c->partials, c->dout, c->records})
     if (p) cudaFree(p);
+  if (c->rec_host) cudaFreeHost(c->rec_host);
   for (int a = 0; a < 3; ++a)
     for (double* p : {c->dh[a], c->djac[a], c->dlift[a]})
       if (p) cudaFree(p);
@@ -1487,7 +1503,7 @@ int perrk_krylov_hessenberg(perrk_ctx* c, const double* base, double t, double e
       }
       double umax = 0.0;
       for (long long i = 0; i < M; ++i) umax = std::max(umax, std::fabs(bsrc[i]));
-      CK(cudaMemcpyAsync(dbase, bsrc, vb, cudaMemcpyHostToDevice, c->stream));
+      upload(c, dbase, bsrc);
       const double h = epsilon * (1.0 + umax);
       std::vector<double> Hh(static_cast<size_t>(m + 1) * m, 0.0), c1(m + 1), c2(m + 1);
       auto norm2 = [&](const double* x) {
@@ -1593,8 +1609,8 @@ int perrk_probe_jacobian(perrk_ctx* c, const double* base, double t, double epsi
       std::vector<int> all(nc);
       for (int p = 0; p < nc; ++p) all[p] = p;
       CK(cudaMemcpyAsync(dall, all.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, c->stream));
-      CK(cudaMemcpyAsync(dbase, base, vb, cudaMemcpyHostToDevice, c->stream));
-      CK(cudaMemcpyAsync(dh, h.data(), vb, cudaMemcpyHostToDevice, c->stream));
+      upload(c, dbase, base);  // both to the device layout; the scatter writes J canonically
+      upload(c, dh, h.data());
       CK(cudaMemcpyAsync(up, dbase, vb, cudaMemcpyDeviceToDevice, c->stream));
       CK(cudaMemcpyAsync(um, dbase, vb, cudaMemcpyDeviceToDevice, c->stream));
       CK(cudaMemsetAsync(dJ, 0, vb * M, c->stream));
@@ -1616,7 +1632,8 @@ int perrk_probe_jacobian(perrk_ctx* c, const double* base, double t, double epsi
           rhs_full_device(c, up, fp, dall);
           rhs_full_device(c, um, fm, dall);
           CK(launch_probe_set(up, um, dbase, dh, dcells, n, stride, l, 0, c->stream));
-          CK(launch_probe_scatter(dJ, fp, fm, dh, downer, M, stride, l, sgrid, c->stream));
+          CK(launch_probe_scatter(dJ, fp, fm, dh, downer, M, stride, l, c->npc, sgrid,
+                                  c->stream));
         }
         CK(cudaStreamSynchronize(c->stream));  // owner / cells host vectors die here
       }
@@ -1646,9 +1663,8 @@ int perrk_br1_gradients(perrk_ctx* c, double t, const double* U, double* grads) 
     a.U = a.K1 = c->tU;
     a.n = static_cast<int>(c->ncells);
     CK(launch_grad(a, c->mesh(), c->ph, c->st, c->G, c->ndofs, 1, c->grid_stage, c->stream));
-    CK(cudaMemcpyAsync(grads, c->G, sizeof(double) * 2 * c->ndofs, cudaMemcpyDeviceToHost,
-                       c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    download(c, grads, c->G);                 // [0][dofs]: d/dx
+    download(c, grads + c->ndofs, c->G + c->ndofs);  // [1][dofs]: d/dy
   });
 }
 
@@ -1829,6 +1845,19 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
         CK(cudaMalloc(&m->records, sizeof(double) * dev::REC_COLS * nsteps));
         m->records_cap = nsteps;
       }
+    if (rec && c->rec_host_cap < nsteps) {
+      if (c->rec_host) cudaFreeHost(c->rec_host);
+      c->rec_host = nullptr;
+      CK(cudaMallocHost(&c->rec_host, sizeof(double) * dev::REC_COLS * nsteps));
+      c->rec_host_cap = nsteps;
+    }
+    // each step's StepRecord row leaves for the host right after the step
+    auto stream_rows = [&](int k0, int n) {
+      if (!rec || n <= 0) return;
+      const size_t off = static_cast<size_t>(k0) * dev::REC_COLS;
+      CK(cudaMemcpyAsync(c->rec_host + off, c->records + off, sizeof(double) * dev::REC_COLS * n,
+                         cudaMemcpyDeviceToHost, c->stream));
+    };
     StepMode mode;
     mode.relax = cfg->relax_enabled != 0;
     mode.cfg = cfg->relax;
@@ -1889,15 +1918,23 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
         gr = &c->graphs.back();
       }
       const int per = mode.fused ? 2 : 1;
-      for (int k = 0; k + per <= nsteps; k += per) {
+      int k = 0;
+      for (; k + per <= nsteps; k += per) {
         CK(cudaGraphLaunch(gr->exec, c->stream));
         c->launches += gr->launches;
+        stream_rows(k, per);
       }
-      if (nsteps % per) enqueue_step(g, mode, want_h);
+      if (nsteps % per) {
+        enqueue_step(g, mode, want_h);
+        stream_rows(k, 1);
+      }
     } else {
-      for (int k = 0; k < nsteps; ++k) enqueue_step(g, mode, want_h);
+      for (int k = 0; k < nsteps; ++k) {
+        enqueue_step(g, mode, want_h);
+        stream_rows(k, 1);
+      }
     }
-    const StepState r = get_state(c);
+    const StepState r = get_state(c);  // synchronizes: the streamed rows are on the host
     if (mode.fused) {  // the state of the last step taken (a stopped step writes nothing)
       const bool odd = (r.steps_taken & 1) != 0;
       c->U = odd ? U_second : U_first;
@@ -1911,10 +1948,8 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
     for (perrk_ctx* m : g.members)
       m->evals += evals_per_step(m) * static_cast<uint64_t>(r.steps_taken + (r.aborted ? 1 : 0));
     if (rec && r.steps_taken > 0) {
-      std::vector<double> raw(static_cast<size_t>(dev::REC_COLS) * r.steps_taken);
-      CK(cudaMemcpy(raw.data(), c->records, sizeof(double) * raw.size(), cudaMemcpyDeviceToHost));
       for (int k = 0; k < r.steps_taken; ++k) {
-        const double* row = &raw[static_cast<size_t>(k) * dev::REC_COLS];
+        const double* row = c->rec_host + static_cast<size_t>(k) * dev::REC_COLS;
         perrk_step_record& o = log[k];
         o.t = row[0];
         o.dt = row[1];

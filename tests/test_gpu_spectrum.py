@@ -156,5 +156,7 @@ def test_krylov_envelope_3d_partial_space():
     rho_dense = np.abs(P.probe_spectrum(semi, U)).max()
     r = [np.abs(P.krylov_spectrum(semi, U, m=m)).max() for m in (60, 200)]
     print({"rho_dense": rho_dense, "ritz_rho_m60": r[0], "ritz_rho_m200": r[1]})
-    assert abs(r[1] - rho_dense) < 0.05 * rho_dense
-    assert abs(r[1] - rho_dense) <= abs(r[0] - rho_dense) + 1e-9 * rho_dense
+    # measured: 1.5e-7 (m = 60) and 2.8e-7 (m = 200) relative, the
+    # central-difference noise of the two probes
+    for x in r:
+        assert abs(x - rho_dense) < 1e-5 * rho_dense
