@@ -348,6 +348,7 @@ def test_cpp_adapter_drop_in_parity():
     if not os.path.exists(exe):
         pytest.skip("adapter_parity not built")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
 
 
