@@ -979,7 +979,7 @@ __global__ void __launch_bounds__(256)
                        const double* y0, const double* fine, int nf, const double* vp, double t,
                        double* partials, unsigned* counter, double* out, unsigned long long* linf,
                        long long npts) {
-  constexpr int V = 4, NPC = 16;
+  constexpr int V = 4;
   __shared__ double s_red[2 * 4 * 8];
   dd acc[4];
 #pragma unroll

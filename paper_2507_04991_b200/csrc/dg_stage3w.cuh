@@ -44,6 +44,10 @@ namespace dev {
 #define PERRK_W3_WPB 8  // warps (cells in flight) per block
 #endif
 
+#ifndef PERRK_W3_EPI
+#define PERRK_W3_EPI 1  // 1: the epilogue's U / K1 blocks arrive by bulk copies issued at cell start
+#endif
+
 struct W3 {
   static constexpr int V = 5, NPC = 64, FP = 16, WPB = PERRK_W3_WPB, T = 32 * WPB;
   // Shared-memory layouts chosen so that every warp access of the kernel is
@@ -62,8 +66,14 @@ struct W3 {
   static constexpr int SM_PR = NPR * NPC;
   static constexpr int FS = 5;
   static constexpr int SM_FS = (96 + 4 * 5) * FS;
-  static constexpr int SM_WARP = SM_PR + SM_FS;
-  static_assert(SM_WARP >= 3 * NPC * V, "the epilogue stages U, K1 and d in the slice");
+  // PERRK_W3_EPI: a dedicated [U | K1] epilogue block pair after the slice,
+  // filled by two bulk copies at the start of the cell (their latency hides
+  // behind the cell's whole volume and surface phases); d (b-stages only)
+  // still comes through the dead slice
+  static constexpr int SM_EP = PERRK_W3_EPI ? 2 * NPC * V : 0;
+  static constexpr int SM_WARP = SM_PR + SM_FS + SM_EP;
+  static_assert(SM_PR + SM_FS >= (PERRK_W3_EPI ? 1 : 3) * NPC * V,
+                "the epilogue stages its blocks in the slice");
   static_assert(SM_WARP % 2 == 0, "16-byte aligned slices");
   static constexpr int SM_TOTAL = WPB * SM_WARP;  // doubles per block
 };
@@ -162,6 +172,44 @@ __device__ __forceinline__ void bulk_wait_read() {
 
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// per-warp mbarrier of the epilogue blocks (PERRK_W3_EPI): lane 0 arms it
+// with the byte count and issues the bulk loads, which complete the
+// transaction; the lanes wait on the phase parity before reading
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(double* sdst, const double* gsrc, unsigned bytes,
+                                          unsigned long long* bar) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(d), "l"(gsrc), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W3_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W3_WAIT;\n"
+      "}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
 }
 
 // one cell's contiguous block of a state array (64 V doubles) into the warp's slice
@@ -276,10 +324,19 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   extern __shared__ double smem[];
   __shared__ double s_red[2 * 2 * S::WPB];
   __shared__ CellRec s_rec[S::WPB][2];  // descriptors, prefetched one cell ahead
+#if PERRK_W3_EPI
+  __shared__ unsigned long long s_mbar[S::WPB];
+#endif
   if (st->aborted || st->finished) return;  // uniform across the grid
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* pr = smem + wib * S::SM_WARP;  // [4][64] double2, swizzled (w3_sw)
   double* fs = pr + S::SM_PR;            // face slots (w3_fs): staged traces, then surface terms
+#if PERRK_W3_EPI
+  double* ep = fs + S::SM_FS;            // epilogue blocks [U | K1] (device layout)
+  unsigned ep_phase = 0;
+  if (lane == 0) mbar_init(&s_mbar[wib]);
+  __syncwarp();
+#endif
   // descriptor of one cell into the warp's buffer b (lanes 0-5, 16 B each)
   auto fetch_rec = [&](int b, int c) {
     if (c >= 0 && lane < static_cast<int>(sizeof(CellRec) / 16))
@@ -328,6 +385,15 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     // device layout (sidx): variable v of node n at cbase + v N + n, so each
     // load below is one coalesced 256-byte warp access
     const size_t cbase = static_cast<size_t>(cell) * N * V;
+#if PERRK_W3_EPI
+    // the epilogue's U (and K1) blocks, in flight for the whole cell
+    if (a.write_next && lane == 0) {
+      constexpr unsigned kBytes = N * V * sizeof(double);
+      mbar_expect_tx(&s_mbar[wib], a.form ? 2 * kBytes : kBytes);
+      bulk_load(ep, a.U + cbase, kBytes, &s_mbar[wib]);
+      if (a.form) bulk_load(ep + N * V, a.K1 + cbase, kBytes, &s_mbar[wib]);
+    }
+#endif
     const size_t gA = cbase + lane, gB = gA + 32;
     double uA[V], uB[V];
     if (!a.form) {
@@ -529,6 +595,22 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     // 40-byte-stride LDG.64 / STG.64 touches 10 lines per instruction.
     //   slice: U [0, 64V) | K1 or K_0 [64V, 128V) | d [128V, 192V)
     {
+#if PERRK_W3_EPI
+      double* eu = ep;
+      double* ek = ep + N * V;
+      double* ed = pr;
+      __syncwarp();  // every lane is done with the primitives and face slots
+      if (a.d_mode == 2) {
+        w3_stage_cell(ed, a.d + cbase, lane);
+        cp_async_commit();
+        cp_async_wait<0>();
+      }
+      if (a.write_next) {
+        mbar_wait(&s_mbar[wib], ep_phase);
+        ep_phase ^= 1u;
+      }
+      __syncwarp();
+#else
       double* eu = pr;
       double* ek = pr + N * V;
       double* ed = pr + 2 * N * V;
@@ -539,6 +621,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       cp_async_commit();
       cp_async_wait<0>();
       __syncwarp();
+#endif
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double* K = h ? KB : KA;
