@@ -9,7 +9,8 @@ workload without one importing the other.  Nothing here loads a native
 library.
 
   C1  uniform 16^2 on [-10,10]^2, vortex I=5 (p_inf = 1), EC + Rusanov,
-      p2 S=4 E={4} with (a21, a32) = (0.2, 0.35), CFL 0.9, 100 steps
+      p2 S=4 E={4} with (a21, a32) = (0.204, 0.42) (linearly stable at CFL 0.9
+      on the probed spectrum, configs/c1_pair_scan.py), CFL 0.9, 100 steps
   C2  64^2 "+"-refined mesh (16 h | 32 h/2 | 16 h per axis, h = 20/48),
       EC + HLLE, p3 {4,7}, 500 steps
   C3  256^2 three-level "+" mesh on [0,2pi]^2, seeded random Fourier state,

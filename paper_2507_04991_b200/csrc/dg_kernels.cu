@@ -316,6 +316,13 @@ __device__ void relax_update(StepState* st, dd A, dd B) {
   st->iters = it;
 }
 
+#ifndef PERRK_RELAX_DIRECT
+// 1: the relaxation / update kernels read U and d with direct coalesced loads
+// (one 256-byte warp access per variable in the device layout); 0: the
+// blocks are staged through shared memory by cp.async first
+#define PERRK_RELAX_DIRECT 1
+#endif
+
 // One warp's 32-node block k of two state arrays (U and d) into shared
 // memory by coalesced 16-byte cp.async, one commit group per call (empty past
 // the end).  In the device layout (sidx) a block's variable v is 32 (3D) or
@@ -328,17 +335,47 @@ __device__ __forceinline__ void stage_pair(const double* A, const double* B, lon
   constexpr int V = DIM + 2;
   if (k < nblk) {
     const long long n0 = k * 32;
+    // this lane's piece p (nodes n0 + 2p, n0 + 2p + 1: one cell, NPC is even)
+    // of variables v = (lane >> 4) + 2 r
+    const int p = lane & 15;
+    const long long n = n0 + 2 * p;
+    if (n < nnodes) {
+      const long long g = sidx_n<DIM>(n, lane >> 4);  // + 2 r NPC per round
 #pragma unroll
-    for (int q = lane; q < V * 16; q += 32) {
-      const int v = q >> 4, p = q & 15;
-      const long long n = n0 + 2 * p;  // nodes n, n + 1: same cell (NPC is even)
-      if (n < nnodes) {
-        cp_async16(sa + v * 32 + 2 * p, A + sidx_n<DIM>(n, v));
-        cp_async16(sb + v * 32 + 2 * p, B + sidx_n<DIM>(n, v));
+      for (int r = 0; r < (V + 1) / 2; ++r) {
+        const int v = (lane >> 4) + 2 * r;
+        if (v < V) {
+          cp_async16(sa + v * 32 + 2 * p, A + g + 2 * r * Geo<DIM>::NPC);
+          cp_async16(sb + v * 32 + 2 * p, B + g + 2 * r * Geo<DIM>::NPC);
+        }
       }
     }
   }
   cp_async_commit();
+}
+
+// node n's U and d: from the warp's staged block, or straight from global
+// memory (PERRK_RELAX_DIRECT: coalesced in the device layout)
+template <int DIM>
+__device__ __forceinline__ void load_pair(const double* __restrict__ A,
+                                          const double* __restrict__ B, long long n,
+                                          const double* sa, const double* sb, int lane,
+                                          double* ua, double* ub) {
+  constexpr int V = DIM + 2;
+  if (PERRK_RELAX_DIRECT) {
+    const long long g = sidx_n<DIM>(n, 0);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      ua[v] = __ldg(A + g + v * Geo<DIM>::NPC);
+      ub[v] = __ldg(B + g + v * Geo<DIM>::NPC);
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      ua[v] = sa[32 * v + lane];
+      ub[v] = sb[32 * v + lane];
+    }
+  }
 }
 
 // One relaxation pass.  Each warp walks blocks of 32 consecutive nodes: the
@@ -348,7 +385,7 @@ __device__ __forceinline__ void stage_pair(const double* A, const double* B, lon
 // free).  The previous layout (a thread's own node straight from global
 // memory, stride V doubles) cost 5x the L1 wavefronts per byte.
 template <int DIM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     relax_pass_kernel(const double* __restrict__ U, const double* __restrict__ d, MeshDev m,
                       Phys ph, StepState* st, double* partials, unsigned* counter, long long nnodes) {
   constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC, BLK = 32 * V;  // doubles per block and array
@@ -377,7 +414,8 @@ __global__ void __launch_bounds__(256)
   const long long nblk = (nnodes + 31) / 32;
   const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   auto stage = [&](long long k, int b) {
-    stage_pair<DIM>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
+    if (!PERRK_RELAX_DIRECT)
+      stage_pair<DIM>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
   };
   ksum A = ks_zero(), B = ks_zero();
   long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
@@ -385,20 +423,14 @@ __global__ void __launch_bounds__(256)
   stage(k, 0);
   for (; k < nblk; k += stride, b ^= 1) {
     stage(k + stride, b ^ 1);
-    cp_async_wait<1>();
+    if (!PERRK_RELAX_DIRECT) cp_async_wait<1>();
     __syncwarp();
     const long long n = k * 32 + lane;
     if (n < nnodes) {
       const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
       const double om = node_measure_rec<DIM>(m, cell, l);
-      const double* su = s_stage[wib][b][0] + lane;
-      const double* sd = s_stage[wib][b][1] + lane;
       double u[V], dv[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        u[v] = su[32 * v];
-        dv[v] = sd[32 * v];
-      }
+      load_pair<DIM>(U, d, n, s_stage[wib][b][0], s_stage[wib][b][1], lane, u, dv);
       if (numerics == 1) {
         double du[V], ra, rb;
         // rounded products (never contracted into later sums): the same bits
@@ -520,7 +552,7 @@ __device__ void finish_step(StepState* st, double gamma, const dd* tot, int V, i
 // coalesced cp.async, launched on relax_pass_kernel's grid), so the StepRecord
 // sums come out bitwise the same as relax_spec_kernel's.
 template <int DIM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     update_kernel(double* Uout, const double* Uin, const double* __restrict__ d, MeshDev m,
                   Phys ph, StepState* st, double* partials, unsigned* counter, long long nnodes,
                   int want_nu, int want_record, double* records) {
@@ -539,22 +571,25 @@ __global__ void __launch_bounds__(256)
   for (int r = 0; r < 6; ++r) acc[r] = ks_zero();
   long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
   int b = 0;
-  stage_pair<DIM>(Uin, d, nnodes, nblk, k, s_stage[wib][0][0], s_stage[wib][0][1], lane);
+  if (!PERRK_RELAX_DIRECT)
+    stage_pair<DIM>(Uin, d, nnodes, nblk, k, s_stage[wib][0][0], s_stage[wib][0][1], lane);
   for (; k < nblk; k += stride, b ^= 1) {
-    stage_pair<DIM>(Uin, d, nnodes, nblk, k + stride, s_stage[wib][b ^ 1][0],
-                    s_stage[wib][b ^ 1][1], lane);
-    cp_async_wait<1>();
+    if (!PERRK_RELAX_DIRECT) {
+      stage_pair<DIM>(Uin, d, nnodes, nblk, k + stride, s_stage[wib][b ^ 1][0],
+                      s_stage[wib][b ^ 1][1], lane);
+      cp_async_wait<1>();
+    }
     __syncwarp();
     const long long n = k * 32 + lane;
     if (n < nnodes) {
-      double u0[V], u[V], du[V];
+      double u0[V], u[V], du[V], dv[V];
+      const long long gb = sidx_n<DIM>(n, 0);
+      load_pair<DIM>(Uin, d, n, s_stage[wib][b][0], s_stage[wib][b][1], lane, u0, dv);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        u0[v] = s_stage[wib][b][0][32 * v + lane];
-        const double dv = s_stage[wib][b][1][32 * v + lane];
-        u[v] = fma(scale, dv, u0[v]);
-        du[v] = __dmul_rn(scale, dv);
-        Uout[sidx_n<DIM>(n, v)] = u[v];
+        u[v] = fma(scale, dv[v], u0[v]);
+        du[v] = __dmul_rn(scale, dv[v]);
+        Uout[gb + v * Geo<DIM>::NPC] = u[v];
       }
       const double s_new = want_record ? trial_entropy(ph, trial_state<DIM>(ph, u0, du)) : 0.0;
       if (want_nu || want_record)
@@ -615,11 +650,12 @@ __global__ void __launch_bounds__(256, 3)
   const long long nblk = (nnodes + 31) / 32;
   const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   auto stage = [&](long long k, int b) {
-    stage_pair<DIM>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
+    if (!PERRK_RELAX_DIRECT)
+      stage_pair<DIM>(U, d, nnodes, nblk, k, s_stage[wib][b][0], s_stage[wib][b][1], lane);
   };
   ksum acc[2];  // A, B in registers; the update's six record sums in shared memory
   acc[0] = acc[1] = ks_zero();
-  ksum* s_acc = reinterpret_cast<ksum*>(spec_smem + 8 * 2 * 2 * BLK);  // [6][blockDim]
+  ksum* s_acc = reinterpret_cast<ksum*>(spec_smem + (PERRK_RELAX_DIRECT ? 0 : 8 * 2 * 2 * BLK));
   const KsShared racc{s_acc + threadIdx.x, static_cast<int>(blockDim.x)};
 #pragma unroll
   for (int r = 0; r < 6; ++r) racc[r] = ks_zero();
@@ -629,15 +665,15 @@ __global__ void __launch_bounds__(256, 3)
   stage(k, 0);
   for (; k < nblk; k += stride, b ^= 1) {
     stage(k + stride, b ^ 1);
-    cp_async_wait<1>();
+    if (!PERRK_RELAX_DIRECT) cp_async_wait<1>();
     __syncwarp();
     const long long n = k * 32 + lane;
     if (n < nnodes) {
       double u[V], dv[V], du[V], T[V], ra, rb;
+      const long long gb = sidx_n<DIM>(n, 0);
+      load_pair<DIM>(U, d, n, s_stage[wib][b][0], s_stage[wib][b][1], lane, u, dv);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        u[v] = s_stage[wib][b][0][32 * v + lane];
-        dv[v] = s_stage[wib][b][1][32 * v + lane];
         du[v] = __dmul_rn(gdt, dv[v]);
         T[v] = fma(gdt, dv[v], u[v]);  // update_kernel's U + (gamma dt) d
       }
@@ -648,7 +684,7 @@ __global__ void __launch_bounds__(256, 3)
       ks_add_prod(acc[0], om, ra);
       ks_add_prod(acc[1], om, rb);
 #pragma unroll
-      for (int v = 0; v < V; ++v) Uout[sidx_n<DIM>(n, v)] = T[v];
+      for (int v = 0; v < V; ++v) Uout[gb + v * Geo<DIM>::NPC] = T[v];
       if (want_nu || want_record)
         update_node_terms<DIM>(m, ph, T, n, want_nu, want_record, trial_entropy(ph, tr), numax,
                                racc);
@@ -1275,8 +1311,9 @@ cudaError_t launch_update(int dim, double* Uout, const double* Uin, const double
 }
 
 template <int DIM>
-static size_t spec_smem_bytes() {
-  return sizeof(double) * 8 * 2 * 2 * 32 * (DIM + 2) + sizeof(ksum) * 6 * 256;
+static size_t spec_smem_bytes() {  // [staging] + the six [256] record sums
+  return (PERRK_RELAX_DIRECT ? 0 : sizeof(double) * 8 * 2 * 2 * 32 * (DIM + 2)) +
+         sizeof(ksum) * 6 * 256;
 }
 
 template <int DIM>

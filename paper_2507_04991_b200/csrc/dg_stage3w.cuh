@@ -45,7 +45,7 @@ namespace dev {
 #endif
 
 #ifndef PERRK_W3_EPI
-#define PERRK_W3_EPI 1  // 1: the epilogue's U / K1 blocks arrive by bulk copies issued at cell start
+#define PERRK_W3_EPI 0  // 1: the epilogue's U / K1 blocks arrive by bulk copies issued at cell start
 #endif
 
 struct W3 {

@@ -97,7 +97,10 @@ def load_config_family(name):
 
 
 def c1_family():
-    return P.build_perk2(4, [4], [[0.2, 0.35]])
+    """C1's p2 S = 4 member: (a21, a32) = (0.204, 0.42), linearly stable at
+    CFL 0.9 on C1's probed spectrum (max |P| = 1.000000, 1.000003 at 5% above;
+    configs/c1_pair_scan.py).  The survey's (0.2, 0.35) reached 1.60."""
+    return P.build_perk2(4, [4], [[0.204, 0.42]])
 
 
 def _mesh(ms):

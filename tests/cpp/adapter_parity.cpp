@@ -38,7 +38,7 @@ int main() {
   StateVector U0 = ref.project([&](double x, double y, double* u) {
     isentropic_vortex_state(vp, x, y, 0.0, u);
   });
-  const PartitionFamily fam = build_perk2(4, {4}, {{0.2, 0.35}});
+  const PartitionFamily fam = build_perk2(4, {4}, {{0.204, 0.42}});  // C1's family
   const PartitionMap map = make_partition_map(spec.mesh, std::vector<int>(mesh.num_cells(), 1), 1);
   RelaxationConfig rc;
   PerkStepOptions opts;

@@ -35,9 +35,9 @@ def test_spec_matches_product(name):
 
 
 def test_c1_family_fixture_is_build_perk2():
-    """configs/c1_p2_4.family is build_perk2(4, {4}, {{0.2, 0.35}}) (butcher.cpp:24-105)."""
+    """configs/c1_p2_4.family is build_perk2(4, {4}, {{0.204, 0.42}}) (butcher.cpp:24-105)."""
     ft = CR.S.make_spec("c1").family()
-    fam = P.build_perk2(4, [4], [[0.2, 0.35]])
+    fam = P.build_perk2(4, [4], [[0.204, 0.42]])
     assert np.array_equal(ft.A, fam.A) and np.array_equal(ft.b, fam.b)
     assert np.array_equal(ft.c, fam.c)
 
