@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libperrk_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["dg_kernels.cu", "host.cpp"]
-DEPS = SOURCES + ["dg_device.cuh", "dg_launch.hpp", "dg_stage.cuh", "dg_stage3w.cuh", "dg_visc.cuh", "dg_advection.cuh", "dg_krylov.cuh"]
+DEPS = SOURCES + ["dg_device.cuh", "dg_launch.hpp", "dg_stage.cuh", "dg_stage3w.cuh", "dg_stage2w.cuh", "dg_visc.cuh", "dg_advection.cuh", "dg_krylov.cuh"]
 
 
 def _stale():

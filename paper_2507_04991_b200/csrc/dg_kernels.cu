@@ -80,6 +80,7 @@ __device__ __forceinline__ void report_bad(StepState* st, int stage, long long n
 
 #include "dg_stage.cuh"
 #include "dg_stage3w.cuh"
+#include "dg_stage2w.cuh"
 #include "dg_visc.cuh"
 #include "dg_advection.cuh"
 #include "dg_krylov.cuh"
@@ -1164,12 +1165,13 @@ static bool use_w3(int dim, int surf, int vol, bool visc) {
 #endif
 }
 
-template <int SURF>
+template <int SURF, int FORM = -1, int NEXT = -1, int DM = -1>
 static void configure_w3() {
   static bool configured[MAX_DEVICES] = {};
   const int dev = current_device();
   if (!configured[dev]) {
-    cudaFuncSetAttribute(stage3w_kernel<SURF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(stage3w_kernel<SURF, FORM, NEXT, DM>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(double) * W3::SM_TOTAL));
     configured[dev] = true;
   }
@@ -1184,20 +1186,88 @@ static int w3_occ() {
   return n;
 }
 
+template <int SURF, int FORM = -1, int NEXT = -1, int DM = -1>
+static cudaError_t launch_w3_k(const StageArgs& a, const MeshDev& m, const Phys& ph,
+                               StepState* st, double* partials, unsigned* counter, int g,
+                               cudaStream_t s) {
+  configure_w3<SURF, FORM, NEXT, DM>();
+  stage3w_kernel<SURF, FORM, NEXT, DM><<<g, W3::T, sizeof(double) * W3::SM_TOTAL, s>>>(
+      a, m, ph, st, partials, counter);
+  return cudaGetLastError();
+}
+
+#ifndef PERRK_W3_SPECIALIZE
+#define PERRK_W3_SPECIALIZE 1  // compile-time stage kinds (stage3w_kernel FORM / NEXT / DM)
+#endif
+
 template <int SURF>
 static cudaError_t launch_w3(const StageArgs& a, const MeshDev& m, const Phys& ph, StepState* st,
                              double* partials, unsigned* counter, int grid, cudaStream_t s) {
-  configure_w3<SURF>();
   const int blocks = (a.n + W3::WPB - 1) / W3::WPB;
   const int g = blocks < grid ? blocks : grid;
   if (g <= 0) return cudaSuccess;
-  stage3w_kernel<SURF><<<g, W3::T, sizeof(double) * W3::SM_TOTAL, s>>>(a, m, ph, st, partials,
+  if constexpr (PERRK_W3_SPECIALIZE && SURF == 2) {
+    // the stage kinds of the p4 families: stage 0, interior stages, the first
+    // and the last b-stage (host.cpp build_plan)
+    const int key = a.form * 100 + a.write_next * 10 + a.d_mode;
+    switch (key) {
+      case 10: return launch_w3_k<SURF, 0, 1, 0>(a, m, ph, st, partials, counter, g, s);
+      case 110: return launch_w3_k<SURF, 1, 1, 0>(a, m, ph, st, partials, counter, g, s);
+      case 111: return launch_w3_k<SURF, 1, 1, 1>(a, m, ph, st, partials, counter, g, s);
+      case 102: return launch_w3_k<SURF, 1, 0, 2>(a, m, ph, st, partials, counter, g, s);
+      default: break;
+    }
+  }
+  return launch_w3_k<SURF>(a, m, ph, st, partials, counter, g, s);
+}
+
+// 2D EC volume with the Rusanov or central surface flux: the warp-per-four-
+// cells kernel (dg_stage2w.cuh)
+static bool use_w2(int dim, int surf, int vol, bool visc) {
+#if defined(PERRK_NO_W2)
+  (void)dim; (void)surf; (void)vol; (void)visc;
+  return false;
+#else
+  return dim == 2 && vol == VOL_EC && !visc && (surf == 0 || surf == 2);
+#endif
+}
+
+template <int SURF>
+static void configure_w2() {
+  static bool configured[MAX_DEVICES] = {};
+  const int dev = current_device();
+  if (!configured[dev]) {
+    cudaFuncSetAttribute(stage2w_kernel<SURF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(double) * W2::SM_TOTAL));
+    configured[dev] = true;
+  }
+}
+
+template <int SURF>
+static int w2_occ() {
+  configure_w2<SURF>();
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, stage2w_kernel<SURF>, W2::T,
+                                                sizeof(double) * W2::SM_TOTAL);
+  return n;
+}
+
+template <int SURF>
+static cudaError_t launch_w2(const StageArgs& a, const MeshDev& m, const Phys& ph, StepState* st,
+                             double* partials, unsigned* counter, int grid, cudaStream_t s) {
+  configure_w2<SURF>();
+  const int warps = (a.n + W2::CPW - 1) / W2::CPW;
+  const int blocks = (warps + W2::WPB - 1) / W2::WPB;
+  const int g = blocks < grid ? blocks : grid;
+  if (g <= 0) return cudaSuccess;
+  stage2w_kernel<SURF><<<g, W2::T, sizeof(double) * W2::SM_TOTAL, s>>>(a, m, ph, st, partials,
                                                                        counter);
   return cudaGetLastError();
 }
 
 int stage_blocks_per_sm(int dim, int surf, int vol) {
   if (use_w3(dim, surf, vol, false)) return surf == 2 ? w3_occ<2>() : w3_occ<0>();
+  if (use_w2(dim, surf, vol, false)) return surf == 2 ? w2_occ<2>() : w2_occ<0>();
   const bool simple = vol != VOL_EC;
   if (dim == 2) return simple ? stage_occ_d<2, true>(surf) : stage_occ_d<2, false>(surf);
   return simple ? stage_occ_d<3, true>(surf) : stage_occ_d<3, false>(surf);
@@ -1217,6 +1287,9 @@ cudaError_t launch_stage(int dim, int surf, int vol, const StageArgs& a0, const 
   if (use_w3(dim, surf, vol, false))
     return surf == 2 ? launch_w3<2>(a, m, ph, st, partials, counter, grid, s)
                      : launch_w3<0>(a, m, ph, st, partials, counter, grid, s);
+  if (use_w2(dim, surf, vol, false))
+    return surf == 2 ? launch_w2<2>(a, m, ph, st, partials, counter, grid, s)
+                     : launch_w2<0>(a, m, ph, st, partials, counter, grid, s);
   if (vol == VOL_EC)
     return dim == 2 ? launch_stage_d<2, false, false>(surf, a, m, ph, st, partials, counter, grid, s)
                     : launch_stage_d<3, false, false>(surf, a, m, ph, st, partials, counter, grid, s);

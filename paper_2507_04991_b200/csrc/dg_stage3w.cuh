@@ -315,12 +315,18 @@ __device__ __forceinline__ void w3_z(const Phys& ph, const double* pr, int lane,
   }
 }
 
-template <int SURF>
+// FORM / NEXT / DM >= 0 fix a.form, a.write_next and a.d_mode at compile time
+// (the stage kinds every P-ERK step launches: stage 0, interior stages, the
+// b-stages); -1 reads them from the arguments
+template <int SURF, int FORM = -1, int NEXT = -1, int DM = -1>
 __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     stage3w_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* partials,
                    unsigned* counter) {
   using S = W3;
   constexpr int V = S::V, N = S::NPC, FP = S::FP;
+  const bool form_ = FORM >= 0 ? (FORM != 0) : (a.form != 0);
+  const bool next_ = NEXT >= 0 ? (NEXT != 0) : (a.write_next != 0);
+  const int dm_ = DM >= 0 ? DM : a.d_mode;
   extern __shared__ double smem[];
   __shared__ double s_red[2 * 2 * S::WPB];
   __shared__ CellRec s_rec[S::WPB][2];  // descriptors, prefetched one cell ahead
@@ -367,10 +373,10 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     if (lane == 0 && ncell >= 0) {
       constexpr unsigned kBytes = N * V * sizeof(double);
       const size_t off = static_cast<size_t>(ncell) * N * V;
-      if (a.form) l2_prefetch(a.Us + off, kBytes);
-      if (!a.form || a.write_next) l2_prefetch(a.U + off, kBytes);  // stage 0 state / epilogue
-      if (a.write_next && a.form) l2_prefetch(a.K1 + off, kBytes);
-      if (a.d_mode == 2) l2_prefetch(a.d + off, kBytes);
+      if (form_) l2_prefetch(a.Us + off, kBytes);
+      if (!form_ || next_) l2_prefetch(a.U + off, kBytes);  // stage 0 state / epilogue
+      if (next_ && form_) l2_prefetch(a.K1 + off, kBytes);
+      if (dm_ == 2) l2_prefetch(a.d + off, kBytes);
     }
     // ---- descriptor (host.cpp build_cell_records), fetched a cell ago -------
     cp_async_wait<0>();
@@ -387,16 +393,16 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     const size_t cbase = static_cast<size_t>(cell) * N * V;
 #if PERRK_W3_EPI
     // the epilogue's U (and K1) blocks, in flight for the whole cell
-    if (a.write_next && lane == 0) {
+    if (next_ && lane == 0) {
       constexpr unsigned kBytes = N * V * sizeof(double);
-      mbar_expect_tx(&s_mbar[wib], a.form ? 2 * kBytes : kBytes);
+      mbar_expect_tx(&s_mbar[wib], form_ ? 2 * kBytes : kBytes);
       bulk_load(ep, a.U + cbase, kBytes, &s_mbar[wib]);
-      if (a.form) bulk_load(ep + N * V, a.K1 + cbase, kBytes, &s_mbar[wib]);
+      if (form_) bulk_load(ep + N * V, a.K1 + cbase, kBytes, &s_mbar[wib]);
     }
 #endif
     const size_t gA = cbase + lane, gB = gA + 32;
     double uA[V], uB[V];
-    if (!a.form) {
+    if (!form_) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         uA[v] = __ldg(a.U + gA + v * N);
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       } else {
         const size_t gi = static_cast<size_t>(nbc) * N * V + w3_face_node(d, 1 - side, pt);
         const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
-        if (!a.form) {
+        if (!form_) {
 #pragma unroll
           for (int v = 0; v < V; ++v) cp_async8(dst + v, a.U + gi + v * N);
         } else if (a.formed[l2]) {
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       double* slotp = fs + w3_fs(d * 32 + lane);
       const int nbc = rp->nb[2 * d + side];
       double un[V];
-      if (nbc >= 0 && a.form) {
+      if (nbc >= 0 && form_) {
         const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
         if (a.formed[l2]) {
           w3_slot_load(slotp, un);
@@ -600,12 +606,12 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       double* ek = ep + N * V;
       double* ed = pr;
       __syncwarp();  // every lane is done with the primitives and face slots
-      if (a.d_mode == 2) {
+      if (dm_ == 2) {
         w3_stage_cell(ed, a.d + cbase, lane);
         cp_async_commit();
         cp_async_wait<0>();
       }
-      if (a.write_next) {
+      if (next_) {
         mbar_wait(&s_mbar[wib], ep_phase);
         ep_phase ^= 1u;
       }
@@ -615,9 +621,9 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       double* ek = pr + N * V;
       double* ed = pr + 2 * N * V;
       __syncwarp();  // every lane is done with the primitives and face slots
-      if (a.write_next) w3_stage_cell(eu, a.U + cbase, lane);
-      if (a.write_next && a.form) w3_stage_cell(ek, a.K1 + cbase, lane);
-      if (a.d_mode == 2) w3_stage_cell(ed, a.d + cbase, lane);
+      if (next_) w3_stage_cell(eu, a.U + cbase, lane);
+      if (next_ && form_) w3_stage_cell(ek, a.K1 + cbase, lane);
+      if (dm_ == 2) w3_stage_cell(ed, a.d + cbase, lane);
       cp_async_commit();
       cp_async_wait<0>();
       __syncwarp();
@@ -630,9 +636,9 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
           for (int v = 0; v < V; ++v) ek[o + v * N] = K[v];
         }
-        if (a.write_next) {
+        if (next_) {
           double x[V];
-          if (a.form) {
+          if (form_) {
 #pragma unroll
             for (int v = 0; v < V; ++v) x[v] = eu[o + v * N] + fma(an, ek[o + v * N], pn * K[v]);
           } else {
@@ -642,10 +648,10 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
           for (int v = 0; v < V; ++v) eu[o + v * N] = x[v];
         }
-        if (a.d_mode) {
+        if (dm_) {
 #pragma unroll
           for (int v = 0; v < V; ++v) {
-            const double x = a.d_mode == 2 ? fma(a.b, K[v], ed[o + v * N]) : a.b * K[v];
+            const double x = dm_ == 2 ? fma(a.b, K[v], ed[o + v * N]) : a.b * K[v];
             ed[o + v * N] = x;
             const unsigned long long bits =
                 static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7fffffffffffffffULL;
@@ -657,9 +663,9 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       __syncwarp();
       if (lane == 0) {
         constexpr unsigned kBytes = N * V * sizeof(double);
-        if (a.write_next) bulk_store(a.Usn + cbase, eu, kBytes);
+        if (next_) bulk_store(a.Usn + cbase, eu, kBytes);
         if (a.write_k) bulk_store(a.Kout + cbase, ek, kBytes);
-        if (a.d_mode) bulk_store(a.d + cbase, ed, kBytes);
+        if (dm_) bulk_store(a.d + cbase, ed, kBytes);
       }
     }
 #else
@@ -678,10 +684,10 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const double* K = h ? KB : KA;
       const size_t g = h ? gB : gA;  // variable v at g + v N (coalesced)
       double x[V], y[V];
-      if (a.write_next) {
+      if (next_) {
 #pragma unroll
         for (int v = 0; v < V; ++v) x[v] = a.U[g + v * N];
-        if (a.form) {
+        if (form_) {
 #pragma unroll
           for (int v = 0; v < V; ++v) y[v] = a.K1[g + v * N];
 #pragma unroll
@@ -691,8 +697,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
           for (int v = 0; v < V; ++v) a.Usn[g + v * N] = fma(an, K[v], x[v]);
         }
       }
-      if (a.d_mode) {
-        if (a.d_mode == 2) {
+      if (dm_) {
+        if (dm_ == 2) {
 #pragma unroll
           for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], a.d[g + v * N]);
         } else {
