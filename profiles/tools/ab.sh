@@ -6,7 +6,7 @@ R=$1; shift
 for i in $(seq 1 $R); do
   for v in "$@"; do
     cp ab/$v.so $LIB
-    r=$(timeout 300 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.4g %.4f %s' % (d['value'], d['roofline']['ms_per_launch'], d['clocks']['sm_mhz']))" 2>&1)
+    r=$(timeout 300 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline $AB_ARGS 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.4g %.4f %s' % (d['value'], d['roofline']['ms_per_launch'], d['clocks']['sm_mhz']))" 2>&1)
     echo "$v $r"
   done
 done

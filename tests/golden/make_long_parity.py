@@ -16,7 +16,8 @@ Writes, per config:
       seconds  oracle wall time, threads
   baseline/_ref/parity/<cfg>_U.npy   (git-ignored; travels to the GPU box)
       the full final state, for the full-field comparison in
-      tests/long_parity.py
+      tests/long_parity.py (C5's 640 MiB is kept in parity_full/, which the
+      box snapshot leaves out)
 
 The oracle's threading only splits the per-cell volume pass (parallel_cells,
 semidisc.cpp:75-89); faces, stage formation and every reduction are serial

@@ -9,8 +9,9 @@ numerics the configs run with; stepper.cpp:144-188, relax.cpp:51-104) and
 committed as tests/golden/long_<cfg>.npz: the full step log (t, dt, gamma,
 iterations, H, fell_back, invariants, delta_h, compensated H) and the final
 state at a seeded sample of 32768 nodes.  Where the full oracle state is
-present (baseline/_ref/parity/<cfg>_U.npy, written by the same script; it is
-git-ignored), the state metrics are ALSO computed over every node.
+present (baseline/_ref/parity/ or parity_full/<cfg>_U.npy, written by the
+same script; git-ignored), the state metrics are ALSO computed over every
+node.
 
 Metrics (all reported; `gate` lists the north_star ones):
   state_rel[v]      ||U_gpu[:,v] - U_orc[:,v]|| / ||U_orc[:,v]||, literal,
@@ -40,7 +41,10 @@ for p in (ROOT, os.path.join(ROOT, "oracle"), HERE):
         sys.path.insert(0, p)
 
 GOLDEN = os.path.join(HERE, "golden")
-FULL = os.path.join(ROOT, "baseline", "_ref", "parity")
+# full oracle final states: baseline/_ref/parity travels to the GPU box
+# (git-ignored; C2-C4, <= 128 MiB each), parity_full/ stays here (C5's 640 MiB
+# exceeds the box snapshot limit)
+FULL_DIRS = [os.path.join(ROOT, "baseline", "_ref", "parity"), os.path.join(ROOT, "parity_full")]
 TOL_STATE = 1e-11
 TOL_GAMMA = 1e-12
 TOL_DH = 1e-12
@@ -116,8 +120,9 @@ def compare(name, device=0):
         "state_rel_sample": _rel(U[idx], fx["sample"]),
         "state_rel_mom_sample": _rel(U[idx], fx["sample"], mom=True),
     }
-    full = os.path.join(FULL, f"{name}_U.npy")
-    if os.path.exists(full):
+    full = next((p for p in (os.path.join(d, f"{name}_U.npy") for d in FULL_DIRS)
+                 if os.path.exists(p)), None)
+    if full:
         Uo = np.load(full).reshape(-1, V)
         m["state_rel_full"] = _rel(U, Uo)
         m["state_rel_mom_full"] = _rel(U, Uo, mom=True)

@@ -9,7 +9,7 @@ reference with its own relaxation numerics (c1ref).
 Tolerances (written here, as the gate states them):
   state    1e-11 relative L2 per conserved variable (literal per variable),
            on the fixture's 32768-node sample and, where the full oracle state
-           is present (baseline/_ref/parity), over every node
+           is present (baseline/_ref/parity, parity_full), over every node
   gamma    1e-12 absolute, every step
   delta_h  1e-12 absolute, every step (PerkStepResult::delta_h)
   H_n-H_0  1e-12 absolute, every step (compensated sums on both sides)
