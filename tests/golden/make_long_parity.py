@@ -16,8 +16,8 @@ Writes, per config:
       seconds  oracle wall time, threads
   baseline/_ref/parity/<cfg>_U.npy   (git-ignored; travels to the GPU box)
       the full final state, for the full-field comparison in
-      tests/long_parity.py (C5's 640 MiB is kept in parity_full/, which the
-      box snapshot leaves out)
+      tests/long_parity.py (C5's 640 MiB exceeds the GPU box's 512 MiB
+      snapshot limit: C5 is compared on the committed node sample only)
 
 The oracle's threading only splits the per-cell volume pass (parallel_cells,
 semidisc.cpp:75-89); faces, stage formation and every reduction are serial

@@ -368,7 +368,12 @@ def test_bisection_secant_relaxation_vs_reference(method):
                              P.PerkStepOptions(relaxation=rx))
         tr, rr = ref.perk_step(Ur, tr, dt, cfg.family, cfg.partition_map().effective_level, rx)
         assert rg.fell_back == bool(rr.fell_back)
-        assert rg.iterations == rr.iterations
+        # the stop test |r| <= residual_tol (relax.cpp:105-148) sits at the
+        # residual's rounding noise here (|r| ~ 9e-15 against 1e-14), so an
+        # ulp-level difference of the RHS may stop one iteration earlier or
+        # later; the root itself must agree to 1e-12
+        assert abs(rg.iterations - rr.iterations) <= (
+            0 if max(abs(rg.residual), abs(rr.residual)) > 0.5 * rx.residual_tol else 1)
         assert abs(rg.gamma - rr.gamma) < 1e-12
     assert rel_err(Ug, Ur, 4) < 1e-12
 
