@@ -191,7 +191,9 @@ __device__ __forceinline__ void lmeans(double rl, double rr, double bl, double b
 // with sigma = v_l + v_r, t = logmean(rho) sigma_d / 4,
 //   f_rho = 2 t,  f_m,i = t sigma_i + delta_id (p_l + p_r) / 2,
 //   f_E = f_rho (v_l.v_r / 2 + 1 / ((gamma - 1) logmean(beta))) + (p_l v_r,d + p_r v_l,d) / 2
-template <int DIM, bool SMOOTH = false>
+// HP: pl and pr arrive halved (p / 2, as the warp kernels store them), which
+// folds the two 1/2 factors of the pressure terms into the stored value
+template <int DIM, bool SMOOTH = false, bool HP = false>
 __device__ __forceinline__ void ec2(const Phys& ph, int d, double rl, const double (&vl)[DIM],
                                     double pl, double bl, double rr, const double (&vr)[DIM],
                                     double pr, double br, double* f) {
@@ -206,10 +208,11 @@ __device__ __forceinline__ void ec2(const Phys& ph, int d, double rl, const doub
   const double t = lq * pick<DIM>(sg, d);
   const double fr = t + t;
   f[0] = fr;
-  const double pavg = 0.5 * (pl + pr);
+  const double pavg = HP ? pl + pr : 0.5 * (pl + pr);
 #pragma unroll
   for (int i = 0; i < DIM; ++i) f[1 + i] = i == d ? fma(t, sg[i], pavg) : t * sg[i];
-  f[DIM + 1] = fma(fr, fma(0.5, vlvr, ib), 0.5 * fma(pl, pick<DIM>(vr, d), pr * pick<DIM>(vl, d)));
+  const double pv = fma(pl, pick<DIM>(vr, d), pr * pick<DIM>(vl, d));
+  f[DIM + 1] = fma(fr, fma(0.5, vlvr, ib), HP ? pv : 0.5 * pv);
 }
 
 // Roe-average wave speed estimates (physics.cpp:181-203)

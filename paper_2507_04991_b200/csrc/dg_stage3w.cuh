@@ -44,6 +44,10 @@ namespace dev {
 #define PERRK_W3_WPB 8  // warps (cells in flight) per block
 #endif
 
+#ifndef PERRK_W3_HALFP
+#define PERRK_W3_HALFP 1  // 1: the slice holds p / 2 (the EC flux's pressure terms take it as is)
+#endif
+
 #ifndef PERRK_W3_EPI
 #define PERRK_W3_EPI 0  // 1: the epilogue's U / K1 blocks arrive by bulk copies issued at cell start
 #endif
@@ -223,7 +227,7 @@ __device__ __forceinline__ void w3_stage_cell(double* dst, const double* src, in
 template <int D, bool SM>
 __device__ __forceinline__ void w3_ec(const Phys& ph, const double* pr, int p, int q, double* f) {
   const W3Prim L = w3_load(pr, p), R = w3_load(pr, q);
-  ec2<3, SM>(ph, D, L.rho, L.v, L.p, L.beta, R.rho, R.v, R.p, R.beta, f);
+  ec2<3, SM, PERRK_W3_HALFP != 0>(ph, D, L.rho, L.v, L.p, L.beta, R.rho, R.v, R.p, R.beta, f);
 }
 
 // x / y lines (D = 0, 1): the lane's two layers.  Each node evaluates
@@ -362,14 +366,16 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   unsigned long long dmax_bits = 0;
   const int nw = gridDim.x * S::WPB;
   int slot = blockIdx.x * S::WPB + wib;
-  int cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
+  auto cell_at = [&](int sl) { return sl < a.n ? (a.list ? a.list[sl] : sl) : -1; };
+  int cell = cell_at(slot);
+  int ncell = cell_at(slot + nw);  // list entries are read one cell ahead of their use
   int rb = 0;
   fetch_rec(0, cell);
 
   while (cell >= 0) {
-    // next cell: list entry now, its state arrays to L2 (bulk prefetch)
+    // next cell: its state arrays to L2 (bulk prefetch); the one after: list entry
     const int nslot = slot + nw;
-    const int ncell = nslot < a.n ? (a.list ? a.list[nslot] : nslot) : -1;
+    const int nncell = cell_at(nslot + nw);
     if (lane == 0 && ncell >= 0) {
       constexpr unsigned kBytes = N * V * sizeof(double);
       const size_t off = static_cast<size_t>(ncell) * N * V;
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       double2* dst = reinterpret_cast<double2*>(pr) + w3_sw(n);
       dst[0] = make_double2(q.rho, be);
       dst[N] = make_double2(q.v[0], q.v[1]);
-      dst[2 * N] = make_double2(q.v[2], q.p);
+      dst[2 * N] = make_double2(q.v[2], PERRK_W3_HALFP ? 0.5 * q.p : q.p);
       dst[3 * N] = make_double2(q.E, SURF == 2 ? fsqrt(ph.gamma * q.p * ir) : 0.0);
       const unsigned hr = static_cast<unsigned>(__double2hiint(q.rho));
       const unsigned hb = static_cast<unsigned>(__double2hiint(be));
@@ -533,7 +539,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const double2* on = reinterpret_cast<const double2*>(pr) + w3_sw(w3_face_node(d, side, pt));
       const double2 o0 = on[0], o1 = on[N], o2 = on[2 * N], o3 = on[3 * N];
       const double vo[3] = {o1.x, o1.y, o2.x};
-      const bool ok = rus_lift_v<3, SURF>(ph, o0.x, vo, o2.y, o3.x, o3.y, un, d, side,
+      const bool ok = rus_lift_v<3, SURF>(ph, o0.x, vo, PERRK_W3_HALFP ? o2.y + o2.y : o2.y,
+                                          o3.x, o3.y, un, d, side,
                                           J2 * c_D[j * N1 + j], side ? -lift : lift, false, o5);
       if (!ok)
         report_bad(st, a.stage, a.ncells,
@@ -718,6 +725,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     __syncwarp();  // the slice is rewritten by the next cell
     slot = nslot;
     cell = ncell;
+    ncell = nncell;
     rb ^= 1;
   }
 
