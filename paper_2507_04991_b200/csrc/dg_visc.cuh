@@ -21,12 +21,15 @@ namespace dev {
 // g: d/dx then d/dy of the conserved variables.
 __device__ __forceinline__ void visc_flux2(const Phys& ph, const double* u, const double* gx,
                                            const double* gy, double* fx, double* fy) {
-  const double rho = u[0];
-  const double vx = u[1] / rho, vy = u[2] / rho;
-  const double vx_x = (gx[1] - vx * gx[0]) / rho, vy_x = (gx[2] - vy * gx[0]) / rho;
-  const double vx_y = (gy[1] - vx * gy[0]) / rho, vy_y = (gy[2] - vy * gy[0]) / rho;
-  const double t_x = ph.gm1 * (gx[3] / rho - u[3] * gx[0] / (rho * rho) - (vx * vx_x + vy * vy_x));
-  const double t_y = ph.gm1 * (gy[3] / rho - u[3] * gy[0] / (rho * rho) - (vx * vx_y + vy * vy_y));
+  // one reciprocal of rho (frcp: full double precision) instead of eight
+  // IEEE divisions
+  const double rho = u[0], ir = frcp(rho);
+  const double vx = u[1] * ir, vy = u[2] * ir;
+  const double vx_x = (gx[1] - vx * gx[0]) * ir, vy_x = (gx[2] - vy * gx[0]) * ir;
+  const double vx_y = (gy[1] - vx * gy[0]) * ir, vy_y = (gy[2] - vy * gy[0]) * ir;
+  const double e = u[3] * ir * ir;
+  const double t_x = ph.gm1 * (gx[3] * ir - e * gx[0] - (vx * vx_x + vy * vy_x));
+  const double t_y = ph.gm1 * (gy[3] * ir - e * gy[0] - (vx * vx_y + vy * vy_y));
   const double tau_xx = ph.mu * (4.0 / 3.0 * vx_x - 2.0 / 3.0 * vy_y);
   const double tau_yy = ph.mu * (4.0 / 3.0 * vy_y - 2.0 / 3.0 * vx_x);
   const double tau_xy = ph.mu * (vx_y + vy_x);

@@ -70,3 +70,13 @@ def test_reference_arm_does_not_load_the_product():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference"
     assert line["config"] == CR.S.bench_config(CR.S.make_spec("c1"))
+
+
+def test_bench_gpus_n_fails_loudly_without_the_gpus():
+    """bench.py --gpus N without a launcher re-executes under torchrun with N
+    ranks; with fewer than N visible GPUs it exits 2 (never one silent rank)."""
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "0"],
+                       cwd=CR.ROOT, capture_output=True, text=True, timeout=300,
+                       env={**__import__("os").environ, "CUDA_VISIBLE_DEVICES": ""})
+    assert r.returncode == 2, (r.returncode, r.stderr)
+    assert "needs 2 visible GPUs" in r.stderr
