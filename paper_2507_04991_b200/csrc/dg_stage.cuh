@@ -219,8 +219,9 @@ __device__ __forceinline__ void ec2(const Phys& ph, int d, double rl, const doub
 template <int DIM>
 __device__ __forceinline__ void wse(const Phys& ph, const Prim<DIM>& l, const Prim<DIM>& r, int d,
                                     double& sl, double& sr) {
-  const double cl = sqrt(ph.gamma * l.p * frcp(l.rho)), cr = sqrt(ph.gamma * r.p * frcp(r.rho));
-  const double sql = sqrt(l.rho), sqr = sqrt(r.rho);
+  // fsqrt (~1 ulp, no slow path) on the admissible states' positive arguments
+  const double cl = fsqrt(ph.gamma * l.p * frcp(l.rho)), cr = fsqrt(ph.gamma * r.p * frcp(r.rho));
+  const double sql = fsqrt(l.rho), sqr = fsqrt(r.rho);
   const double iw = frcp(sql + sqr);
   const double hl = (l.E + l.p) * frcp(l.rho), hr = (r.E + r.p) * frcp(r.rho);
   double v2 = 0.0, vd = 0.0;
@@ -231,7 +232,8 @@ __device__ __forceinline__ void wse(const Phys& ph, const Prim<DIM>& l, const Pr
     if (i == d) vd = vroe;
   }
   const double hroe = (sql * hl + sqr * hr) * iw;
-  const double croe = sqrt(fmax(0.0, ph.gm1 * (hroe - 0.5 * v2)));
+  const double c2roe = ph.gm1 * (hroe - 0.5 * v2);
+  const double croe = c2roe > 0.0 ? fsqrt(c2roe) : 0.0;
   sl = fmin(pick<DIM>(l.v, d) - cl, vd - croe);
   sr = fmax(pick<DIM>(r.v, d) + cr, vd + croe);
 }
@@ -261,8 +263,8 @@ __device__ __forceinline__ void sflux(const Phys& ph, const Prim<DIM>& l, const 
 #pragma unroll
     for (int v = 0; v < V; ++v) f[v] = 0.5 * (fl[v] + fr[v]);
   } else if constexpr (SURF == 2) {
-    const double lam = fmax(fabs(pick<DIM>(l.v, d)) + sqrt(ph.gamma * l.p * frcp(l.rho)),
-                            fabs(pick<DIM>(r.v, d)) + sqrt(ph.gamma * r.p * frcp(r.rho)));
+    const double lam = fmax(fabs(pick<DIM>(l.v, d)) + fsqrt(ph.gamma * l.p * frcp(l.rho)),
+                            fabs(pick<DIM>(r.v, d)) + fsqrt(ph.gamma * r.p * frcp(r.rho)));
     double ul[V], ur[V];
     cons_of<DIM>(l, ul);
     cons_of<DIM>(r, ur);
