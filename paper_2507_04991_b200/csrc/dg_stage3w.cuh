@@ -48,6 +48,10 @@ namespace dev {
 #define PERRK_W3_HALFP 1  // 1: the slice holds p / 2 (the EC flux's pressure terms take it as is)
 #endif
 
+#ifndef PERRK_W3_OWNPF
+#define PERRK_W3_OWNPF 0  // 1: the next cell's own stage-state block arrives by cp.async a cell ahead
+#endif
+
 #ifndef PERRK_W3_EPI
 #define PERRK_W3_EPI 0  // 1: the epilogue's U / K1 blocks arrive by bulk copies issued at cell start
 #endif
@@ -75,7 +79,10 @@ struct W3 {
   // behind the cell's whole volume and surface phases); d (b-stages only)
   // still comes through the dead slice
   static constexpr int SM_EP = PERRK_W3_EPI ? 2 * NPC * V : 0;
-  static constexpr int SM_WARP = SM_PR + SM_FS + SM_EP;
+  // PERRK_W3_OWNPF: the next cell's own stage-state block ([v][64], read by
+  // lane with conflict-free 8-byte loads)
+  static constexpr int SM_OB = PERRK_W3_OWNPF ? NPC * V : 0;
+  static constexpr int SM_WARP = SM_PR + SM_FS + SM_EP + SM_OB;
   static_assert(SM_PR + SM_FS >= (PERRK_W3_EPI ? 1 : 3) * NPC * V,
                 "the epilogue stages its blocks in the slice");
   static_assert(SM_WARP % 2 == 0, "16-byte aligned slices");
@@ -341,6 +348,12 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* pr = smem + wib * S::SM_WARP;  // [4][64] double2, swizzled (w3_sw)
   double* fs = pr + S::SM_PR;            // face slots (w3_fs): staged traces, then surface terms
+#if PERRK_W3_OWNPF
+  double* ob = fs + S::SM_FS + S::SM_EP;  // the next cell's own block
+  // the block a cell's own state comes from: Us (formed) or U (stage 0);
+  // a cell formed from the first column (rare) reads U and K1 directly
+  const double* own_src = form_ ? a.Us : a.U;
+#endif
 #if PERRK_W3_EPI
   double* ep = fs + S::SM_FS;            // epilogue blocks [U | K1] (device layout)
   unsigned ep_phase = 0;
@@ -371,6 +384,12 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   int ncell = cell_at(slot + nw);  // list entries are read one cell ahead of their use
   int rb = 0;
   fetch_rec(0, cell);
+#if PERRK_W3_OWNPF
+  if (cell >= 0) {
+    w3_stage_cell(ob, own_src + static_cast<size_t>(cell) * N * V, lane);
+    cp_async_commit();
+  }
+#endif
 
   while (cell >= 0) {
     // next cell: its state arrays to L2 (bulk prefetch); the one after: list entry
@@ -408,6 +427,15 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #endif
     const size_t gA = cbase + lane, gB = gA + 32;
     double uA[V], uB[V];
+#if PERRK_W3_OWNPF
+    if (!form_ || a.formed[lev]) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        uA[v] = ob[v * N + lane];
+        uB[v] = ob[v * N + lane + 32];
+      }
+    } else
+#endif
     if (!form_) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -452,6 +480,11 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     }
     cp_async_commit();
     fetch_rec(rb ^ 1, ncell);  // the next cell's descriptor
+#if PERRK_W3_OWNPF
+    __syncwarp();  // every lane has its own state out of the buffer
+    if (ncell >= 0) w3_stage_cell(ob, own_src + static_cast<size_t>(ncell) * N * V, lane);
+    cp_async_commit();  // (empty past the end) waited at the top of the next cell
+#endif
     // ---- primitives of A and B -> the warp's slice -------------------------
     bool okAB = true;
     // range of rho and beta over the cell from the high words of the doubles
@@ -511,7 +544,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 
     // ---- surface flux + lift + endpoint diagonal at the lane's three face
     // points (semidisc.cpp:489-556, :450-454) ---------------------------------
-    cp_async_wait<1>();  // traces and epilogue blocks (the next descriptor may fly on)
+    // the traces (the next descriptor, and with PERRK_W3_OWNPF the next own block, fly on)
+    cp_async_wait<PERRK_W3_OWNPF ? 2 : 1>();
     __syncwarp();
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
