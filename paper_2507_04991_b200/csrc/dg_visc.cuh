@@ -44,14 +44,19 @@ __device__ __forceinline__ void visc_flux2(const Phys& ph, const double* u, cons
 }
 
 // out: mode 0 -> viscous flux G [2][nodes][V]; mode 1 -> gradients [2][nodes][V]
+// (both in the device layout).  Per group of eight cells the descriptors come
+// from the static cell records (host.cpp build_cell_records: neighbours,
+// levels, 4/h, lift; no dependent level loads), and the stage state and the
+// neighbour traces sit in shared memory variable-major ([V][node]: the
+// 8-byte accesses of a warp are conflict free).
 __global__ void __launch_bounds__(128)
     grad_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* out, long long ndofs,
                 int mode) {
   constexpr int DIM = 2, V = 4, NPC = 16, FP = 4, NFP = 4 * FP, T = 128, CPB = T / NPC;
-  __shared__ double su[CPB * NPC * V];      // formed stage state
-  __shared__ double sn[CPB * NFP * V];      // neighbour traces [cell][face][pt][V]
-  __shared__ int s_cell[CPB], s_coord[CPB][2], s_nbc[CPB][4];
-  __shared__ double s_ca1[CPB], s_na1[CPB][4];
+  __shared__ double su[V][T];             // formed stage state
+  __shared__ double sn[V][CPB * NFP];     // neighbour traces [cell][face][pt]
+  __shared__ int s_cell[CPB], s_nbc[CPB][4];
+  __shared__ double s_ca1[CPB], s_na1[CPB][4], s_jac[CPB][2], s_lift[CPB][2];
   __shared__ signed char s_cform[CPB], s_nform[CPB][4];
   if (st->aborted || st->finished) return;
   const int tid = threadIdx.x;
@@ -65,23 +70,23 @@ __global__ void __launch_bounds__(128)
       const int slot = grp * CPB + tid;
       const int cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
       s_cell[tid] = cell;
-      const int cc = cell < 0 ? 0 : cell;
-      const int co[2] = {cc % m.nc[0], cc / m.nc[0]};
-      s_coord[tid][0] = co[0];
-      s_coord[tid][1] = co[1];
-      const int lev = m.level[cc];
-      s_ca1[tid] = dt * a.a1[lev];
-      s_cform[tid] = a.formed[lev];
-      for (int f = 0; f < 4; ++f) {
-        const int d = f >> 1, side = f & 1;
-        int c2[2] = {co[0], co[1]};
-        const int nd = m.nc[d];
-        c2[d] = side ? (c2[d] + 1 == nd ? 0 : c2[d] + 1) : (c2[d] == 0 ? nd - 1 : c2[d] - 1);
-        const int nbc = c2[0] + m.nc[0] * c2[1];
-        const int l2 = m.level[nbc];
-        s_nbc[tid][f] = nbc;
-        s_na1[tid][f] = dt * a.a1[l2];
-        s_nform[tid][f] = a.formed[l2];
+      if (cell >= 0) {
+        const CellRec* r = m.rec + cell;
+        const int lev = r->lev[0];
+        s_ca1[tid] = dt * a.a1[lev];
+        s_cform[tid] = a.formed[lev];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {  // face 2 d + side; the whole mesh is local (no slabs)
+          const int l2 = r->lev[1 + f];
+          s_nbc[tid][f] = r->nb[f];
+          s_na1[tid][f] = dt * a.a1[l2];
+          s_nform[tid][f] = a.formed[l2];
+        }
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          s_jac[tid][d] = 0.5 * r->J2[d];  // 2 / h (J2 = 2 (2 / h): exact)
+          s_lift[tid][d] = r->lift[d];
+        }
       }
     }
     __syncthreads();
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(128)
         if (!a.form) u = __ldg(a.U + g);
         else if (s_cform[cs]) u = __ldg(a.Us + g);
         else u = fma(s_ca1[cs], __ldg(a.K1 + g), __ldg(a.U + g));
-        su[tid * V + v] = u;
+        su[v][tid] = u;
       }
     }
     for (int q = tid; q < CPB * NFP; q += T) {
@@ -112,38 +117,40 @@ __global__ void __launch_bounds__(128)
         if (!a.form) u = __ldg(a.U + g);
         else if (s_nform[c2][f]) u = __ldg(a.Us + g);
         else u = fma(s_na1[c2][f], __ldg(a.K1 + g), __ldg(a.U + g));
-        sn[q * V + v] = u;
+        sn[v][q] = u;
       }
     }
     __syncthreads();
     if (cell < 0) continue;
+    double uo[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) uo[v] = su[v][tid];
     double g[2][V];
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       const int stride = d == 0 ? 1 : N1;
       const int j = il[d];
-      const int cd = s_coord[cs][d];
-      const double jac = m.jac[d][cd];
+      const double jac = s_jac[cs][d];
 #pragma unroll
       for (int v = 0; v < V; ++v) g[d][v] = 0.0;
       // strong-form derivative along the line (gradients_1d, semidisc.cpp:266-281)
 #pragma unroll
       for (int k = 0; k < N1; ++k) {
         const double coef = jac * c_D[j * N1 + k];
-        const double* uk = su + (tid + (k - j) * stride) * V;
+        const int tk = tid + (k - j) * stride;
 #pragma unroll
-        for (int v = 0; v < V; ++v) g[d][v] += coef * uk[v];
+        for (int v = 0; v < V; ++v) g[d][v] += coef * su[v][tk];
       }
       // central interface lift (semidisc.cpp:283-318)
       if (j == 0 || j == N1 - 1) {
         const int e = j == 0 ? 0 : 1;
         const int pt = d == 0 ? il[1] : il[0];
-        const double* un = sn + ((cs * 4 + 2 * d + e) * FP + pt) * V;
-        const double* uo = su + tid * V;
-        const double coef = m.lift[d][cd];
+        const int qn = (cs * 4 + 2 * d + e) * FP + pt;
+        const double coef = s_lift[cs][d];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          const double ustar = 0.5 * (e ? uo[v] + un[v] : un[v] + uo[v]);
+          const double un = sn[v][qn];
+          const double ustar = 0.5 * (e ? uo[v] + un : un + uo[v]);
           g[d][v] += (e ? coef : -coef) * (ustar - uo[v]);
         }
       }
@@ -157,7 +164,7 @@ __global__ void __launch_bounds__(128)
       }
     } else {
       double fx[V], fy[V];
-      visc_flux2(ph, su + tid * V, g[0], g[1], fx, fy);
+      visc_flux2(ph, uo, g[0], g[1], fx, fy);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         out[gi + v * NPC] = fx[v];
