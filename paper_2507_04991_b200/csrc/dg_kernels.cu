@@ -28,6 +28,7 @@ namespace dev {
 
 __constant__ double c_D[N1 * N1];  // SBP derivative matrix, row-major D[l][m]
 __constant__ double c_w[N1];       // LGL weights
+__constant__ double c_Dw[N1 * N1];  // weak-form transpose coefficients D[k][j] w[k] / w[j]
 
 constexpr long long kNoBad = LLONG_MAX;
 
@@ -1135,6 +1136,11 @@ double measure_fp64_peak() {
 cudaError_t upload_basis(const double* D, const double* w) {
   cudaError_t e = cudaMemcpyToSymbol(c_D, D, sizeof(double) * N1 * N1);
   if (e != cudaSuccess) return e;
+  double Dw[N1 * N1];
+  for (int k = 0; k < N1; ++k)
+    for (int j = 0; j < N1; ++j) Dw[k * N1 + j] = D[k * N1 + j] * w[k] / w[j];
+  e = cudaMemcpyToSymbol(c_Dw, Dw, sizeof(double) * N1 * N1);
+  if (e != cudaSuccess) return e;
   return cudaMemcpyToSymbol(c_w, w, sizeof(double) * N1);
 }
 
@@ -1308,10 +1314,18 @@ cudaError_t launch_adv_final(const double* d, long long M, long long col0, int n
   return cudaGetLastError();
 }
 
+template <typename K>
+static int resident_grid(K kernel, int threads, int cap);
+
 cudaError_t launch_grad(const StageArgs& a, const MeshDev& m, const Phys& ph, StepState* st,
                         double* out, long long ndofs, int mode, int grid, cudaStream_t s) {
+  // its own resident capacity (per device), not the stage kernel's grid
+  static int resident[MAX_DEVICES] = {};
+  const int dev = current_device();
+  if (!resident[dev]) resident[dev] = resident_grid(grad_kernel, 128, 1 << 30);
+  (void)grid;
   const int groups = (a.n + 7) / 8;
-  const int g = groups < grid ? groups : grid;
+  const int g = groups < resident[dev] ? groups : resident[dev];
   if (g <= 0) return cudaSuccess;
   grad_kernel<<<g, 128, 0, s>>>(a, m, ph, st, out, ndofs, mode);
   return cudaGetLastError();

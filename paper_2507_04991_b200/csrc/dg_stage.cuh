@@ -806,9 +806,9 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
       if (cell >= 0) {
         const size_t gi = static_cast<size_t>(cell) * NPC * V + l;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          vg[tid * V + v] = a.G[gi + v * NPC];
-          vg[(T + tid) * V + v] = a.G[nd + gi + v * NPC];
+        for (int v = 0; v < V; ++v) {  // [dir][V][T]: conflict-free 8-byte accesses
+          vg[v * T + tid] = a.G[gi + v * NPC];
+          vg[(V + v) * T + tid] = a.G[nd + gi + v * NPC];
         }
       }
       for (int q = tid; q < CPB * NFP; q += T) {
@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
             line_base<DIM>(d, pt % N1, pt / N1) + (side ? 0 : N1 - 1) * line_stride(d);
         const size_t gi = static_cast<size_t>(s_nbc[c2][f]) * NPC * V + node + d * nd;
 #pragma unroll
-        for (int v = 0; v < V; ++v) vn[q * V + v] = a.G[gi + v * NPC];
+        for (int v = 0; v < V; ++v) vn[v * (CPB * NFP) + q] = a.G[gi + v * NPC];  // [V][face pt]
       }
     }
     __syncthreads();
@@ -932,20 +932,21 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
           const double jac = 0.5 * s_J2[cs][d];
 #pragma unroll
           for (int k = 0; k < N1; ++k) {
-            const double coef = jac * c_D[k * N1 + j] * c_w[k] / c_w[j];
-            const double* gk = vg + (d * T + tid + (k - j) * stride) * V;
+            const double coef = jac * c_Dw[k * N1 + j];
+            const double* gk = vg + d * V * T + tid + (k - j) * stride;
 #pragma unroll
-            for (int v = 0; v < V; ++v) K[v] -= coef * gk[v];
+            for (int v = 0; v < V; ++v) K[v] -= coef * gk[v * T];
           }
           if (j == 0 || j == N1 - 1) {
             const int e = j == 0 ? 0 : 1;
             const int pt = d == 0 ? il[1] : il[0];
-            const double* gn = vn + ((cs * 2 * DIM + 2 * d + e) * FP + pt) * V;
-            const double* go = vg + (d * T + tid) * V;
+            const double* gn = vn + (cs * 2 * DIM + 2 * d + e) * FP + pt;
+            const double* go = vg + d * V * T + tid;
             const double coef = s_lift[cs][d];
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-              const double gs = 0.5 * (e ? go[v] + gn[v] : gn[v] + go[v]);
+              const double gs = 0.5 * (e ? go[v * T] + gn[v * CPB * NFP]
+                                         : gn[v * CPB * NFP] + go[v * T]);
               K[v] += (e ? coef : -coef) * gs;
             }
           }
