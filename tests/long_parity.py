@@ -115,6 +115,11 @@ def compare(name, device=0):
         "dH_total_scale": float(np.abs(log[:, hcol] - h0o).max()),
         "H0": float(H0), "H0_oracle": h0o,
         "iters_gpu": [int(r.newton_iters) for r in recs][:8],
+        "iters_mismatch_steps": int(np.sum(np.array([r.newton_iters for r in recs]) != log[:, 3])),
+        "gamma_argmax_step": int(np.argmax(np.abs(g - log[:, 2]))) + 1,
+        "gamma_minus_1_at_argmax": float(log[int(np.argmax(np.abs(g - log[:, 2]))), 2] - 1.0),
+        "gamma_rel_err_of_gamma_minus_1": float(
+            np.abs(g - log[:, 2]).max() / max(np.abs(log[:, 2] - 1.0).max(), 1e-300)),
         "fell_back_gpu": fb, "fell_back_oracle": int(log[:, 5].sum()),
         "sample_nodes": int(idx.size),
         "state_rel_sample": _rel(U[idx], fx["sample"]),
