@@ -52,6 +52,25 @@ namespace dev {
 #define PERRK_W3_OWNPF 0  // 1: the next cell's own stage-state block arrives by cp.async a cell ahead
 #endif
 
+#ifndef PERRK_W3_REGPF
+// the next cell's own stage state is loaded into registers a cell ahead
+// (coalesced loads of the device layout; its L2 latency hides behind the
+// current cell's 1: surface phase and epilogue, 2: epilogue); 0: loaded at
+// the top of its own cell
+#define PERRK_W3_REGPF 0
+#endif
+
+#ifndef PERRK_W3_L2PF
+#define PERRK_W3_L2PF 1  // 1: the next cell's state blocks are bulk-prefetched to L2
+#endif
+
+#ifndef PERRK_W3_CS
+// 1: the direct epilogue's read-once / write-once streams (U, K1, d, U_{i+1},
+// K_0) use the streaming cache operator (evict first), so that L2 keeps the
+// stage-state blocks the neighbours' traces come from
+#define PERRK_W3_CS 0
+#endif
+
 #ifndef PERRK_W3_EPI
 #define PERRK_W3_EPI 0  // 1: the epilogue's U / K1 blocks arrive by bulk copies issued at cell start
 #endif
@@ -230,10 +249,35 @@ __device__ __forceinline__ void w3_stage_cell(double* dst, const double* src, in
     cp_async16(dst + 2 * (lane + 32 * k), src + 2 * (lane + 32 * k));
 }
 
-// EC flux between smem nodes p and q in direction D (compile time)
+#ifndef PERRK_W3_SWZ
+#define PERRK_W3_SWZ 1  // 1: partner entries by XOR masks of the own entry (no per-load swizzle arithmetic)
+#endif
+
+// the same from a swizzled entry e = w3_sw(n)
+__device__ __forceinline__ W3Prim w3_load_e(const double* pr, int e) {
+  const double2* q = reinterpret_cast<const double2*>(pr) + e;
+  const double2 a = q[0], b = q[W3::NPC], c = q[2 * W3::NPC];
+  W3Prim r;
+  r.rho = a.x;
+  r.beta = a.y;
+  r.v[0] = b.x;
+  r.v[1] = b.y;
+  r.v[2] = c.x;
+  r.p = c.y;
+  return r;
+}
+
+// EC flux between smem nodes p and q in direction D (compile time).  With
+// PERRK_W3_SWZ p and q are swizzled entries: w3_sw(n) = n ^ (iy >> 1) ^ 6 (iz & 1),
+// so the entry of a node that differs from n in given coordinate bits is the
+// entry of n XOR a mask, and the entry of n + 32 is the entry of n plus 32.
 template <int D, bool SM>
 __device__ __forceinline__ void w3_ec(const Phys& ph, const double* pr, int p, int q, double* f) {
+#if PERRK_W3_SWZ
+  const W3Prim L = w3_load_e(pr, p), R = w3_load_e(pr, q);
+#else
   const W3Prim L = w3_load(pr, p), R = w3_load(pr, q);
+#endif
   ec2<3, SM, PERRK_W3_HALFP != 0>(ph, D, L.rho, L.v, L.p, L.beta, R.rho, R.v, R.p, R.beta, f);
 }
 
@@ -251,15 +295,35 @@ __device__ __forceinline__ void w3_inplane(const Phys& ph, const double* pr, int
   const int pn = lane + (kn - j) * st;  // partner lane for (j, j+1)
   const int src = lane + (kp - j) * st;
   double f[V];
+#if PERRK_W3_SWZ
+  // entries: own A (eA), its line partner (j, j+1 mod 4), and the distance-2 partner
+  const int eA = w3_sw(lane);
+  const int mnext = D == 0 ? (1 | ((j & 1) << 1)) : (4 | ((j & 1) * 9));
+  const int ePn = eA ^ mnext;
+  constexpr int m2 = D == 0 ? 2 : 9;
+#define W3_NODE_A eA
+#define W3_NODE_PA ePn
+#define W3_NODE_B (eA + 32)
+#define W3_NODE_PB (ePn + 32)
+#else
+#define W3_NODE_A lane
+#define W3_NODE_PA pn
+#define W3_NODE_B (lane + 32)
+#define W3_NODE_PB (pn + 32)
+#endif
   // A layer
-  w3_ec<D, SM>(ph, pr, lane, pn, f);
+  w3_ec<D, SM>(ph, pr, W3_NODE_A, W3_NODE_PA, f);
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     KA[v] = fma(-cn, f[v], KA[v]);
     KA[v] = fma(-cp, __shfl_sync(0xffffffffu, f[v], src), KA[v]);
   }
   // B layer
-  w3_ec<D, SM>(ph, pr, lane + 32, pn + 32, f);
+  w3_ec<D, SM>(ph, pr, W3_NODE_B, W3_NODE_PB, f);
+#undef W3_NODE_A
+#undef W3_NODE_PA
+#undef W3_NODE_B
+#undef W3_NODE_PB
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     KB[v] = fma(-cn, f[v], KB[v]);
@@ -267,8 +331,13 @@ __device__ __forceinline__ void w3_inplane(const Phys& ph, const double* pr, int
   }
   // distance 2: j < 2 -> (A_j, A_j+2); j >= 2 -> (B_j, B_j-2)
   const bool lo = j < 2;
+#if PERRK_W3_SWZ
+  const int own = lo ? eA : eA + 32;
+  w3_ec<D, SM>(ph, pr, own, own ^ m2, f);
+#else
   const int own = lo ? lane : lane + 32;
   w3_ec<D, SM>(ph, pr, own, own ^ (2 * st), f);
+#endif
 #if PERRK_W3_NOSEL
   // no selects: the pair's two terms weighted by c2 or 0 (DFMA instead of FSEL pairs)
   const double cA = lo ? c2 : 0.0, cB = lo ? 0.0 : c2;
@@ -295,8 +364,13 @@ __device__ __forceinline__ void w3_z(const Phys& ph, const double* pr, int lane,
   constexpr int V = W3::V;
   const int zB = zA + 2;
   double f[V];
+#if PERRK_W3_SWZ
+  const int nA = w3_sw(lane), nB = nA + 32;  // own entries
+#else
+  const int nA = lane, nB = lane + 32;
+#endif
   // distance 2 inside the lane: (A, B)
-  w3_ec<2, SM>(ph, pr, lane, lane + 32, f);
+  w3_ec<2, SM>(ph, pr, nA, nB, f);
   const double cab = J2 * c_D[zA * N1 + zB], cba = J2 * c_D[zB * N1 + zA];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -305,13 +379,17 @@ __device__ __forceinline__ void w3_z(const Phys& ph, const double* pr, int lane,
   }
   // (j, j+1 mod 4) of both nodes; partner lane l^16 holds the j+1 nodes:
   // zA = 0: A(0)-A'(1), B(2)-B'(3);  zA = 1: A(1)-B'(2), B(3)-A'(0)
+#if PERRK_W3_SWZ
+  const int pl = nA ^ 22;  // lane ^ 16 flips iz & 1: node bit 4 and the swizzle's 6
+#else
   const int pl = lane ^ 16;
+#endif
   const int pA = zA ? pl + 32 : pl, pB = zA ? pl : pl + 32;
   const double cnA = J2 * c_D[zA * N1 + ((zA + 1) & 3)], cnB = J2 * c_D[zB * N1 + ((zB + 1) & 3)];
   const double cpA = J2 * c_D[zA * N1 + ((zA + 3) & 3)], cpB = J2 * c_D[zB * N1 + ((zB + 3) & 3)];
   double g[V];
-  w3_ec<2, SM>(ph, pr, lane, pA, f);       // A's (j, j+1): to the partner's node pA
-  w3_ec<2, SM>(ph, pr, lane + 32, pB, g);  // B's (j, j+1): to the partner's node pB
+  w3_ec<2, SM>(ph, pr, nA, pA, f);  // A's (j, j+1): to the partner's node pA
+  w3_ec<2, SM>(ph, pr, nB, pB, g);  // B's (j, j+1): to the partner's node pB
   // received: the partner's pair ending at my node.  Partner zA' = 1 - zA:
   // zA = 0 -> its A pair (1,2) ends at my B, its B pair (3,0) at my A;
   // zA = 1 -> its A pair (0,1) ends at my A, its B pair (2,3) at my B.
@@ -391,11 +469,28 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   }
 #endif
 
+#if PERRK_W3_REGPF
+  // own stage state of a cell into registers (coalesced: variable v of node
+  // n at block + v N + n); a cell formed from the first column reads stale
+  // Us here and is redone at its top
+  double uA[V], uB[V];
+  const double* own_reg = form_ ? a.Us : a.U;
+  auto load_own = [&](int c) {
+    const double* g = own_reg + static_cast<size_t>(c) * N * V + lane;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      uA[v] = __ldg(g + v * N);
+      uB[v] = __ldg(g + v * N + 32);
+    }
+  };
+  if (cell >= 0) load_own(cell);
+#endif
+
   while (cell >= 0) {
     // next cell: its state arrays to L2 (bulk prefetch); the one after: list entry
     const int nslot = slot + nw;
     const int nncell = cell_at(nslot + nw);
-    if (lane == 0 && ncell >= 0) {
+    if (PERRK_W3_L2PF && lane == 0 && ncell >= 0) {
       constexpr unsigned kBytes = N * V * sizeof(double);
       const size_t off = static_cast<size_t>(ncell) * N * V;
       if (form_) l2_prefetch(a.Us + off, kBytes);
@@ -426,8 +521,22 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     }
 #endif
     const size_t gA = cbase + lane, gB = gA + 32;
+#if PERRK_W3_REGPF
+    // uA / uB arrived a cell ago from Us (U at stage 0); a cell formed from
+    // the first column (first active stage of its level) is redone here
+    if (form_ && !a.formed[lev]) {
+      const double a1 = dt * a.a1[lev];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        uA[v] = fma(a1, __ldg(a.K1 + gA + v * N), __ldg(a.U + gA + v * N));
+        uB[v] = fma(a1, __ldg(a.K1 + gB + v * N), __ldg(a.U + gB + v * N));
+      }
+    }
+#else
     double uA[V], uB[V];
-#if PERRK_W3_OWNPF
+#endif
+#if PERRK_W3_REGPF
+#elif PERRK_W3_OWNPF
     if (!form_ || a.formed[lev]) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -436,6 +545,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       }
     } else
 #endif
+#if !PERRK_W3_REGPF
     if (!form_) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -456,6 +566,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         uB[v] = fma(a1, __ldg(a.K1 + gB + v * N), __ldg(a.U + gB + v * N));
       }
     }
+#endif
     // ---- neighbour face traces -> the warp's face slots (cp.async), one
     // direction per round: round d, face 2 d + side, point pt -------------------
 #pragma unroll
@@ -544,6 +655,9 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 
     // ---- surface flux + lift + endpoint diagonal at the lane's three face
     // points (semidisc.cpp:489-556, :450-454) ---------------------------------
+#if PERRK_W3_REGPF == 1
+    if (ncell >= 0) load_own(ncell);
+#endif
     // the traces (the next descriptor, and with PERRK_W3_OWNPF the next own block, fly on)
     cp_async_wait<PERRK_W3_OWNPF ? 2 : 1>();
     __syncwarp();
@@ -605,6 +719,9 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       }
     }
 
+#if PERRK_W3_REGPF == 2
+    if (ncell >= 0) load_own(ncell);
+#endif
     // ---- epilogue (stepper.cpp:52-55, 60-72, 89-92) ---------------------------
     if (a.want_dh || a.want_h) {
       const double meas = rp->meas;
@@ -710,11 +827,18 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       }
     }
 #else
+#if PERRK_W3_CS
+#define W3_LD(p) __ldcs(p)
+#define W3_ST(p, x) __stcs(p, x)
+#else
+#define W3_LD(p) (*(p))
+#define W3_ST(p, x) (*(p) = (x))
+#endif
     if (a.write_k) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        a.Kout[gA + v * N] = KA[v];
-        a.Kout[gB + v * N] = KB[v];
+        W3_ST(a.Kout + gA + v * N, KA[v]);
+        W3_ST(a.Kout + gB + v * N, KB[v]);
       }
     }
     // U_{i+1} and d node by node, each batch with all its loads issued before
@@ -727,34 +851,36 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       double x[V], y[V];
       if (next_) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) x[v] = a.U[g + v * N];
+        for (int v = 0; v < V; ++v) x[v] = W3_LD(a.U + g + v * N);
         if (form_) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) y[v] = a.K1[g + v * N];
+          for (int v = 0; v < V; ++v) y[v] = W3_LD(a.K1 + g + v * N);
 #pragma unroll
-          for (int v = 0; v < V; ++v) a.Usn[g + v * N] = x[v] + fma(an, y[v], pn * K[v]);
+          for (int v = 0; v < V; ++v) W3_ST(a.Usn + g + v * N, x[v] + fma(an, y[v], pn * K[v]));
         } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v) a.Usn[g + v * N] = fma(an, K[v], x[v]);
+          for (int v = 0; v < V; ++v) W3_ST(a.Usn + g + v * N, fma(an, K[v], x[v]));
         }
       }
       if (dm_) {
         if (dm_ == 2) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], a.d[g + v * N]);
+          for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], W3_LD(a.d + g + v * N));
         } else {
 #pragma unroll
           for (int v = 0; v < V; ++v) x[v] = a.b * K[v];
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          a.d[g + v * N] = x[v];
+          W3_ST(a.d + g + v * N, x[v]);
           const unsigned long long bits =
               static_cast<unsigned long long>(__double_as_longlong(x[v])) & 0x7fffffffffffffffULL;
           if (a.want_dmax) dmax_bits = bits > dmax_bits ? bits : dmax_bits;
         }
       }
     }
+#undef W3_LD
+#undef W3_ST
 #endif
     __syncwarp();  // the slice is rewritten by the next cell
     slot = nslot;

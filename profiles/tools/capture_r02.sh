@@ -20,6 +20,18 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:stag
 timeout 900 ncu --set full --clock-control none -k regex:relax --launch-skip 2 -c 2 -f -o $O/relax python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:stage2w --launch-skip 20 -c 1 -f -o $O/c3_stage2w python bench.py --config c3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:"grad_kernel|stage_kernel" --launch-skip 8 -c 2 -f -o $O/c4_kernels python bench.py --config c4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+# text exports on the box (gpurun copies back at most 64 MiB: the .ncu-rep files stay there)
+for r in w3_stage0 w3_stage6 relax c3_stage2w c4_kernels; do
+  [ -f $O/$r.ncu-rep ] && python profiles/summarize_ncu.py $O/$r.ncu-rep > $O/${r}_ncu.txt 2>&1
+done
+ncu -i $O/w3_stage6.ncu-rep --page source --csv --print-source sass > $O/w3_stage6_sass.csv 2>/dev/null
+ncu -i $O/w3_stage6.ncu-rep --page source --csv --print-source cuda,sass > $O/w3_stage6_lines.csv 2>/dev/null
+python profiles/tools/sass_mix.py $O/w3_stage6_sass.csv > $O/sass_mix.txt 2>&1
+python profiles/tools/line_mix.py $O/w3_stage6_lines.csv >> $O/sass_mix.txt 2>&1
+ncu -i $O/w3_stage6.ncu-rep --page details > $O/w3_stage6_details.txt 2>/dev/null
+gzip -f $O/w3_stage6_sass.csv $O/w3_stage6_lines.csv
+rm -f $O/*.ncu-rep
+du -sh gpurun_out
 # the reference arm at the driver's default K / W (full C5 mesh, all host threads)
 timeout 1500 python bench.py --impl reference > $O/reference_arm.json 2> $O/reference_arm.err
 echo done
