@@ -41,6 +41,10 @@ namespace perrk {
 namespace dev {
 
 // cp.async.bulk.prefetch.L2 (sm_90+): bytes a multiple of 16, 16-byte aligned
+#ifndef PERRK_ST_L2PF
+#define PERRK_ST_L2PF 0  // 1: the 2D / block-per-cell stage kernels prefetch the next group's blocks to L2
+#endif
+
 __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -719,7 +723,7 @@ __global__ void __launch_bounds__(StageGeo<DIM>::T, (VISC || SURF >= 3) ? 8 : PE
     const int cell = s_cell[cs];
     // the next group's own cells go to L2 now (bulk prefetch, contiguous
     // NPC*V doubles per array), so its loads hit L2 instead of HBM
-    if (dt_t >= 0 && nx_cell >= 0) {
+    if (PERRK_ST_L2PF && dt_t >= 0 && nx_cell >= 0) {
       constexpr unsigned kBytes = NPC * V * sizeof(double);
       const size_t off = static_cast<size_t>(nx_cell) * NPC * V;
       if (a.form) l2_prefetch(a.Us + off, kBytes);

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(W2::T, 2)
     const int cell = cell_at(g0 + cs);  // -1: padding lanes (tail group)
     const bool live = cell >= 0;
     const int ng0 = g0 + nw * CPW;
-    if (s == 0) {  // the next group's state arrays to L2
+    if (PERRK_ST_L2PF && s == 0) {  // the next group's state arrays to L2
       const int ncell = cell_at(ng0 + cs);
       if (ncell >= 0) {
         constexpr unsigned kBytes = N * V * sizeof(double);

@@ -37,11 +37,16 @@ namespace dev {
 #endif
 
 #ifndef PERRK_W3_COAL
-#define PERRK_W3_COAL 1  // epilogue U / K1 / U_{i+1} blocks through the slice (coalesced)
+// 1: epilogue U / K1 / U_{i+1} blocks through the slice (the round-1 form, for
+// the canonical AoS layout); 0: direct loads and stores, which the device
+// layout makes coalesced 256-byte warp accesses (A/B: -4% stage time)
+#define PERRK_W3_COAL 0
 #endif
 
 #ifndef PERRK_W3_WPB
-#define PERRK_W3_WPB 8  // warps (cells in flight) per block
+// warps (cells in flight) per block; the default is one 12-warp block per SM
+// at 168 registers (two 8-warp blocks at 128 registers: PERRK_W3_WPB=8)
+#define PERRK_W3_WPB 12
 #endif
 
 #ifndef PERRK_W3_HALFP
@@ -61,14 +66,28 @@ namespace dev {
 #endif
 
 #ifndef PERRK_W3_L2PF
-#define PERRK_W3_L2PF 1  // 1: the next cell's state blocks are bulk-prefetched to L2
+#define PERRK_W3_L2PF 0  // 1: the next cell's state blocks are bulk-prefetched to L2 a cell ahead; 2: see below
 #endif
 
 #ifndef PERRK_W3_CS
 // 1: the direct epilogue's read-once / write-once streams (U, K1, d, U_{i+1},
 // K_0) use the streaming cache operator (evict first), so that L2 keeps the
 // stage-state blocks the neighbours' traces come from
-#define PERRK_W3_CS 0
+#define PERRK_W3_CS 1
+#endif
+
+#ifndef PERRK_W3_EPIREG
+// 1 (direct epilogue only): the epilogue's U and K1 values are loaded into
+// registers right after the volume phase, so their latency hides behind the
+// surface phase
+#define PERRK_W3_EPIREG 1
+#endif
+
+#ifndef PERRK_W3_EPIPF
+// 1: the lines of the epilogue's U / K1 blocks are prefetched (prefetch.global.L1,
+// one or two lines per lane) right after the volume phase: the register-free
+// form of PERRK_W3_EPIREG for the 128-register configuration
+#define PERRK_W3_EPIPF 0
 #endif
 
 #ifndef PERRK_W3_EPI
@@ -490,7 +509,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     // next cell: its state arrays to L2 (bulk prefetch); the one after: list entry
     const int nslot = slot + nw;
     const int nncell = cell_at(nslot + nw);
-    if (PERRK_W3_L2PF && lane == 0 && ncell >= 0) {
+    if (PERRK_W3_L2PF == 1 && lane == 0 && ncell >= 0) {
       constexpr unsigned kBytes = N * V * sizeof(double);
       const size_t off = static_cast<size_t>(ncell) * N * V;
       if (form_) l2_prefetch(a.Us + off, kBytes);
@@ -657,6 +676,36 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     // points (semidisc.cpp:489-556, :450-454) ---------------------------------
 #if PERRK_W3_REGPF == 1
     if (ncell >= 0) load_own(ncell);
+#endif
+    // PERRK_W3_L2PF == 2: only the next cell's own stage-state block, and only
+    // now (a surface phase and an epilogue ahead of its use)
+    if (PERRK_W3_L2PF == 2 && lane == 0 && ncell >= 0)
+      l2_prefetch((form_ ? a.Us : a.U) + static_cast<size_t>(ncell) * N * V,
+                  N * V * sizeof(double));
+#if PERRK_W3_EPIPF
+    if (next_) {
+      // 2560-byte blocks: 20 lines of 128 bytes each; lanes 0-19 take U, and
+      // (formed stages) lanes 12-31 take K1
+      const char* pu = reinterpret_cast<const char*>(a.U + cbase);
+      const char* pk = reinterpret_cast<const char*>(a.K1 + cbase);
+      if (lane < 20) asm volatile("prefetch.global.L1 [%0];" ::"l"(pu + 128 * lane));
+      if (form_ && lane >= 12) asm volatile("prefetch.global.L1 [%0];" ::"l"(pk + 128 * (lane - 12)));
+    }
+#endif
+#if PERRK_W3_EPIREG
+    static_assert(!PERRK_W3_COAL, "PERRK_W3_EPIREG needs the direct epilogue");
+    double eU[2][V], eK[2][V];
+    if (next_) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const size_t g = h ? gB : gA;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          eU[h][v] = PERRK_W3_CS ? __ldcs(a.U + g + v * N) : __ldg(a.U + g + v * N);
+          if (form_) eK[h][v] = PERRK_W3_CS ? __ldcs(a.K1 + g + v * N) : __ldg(a.K1 + g + v * N);
+        }
+      }
+    }
 #endif
     // the traces (the next descriptor, and with PERRK_W3_OWNPF the next own block, fly on)
     cp_async_wait<PERRK_W3_OWNPF ? 2 : 1>();
@@ -827,6 +876,13 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       }
     }
 #else
+#if PERRK_W3_EPIREG
+#define W3_EU(h, v) eU[h][v]
+#define W3_EK(h, v) eK[h][v]
+#else
+#define W3_EU(h, v) 0.0
+#define W3_EK(h, v) 0.0
+#endif
 #if PERRK_W3_CS
 #define W3_LD(p) __ldcs(p)
 #define W3_ST(p, x) __stcs(p, x)
@@ -851,10 +907,10 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       double x[V], y[V];
       if (next_) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) x[v] = W3_LD(a.U + g + v * N);
+        for (int v = 0; v < V; ++v) x[v] = PERRK_W3_EPIREG ? W3_EU(h, v) : W3_LD(a.U + g + v * N);
         if (form_) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) y[v] = W3_LD(a.K1 + g + v * N);
+          for (int v = 0; v < V; ++v) y[v] = PERRK_W3_EPIREG ? W3_EK(h, v) : W3_LD(a.K1 + g + v * N);
 #pragma unroll
           for (int v = 0; v < V; ++v) W3_ST(a.Usn + g + v * N, x[v] + fma(an, y[v], pn * K[v]));
         } else {
@@ -881,6 +937,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     }
 #undef W3_LD
 #undef W3_ST
+#undef W3_EU
+#undef W3_EK
 #endif
     __syncwarp();  // the slice is rewritten by the next cell
     slot = nslot;

@@ -467,11 +467,14 @@ std::vector<int> with_neighbours_2d(const perrk_ctx* c, const std::vector<char>&
 // on a 64^3 mesh), and their face traces are fetched from HBM a second time.
 // Ordering the list by bricks of B^3 cells (x-fastest inside a brick and
 // between bricks) brings every neighbour within B^2 entries except across
-// brick faces.  PERRK_BRICK=0 keeps the natural order; the default is 8.
+// brick faces.  Measured on C5 (profiles/r02_ab.txt): no change in stage time,
+// DRAM bytes -2% with the round-1 kernel and +2% with the direct streaming
+// epilogue (shorter contiguous runs), so the natural order is the default;
+// PERRK_BRICK=B orders by bricks of B^3.
 int brick_edge() {
   static const int b = [] {
     const char* e = std::getenv("PERRK_BRICK");
-    const int v = e ? std::atoi(e) : 8;
+    const int v = e ? std::atoi(e) : 0;
     return v < 0 ? 0 : v;
   }();
   return b;
