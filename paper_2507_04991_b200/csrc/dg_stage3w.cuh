@@ -90,6 +90,23 @@ namespace dev {
 #define PERRK_W3_EPIPF 0
 #endif
 
+#ifndef PERRK_W3_DESCREG
+// 1: the next cell's descriptor travels through a register of lanes 0-5
+// (one 16-byte load a cell ahead, one 16-byte shared store at the top of its
+// cell) instead of cp.async (13 L1 wavefronts per cell for its 96 bytes)
+#define PERRK_W3_DESCREG 1
+#endif
+
+#ifndef PERRK_W3_ZREG
+// 1 (with PERRK_W3_ZOWN and PERRK_W3_OWNREG): the z-face round runs first and
+// takes its own-side primitives, E and c from the lane's registers
+#define PERRK_W3_ZREG 1
+#endif
+
+#ifndef PERRK_W3_ZOWN
+#define PERRK_W3_ZOWN 1  // 1: z-face terms are added by the lane that computes them (it owns the node)
+#endif
+
 #ifndef PERRK_W3_EPI
 #define PERRK_W3_EPI 0  // 1: the epilogue's U / K1 blocks arrive by bulk copies issued at cell start
 #endif
@@ -300,13 +317,39 @@ __device__ __forceinline__ void w3_ec(const Phys& ph, const double* pr, int p, i
   ec2<3, SM, PERRK_W3_HALFP != 0>(ph, D, L.rho, L.v, L.p, L.beta, R.rho, R.v, R.p, R.beta, f);
 }
 
+#ifndef PERRK_W3_OWNREG
+// 1: the lane's own primitives stay in registers from the primitive pass
+// (the slice is read for partners only): 12 fewer 16-byte shared loads per
+// lane and cell; the L1 data pipe, at 70-80% of its peak, binds this kernel
+#define PERRK_W3_OWNREG 1
+#endif
+
+// EC flux between the register-held node L and the smem entry q (needs PERRK_W3_SWZ)
+template <int D, bool SM>
+__device__ __forceinline__ void w3_ec_r(const Phys& ph, const double* pr, const W3Prim& L, int q,
+                                        double* f) {
+  const W3Prim R = w3_load_e(pr, q);
+  ec2<3, SM, PERRK_W3_HALFP != 0>(ph, D, L.rho, L.v, L.p, L.beta, R.rho, R.v, R.p, R.beta, f);
+}
+
+__device__ __forceinline__ W3Prim w3_select(bool first, const W3Prim& a, const W3Prim& b) {
+  W3Prim r;
+  r.rho = first ? a.rho : b.rho;
+  r.beta = first ? a.beta : b.beta;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r.v[i] = first ? a.v[i] : b.v[i];
+  r.p = first ? a.p : b.p;
+  return r;
+}
+
 // x / y lines (D = 0, 1): the lane's two layers.  Each node evaluates
 // f(j, j+1 mod 4) and receives f(j-1, j); the distance-2 pairs: lanes with
 // j < 2 evaluate the A layer's (j, j+2), lanes with j >= 2 the B layer's
 // (j-2, j), exchanged with the lane 2 stride(D) positions away.
 template <int D, bool SM>
 __device__ __forceinline__ void w3_inplane(const Phys& ph, const double* pr, int lane, int j,
-                                           double J2, double* KA, double* KB) {
+                                           double J2, double* KA, double* KB, const W3Prim& oA,
+                                           const W3Prim& oB) {
   constexpr int V = W3::V;
   constexpr int st = D == 0 ? 1 : 4;  // lane / node stride along the line
   const int kn = (j + 1) & 3, kp = (j + 3) & 3;
@@ -331,14 +374,22 @@ __device__ __forceinline__ void w3_inplane(const Phys& ph, const double* pr, int
 #define W3_NODE_PB (pn + 32)
 #endif
   // A layer
+#if PERRK_W3_OWNREG
+  w3_ec_r<D, SM>(ph, pr, oA, W3_NODE_PA, f);
+#else
   w3_ec<D, SM>(ph, pr, W3_NODE_A, W3_NODE_PA, f);
+#endif
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     KA[v] = fma(-cn, f[v], KA[v]);
     KA[v] = fma(-cp, __shfl_sync(0xffffffffu, f[v], src), KA[v]);
   }
   // B layer
+#if PERRK_W3_OWNREG
+  w3_ec_r<D, SM>(ph, pr, oB, W3_NODE_PB, f);
+#else
   w3_ec<D, SM>(ph, pr, W3_NODE_B, W3_NODE_PB, f);
+#endif
 #undef W3_NODE_A
 #undef W3_NODE_PA
 #undef W3_NODE_B
@@ -352,7 +403,11 @@ __device__ __forceinline__ void w3_inplane(const Phys& ph, const double* pr, int
   const bool lo = j < 2;
 #if PERRK_W3_SWZ
   const int own = lo ? eA : eA + 32;
+#if PERRK_W3_OWNREG
+  w3_ec_r<D, SM>(ph, pr, w3_select(lo, oA, oB), own ^ m2, f);
+#else
   w3_ec<D, SM>(ph, pr, own, own ^ m2, f);
+#endif
 #else
   const int own = lo ? lane : lane + 32;
   w3_ec<D, SM>(ph, pr, own, own ^ (2 * st), f);
@@ -379,7 +434,8 @@ __device__ __forceinline__ void w3_inplane(const Phys& ph, const double* pr, int
 // z lines: lane l holds z = zA and zA + 2, lane l^16 the other two.
 template <bool SM>
 __device__ __forceinline__ void w3_z(const Phys& ph, const double* pr, int lane, int zA,
-                                     double J2, double* KA, double* KB) {
+                                     double J2, double* KA, double* KB, const W3Prim& oA,
+                                     const W3Prim& oB) {
   constexpr int V = W3::V;
   const int zB = zA + 2;
   double f[V];
@@ -389,7 +445,11 @@ __device__ __forceinline__ void w3_z(const Phys& ph, const double* pr, int lane,
   const int nA = lane, nB = lane + 32;
 #endif
   // distance 2 inside the lane: (A, B)
+#if PERRK_W3_OWNREG
+  ec2<3, SM, PERRK_W3_HALFP != 0>(ph, 2, oA.rho, oA.v, oA.p, oA.beta, oB.rho, oB.v, oB.p, oB.beta, f);
+#else
   w3_ec<2, SM>(ph, pr, nA, nB, f);
+#endif
   const double cab = J2 * c_D[zA * N1 + zB], cba = J2 * c_D[zB * N1 + zA];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -407,8 +467,13 @@ __device__ __forceinline__ void w3_z(const Phys& ph, const double* pr, int lane,
   const double cnA = J2 * c_D[zA * N1 + ((zA + 1) & 3)], cnB = J2 * c_D[zB * N1 + ((zB + 1) & 3)];
   const double cpA = J2 * c_D[zA * N1 + ((zA + 3) & 3)], cpB = J2 * c_D[zB * N1 + ((zB + 3) & 3)];
   double g[V];
+#if PERRK_W3_OWNREG
+  w3_ec_r<2, SM>(ph, pr, oA, pA, f);  // A's (j, j+1): to the partner's node pA
+  w3_ec_r<2, SM>(ph, pr, oB, pB, g);  // B's (j, j+1): to the partner's node pB
+#else
   w3_ec<2, SM>(ph, pr, nA, pA, f);  // A's (j, j+1): to the partner's node pA
   w3_ec<2, SM>(ph, pr, nB, pB, g);  // B's (j, j+1): to the partner's node pB
+#endif
   // received: the partner's pair ending at my node.  Partner zA' = 1 - zA:
   // zA = 0 -> its A pair (1,2) ends at my B, its B pair (3,0) at my A;
   // zA = 1 -> its A pair (0,1) ends at my A, its B pair (2,3) at my B.
@@ -458,6 +523,14 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   __syncwarp();
 #endif
   // descriptor of one cell into the warp's buffer b (lanes 0-5, 16 B each)
+#if PERRK_W3_DESCREG
+  static_assert(!PERRK_W3_OWNPF, "PERRK_W3_DESCREG assumes the trace group is the only cp.async group");
+  int4 recq = make_int4(0, 0, 0, 0);
+  auto fetch_rec = [&](int, int c) {
+    if (c >= 0 && lane < static_cast<int>(sizeof(CellRec) / 16))
+      recq = __ldg(reinterpret_cast<const int4*>(m.rec + c) + lane);
+  };
+#else
   auto fetch_rec = [&](int b, int c) {
     if (c >= 0 && lane < static_cast<int>(sizeof(CellRec) / 16))
 #if PERRK_W3_DESC_CA
@@ -469,6 +542,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #endif
     cp_async_commit();
   };
+#endif
   const double dt = st->dt;
   const int ix = lane & 3, iy = (lane >> 2) & 3, zA = lane >> 4, zB = zA + 2;
   const int side = zA, pt = lane & 15;
@@ -518,10 +592,15 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       if (dm_ == 2) l2_prefetch(a.d + off, kBytes);
     }
     // ---- descriptor (host.cpp build_cell_records), fetched a cell ago -------
+#if PERRK_W3_DESCREG
+    if (lane < static_cast<int>(sizeof(CellRec) / 16))
+      reinterpret_cast<int4*>(&s_rec[wib][0])[lane] = recq;
+#else
     cp_async_wait<0>();
+#endif
     if (PERRK_W3_COAL && lane == 0) bulk_wait_read();  // the previous U_{i+1} left the slice
     __syncwarp();
-    const CellRec* rp = &s_rec[wib][rb];
+    const CellRec* rp = &s_rec[wib][PERRK_W3_DESCREG ? 0 : rb];
     const unsigned long long lv =
         static_cast<unsigned long long>(*reinterpret_cast<const long long*>(rp->lev));
     const int lev = static_cast<int>(lv & 0xff);
@@ -617,6 +696,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #endif
     // ---- primitives of A and B -> the warp's slice -------------------------
     bool okAB = true;
+    W3Prim own[2];  // the lane's nodes A and B (PERRK_W3_OWNREG: used by the volume phase)
+    double2 ownEc[2];  // (E, c) of A and B (PERRK_W3_ZREG: the z-face round)
     // range of rho and beta over the cell from the high words of the doubles
     // (monotone for positive values; a negative or NaN value lands at the top)
     unsigned hr_lo = 0xffffffffu, hr_hi = 0u, hb_lo = 0xffffffffu, hb_hi = 0u;
@@ -628,10 +709,17 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       okAB = okAB && prim_ok<3>(q);
       const double be = q.rho * frcp(q.p);
       double2* dst = reinterpret_cast<double2*>(pr) + w3_sw(n);
+      own[h].rho = q.rho;
+      own[h].beta = be;
+      own[h].v[0] = q.v[0];
+      own[h].v[1] = q.v[1];
+      own[h].v[2] = q.v[2];
+      own[h].p = PERRK_W3_HALFP ? 0.5 * q.p : q.p;
       dst[0] = make_double2(q.rho, be);
       dst[N] = make_double2(q.v[0], q.v[1]);
       dst[2 * N] = make_double2(q.v[2], PERRK_W3_HALFP ? 0.5 * q.p : q.p);
-      dst[3 * N] = make_double2(q.E, SURF == 2 ? fsqrt(ph.gamma * q.p * ir) : 0.0);
+      ownEc[h] = make_double2(q.E, SURF == 2 ? fsqrt(ph.gamma * q.p * ir) : 0.0);
+      dst[3 * N] = ownEc[h];
       const unsigned hr = static_cast<unsigned>(__double2hiint(q.rho));
       const unsigned hb = static_cast<unsigned>(__double2hiint(be));
       hr_lo = min(hr_lo, hr);
@@ -663,13 +751,13 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
     for (int v = 0; v < V; ++v) KA[v] = KB[v] = 0.0;
     if (smooth) {
-      w3_inplane<0, true>(ph, pr, lane, ix, J2x, KA, KB);
-      w3_inplane<1, true>(ph, pr, lane, iy, J2y, KA, KB);
-      w3_z<true>(ph, pr, lane, zA, J2z, KA, KB);
+      w3_inplane<0, true>(ph, pr, lane, ix, J2x, KA, KB, own[0], own[1]);
+      w3_inplane<1, true>(ph, pr, lane, iy, J2y, KA, KB, own[0], own[1]);
+      w3_z<true>(ph, pr, lane, zA, J2z, KA, KB, own[0], own[1]);
     } else {
-      w3_inplane<0, false>(ph, pr, lane, ix, J2x, KA, KB);
-      w3_inplane<1, false>(ph, pr, lane, iy, J2y, KA, KB);
-      w3_z<false>(ph, pr, lane, zA, J2z, KA, KB);
+      w3_inplane<0, false>(ph, pr, lane, ix, J2x, KA, KB, own[0], own[1]);
+      w3_inplane<1, false>(ph, pr, lane, iy, J2y, KA, KB, own[0], own[1]);
+      w3_z<false>(ph, pr, lane, zA, J2z, KA, KB, own[0], own[1]);
     }
 
     // ---- surface flux + lift + endpoint diagonal at the lane's three face
@@ -708,10 +796,12 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     }
 #endif
     // the traces (the next descriptor, and with PERRK_W3_OWNPF the next own block, fly on)
-    cp_async_wait<PERRK_W3_OWNPF ? 2 : 1>();
+    cp_async_wait<PERRK_W3_DESCREG ? 0 : (PERRK_W3_OWNPF ? 2 : 1)>();
     __syncwarp();
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
+    for (int kd = 0; kd < 3; ++kd) {
+      // z faces first with PERRK_W3_ZREG (the own registers die early)
+      const int d = PERRK_W3_ZREG ? (kd == 0 ? 2 : kd - 1) : kd;
       double* slotp = fs + w3_fs(d * 32 + lane);
       const int nbc = rp->nb[2 * d + side];
       double un[V];
@@ -733,8 +823,21 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const double lift = rp->lift[d];
       const int j = side ? N1 - 1 : 0;
       double o5[V];
-      const double2* on = reinterpret_cast<const double2*>(pr) + w3_sw(w3_face_node(d, side, pt));
-      const double2 o0 = on[0], o1 = on[N], o2 = on[2 * N], o3 = on[3 * N];
+      double2 o0, o1, o2, o3;
+      if (PERRK_W3_ZREG && PERRK_W3_ZOWN && PERRK_W3_OWNREG && d == 2) {
+        const W3Prim w = w3_select(side == 0, own[0], own[1]);
+        o0 = make_double2(w.rho, w.beta);
+        o1 = make_double2(w.v[0], w.v[1]);
+        o2 = make_double2(w.v[2], w.p);
+        o3 = side ? ownEc[1] : ownEc[0];
+      } else {
+        const double2* on =
+            reinterpret_cast<const double2*>(pr) + w3_sw(w3_face_node(d, side, pt));
+        o0 = on[0];
+        o1 = on[N];
+        o2 = on[2 * N];
+        o3 = on[3 * N];
+      }
       const double vo[3] = {o1.x, o1.y, o2.x};
       const bool ok = rus_lift_v<3, SURF>(ph, o0.x, vo, PERRK_W3_HALFP ? o2.y + o2.y : o2.y,
                                           o3.x, o3.y, un, d, side,
@@ -742,7 +845,19 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       if (!ok)
         report_bad(st, a.stage, a.ncells,
                    nbc < 0 ? m.ghost_gid[-1 - nbc] : (m.gid ? m.gid[nbc] : nbc));
-      w3_slot_store(slotp, o5);
+      if (PERRK_W3_ZOWN && d == 2) {
+        // z faces: face point (2, side, pt) of lane 16 side + pt belongs to the
+        // lane's own node (A on side 0, B on side 1): no trip through the slots
+        if (side) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) KB[v] += o5[v];
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) KA[v] += o5[v];
+        }
+      } else {
+        w3_slot_store(slotp, o5);
+      }
     }
     __syncwarp();
     // gather: node A / B on face (d, side) takes the term of face point
@@ -750,7 +865,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     {
       const int jA[3] = {ix, iy, zA}, jB[3] = {ix, iy, zB};
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
+      for (int d = 0; d < (PERRK_W3_ZOWN ? 2 : 3); ++d) {
         const int ptA = d == 0 ? iy + 4 * zA : (d == 1 ? ix + 4 * zA : ix + 4 * iy);
         const int ptB = d == 0 ? iy + 4 * zB : (d == 1 ? ix + 4 * zB : ix + 4 * iy);
         if (jA[d] == 0 || jA[d] == N1 - 1) {
