@@ -100,7 +100,15 @@ namespace dev {
 #ifndef PERRK_W3_ZREG
 // 1 (with PERRK_W3_ZOWN and PERRK_W3_OWNREG): the z-face round runs first and
 // takes its own-side primitives, E and c from the lane's registers
-#define PERRK_W3_ZREG 1
+#define PERRK_W3_ZREG 0
+#endif
+
+#ifndef PERRK_W3_HOIST
+// 1: the descriptor's neighbour ids and the neighbours' formed flags are read
+// once at the top of the cell (their shared / constant load latencies
+// overlap), the surface phase loads its slot unconditionally, and the
+// gather is branch free (0/1 weights instead of divergent blocks)
+#define PERRK_W3_HOIST 1
 #endif
 
 #ifndef PERRK_W3_ZOWN
@@ -667,9 +675,24 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #endif
     // ---- neighbour face traces -> the warp's face slots (cp.async), one
     // direction per round: round d, face 2 d + side, point pt -------------------
+#if PERRK_W3_HOIST
+    int nb3[3];
+    unsigned unf = 0;  // bit d: the neighbour on (d, side) is formed from U and K1 in the surface phase
+#pragma unroll
+    for (int d = 0; d < 3; ++d) nb3[d] = rp->nb[2 * d + side];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
+      const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
+      if (form_ && nb3[d] >= 0 && !a.formed[l2]) unf |= 1u << d;
+    }
+#endif
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+#if PERRK_W3_HOIST
+      const int nbc = nb3[d];
+#else
       const int nbc = rp->nb[2 * d + side];
+#endif
       double* dst = fs + w3_fs(d * 32 + lane);
       if (nbc < 0) {
         const double* g = m.ghost + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
@@ -677,6 +700,13 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         for (int v = 0; v < V; ++v) cp_async8(dst + v, g + v);
       } else {
         const size_t gi = static_cast<size_t>(nbc) * N * V + w3_face_node(d, 1 - side, pt);
+#if PERRK_W3_HOIST
+        if (!((unf >> d) & 1u)) {
+          const double* src = (form_ ? a.Us : a.U) + gi;
+#pragma unroll
+          for (int v = 0; v < V; ++v) cp_async8(dst + v, src + v * N);
+        }  // else: formed from U and K1 in the surface phase (first active stage only)
+#else
         const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
         if (!form_) {
 #pragma unroll
@@ -685,6 +715,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #pragma unroll
           for (int v = 0; v < V; ++v) cp_async8(dst + v, a.Us + gi + v * N);
         }  // else: formed from U and K1 in the surface phase (first active stage only)
+#endif
       }
     }
     cp_async_commit();
@@ -803,6 +834,19 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       // z faces first with PERRK_W3_ZREG (the own registers die early)
       const int d = PERRK_W3_ZREG ? (kd == 0 ? 2 : kd - 1) : kd;
       double* slotp = fs + w3_fs(d * 32 + lane);
+#if PERRK_W3_HOIST
+      const int nbc = nb3[d];
+      double un[V];
+      w3_slot_load(slotp, un);  // (stale where the neighbour is formed below)
+      if ((unf >> d) & 1u) {
+        const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
+        const size_t gi = static_cast<size_t>(nbc) * N * V + w3_face_node(d, 1 - side, pt);
+        const double b1 = dt * a.a1[l2];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          un[v] = fma(b1, __ldg(a.K1 + gi + v * N), __ldg(a.U + gi + v * N));
+      }
+#else
       const int nbc = rp->nb[2 * d + side];
       double un[V];
       if (nbc >= 0 && form_) {
@@ -819,6 +863,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       } else {
         w3_slot_load(slotp, un);
       }
+#endif
       const double J2 = d == 0 ? J2x : (d == 1 ? J2y : J2z);
       const double lift = rp->lift[d];
       const int j = side ? N1 - 1 : 0;
@@ -868,6 +913,20 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       for (int d = 0; d < (PERRK_W3_ZOWN ? 2 : 3); ++d) {
         const int ptA = d == 0 ? iy + 4 * zA : (d == 1 ? ix + 4 * zA : ix + 4 * iy);
         const int ptB = d == 0 ? iy + 4 * zB : (d == 1 ? ix + 4 * zB : ix + 4 * iy);
+#if PERRK_W3_HOIST
+        // every lane reads a written slot (finite values); nodes off the face weigh it with 0
+        const double mA = (jA[d] == 0 || jA[d] == N1 - 1) ? 1.0 : 0.0;
+        const double mB = (jB[d] == 0 || jB[d] == N1 - 1) ? 1.0 : 0.0;
+        double cA[V], cB[V];
+        w3_slot_load(fs + w3_fs(d * 32 + 16 * (jA[d] ? 1 : 0) + ptA), cA);
+        w3_slot_load(fs + w3_fs(d * 32 + 16 * (jB[d] ? 1 : 0) + ptB), cB);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          KA[v] = fma(mA, cA[v], KA[v]);
+          KB[v] = fma(mB, cB[v], KB[v]);
+        }
+        continue;
+#endif
         if (jA[d] == 0 || jA[d] == N1 - 1) {
           double c[V];
           w3_slot_load(fs + w3_fs(d * 32 + 16 * (jA[d] ? 1 : 0) + ptA), c);
