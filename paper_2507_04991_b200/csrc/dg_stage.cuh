@@ -115,9 +115,9 @@ __device__ __forceinline__ Prim<DIM> prim_of(const Phys& ph, const double* u) {
 
 template <int DIM>
 __device__ __forceinline__ bool prim_ok(const Prim<DIM>& q) {
-  bool ok = q.rho > 0.0 && q.p > 0.0 && isfinite(q.E);
+  bool ok = (q.rho > 0.0) & (q.p > 0.0) & static_cast<bool>(isfinite(q.E));
 #pragma unroll
-  for (int d = 0; d < DIM; ++d) ok = ok && isfinite(q.v[d]);
+  for (int d = 0; d < DIM; ++d) ok = ok & static_cast<bool>(isfinite(q.v[d]));
   return ok;
 }
 
@@ -356,9 +356,10 @@ __device__ __forceinline__ bool rus_lift_v(const Phys& ph, double ro, const doub
     kin = fma(un[1 + i], vn[i], kin);
   }
   const double pn = ph.gm1 * (En - 0.5 * kin);
-  bool ok = rn > 0.0 && pn > 0.0 && isfinite(En);
+  // (no short-circuit: the tests stay straight-line code)
+  bool ok = (rn > 0.0) & (pn > 0.0) & static_cast<bool>(isfinite(En));
 #pragma unroll
-  for (int i = 0; i < DIM; ++i) ok = ok && isfinite(vn[i]);
+  for (int i = 0; i < DIM; ++i) ok = ok & static_cast<bool>(isfinite(vn[i]));
   const double vod = pick_rt<DIM>(vo, 0, d), vnd = pick_rt<DIM>(vn, 0, d);
   const double mnd = pick_rt<DIM>(un, 1, d), mod = ro * vod;
   double fo[V], g[V];

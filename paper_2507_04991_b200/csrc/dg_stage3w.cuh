@@ -111,6 +111,21 @@ namespace dev {
 #define PERRK_W3_HOIST 1
 #endif
 
+#ifndef PERRK_W3_FLAT
+// 1 (with PERRK_W3_HOIST): the three surface rounds form one straight-line
+// block.  Neighbours formed from U and K1 (first active stage of a level) are
+// written into their slots by a warp-uniform pre-pass, the admissibility
+// report is made once after the rounds, and the z-face terms are added with
+// 0/1 weights, so the scheduler can overlap the rounds' dependent chains.
+#define PERRK_W3_FLAT 1
+#endif
+
+#ifndef PERRK_W3_OWNL1PF
+// 1: the 20 lines of the next cell's own stage-state block are prefetched to
+// L1 (prefetch.global.L1, lanes 0-19) after the volume phase; 2: after the gather
+#define PERRK_W3_OWNL1PF 0
+#endif
+
 #ifndef PERRK_W3_ZOWN
 #define PERRK_W3_ZOWN 1  // 1: z-face terms are added by the lane that computes them (it owns the node)
 #endif
@@ -694,6 +709,22 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const int nbc = rp->nb[2 * d + side];
 #endif
       double* dst = fs + w3_fs(d * 32 + lane);
+#if PERRK_W3_FLAT && PERRK_W3_HOIST
+      {
+        // branch free: a ghost trace is point-major [pt][V], a cell block
+        // variable-major; a neighbour that is formed in the surface pre-pass
+        // has its (stale) stage-state trace copied all the same
+        const bool gh = nbc < 0;
+        const double* src =
+            gh ? m.ghost + (static_cast<size_t>(-1 - nbc) * FP + pt) * V
+               : (form_ ? a.Us : a.U) + static_cast<size_t>(nbc) * N * V +
+                     w3_face_node(d, 1 - side, pt);
+        const int vs = gh ? 1 : N;
+#pragma unroll
+        for (int v = 0; v < V; ++v) cp_async8(dst + v, src + v * vs);
+        continue;
+      }
+#endif
       if (nbc < 0) {
         const double* g = m.ghost + (static_cast<size_t>(-1 - nbc) * FP + pt) * V;
 #pragma unroll
@@ -737,7 +768,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const int n = lane + 32 * h;
       double ir;
       const Prim<3> q = prim_of<3>(ph, h ? uB : uA, ir);
-      okAB = okAB && prim_ok<3>(q);
+      okAB = okAB & prim_ok<3>(q);
       const double be = q.rho * frcp(q.p);
       double2* dst = reinterpret_cast<double2*>(pr) + w3_sw(n);
       own[h].rho = q.rho;
@@ -796,6 +827,10 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #if PERRK_W3_REGPF == 1
     if (ncell >= 0) load_own(ncell);
 #endif
+    if (PERRK_W3_OWNL1PF == 1 && ncell >= 0 && lane < 20)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(
+          reinterpret_cast<const char*>((form_ ? a.Us : a.U) + static_cast<size_t>(ncell) * N * V) +
+          128 * lane));
     // PERRK_W3_L2PF == 2: only the next cell's own stage-state block, and only
     // now (a surface phase and an epilogue ahead of its use)
     if (PERRK_W3_L2PF == 2 && lane == 0 && ncell >= 0)
@@ -829,12 +864,33 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     // the traces (the next descriptor, and with PERRK_W3_OWNPF the next own block, fly on)
     cp_async_wait<PERRK_W3_DESCREG ? 0 : (PERRK_W3_OWNPF ? 2 : 1)>();
     __syncwarp();
+#if PERRK_W3_FLAT && PERRK_W3_HOIST
+    if (__any_sync(0xffffffffu, unf != 0u)) {  // rare: a level's first active stage
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        if ((unf >> d) & 1u) {
+          const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
+          const size_t gi = static_cast<size_t>(nb3[d]) * N * V + w3_face_node(d, 1 - side, pt);
+          const double b1 = dt * a.a1[l2];
+          double un[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            un[v] = fma(b1, __ldg(a.K1 + gi + v * N), __ldg(a.U + gi + v * N));
+          w3_slot_store(fs + w3_fs(d * 32 + lane), un);  // the lane's own slot
+        }
+      }
+    }
+    unsigned badf = 0;  // bit d: the neighbour's trace on (d, side) is inadmissible
+#endif
 #pragma unroll
     for (int kd = 0; kd < 3; ++kd) {
       // z faces first with PERRK_W3_ZREG (the own registers die early)
       const int d = PERRK_W3_ZREG ? (kd == 0 ? 2 : kd - 1) : kd;
       double* slotp = fs + w3_fs(d * 32 + lane);
-#if PERRK_W3_HOIST
+#if PERRK_W3_FLAT && PERRK_W3_HOIST
+      double un[V];
+      w3_slot_load(slotp, un);
+#elif PERRK_W3_HOIST
       const int nbc = nb3[d];
       double un[V];
       w3_slot_load(slotp, un);  // (stale where the neighbour is formed below)
@@ -887,9 +943,24 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       const bool ok = rus_lift_v<3, SURF>(ph, o0.x, vo, PERRK_W3_HALFP ? o2.y + o2.y : o2.y,
                                           o3.x, o3.y, un, d, side,
                                           J2 * c_D[j * N1 + j], side ? -lift : lift, false, o5);
+#if PERRK_W3_FLAT && PERRK_W3_HOIST
+      if (!ok) badf |= 1u << d;
+      if (PERRK_W3_ZOWN && d == 2) {
+        const double mA = side ? 0.0 : 1.0, mB = side ? 1.0 : 0.0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          KA[v] = fma(mA, o5[v], KA[v]);
+          KB[v] = fma(mB, o5[v], KB[v]);
+        }
+      } else {
+        w3_slot_store(slotp, o5);
+      }
+      continue;
+#else
       if (!ok)
         report_bad(st, a.stage, a.ncells,
                    nbc < 0 ? m.ghost_gid[-1 - nbc] : (m.gid ? m.gid[nbc] : nbc));
+#endif
       if (PERRK_W3_ZOWN && d == 2) {
         // z faces: face point (2, side, pt) of lane 16 side + pt belongs to the
         // lane's own node (A on side 0, B on side 1): no trip through the slots
@@ -904,6 +975,13 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         w3_slot_store(slotp, o5);
       }
     }
+#if PERRK_W3_FLAT && PERRK_W3_HOIST
+    if (badf) {
+      const int nbc = (badf & 1u) ? nb3[0] : ((badf & 2u) ? nb3[1] : nb3[2]);
+      report_bad(st, a.stage, a.ncells,
+                 nbc < 0 ? m.ghost_gid[-1 - nbc] : (m.gid ? m.gid[nbc] : nbc));
+    }
+#endif
     __syncwarp();
     // gather: node A / B on face (d, side) takes the term of face point
     // (d, side, pt(node, d)) = slot d * 32 + 16 side + pt
@@ -945,6 +1023,10 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #if PERRK_W3_REGPF == 2
     if (ncell >= 0) load_own(ncell);
 #endif
+    if (PERRK_W3_OWNL1PF == 2 && ncell >= 0 && lane < 20)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(
+          reinterpret_cast<const char*>((form_ ? a.Us : a.U) + static_cast<size_t>(ncell) * N * V) +
+          128 * lane));
     // ---- epilogue (stepper.cpp:52-55, 60-72, 89-92) ---------------------------
     if (a.want_dh || a.want_h) {
       const double meas = rp->meas;
