@@ -252,7 +252,18 @@ def perrk_arm(args):
             dist.barrier()
 
     # warm-up
-    t, taken, aborted, _ = P.advance(semi, fam, pm, rc, 0.0, args.warmup, records=False)
+    # W warm-up steps.  perrk_advance replays a captured graph of two steps (the
+    # fused relaxation alternates two state buffers) and caches it by a key
+    # that holds the current buffer and the record flag; an odd trailing step
+    # leaves the state in the other buffer.  An odd W is therefore run as
+    # 1 + (W - 1) steps, so that the graph the timed region replays is the one
+    # the warm-up captured and no capture falls into the timed region.
+    t, taken, aborted = 0.0, 0, False
+    for n in ([1, args.warmup - 1] if args.warmup >= 3 and args.warmup % 2 else [args.warmup]):
+        t, k, aborted, _ = P.advance(semi, fam, pm, rc, t, n, records=True)
+        taken += k
+        if aborted:
+            break
     if aborted or taken != args.warmup:
         raise RuntimeError(f"warm-up aborted after {taken} steps")
     torch.cuda.synchronize()

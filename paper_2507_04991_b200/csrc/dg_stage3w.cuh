@@ -23,6 +23,16 @@
 // live in the warp's own shared-memory slice, ordered by __syncwarp.  The
 // neighbours' face traces are staged into that slice with cp.async while the
 // volume terms are computed.
+//
+// What binds it (profiles/r02_stage_kernel_ncu.txt): the L1 data pipe (shared
+// loads / stores, shuffles, global accesses: 70% of its peak), the FP64 pipe
+// (50%) and the issue slots (55%) together, at 3 warps per scheduler.  The
+// defaults below are the winners of the same-box A/B runs in
+// profiles/r02_ab.txt: fewer wavefronts (own primitives, descriptor and
+// z-face terms through registers), straight-line phases (hoisted descriptor
+// reads, branch-free staging / surface / gather), and no cache pollution
+// (direct streaming epilogue, no bulk L2 prefetch).  The switches keep the
+// rejected forms buildable (profiles/tools/mk_variant.sh).
 #pragma once
 
 namespace perrk {
@@ -712,12 +722,12 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #if PERRK_W3_FLAT && PERRK_W3_HOIST
       {
         // branch free: a ghost trace is point-major [pt][V], a cell block
-        // variable-major; a neighbour that is formed in the surface pre-pass
-        // has its (stale) stage-state trace copied all the same
+        // variable-major; of a neighbour that is formed in the surface
+        // pre-pass the U trace is copied (K1 is added there)
         const bool gh = nbc < 0;
         const double* src =
             gh ? m.ghost + (static_cast<size_t>(-1 - nbc) * FP + pt) * V
-               : (form_ ? a.Us : a.U) + static_cast<size_t>(nbc) * N * V +
+               : ((form_ && !((unf >> d) & 1u)) ? a.Us : a.U) + static_cast<size_t>(nbc) * N * V +
                      w3_face_node(d, 1 - side, pt);
         const int vs = gh ? 1 : N;
 #pragma unroll
@@ -872,11 +882,11 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
           const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
           const size_t gi = static_cast<size_t>(nb3[d]) * N * V + w3_face_node(d, 1 - side, pt);
           const double b1 = dt * a.a1[l2];
+          double* sl = fs + w3_fs(d * 32 + lane);  // the lane's own slot: the U trace
           double un[V];
 #pragma unroll
-          for (int v = 0; v < V; ++v)
-            un[v] = fma(b1, __ldg(a.K1 + gi + v * N), __ldg(a.U + gi + v * N));
-          w3_slot_store(fs + w3_fs(d * 32 + lane), un);  // the lane's own slot
+          for (int v = 0; v < V; ++v) un[v] = fma(b1, __ldg(a.K1 + gi + v * N), sl[v]);
+          w3_slot_store(sl, un);
         }
       }
     }
@@ -1060,8 +1070,10 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     // coalesced 16-byte cp.async, are read node-wise with conflict-free 8-byte
     // loads, and the results, U_{i+1} = U + dt (a_{i+1,1} K1 + a_{i+1,i} K_i)
     // in place of U, K1 = K_0 (stage 0) and d in place, leave as bulk copies
-    // (cp.async.bulk, the TMA path: no per-lane store wavefronts).  A direct
-    // 40-byte-stride LDG.64 / STG.64 touches 10 lines per instruction.
+    // (cp.async.bulk, the TMA path: no per-lane store wavefronts).  This was
+    // the round-1 form, for the canonical layout (a direct 40-byte-stride
+    // LDG.64 / STG.64 touched 10 lines per instruction); with the device
+    // layout the direct form below is coalesced and costs fewer L1 wavefronts.
     //   slice: U [0, 64V) | K1 or K_0 [64V, 128V) | d [128V, 192V)
     {
 #if PERRK_W3_EPI

@@ -471,13 +471,10 @@ std::vector<int> with_neighbours_2d(const perrk_ctx* c, const std::vector<char>&
 // DRAM bytes -2% with the round-1 kernel and +2% with the direct streaming
 // epilogue (shorter contiguous runs), so the natural order is the default;
 // PERRK_BRICK=B orders by bricks of B^3.
-int brick_edge() {
-  static const int b = [] {
-    const char* e = std::getenv("PERRK_BRICK");
-    const int v = e ? std::atoi(e) : 0;
-    return v < 0 ? 0 : v;
-  }();
-  return b;
+int brick_edge() {  // read at every perrk_set_family
+  const char* e = std::getenv("PERRK_BRICK");
+  const int v = e ? std::atoi(e) : 0;
+  return v < 0 ? 0 : v;
 }
 
 bool brick_order(const perrk_ctx* c, std::vector<int>& list) {
