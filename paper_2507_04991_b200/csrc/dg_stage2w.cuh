@@ -26,6 +26,10 @@
 namespace perrk {
 namespace dev {
 
+#ifndef PERRK_W2_COAL
+#define PERRK_W2_COAL 0  // 1: epilogue blocks through the slice and bulk stores (the round-2 session-1 form)
+#endif
+
 struct W2 {
   static constexpr int V = 4, NPC = 16, FP = 4, CPW = 4, WPB = 8, T = 32 * WPB;
   static constexpr int NQ = CPW * NPC;  // nodes per warp (64)
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(W2::T, 2)
       auto node = [&](int n, const double* K, int iy) {
         const W2Prim q = w2_load(pr, w2_sw(cs, n));
         const double be = q.beta;
-        const double s_therm = -(flog(be) + ph.gm1 * flog(q.rho));
+        const double s_therm = -(flog_core(be) + ph.gm1 * flog_core(q.rho));  // admissible here
         const double om = meas * c_w[ix] * c_w[iy];
         if (a.want_dh) {
           double v2 = 0.0, dot = 0.0;
@@ -407,6 +411,52 @@ __global__ void __launch_bounds__(W2::T, 2)
       node(s + 8, KB, yB);
     }
     const double an = dt * a.a1n[lev], pn = dt * a.apn[lev];
+#if !PERRK_W2_COAL
+    // Direct epilogue: in the device layout variable v of node n lies at
+    // cbase + v N + n, so the eight lanes of a cell read and write 64
+    // contiguous bytes per access (as stage3w_kernel's direct epilogue).
+    if (live) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double* K = h ? KB : KA;
+        const size_t g = cbase + s + 8 * h;
+        if (a.write_k) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) a.Kout[g + v * N] = K[v];
+        }
+        double x[V], y[V];
+        if (a.write_next) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) x[v] = __ldg(a.U + g + v * N);
+          if (a.form) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) y[v] = __ldg(a.K1 + g + v * N);
+#pragma unroll
+            for (int v = 0; v < V; ++v) a.Usn[g + v * N] = x[v] + fma(an, y[v], pn * K[v]);
+          } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) a.Usn[g + v * N] = fma(an, K[v], x[v]);
+          }
+        }
+        if (a.d_mode) {
+          if (a.d_mode == 2) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], a.d[g + v * N]);
+          } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) x[v] = a.b * K[v];
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            a.d[g + v * N] = x[v];
+            const unsigned long long bits =
+                static_cast<unsigned long long>(__double_as_longlong(x[v])) & 0x7fffffffffffffffULL;
+            if (a.want_dmax) dmax_bits = bits > dmax_bits ? bits : dmax_bits;
+          }
+        }
+      }
+    }
+#else
     // Epilogue through the slice (dead after the gather and the dH terms): the
     // cells' U, K1 and d blocks (512 contiguous bytes each) arrive by 16-byte
     // cp.async, the results leave as bulk copies, per cell slot.
@@ -471,6 +521,7 @@ __global__ void __launch_bounds__(W2::T, 2)
         if (a.d_mode) bulk_store(a.d + cbase, ed, kBytes);
       }
     }
+#endif
     __syncwarp();  // the slice is rewritten by the next group
     g0 = ng0;
     rb ^= 1;

@@ -70,7 +70,8 @@ namespace dev {
 #ifndef PERRK_W3_REGPF
 // the next cell's own stage state is loaded into registers a cell ahead
 // (coalesced loads of the device layout; its L2 latency hides behind the
-// current cell's 1: surface phase and epilogue, 2: epilogue); 0: loaded at
+// current cell's 1: surface phase and epilogue, 2: epilogue; 3: issued after
+// the epilogue, ahead of the next cell's descriptor round trip); 0: loaded at
 // the top of its own cell
 #define PERRK_W3_REGPF 0
 #endif
@@ -1045,7 +1046,9 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       auto node = [&](int n, const double* K, int iz) {
         const W3Prim q = w3_load(pr, n);
         const double be = q.beta;
-        const double s_therm = -(flog(be) + ph.gm1 * flog(q.rho));
+        // (admissible here: an inadmissible cell was reported above and the step is
+        // discarded, so the unguarded logarithm body is enough)
+        const double s_therm = -(flog_core(be) + ph.gm1 * flog_core(q.rho));
         const double om = meas * wxy * c_w[iz];
         if (a.want_dh) {
           double v2 = 0.0, dot = 0.0;
@@ -1207,6 +1210,9 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #undef W3_ST
 #undef W3_EU
 #undef W3_EK
+#endif
+#if PERRK_W3_REGPF == 3
+    if (ncell >= 0) load_own(ncell);  // the last thing of the cell: ahead of the next cell's descriptor round trip
 #endif
     __syncwarp();  // the slice is rewritten by the next cell
     slot = nslot;

@@ -1875,17 +1875,29 @@ int perrk_advance(perrk_ctx* c, const perrk_run_cfg* cfg, double* t, int nsteps,
       put_state(m, slab_state(m, s));
     }
     const bool rec = cfg->records && log;
+    // record rows: at least 256, doubling, so that calls of growing length
+    // keep the buffer (its address is part of the step-graph key below)
+    auto rows_for = [](int have, int need) {
+      int n = have > 256 ? have : 256;
+      while (n < need) n *= 2;
+      return n;
+    };
     for (perrk_ctx* m : g.members)
       if (rec && m->records_cap < nsteps) {
+        const int rows = rows_for(m->records_cap, nsteps);
         if (m->records) cudaFree(m->records);
-        CK(cudaMalloc(&m->records, sizeof(double) * dev::REC_COLS * nsteps));
-        m->records_cap = nsteps;
+        m->records = nullptr;
+        m->records_cap = 0;
+        CK(cudaMalloc(&m->records, sizeof(double) * dev::REC_COLS * rows));
+        m->records_cap = rows;
       }
     if (rec && c->rec_host_cap < nsteps) {
+      const int rows = rows_for(c->rec_host_cap, nsteps);
       if (c->rec_host) cudaFreeHost(c->rec_host);
       c->rec_host = nullptr;
-      CK(cudaMallocHost(&c->rec_host, sizeof(double) * dev::REC_COLS * nsteps));
-      c->rec_host_cap = nsteps;
+      c->rec_host_cap = 0;
+      CK(cudaMallocHost(&c->rec_host, sizeof(double) * dev::REC_COLS * rows));
+      c->rec_host_cap = rows;
     }
     // each step's StepRecord row leaves for the host right after the step
     auto stream_rows = [&](int k0, int n) {

@@ -17,7 +17,7 @@ timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
 # full captures: stage 0 (all cells) and a level-1 stage of the warp-per-cell kernel
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:stage3w --launch-skip 14 -c 1 -f -o $O/w3_stage0 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:stage3w --launch-skip 20 -c 1 -f -o $O/w3_stage6 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none -k regex:relax --launch-skip 2 -c 2 -f -o $O/relax python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:relax --launch-skip 0 -c 2 -f -o $O/relax python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:stage2w --launch-skip 20 -c 1 -f -o $O/c3_stage2w python bench.py --config c3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:"grad_kernel|stage_kernel" --launch-skip 8 -c 2 -f -o $O/c4_kernels python bench.py --config c4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 # text exports on the box (gpurun copies back at most 64 MiB: the .ncu-rep files stay there)
