@@ -324,6 +324,15 @@ __device__ void relax_update(StepState* st, dd A, dd B) {
 // blocks are staged through shared memory by cp.async first
 #define PERRK_RELAX_DIRECT 1
 #endif
+#ifndef PERRK_RELAX_MINB
+#define PERRK_RELAX_MINB 3  // resident 256-thread blocks per SM the relaxation kernels are compiled for
+#endif
+#ifndef PERRK_RELAX_PF
+// 1 (direct loads): the next block's U and d are loaded into registers before
+// the current block's terms are evaluated (twice the bytes in flight per warp;
+// the per-lane order of the sums, and so every bit of the result, is unchanged)
+#define PERRK_RELAX_PF 1
+#endif
 
 // One warp's 32-node block k of two state arrays (U and d) into shared
 // memory by coalesced 16-byte cp.async, one commit group per call (empty past
@@ -387,7 +396,7 @@ __device__ __forceinline__ void load_pair(const double* __restrict__ A,
 // free).  The previous layout (a thread's own node straight from global
 // memory, stride V doubles) cost 5x the L1 wavefronts per byte.
 template <int DIM>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, PERRK_RELAX_MINB)
     relax_pass_kernel(const double* __restrict__ U, const double* __restrict__ d, MeshDev m,
                       Phys ph, StepState* st, double* partials, unsigned* counter, long long nnodes) {
   constexpr int V = DIM + 2, NPC = Geo<DIM>::NPC, BLK = 32 * V;  // doubles per block and array
@@ -423,16 +432,33 @@ __global__ void __launch_bounds__(256, 3)
   long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
   int b = 0;
   stage(k, 0);
+  constexpr bool kPf = PERRK_RELAX_DIRECT && PERRK_RELAX_PF;
+  double un[V], dn[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) un[v] = dn[v] = 0.0;
+  auto prefetch = [&](long long kk) {
+    const long long nn = kk * 32 + lane;
+    if (kPf && kk < nblk && nn < nnodes) load_pair<DIM>(U, d, nn, nullptr, nullptr, lane, un, dn);
+  };
+  prefetch(k);
   for (; k < nblk; k += stride, b ^= 1) {
     stage(k + stride, b ^ 1);
     if (!PERRK_RELAX_DIRECT) cp_async_wait<1>();
     __syncwarp();
     const long long n = k * 32 + lane;
+    double u[V], dv[V];
+    if (kPf) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        u[v] = un[v];
+        dv[v] = dn[v];
+      }
+      prefetch(k + stride);
+    }
     if (n < nnodes) {
       const int cell = static_cast<int>(n / NPC), l = static_cast<int>(n % NPC);
       const double om = node_measure_rec<DIM>(m, cell, l);
-      double u[V], dv[V];
-      load_pair<DIM>(U, d, n, s_stage[wib][b][0], s_stage[wib][b][1], lane, u, dv);
+      if (!kPf) load_pair<DIM>(U, d, n, s_stage[wib][b][0], s_stage[wib][b][1], lane, u, dv);
       if (numerics == 1) {
         double du[V], ra, rb;
         // rounded products (never contracted into later sums): the same bits
@@ -632,7 +658,7 @@ __global__ void __launch_bounds__(256, 3)
 // passes and update_kernel proceed from the untouched U_in.  One full read of
 // U and d per step is saved (SURVEY.md 7.3 H1 numerics only).
 template <int DIM>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, PERRK_RELAX_MINB)
     relax_spec_kernel(const double* __restrict__ U, const double* __restrict__ d,
                       double* __restrict__ Uout, MeshDev m, Phys ph, StepState* st,
                       double* partials, unsigned* counter, long long nnodes, int want_nu,
@@ -665,15 +691,33 @@ __global__ void __launch_bounds__(256, 3)
   long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + wib;
   int b = 0;
   stage(k, 0);
+  constexpr bool kPf = PERRK_RELAX_DIRECT && PERRK_RELAX_PF;
+  double un[V], dn[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) un[v] = dn[v] = 0.0;
+  auto prefetch = [&](long long kk) {
+    const long long nn = kk * 32 + lane;
+    if (kPf && kk < nblk && nn < nnodes) load_pair<DIM>(U, d, nn, nullptr, nullptr, lane, un, dn);
+  };
+  prefetch(k);
   for (; k < nblk; k += stride, b ^= 1) {
     stage(k + stride, b ^ 1);
     if (!PERRK_RELAX_DIRECT) cp_async_wait<1>();
     __syncwarp();
     const long long n = k * 32 + lane;
+    double u[V], dv[V];
+    if (kPf) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        u[v] = un[v];
+        dv[v] = dn[v];
+      }
+      prefetch(k + stride);
+    }
     if (n < nnodes) {
-      double u[V], dv[V], du[V], T[V], ra, rb;
+      double du[V], T[V], ra, rb;
       const long long gb = sidx_n<DIM>(n, 0);
-      load_pair<DIM>(U, d, n, s_stage[wib][b][0], s_stage[wib][b][1], lane, u, dv);
+      if (!kPf) load_pair<DIM>(U, d, n, s_stage[wib][b][0], s_stage[wib][b][1], lane, u, dv);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         du[v] = __dmul_rn(gdt, dv[v]);
