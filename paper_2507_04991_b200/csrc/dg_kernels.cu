@@ -330,8 +330,12 @@ __device__ void relax_update(StepState* st, dd A, dd B) {
 #ifndef PERRK_RELAX_PF
 // 1 (direct loads): the next block's U and d are loaded into registers before
 // the current block's terms are evaluated (twice the bytes in flight per warp;
-// the per-lane order of the sums, and so every bit of the result, is unchanged)
-#define PERRK_RELAX_PF 1
+// the per-lane order of the sums, and so every bit of the result, is unchanged).
+// Measured (profiles/r02_ab.txt, pass 11): slower, 318 -> 387 us (pass) and
+// 551 -> 710 us (fused pass 2) at 3 blocks per SM (spills), 376 / 620 us at 2:
+// these kernels run the FP64 pipe at 55% (two logarithms per node), they are
+// not waiting for memory
+#define PERRK_RELAX_PF 0
 #endif
 
 // One warp's 32-node block k of two state arrays (U and d) into shared
