@@ -1,0 +1,13 @@
+# Round-2 (session 4) A/B, twelfth pass: out-of-line pre-pass with batched K1 loads (unf2)
+set -x
+O=gpurun_out/ab_r2n
+mkdir -p $O
+bash profiles/tools/ab_env.sh 3 new:: unf2:unf2: > $O/ab.txt 2>&1
+LIB=paper_2507_04991_b200/libperrk_b200.so
+cp $LIB ab/orig.so.bak
+cp ab/unf2.so $LIB
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_slab.py -q -x -p no:cacheprovider > $O/gpu_tests.txt 2>&1
+echo "pytest rc=$?" >> $O/gpu_tests.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:stage3w --launch-skip 14 -c 14 --csv --log-file $O/launch_unf2.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+cp ab/orig.so.bak $LIB
+echo done
