@@ -860,6 +860,15 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
 #if PERRK_W3_EPIREG
     static_assert(!PERRK_W3_COAL, "PERRK_W3_EPIREG needs the direct epilogue");
     double eU[2][V], eK[2][V];
+    if (!next_ && dm_ == 2) {  // last b-stage: no U / K1, the d block takes their place
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const size_t g = h ? gB : gA;
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          eU[h][v] = PERRK_W3_CS ? __ldcs(a.d + g + v * N) : __ldg(a.d + g + v * N);
+      }
+    }
     if (next_) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -1192,7 +1201,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       if (dm_) {
         if (dm_ == 2) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) x[v] = fma(a.b, K[v], W3_LD(a.d + g + v * N));
+          for (int v = 0; v < V; ++v)
+            x[v] = fma(a.b, K[v], (PERRK_W3_EPIREG && !next_) ? W3_EU(h, v) : W3_LD(a.d + g + v * N));
         } else {
 #pragma unroll
           for (int v = 0; v < V; ++v) x[v] = a.b * K[v];

@@ -1,0 +1,16 @@
+# Round-2 (session 4) A/B, thirteenth pass: d block of the last b-stage into registers after the volume phase (dpf)
+set -x
+O=gpurun_out/ab_r2o
+mkdir -p $O
+bash profiles/tools/ab_env.sh 3 new:: dpf:dpf: > $O/ab.txt 2>&1
+LIB=paper_2507_04991_b200/libperrk_b200.so
+cp $LIB ab/orig.so.bak
+for v in orig dpf; do
+  [ $v = orig ] && cp ab/orig.so.bak $LIB || cp ab/$v.so $LIB
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:stage3w --launch-skip 14 -c 14 --csv --log-file $O/launch_$v.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+done
+cp ab/dpf.so $LIB
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_fused.py -q -x -p no:cacheprovider > $O/gpu_tests.txt 2>&1
+echo "pytest rc=$?" >> $O/gpu_tests.txt
+cp ab/orig.so.bak $LIB
+echo done
