@@ -137,6 +137,10 @@ namespace dev {
 #define PERRK_W3_OWNL1PF 0
 #endif
 
+#ifndef PERRK_W3_UNFPF
+#define PERRK_W3_UNFPF 0  // 1: K1 traces of neighbours formed in the surface pre-pass are prefetched to L2 at staging
+#endif
+
 #ifndef PERRK_W3_ZOWN
 #define PERRK_W3_ZOWN 1  // 1: z-face terms are added by the lane that computes them (it owns the node)
 #endif
@@ -733,6 +737,14 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
         const int vs = gh ? 1 : N;
 #pragma unroll
         for (int v = 0; v < V; ++v) cp_async8(dst + v, src + v * vs);
+#if PERRK_W3_UNFPF
+        // the K1 trace the pre-pass will read: towards L2 now
+        if ((unf >> d) & 1u) {
+          const double* k1 = a.K1 + static_cast<size_t>(nbc) * N * V + w3_face_node(d, 1 - side, pt);
+#pragma unroll
+          for (int v = 0; v < V; ++v) asm volatile("prefetch.global.L2 [%0];" ::"l"(k1 + v * N));
+        }
+#endif
         continue;
       }
 #endif
