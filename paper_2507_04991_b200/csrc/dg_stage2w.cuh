@@ -26,6 +26,14 @@
 namespace perrk {
 namespace dev {
 
+#ifndef PERRK_W2_FLAT
+// 1: as stage3w_kernel's PERRK_W3_HOIST / PERRK_W3_FLAT: neighbour ids and formed
+// flags read once, branch-free trace staging, a warp-uniform pre-pass for
+// neighbours formed from the first column, the two surface rounds as one
+// straight-line block, y-face terms added by the owning lane, branch-free x gather
+#define PERRK_W2_FLAT 1
+#endif
+
 #ifndef PERRK_W2_COAL
 #define PERRK_W2_COAL 0  // 1: epilogue blocks through the slice and bulk stores (the round-2 session-1 form)
 #endif
@@ -245,6 +253,31 @@ __global__ void __launch_bounds__(W2::T, 2)
     }
     // ---- neighbour face traces -> the face slots (cp.async), one direction
     // per round: round d, face 2 d + side, point pt ----------------------------
+#if PERRK_W2_FLAT
+    int nb2[2];
+    unsigned unf = 0;  // bit d: the neighbour on (d, side) is formed from U and K1 in the pre-pass
+#pragma unroll
+    for (int d = 0; d < 2; ++d) nb2[d] = live ? rp->nb[2 * d + side] : 0;
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
+      if (live && a.form && nb2[d] >= 0 && !a.formed[l2]) unf |= 1u << d;
+    }
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      // branch free (padding lanes copy a trace of cell 0: unused)
+      double* dst = fs + w2_fs(cs, d, side, pt);
+      const int nbc = nb2[d];
+      const bool gh = nbc < 0;
+      const double* src =
+          gh ? m.ghost + (static_cast<size_t>(-1 - nbc) * S::FP + pt) * V
+             : ((a.form && !((unf >> d) & 1u)) ? a.Us : a.U) + static_cast<size_t>(nbc) * N * V +
+                   w2_face_node(d, 1 - side, pt);
+      const int vs = gh ? 1 : N;
+#pragma unroll
+      for (int v = 0; v < V; ++v) cp_async8(dst + v, src + v * vs);
+    }
+#else
 #pragma unroll
     for (int d = 0; d < 2; ++d) {
       double* dst = fs + w2_fs(cs, d, side, pt);
@@ -266,6 +299,7 @@ __global__ void __launch_bounds__(W2::T, 2)
         }  // else: formed from U and K1 in the surface phase
       }
     }
+#endif
     cp_async_commit();
     fetch_rec(rb ^ 1, ng0);  // the next group's descriptors
     // ---- primitives of A and B -> the slice; per-warp smoothness range -------
@@ -276,7 +310,7 @@ __global__ void __launch_bounds__(W2::T, 2)
       const int n = s + 8 * h;
       double ir;
       const Prim<2> q = prim_of<2>(ph, h ? uB : uA, ir);
-      okAB = okAB && prim_ok<2>(q);
+      okAB = okAB & prim_ok<2>(q);
       const double be = q.rho * frcp(q.p);
       double2* dst = reinterpret_cast<double2*>(pr) + w2_sw(cs, n);
       dst[0] = make_double2(q.rho, be);
@@ -324,6 +358,73 @@ __global__ void __launch_bounds__(W2::T, 2)
     // points (semidisc.cpp:489-556, :450-454) ----------------------------------
     cp_async_wait<1>();  // the traces (the next descriptors may fly on)
     __syncwarp();
+#if PERRK_W2_FLAT
+    if (__any_sync(0xffffffffu, unf != 0u)) {  // a level's first active stage
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        if ((unf >> d) & 1u) {
+          const int l2 = static_cast<int>((lv >> (8 * (1 + 2 * d + side))) & 0xff);
+          const size_t gi = static_cast<size_t>(nb2[d]) * N * V + w2_face_node(d, 1 - side, pt);
+          const double b1 = dt * a.a1[l2];
+          double* sl = fs + w2_fs(cs, d, side, pt);  // the lane's own slot: the U trace
+          double un[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) un[v] = fma(b1, __ldg(a.K1 + gi + v * N), sl[v]);
+#pragma unroll
+          for (int v = 0; v < V; ++v) sl[v] = un[v];
+        }
+      }
+    }
+    unsigned badf = 0;
+    const double lift2[2] = {live ? rp->lift[0] : 0.0, live ? rp->lift[1] : 0.0};
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      double* slotp = fs + w2_fs(cs, d, side, pt);
+      double un[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) un[v] = slotp[v];
+      const double J2 = d == 0 ? J2x : J2y;
+      const int j = side ? N1 - 1 : 0;
+      double o4[V];
+      const double2* on = reinterpret_cast<const double2*>(pr) + w2_sw(cs, w2_face_node(d, side, pt));
+      const double2 o0 = on[0], o1 = on[S::NQ], o2 = on[2 * S::NQ], o3 = on[3 * S::NQ];
+      const double vo[2] = {o1.x, o1.y};
+      const bool ok = rus_lift_v<2, SURF>(ph, o0.x, vo, o2.x, o2.y, o3.x, un, d, side,
+                                          J2 * c_D[j * N1 + j], side ? -lift2[d] : lift2[d],
+                                          false, o4);
+      if (!ok) badf |= 1u << d;
+      if (d == 1) {
+        // y faces: face point (1, side, pt) of lane (side, pt) belongs to the
+        // lane's own node (A on side 0, B on side 1)
+        const double mA = side ? 0.0 : 1.0, mB = side ? 1.0 : 0.0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          KA[v] = fma(mA, o4[v], KA[v]);
+          KB[v] = fma(mB, o4[v], KB[v]);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) slotp[v] = o4[v];
+      }
+    }
+    if (live && badf) {
+      const int nbc = (badf & 1u) ? nb2[0] : nb2[1];
+      report_bad(st, a.stage, a.ncells,
+                 nbc < 0 ? m.ghost_gid[-1 - nbc] : (m.gid ? m.gid[nbc] : nbc));
+    }
+    __syncwarp();
+    {  // x faces (pt = iy): every lane reads a written slot, nodes off the face weigh it with 0
+      const double mx = (ix == 0 || ix == N1 - 1) ? 1.0 : 0.0;
+      const int sd = ix ? 1 : 0;
+      const double* cA = fs + w2_fs(cs, 0, sd, yA);
+      const double* cB = fs + w2_fs(cs, 0, sd, yB);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        KA[v] = fma(mx, cA[v], KA[v]);
+        KB[v] = fma(mx, cB[v], KB[v]);
+      }
+    }
+#else
 #pragma unroll
     for (int d = 0; d < 2; ++d) {
       double* slotp = fs + w2_fs(cs, d, side, pt);
@@ -385,6 +486,7 @@ __global__ void __launch_bounds__(W2::T, 2)
         for (int v = 0; v < V; ++v) KB[v] += c[v];
       }
     }
+#endif
 
     // ---- epilogue (stepper.cpp:52-55, 60-72, 89-92) ---------------------------
     if ((a.want_dh || a.want_h) && live) {
