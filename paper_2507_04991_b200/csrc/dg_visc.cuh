@@ -49,7 +49,11 @@ __device__ __forceinline__ void visc_flux2(const Phys& ph, const double* u, cons
 // levels, 4/h, lift; no dependent level loads), and the stage state and the
 // neighbour traces sit in shared memory variable-major ([V][node]: the
 // 8-byte accesses of a warp are conflict free).
-__global__ void __launch_bounds__(128)
+#ifndef PERRK_GRAD_MINB
+#define PERRK_GRAD_MINB 12  // resident 128-thread blocks per SM grad_kernel is compiled for (40 registers, no spills; A/B: 114 -> 104 us)
+#endif
+
+__global__ void __launch_bounds__(128, PERRK_GRAD_MINB)
     grad_kernel(StageArgs a, MeshDev m, Phys ph, StepState* st, double* out, long long ndofs,
                 int mode) {
   constexpr int DIM = 2, V = 4, NPC = 16, FP = 4, NFP = 4 * FP, T = 128, CPB = T / NPC;
