@@ -50,7 +50,7 @@ __device__ __forceinline__ void visc_flux2(const Phys& ph, const double* u, cons
 // neighbour traces sit in shared memory variable-major ([V][node]: the
 // 8-byte accesses of a warp are conflict free).
 #ifndef PERRK_GRAD_MINB
-#define PERRK_GRAD_MINB 12  // resident 128-thread blocks per SM grad_kernel is compiled for (40 registers, no spills; A/B: 114 -> 104 us)
+#define PERRK_GRAD_MINB 10  // resident 128-thread blocks per SM grad_kernel is compiled for (48 registers, no spills)
 #endif
 
 __global__ void __launch_bounds__(128, PERRK_GRAD_MINB)
@@ -59,69 +59,58 @@ __global__ void __launch_bounds__(128, PERRK_GRAD_MINB)
   constexpr int DIM = 2, V = 4, NPC = 16, FP = 4, NFP = 4 * FP, T = 128, CPB = T / NPC;
   __shared__ double su[V][T];             // formed stage state
   __shared__ double sn[V][CPB * NFP];     // neighbour traces [cell][face][pt]
-  __shared__ int s_cell[CPB], s_nbc[CPB][4];
-  __shared__ double s_ca1[CPB], s_na1[CPB][4], s_jac[CPB][2], s_lift[CPB][2];
-  __shared__ signed char s_cform[CPB], s_nform[CPB][4];
   if (st->aborted || st->finished) return;
   const int tid = threadIdx.x;
   const int cs = tid / NPC, l = tid % NPC;
   const int il[2] = {l % N1, l / N1};
   const double dt = st->dt;
   const int ngroups = (a.n + CPB - 1) / CPB;
+  // thread tid also fetches one neighbour trace point of its own cell:
+  // item q = tid = (cs, face f, point pt), CPB * NFP = T
+  static_assert(CPB * NFP == T, "one trace point per thread");
+  const int f = (tid % NFP) / FP, pt = tid % FP;
+  const int fd = f >> 1, fside = f & 1;
+  const int fnode = (fd == 0 ? N1 * pt : pt) + (fside ? 0 : N1 - 1) * (fd == 0 ? 1 : N1);
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    __syncthreads();
-    if (tid < CPB) {
-      const int slot = grp * CPB + tid;
-      const int cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
-      s_cell[tid] = cell;
-      if (cell >= 0) {
-        const CellRec* r = m.rec + cell;
-        const int lev = r->lev[0];
-        s_ca1[tid] = dt * a.a1[lev];
-        s_cform[tid] = a.formed[lev];
-#pragma unroll
-        for (int f = 0; f < 4; ++f) {  // face 2 d + side; the whole mesh is local (no slabs)
-          const int l2 = r->lev[1 + f];
-          s_nbc[tid][f] = r->nb[f];
-          s_na1[tid][f] = dt * a.a1[l2];
-          s_nform[tid][f] = a.formed[l2];
-        }
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          s_jac[tid][d] = 0.5 * r->J2[d];  // 2 / h (J2 = 2 (2 / h): exact)
-          s_lift[tid][d] = r->lift[d];
-        }
-      }
-    }
-    __syncthreads();
-    const int cell = s_cell[cs];
+    // every thread reads its cell's descriptor itself (the 16 threads of a
+    // cell load the same words: broadcast), so no thread waits on a
+    // descriptor stage and its barrier
+    const int slot = grp * CPB + cs;
+    const int cell = slot < a.n ? (a.list ? a.list[slot] : slot) : -1;
+    double jac[2] = {0.0, 0.0}, lift[2] = {0.0, 0.0};
+    __syncthreads();  // su / sn of the previous group are read
     if (cell >= 0) {
-      const size_t gi = static_cast<size_t>(cell) * NPC * V + l;  // device layout (sidx)
+      const CellRec* r = m.rec + cell;  // the whole mesh is local (no slabs)
+      const int lev = r->lev[0], l2 = r->lev[1 + f], nbc = r->nb[f];
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        double u;
-        const size_t g = gi + v * NPC;
-        if (!a.form) u = __ldg(a.U + g);
-        else if (s_cform[cs]) u = __ldg(a.Us + g);
-        else u = fma(s_ca1[cs], __ldg(a.K1 + g), __ldg(a.U + g));
-        su[v][tid] = u;
+      for (int d = 0; d < DIM; ++d) {
+        jac[d] = 0.5 * r->J2[d];  // 2 / h (J2 = 2 (2 / h): exact)
+        lift[d] = r->lift[d];
       }
-    }
-    for (int q = tid; q < CPB * NFP; q += T) {
-      const int c2 = q / NFP, r = q % NFP, f = r / FP, pt = r % FP;
-      if (s_cell[c2] < 0) continue;
-      const int d = f >> 1, side = f & 1;
-      const int nbc = s_nbc[c2][f];
-      const int node = (d == 0 ? N1 * pt : pt) + (side ? 0 : N1 - 1) * (d == 0 ? 1 : N1);
-      const size_t gi = static_cast<size_t>(nbc) * NPC * V + node;
+      const bool cform = a.formed[lev] != 0, nform = a.formed[l2] != 0;
+      const double ca1 = dt * a.a1[lev], na1 = dt * a.a1[l2];
+      const size_t gi = static_cast<size_t>(cell) * NPC * V + l;  // device layout (sidx)
+      const size_t gn = static_cast<size_t>(nbc) * NPC * V + fnode;
+      double uo_[V], un_[V];
+      if (!a.form) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          uo_[v] = __ldg(a.U + gi + v * NPC);
+          un_[v] = __ldg(a.U + gn + v * NPC);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          uo_[v] = cform ? __ldg(a.Us + gi + v * NPC)
+                         : fma(ca1, __ldg(a.K1 + gi + v * NPC), __ldg(a.U + gi + v * NPC));
+          un_[v] = nform ? __ldg(a.Us + gn + v * NPC)
+                         : fma(na1, __ldg(a.K1 + gn + v * NPC), __ldg(a.U + gn + v * NPC));
+        }
+      }
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        double u;
-        const size_t g = gi + v * NPC;
-        if (!a.form) u = __ldg(a.U + g);
-        else if (s_nform[c2][f]) u = __ldg(a.Us + g);
-        else u = fma(s_na1[c2][f], __ldg(a.K1 + g), __ldg(a.U + g));
-        sn[v][q] = u;
+        su[v][tid] = uo_[v];
+        sn[v][tid] = un_[v];
       }
     }
     __syncthreads();
@@ -134,13 +123,13 @@ __global__ void __launch_bounds__(128, PERRK_GRAD_MINB)
     for (int d = 0; d < DIM; ++d) {
       const int stride = d == 0 ? 1 : N1;
       const int j = il[d];
-      const double jac = s_jac[cs][d];
+      const double jacd = jac[d];
 #pragma unroll
       for (int v = 0; v < V; ++v) g[d][v] = 0.0;
       // strong-form derivative along the line (gradients_1d, semidisc.cpp:266-281)
 #pragma unroll
       for (int k = 0; k < N1; ++k) {
-        const double coef = jac * c_D[j * N1 + k];
+        const double coef = jacd * c_D[j * N1 + k];
         const int tk = tid + (k - j) * stride;
 #pragma unroll
         for (int v = 0; v < V; ++v) g[d][v] += coef * su[v][tk];
@@ -150,7 +139,7 @@ __global__ void __launch_bounds__(128, PERRK_GRAD_MINB)
         const int e = j == 0 ? 0 : 1;
         const int pt = d == 0 ? il[1] : il[0];
         const int qn = (cs * 4 + 2 * d + e) * FP + pt;
-        const double coef = s_lift[cs][d];
+        const double coef = lift[d];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const double un = sn[v][qn];
