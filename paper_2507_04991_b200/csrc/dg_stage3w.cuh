@@ -141,6 +141,10 @@ namespace dev {
 #define PERRK_W3_UNFPF 0  // 1: K1 traces of neighbours formed in the surface pre-pass are prefetched to L2 at staging
 #endif
 
+#ifndef PERRK_W3_RSQ
+#define PERRK_W3_RSQ 0  // 1: beta and the sound speed of the own nodes from one reciprocal square root
+#endif
+
 #ifndef PERRK_W3_ZOWN
 #define PERRK_W3_ZOWN 1  // 1: z-face terms are added by the lane that computes them (it owns the node)
 #endif
@@ -582,6 +586,9 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
   };
 #endif
   const double dt = st->dt;
+#if PERRK_W3_RSQ
+  const double sqrt_gamma = sqrt(ph.gamma);
+#endif
   const int ix = lane & 3, iy = (lane >> 2) & 3, zA = lane >> 4, zB = zA + 2;
   const int side = zA, pt = lane & 15;
   dd acc_dh = dd_zero(), acc_h = dd_zero();
@@ -792,7 +799,23 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       double ir;
       const Prim<3> q = prim_of<3>(ph, h ? uB : uA, ir);
       okAB = okAB & prim_ok<3>(q);
+#if PERRK_W3_RSQ
+      // beta = rho / p and c = sqrt(gamma p / rho) from one reciprocal square
+      // root of x = p / rho: beta = y^2, c = sqrt(gamma) x y (Rusanov only)
+      double be, cs_;
+      if (SURF == 2) {
+        const double x = q.p * ir;
+        const double y = frsqrt(x);
+        be = y * y;
+        cs_ = sqrt_gamma * (x * y);
+      } else {
+        be = q.rho * frcp(q.p);
+        cs_ = 0.0;
+      }
+#else
       const double be = q.rho * frcp(q.p);
+      const double cs_ = SURF == 2 ? fsqrt(ph.gamma * q.p * ir) : 0.0;
+#endif
       double2* dst = reinterpret_cast<double2*>(pr) + w3_sw(n);
       own[h].rho = q.rho;
       own[h].beta = be;
@@ -803,7 +826,7 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
       dst[0] = make_double2(q.rho, be);
       dst[N] = make_double2(q.v[0], q.v[1]);
       dst[2 * N] = make_double2(q.v[2], PERRK_W3_HALFP ? 0.5 * q.p : q.p);
-      ownEc[h] = make_double2(q.E, SURF == 2 ? fsqrt(ph.gamma * q.p * ir) : 0.0);
+      ownEc[h] = make_double2(q.E, cs_);
       dst[3 * N] = ownEc[h];
       const unsigned hr = static_cast<unsigned>(__double2hiint(q.rho));
       const unsigned hb = static_cast<unsigned>(__double2hiint(be));
