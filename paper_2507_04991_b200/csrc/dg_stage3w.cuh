@@ -142,7 +142,7 @@ namespace dev {
 #endif
 
 #ifndef PERRK_W3_RSQ
-#define PERRK_W3_RSQ 0  // 1: beta and the sound speed of the own nodes from one reciprocal square root
+#define PERRK_W3_RSQ 1  // 1: beta and the sound speed of the own nodes from one reciprocal square root (A/B -0.8%)
 #endif
 
 #ifndef PERRK_W3_ZOWN
