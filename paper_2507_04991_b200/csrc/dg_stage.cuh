@@ -41,6 +41,10 @@ namespace perrk {
 namespace dev {
 
 // cp.async.bulk.prefetch.L2 (sm_90+): bytes a multiple of 16, 16-byte aligned
+#ifndef PERRK_SURF_RSQ
+#define PERRK_SURF_RSQ 0  // 1: the neighbour trace's sound speed as z rsqrt(z); rejected: the anchored C1 run misses the 1e-12 gamma gate (1.2e-12)
+#endif
+
 #ifndef PERRK_ST_L2PF
 #define PERRK_ST_L2PF 0  // 1: the 2D / block-per-cell stage kernels prefetch the next group's blocks to L2
 #endif
@@ -373,7 +377,9 @@ __device__ __forceinline__ bool rus_lift_v(const Phys& ph, double ro, const doub
   fo[V - 1] = (Eo + po) * vod;
   g[V - 1] = 0.5 * ((En + pn) * vnd - fo[V - 1]);
   if constexpr (SURF == 2) {
-    const double lam = fmax(fabs(vod) + co, fabs(vnd) + fsqrt(ph.gamma * pn * irn));
+    // sqrt(z) = z rsqrt(z), without fsqrt's last correction step (~1.5 ulp)
+    const double zn = ph.gamma * pn * irn;
+    const double lam = fmax(fabs(vod) + co, fabs(vnd) + (PERRK_SURF_RSQ ? zn * frsqrt(zn) : fsqrt(zn)));
     const double hl = side ? -0.5 * lam : 0.5 * lam;
     g[0] = fma(hl, rn - ro, g[0]);
 #pragma unroll

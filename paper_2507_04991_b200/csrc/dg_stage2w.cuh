@@ -34,6 +34,10 @@ namespace dev {
 #define PERRK_W2_FLAT 1
 #endif
 
+#ifndef PERRK_W2_RSQ
+#define PERRK_W2_RSQ 0  // 1: beta and c from one reciprocal square root (no gain on C3; see PERRK_SURF_RSQ)
+#endif
+
 #ifndef PERRK_W2_COAL
 #define PERRK_W2_COAL 0  // 1: epilogue blocks through the slice and bulk stores (the round-2 session-1 form)
 #endif
@@ -195,6 +199,7 @@ __global__ void __launch_bounds__(W2::T, 2)
     cp_async_commit();
   };
   const double dt = st->dt;
+  const double sqrt_gamma = sqrt(ph.gamma);
   dd acc_dh = dd_zero(), acc_h = dd_zero();
   unsigned long long dmax_bits = 0;
   const int nw = gridDim.x * S::WPB;
@@ -311,12 +316,23 @@ __global__ void __launch_bounds__(W2::T, 2)
       double ir;
       const Prim<2> q = prim_of<2>(ph, h ? uB : uA, ir);
       okAB = okAB & prim_ok<2>(q);
-      const double be = q.rho * frcp(q.p);
+      // (Rusanov) beta = rho / p and c = sqrt(gamma p / rho) from one reciprocal
+      // square root y of x = p / rho: beta = y^2, c = sqrt(gamma) x y (as stage3w_kernel)
+      double be, cs_ = 0.0;
+      if (SURF == 2 && PERRK_W2_RSQ) {
+        const double x = q.p * ir;
+        const double y = frsqrt(x);
+        be = y * y;
+        cs_ = sqrt_gamma * (x * y);
+      } else {
+        be = q.rho * frcp(q.p);
+        if (SURF == 2) cs_ = fsqrt(ph.gamma * q.p * ir);
+      }
       double2* dst = reinterpret_cast<double2*>(pr) + w2_sw(cs, n);
       dst[0] = make_double2(q.rho, be);
       dst[S::NQ] = make_double2(q.v[0], q.v[1]);
       dst[2 * S::NQ] = make_double2(q.p, q.E);
-      dst[3 * S::NQ] = make_double2(SURF == 2 ? fsqrt(ph.gamma * q.p * ir) : 0.0, 0.0);
+      dst[3 * S::NQ] = make_double2(cs_, 0.0);
       if (live) {
         const unsigned hr = static_cast<unsigned>(__double2hiint(q.rho));
         const unsigned hb = static_cast<unsigned>(__double2hiint(be));
