@@ -145,6 +145,10 @@ namespace dev {
 #define PERRK_W3_RSQ 1  // 1: beta and the sound speed of the own nodes from one reciprocal square root (A/B -0.8%)
 #endif
 
+#ifndef PERRK_W3_OWNCG
+#define PERRK_W3_OWNCG 0  // 1: the own formed stage state is loaded past L1 (ld.global.cg)
+#endif
+
 #ifndef PERRK_W3_ZOWN
 #define PERRK_W3_ZOWN 1  // 1: z-face terms are added by the lane that computes them (it owns the node)
 #endif
@@ -698,8 +702,8 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     } else if (a.formed[lev]) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        uA[v] = __ldg(a.Us + gA + v * N);
-        uB[v] = __ldg(a.Us + gB + v * N);
+        uA[v] = PERRK_W3_OWNCG ? __ldcg(a.Us + gA + v * N) : __ldg(a.Us + gA + v * N);
+        uB[v] = PERRK_W3_OWNCG ? __ldcg(a.Us + gB + v * N) : __ldg(a.Us + gB + v * N);
       }
     } else {
       const double a1 = dt * a.a1[lev];
