@@ -146,7 +146,7 @@ namespace dev {
 #endif
 
 #ifndef PERRK_W3_OWNCG
-#define PERRK_W3_OWNCG 0  // 1: the own formed stage state is loaded past L1 (ld.global.cg)
+#define PERRK_W3_OWNCG 0  // 1: the own formed stage state is loaded past L1 (ld.global.cg); 2: with L1::evict_last
 #endif
 
 #ifndef PERRK_W3_ZOWN
@@ -322,6 +322,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "}\n" ::"r"(b),
       "r"(parity)
       : "memory");
+}
+
+// a load that asks L1 to keep its line (PERRK_W3_OWNCG == 2)
+__device__ __forceinline__ double w3_ld_l1last(const double* p) {
+  double x;
+  asm volatile("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(x) : "l"(p));
+  return x;
 }
 
 // one cell's contiguous block of a state array (64 V doubles) into the warp's slice
@@ -702,8 +709,10 @@ __global__ void __launch_bounds__(W3::T, PERRK_W3_MINB)
     } else if (a.formed[lev]) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        uA[v] = PERRK_W3_OWNCG ? __ldcg(a.Us + gA + v * N) : __ldg(a.Us + gA + v * N);
-        uB[v] = PERRK_W3_OWNCG ? __ldcg(a.Us + gB + v * N) : __ldg(a.Us + gB + v * N);
+        uA[v] = PERRK_W3_OWNCG == 2 ? w3_ld_l1last(a.Us + gA + v * N)
+                : PERRK_W3_OWNCG  ? __ldcg(a.Us + gA + v * N) : __ldg(a.Us + gA + v * N);
+        uB[v] = PERRK_W3_OWNCG == 2 ? w3_ld_l1last(a.Us + gB + v * N)
+                : PERRK_W3_OWNCG  ? __ldcg(a.Us + gB + v * N) : __ldg(a.Us + gB + v * N);
       }
     } else {
       const double a1 = dt * a.a1[lev];

@@ -2,5 +2,5 @@
 set -x
 O=gpurun_out/ab_r2w
 mkdir -p $O
-bash profiles/tools/ab_env.sh 3 base:base: owncg:owncg: > $O/ab.txt 2>&1
+bash profiles/tools/ab_env.sh 3 base:base: ownel:ownel: > $O/ab.txt 2>&1
 echo done
